@@ -1,0 +1,112 @@
+/*
+ * glod_b200 — C ABI of the B200-native per-view hot path of
+ * "A LoD of Gaussians" (arXiv 2507.01110).
+ *
+ * Plain C: pointers, sizes and a cudaStream_t passed as void*.  Every
+ * pointer marked [dev] is device memory owned by the caller; the library
+ * owns nothing between calls (scratch is caller-provided, sized by the
+ * matching *_scratch_bytes query).  All work is enqueued on `stream`;
+ * nothing synchronises unless stated.  Every call returns GLOD_OK (0) or an
+ * error code; glod_last_error() returns a thread-local message.
+ *
+ * The reference (/root/reference/pkg/src/glod, pure Python) has no FFI: its
+ * boundary is its Python function signatures.  Each entry point below cites
+ * the reference function it replaces; the Python mirror in
+ * paper_2507_01110_b200/ binds these through ctypes.
+ */
+#ifndef GLOD_B200_H
+#define GLOD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference exception classes) ---------- */
+#define GLOD_OK 0
+#define GLOD_ERR_INVALID_ARGUMENT 1   /* ValueError / InvalidParameterError */
+#define GLOD_ERR_CUDA 2               /* RuntimeError                        */
+#define GLOD_ERR_INVALID_INPUT 3      /* renderer.InvalidInputError          */
+
+int glod_version(void);
+const char* glod_last_error(void);
+
+/* ======================================================================= *
+ * LoD selection
+ * ======================================================================= */
+
+/* Static per-HSPT scene data (uploaded once per HSPT version). */
+typedef struct glod_lod_scene {
+  int64_t capacity;             /* hierarchy node slots                       */
+  int32_t root;                 /* Hierarchy.root                             */
+  int32_t _pad0;
+  const int32_t* children;      /* [dev] [capacity*2], -1 = NONE              */
+  const int32_t* kind;          /* [dev] [capacity]: spt_id>=0 | -2 pass | -1 */
+  const double* means;          /* [dev] [capacity*3] live f64 means          */
+  const double* scales;         /* [dev] [capacity*3] live f64 scales         */
+  int32_t num_spts;
+  int32_t key_f64;              /* 1: f64 keys, 0: f32 keys (file scenes)     */
+  int64_t num_records;          /* total SPT records                          */
+  const int64_t* spt_offset;    /* [dev] [S] first record of each SPT         */
+  const int32_t* spt_count;     /* [dev] [S]                                  */
+  const int32_t* spt_root_rec;  /* [dev] [S] record index of the SPT root     */
+  const double* spt_center;     /* [dev] [S*3] Spt.root_center (build time)   */
+  const void* key_self;         /* [dev] [R] f32|f64                          */
+  const void* key_parent;       /* [dev] [R] f32|f64, descending per SPT      */
+  const int32_t* rec_node;      /* [dev] [R] node id of each record           */
+} glod_lod_scene;
+
+/* Per-view parameters: camera position, frustum planes computed on the host
+ * with Frustum.from_camera (core.py:301-328), LodConfig. */
+typedef struct glod_lod_view {
+  double position[3];
+  double planes[24];            /* 6 x (nx, ny, nz, d)                        */
+  int32_t cull;
+  int32_t metric;               /* 0 max_scale, 1 surface_area                */
+  double threshold;
+} glod_lod_view;
+
+typedef struct glod_lod_select_out {
+  int32_t* upper_ids;           /* [dev] [capacity] sorted                    */
+  int32_t* pass_ids;            /* [dev] [capacity] sorted                    */
+  int32_t* spt_ids;             /* [dev] [S] sorted selected spt ids          */
+  double* d_root;               /* [dev] [S]                                  */
+  int32_t* prefix_len;          /* [dev] [S]                                  */
+  int32_t* counts;              /* [dev] [4] n_upper, n_pass, n_spt, levels   */
+} glod_lod_select_out;
+
+/* Replaces hspt.cut_hspt stage 1 + stage-2 prologue (hspt.py:104-153) and
+ * the passthrough hierarchy.bfs_cut calls (hierarchy.py:244-266). */
+int64_t glod_lod_select_scratch_bytes(int64_t capacity, int32_t num_spts);
+int glod_lod_select(const glod_lod_scene* scene, const glod_lod_view* view,
+                    const glod_lod_select_out* out, void* scratch,
+                    int64_t scratch_bytes, void* stream);
+
+typedef struct glod_spt_compact_in {
+  const int32_t* n_spt;         /* [dev] scalar                               */
+  const int32_t* spt_ids;       /* [dev] [n_spt]                              */
+  const double* dist;           /* [dev] [n_spt] cut distance per SPT         */
+} glod_spt_compact_in;
+
+typedef struct glod_spt_compact_out {
+  int32_t* prefix_len;          /* [dev] [S]                                  */
+  int32_t* root_rule;           /* [dev] [S]                                  */
+  int64_t* seg_start;           /* [dev] [S]                                  */
+  int32_t* sel_seg;             /* [dev] [R] segment (index into spt_ids)     */
+  int32_t* sel_pos;             /* [dev] [R] record position within the SPT   */
+  int32_t* sel_node;            /* [dev] [R] node id                          */
+  int64_t* total;               /* [dev] [2] n_selected, virtual length       */
+} glod_spt_compact_out;
+
+/* Replaces spt.cut_spt (spt.py:67-75) for a batch of SPTs and
+ * trainer._spt_positions (trainer.py:302-309). */
+int64_t glod_spt_compact_scratch_bytes(int32_t num_spts, int64_t num_records);
+int glod_spt_compact(const glod_lod_scene* scene, const glod_spt_compact_in* in,
+                     const glod_spt_compact_out* out, void* scratch,
+                     int64_t scratch_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLOD_B200_H */

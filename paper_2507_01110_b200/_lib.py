@@ -1,0 +1,111 @@
+"""ctypes binding of include/glod_b200.h.
+
+The product path has no fallback: if `libglod_b200.so` is missing or a CUDA
+device is absent, `lib()` raises.  (`import paper_2507_01110_b200` works
+without a GPU so the CPU test-suite can check the library's exports.)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libglod_b200.so"
+
+GLOD_OK = 0
+GLOD_ERR_INVALID_ARGUMENT = 1
+GLOD_ERR_CUDA = 2
+GLOD_ERR_INVALID_INPUT = 3
+
+P = C.c_void_p
+
+
+class LodScene(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("root", C.c_int32), ("_pad0", C.c_int32),
+                ("children", P), ("kind", P), ("means", P), ("scales", P),
+                ("num_spts", C.c_int32), ("key_f64", C.c_int32), ("num_records", C.c_int64),
+                ("spt_offset", P), ("spt_count", P), ("spt_root_rec", P), ("spt_center", P),
+                ("key_self", P), ("key_parent", P), ("rec_node", P)]
+
+
+class LodView(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("planes", C.c_double * 24),
+                ("cull", C.c_int32), ("metric", C.c_int32), ("threshold", C.c_double)]
+
+
+class SelectOut(C.Structure):
+    _fields_ = [("upper_ids", P), ("pass_ids", P), ("spt_ids", P), ("d_root", P),
+                ("prefix_len", P), ("counts", P)]
+
+
+class CompactIn(C.Structure):
+    _fields_ = [("n_spt", P), ("spt_ids", P), ("dist", P)]
+
+
+class CompactOut(C.Structure):
+    _fields_ = [("prefix_len", P), ("root_rule", P), ("seg_start", P), ("sel_seg", P),
+                ("sel_pos", P), ("sel_node", P), ("total", P)]
+
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "glod_version": (C.c_int, []),
+    "glod_last_error": (C.c_char_p, []),
+    "glod_lod_select_scratch_bytes": (C.c_int64, [C.c_int64, C.c_int32]),
+    "glod_lod_select": (C.c_int, [C.POINTER(LodScene), C.POINTER(LodView),
+                                  C.POINTER(SelectOut), P, C.c_int64, P]),
+    "glod_spt_compact_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int64]),
+    "glod_spt_compact": (C.c_int, [C.POINTER(LodScene), C.POINTER(CompactIn),
+                                   C.POINTER(CompactOut), P, C.c_int64, P]),
+}
+
+_LIB = None
+
+
+class GlodError(RuntimeError):
+    pass
+
+
+def load(path: Path = LIB_PATH) -> C.CDLL:
+    """dlopen the library and bind every declared symbol (no GPU needed)."""
+    global _LIB
+    if _LIB is None:
+        if not path.exists():
+            raise GlodError(f"{path} not built: run python -m paper_2507_01110_b200.build")
+        lib = C.CDLL(str(path))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = lib
+    return _LIB
+
+
+def lib() -> C.CDLL:
+    """The library, for device work: requires a CUDA device."""
+    import torch
+    if not torch.cuda.is_available():
+        raise GlodError("glod_b200 needs a CUDA device (no CPU fallback)")
+    return load()
+
+
+def check(code: int):
+    if code == GLOD_OK:
+        return
+    msg = load().glod_last_error().decode(errors="replace")
+    if code == GLOD_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if code == GLOD_ERR_INVALID_INPUT:
+        from .renderer import InvalidInputError
+        raise InvalidInputError(msg)
+    raise GlodError(msg)
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None → NULL)."""
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

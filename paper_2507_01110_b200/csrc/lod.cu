@@ -1,0 +1,521 @@
+// LoD selection on the device.
+//
+// K2 `select_kernel` replaces cut_hspt stage 1 (hspt.py:122-144) together
+// with the passthrough bfs_cut calls it makes (hierarchy.py:244-266) and the
+// per-SPT root distance / prefix search of stage 2 (hspt.py:147-153,
+// spt.py:70).  One cooperative launch walks every BFS (the upper tree and
+// all passthrough subtrees at once) level-synchronously with a software
+// grid barrier between levels, marks the selections in bitmaps, compacts
+// the bitmaps into sorted id lists (the reference's np.sort), then computes
+// d_root and prefix_len for every selected SPT.
+//
+// K1 `compact_kernel` replaces cut_spt's interval test (spt.py:71-75) for
+// all selected SPTs at once: the selected prefixes are laid end to end in a
+// virtual index space and compacted by a single order-preserving pass with
+// decoupled look-back, so each key_self is read exactly once.
+#include "common.cuh"
+#include "lod.cuh"
+
+namespace glod {
+
+namespace {
+
+constexpr int kSelectThreads = 512;
+constexpr int kCompactThreads = 512;
+constexpr int kRows = 8;                          // items per thread per tile
+constexpr int kTile = kCompactThreads * kRows;    // 4096 virtual records
+constexpr int kMaxLevels = 250;
+
+constexpr uint32_t kPass = 1u << 31;   // entry belongs to a passthrough BFS
+constexpr uint32_t kStart = 1u << 30;  // first frontier of its BFS (size 1 → gemv order)
+constexpr uint32_t kIdMask = kStart - 1;
+
+inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct SelectScratch {
+  unsigned int* bar;        // [2]
+  unsigned int* lvl_count;  // [kMaxLevels+1]
+  uint32_t* bm_upper;
+  uint32_t* bm_pass;
+  uint32_t* bm_spt;
+  uint32_t* frontier[2];
+  long long* block_cnt;     // [3*grid]
+  size_t zero_bytes;        // bytes to clear from bar onwards
+};
+
+SelectScratch carve_select(void* base, int64_t cap, int32_t S, int grid) {
+  SelectScratch s;
+  char* p = static_cast<char*>(base);
+  size_t w_nodes = (size_t(cap) + 31) / 32, w_spt = (size_t(S) + 31) / 32;
+  s.bar = reinterpret_cast<unsigned int*>(p);
+  s.lvl_count = s.bar + 2;
+  size_t off = align_up(sizeof(unsigned int) * (kMaxLevels + 3));
+  s.bm_upper = reinterpret_cast<uint32_t*>(p + off); off += 4 * w_nodes;
+  s.bm_pass = reinterpret_cast<uint32_t*>(p + off); off += 4 * w_nodes;
+  s.bm_spt = reinterpret_cast<uint32_t*>(p + off); off += 4 * w_spt;
+  s.zero_bytes = off;
+  off = align_up(off);
+  s.frontier[0] = reinterpret_cast<uint32_t*>(p + off); off = align_up(off + 4 * size_t(cap) + 4);
+  s.frontier[1] = reinterpret_cast<uint32_t*>(p + off); off = align_up(off + 4 * size_t(cap) + 4);
+  s.block_cnt = reinterpret_cast<long long*>(p + off);
+  return s;
+}
+
+GLOD_DEV bool sphere_in_frustum(const double* P, double x, double y, double z,
+                                double r, bool gemv) {
+  // sphere_intersects_frustum (core.py:364-372): signed = c @ P[:, :3].T + P[:, 3].
+  // numpy's matmul goes to OpenBLAS: dgemm for a frontier of ≥2 rows,
+  // dgemv for a single row; their FMA chains differ.
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const double a = P[4 * k], b = P[4 * k + 1], c = P[4 * k + 2], d = P[4 * k + 3];
+    double s = gemv ? fma_(z, c, fma_(x, a, mul(y, b))) : fma_(z, c, fma_(y, b, mul(x, a)));
+    s = add(s, d);
+    if (!(s <= r)) return false;
+  }
+  return true;
+}
+
+template <typename K>
+GLOD_DEV int prefix_search(const K* kp, int n, double d) {
+  // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (double(kp[mid]) > d) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+GLOD_DEV int prefix_len_of(const LodScene& sc, int s, double d) {
+  const int64_t off = sc.spt_offset[s];
+  const int n = sc.spt_count[s];
+  return sc.key_f64 ? prefix_search(static_cast<const double*>(sc.key_parent) + off, n, d)
+                    : prefix_search(static_cast<const float*>(sc.key_parent) + off, n, d);
+}
+
+GLOD_DEV double key_self_at(const LodScene& sc, int64_t rec) {
+  return sc.key_f64 ? static_cast<const double*>(sc.key_self)[rec]
+                    : double(static_cast<const float*>(sc.key_self)[rec]);
+}
+
+// Contiguous [lo, hi) share of `n` items for block b of g.
+GLOD_DEV void block_range(long long n, int b, int g, long long& lo, long long& hi) {
+  lo = n * b / g;
+  hi = n * (b + 1) / g;
+}
+
+GLOD_DEV long long block_sum(long long v, long long* sm) {
+  block_excl_scan(v, sm);
+  const int nw = (blockDim.x + 31) >> 5;
+  long long t = sm[nw];
+  __syncthreads();
+  return t;
+}
+
+// Phase A of a grid-wide bitmap compaction: popcount of this block's words.
+GLOD_DEV long long bitmap_block_count(const uint32_t* bm, long long nwords, long long* sm) {
+  long long lo, hi;
+  block_range(nwords, blockIdx.x, gridDim.x, lo, hi);
+  long long c = 0;
+  for (long long w = lo + threadIdx.x; w < hi; w += blockDim.x) c += __popc(ld_cg(bm + w));
+  return block_sum(c, sm);
+}
+
+// Phase B: write the set bit positions of this block's words, in order.
+GLOD_DEV void bitmap_block_write(const uint32_t* bm, long long nwords, long long nbits,
+                                 long long base, int32_t* out, long long* sm) {
+  long long lo, hi;
+  block_range(nwords, blockIdx.x, gridDim.x, lo, hi);
+  long long span = hi - lo;
+  long long chunk = (span + blockDim.x - 1) / blockDim.x;
+  long long w0 = lo + chunk * threadIdx.x, w1 = min(hi, w0 + chunk);
+  long long c = 0;
+  for (long long w = w0; w < w1; ++w) c += __popc(ld_cg(bm + w));
+  long long o = base + block_excl_scan(c, sm);
+  for (long long w = w0; w < w1; ++w) {
+    uint32_t bits = ld_cg(bm + w);
+    while (bits) {
+      int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      long long id = w * 32 + b;
+      if (id < nbits) out[o++] = int32_t(id);
+    }
+  }
+}
+
+GLOD_DEV long long sum_before(const long long* cnt, int b, long long* sm) {
+  long long v = 0;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) v += ld_cg(cnt + i);
+  return block_sum(v, sm);
+}
+
+__global__ void __launch_bounds__(kSelectThreads)
+select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
+  __shared__ long long sm[kSelectThreads / 32 + 1];
+  __shared__ double planes[24];
+  if (threadIdx.x < 24) planes[threadIdx.x] = v.planes[threadIdx.x];
+  const int lane = threadIdx.x & 31;
+  const long long gthreads = (long long)gridDim.x * blockDim.x;
+  const long long gwarp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ws.frontier[0][0] = uint32_t(sc.root) | kStart;
+    ws.lvl_count[0] = 1;
+  }
+  grid_sync(ws.bar);
+
+  // ---- level-synchronous BFS over the upper tree + passthrough subtrees ----
+  int level = 0;
+  for (; level < kMaxLevels; ++level) {
+    const long long n = ld_cg(ws.lvl_count + level);
+    if (n == 0) break;
+    const uint32_t* cur = ws.frontier[level & 1];
+    uint32_t* nxt = ws.frontier[(level + 1) & 1];
+    unsigned int* nxt_count = ws.lvl_count + level + 1;
+    for (long long base = gwarp0; base < n; base += gthreads) {
+      const long long i = base + lane;
+      uint32_t push[2];
+      int npush = 0;
+      if (i < n) {
+        const uint32_t e = ld_cg(cur + i);
+        const int node = int(e & kIdMask);
+        const bool pass = e & kPass, start = e & kStart;
+        const double mx = sc.means[3 * node], my = sc.means[3 * node + 1], mz = sc.means[3 * node + 2];
+        const double s0 = sc.scales[3 * node], s1 = sc.scales[3 * node + 1], s2 = sc.scales[3 * node + 2];
+        bool keep = true;
+        if (v.cull) keep = sphere_in_frustum(planes, mx, my, mz, mul(3.0, max3(s0, s1, s2)), start);
+        if (keep) {
+          const int kd = pass ? -1 : sc.kind[node];
+          if (kd >= 0) {                       // SPT root: stage 2 takes over
+            atomicOr(ws.bm_spt + (kd >> 5), 1u << (kd & 31));
+          } else if (kd == -2) {               // passthrough root: its own bfs_cut
+            push[npush++] = uint32_t(node) | kPass | kStart;
+          } else {
+            const double dist = norm3_plain(sub(mx, v.position[0]), sub(my, v.position[1]), sub(mz, v.position[2]));
+            const double md = min_distance(v.threshold, v.metric, s0, s1, s2);
+            const int c0 = sc.children[2 * node], c1 = sc.children[2 * node + 1];
+            if (dist >= md || c0 == -1) {
+              uint32_t* bm = pass ? ws.bm_pass : ws.bm_upper;
+              atomicOr(bm + (node >> 5), 1u << (node & 31));
+            } else {
+              const uint32_t tag = pass ? kPass : 0u;
+              push[npush++] = uint32_t(c0) | tag;
+              push[npush++] = uint32_t(c1) | tag;
+            }
+          }
+        }
+      }
+      // warp-aggregated append to the next frontier
+      int incl = npush;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned int wbase = 0;
+      if (lane == 31 && wtot) wbase = atomicAdd(nxt_count, unsigned(wtot));
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      const unsigned int o = wbase + incl - npush;
+      for (int k = 0; k < npush; ++k) nxt[o + k] = push[k];
+    }
+    grid_sync(ws.bar);
+  }
+
+  // ---- bitmaps → sorted id lists (np.sort of the concatenated selections) ----
+  const long long wn = (sc.capacity + 31) / 32, ws_ = (sc.num_spts + 31) / 32;
+  long long c_up = bitmap_block_count(ws.bm_upper, wn, sm);
+  long long c_pa = bitmap_block_count(ws.bm_pass, wn, sm);
+  long long c_sp = bitmap_block_count(ws.bm_spt, ws_, sm);
+  if (threadIdx.x == 0) {
+    ws.block_cnt[blockIdx.x] = c_up;
+    ws.block_cnt[gridDim.x + blockIdx.x] = c_pa;
+    ws.block_cnt[2 * gridDim.x + blockIdx.x] = c_sp;
+  }
+  grid_sync(ws.bar);
+  const long long b_up = sum_before(ws.block_cnt, blockIdx.x, sm);
+  const long long b_pa = sum_before(ws.block_cnt + gridDim.x, blockIdx.x, sm);
+  const long long b_sp = sum_before(ws.block_cnt + 2 * gridDim.x, blockIdx.x, sm);
+  bitmap_block_write(ws.bm_upper, wn, sc.capacity, b_up, out.upper_ids, sm);
+  bitmap_block_write(ws.bm_pass, wn, sc.capacity, b_pa, out.pass_ids, sm);
+  bitmap_block_write(ws.bm_spt, ws_, sc.num_spts, b_sp, out.spt_ids, sm);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    out.counts[0] = int32_t(b_up + c_up);
+    out.counts[1] = int32_t(b_pa + c_pa);
+    out.counts[2] = int32_t(b_sp + c_sp);
+    out.counts[3] = level;
+  }
+  grid_sync(ws.bar);
+
+  // ---- stage 2 prologue: d_root (BLAS ddot norm, hspt.py:150) + prefix ----
+  const int n_spt = ld_cg(out.counts + 2);
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_spt; j += gthreads) {
+    const int s = ld_cg(out.spt_ids + j);
+    const double d = norm3_ddot(sub(sc.spt_center[3 * s], v.position[0]),
+                                sub(sc.spt_center[3 * s + 1], v.position[1]),
+                                sub(sc.spt_center[3 * s + 2], v.position[2]));
+    out.d_root[j] = d;
+    out.prefix_len[j] = prefix_len_of(sc, s, d);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: order-preserving compaction of every selected prefix.
+// ---------------------------------------------------------------------------
+struct CompactScratch {
+  unsigned int* bar;            // [2]
+  unsigned long long* status;   // [max_tiles] decoupled look-back words
+  long long* block_cnt;         // [grid]
+  size_t zero_bytes;
+};
+
+size_t max_tiles(int64_t num_records, int32_t S) {
+  return size_t((num_records + S + kTile - 1) / kTile) + 1;
+}
+
+CompactScratch carve_compact(void* base, int32_t S, int64_t R, int grid) {
+  CompactScratch s;
+  char* p = static_cast<char*>(base);
+  s.bar = reinterpret_cast<unsigned int*>(p);
+  size_t off = 256;
+  s.status = reinterpret_cast<unsigned long long*>(p + off);
+  off += 8 * max_tiles(R, S);
+  s.zero_bytes = off;
+  off = align_up(off);
+  s.block_cnt = reinterpret_cast<long long*>(p + off);
+  return s;
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kCompactThreads)
+compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
+  __shared__ long long sm[kCompactThreads / 32 + 1];
+  __shared__ int cnt[kRows][kCompactThreads / 32];
+  __shared__ long long tile_base_sh;
+  __shared__ int seg_lo_sh, seg_hi_sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = kCompactThreads / 32;
+  const long long gthreads = (long long)gridDim.x * blockDim.x;
+  const int n_spt = *in.n_spt;
+
+  // phase A: prefix length and root rule per selected SPT (spt.py:70-73)
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_spt; j += gthreads) {
+    const int s = in.spt_ids[j];
+    const double d = in.dist[j];
+    const int pl = prefix_len_of(sc, s, d);
+    const int rr = d >= key_self_at(sc, sc.spt_offset[s] + sc.spt_root_rec[s]);
+    out.prefix_len[j] = pl;
+    out.root_rule[j] = rr;
+    out.seg_start[j] = rr ? 1 : pl;          // segment length, scanned below
+  }
+  grid_sync(ws.bar);
+
+  // phase B: exclusive scan of segment lengths (block partition + offsets)
+  long long lo, hi;
+  block_range(n_spt, blockIdx.x, gridDim.x, lo, hi);
+  {
+    long long c = 0;
+    for (long long j = lo + threadIdx.x; j < hi; j += blockDim.x) c += ld_cg(out.seg_start + j);
+    c = block_sum(c, sm);
+    if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = c;
+  }
+  grid_sync(ws.bar);
+  {
+    long long base = sum_before(ws.block_cnt, blockIdx.x, sm);
+    long long span = hi - lo, chunk = (span + blockDim.x - 1) / blockDim.x;
+    long long j0 = lo + chunk * threadIdx.x, j1 = min(hi, j0 + chunk);
+    long long c = 0;
+    for (long long j = j0; j < j1; ++j) c += ld_cg(out.seg_start + j);
+    long long o = base + block_excl_scan(c, sm);
+    for (long long j = j0; j < j1; ++j) {
+      long long len = ld_cg(out.seg_start + j);
+      out.seg_start[j] = o;
+      o += len;
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out.total[1] = o;
+  }
+  grid_sync(ws.bar);
+
+  // phase C: tiles of the virtual record space, single pass with look-back
+  const long long total = ld_cg(out.total + 1);
+  const long long ntiles = (total + kTile - 1) / kTile;
+  if (ntiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) out.total[0] = 0;
+    return;
+  }
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long tbase = t * kTile;
+    const long long tend = min(total, tbase + kTile);
+    if (threadIdx.x == 0) {
+      // segments overlapping [tbase, tend): upper_bound(seg_start, x) - 1
+      int a = 0, b = n_spt;
+      while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
+      seg_lo_sh = a - 1;
+      int c = a, e = n_spt;
+      while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
+      seg_hi_sh = c - 1;
+    }
+    __syncthreads();
+    const int jlo = seg_lo_sh, jhi = seg_hi_sh;
+    bool pred[kRows];
+    int seg_of[kRows], pos_of[kRows];
+    int jcur = jlo;
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+      pred[k] = false;
+      seg_of[k] = -1;
+      pos_of[k] = 0;
+      if (vi < tend) {
+        int j = jcur;
+        if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
+          int a = jcur, b = jhi + 1;
+          while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
+          j = a - 1;
+          jcur = j;
+        }
+        const long long local = vi - ld_cg(out.seg_start + j);
+        const int s = in.spt_ids[j];
+        const int64_t off = sc.spt_offset[s];
+        int rec;
+        bool p;
+        if (ld_cg(out.root_rule + j)) {
+          rec = sc.spt_root_rec[s];
+          p = true;
+        } else {
+          rec = int(local);
+          p = key_self_at(sc, off + rec) <= in.dist[j];
+        }
+        pred[k] = p;
+        seg_of[k] = j;
+        pos_of[k] = rec;
+      }
+    }
+    unsigned ball[kRows];
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      ball[k] = __ballot_sync(0xffffffffu, pred[k]);
+      if (lane == 0) cnt[k][warp] = __popc(ball[k]);
+    }
+    __syncthreads();
+    // exclusive scan over (row, warp) in row-major order: kRows*nwarps = 128 values
+    if (warp == 0) {
+      constexpr int per = kRows * (kCompactThreads / 32) / 32;   // 4
+      int vals[per];
+      int s = 0;
+#pragma unroll
+      for (int q = 0; q < per; ++q) {
+        int idx = lane * per + q;
+        vals[q] = cnt[idx / nwarps][idx % nwarps];
+        s += vals[q];
+      }
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int run = incl - s;
+#pragma unroll
+      for (int q = 0; q < per; ++q) {
+        int idx = lane * per + q;
+        cnt[idx / nwarps][idx % nwarps] = run;
+        run += vals[q];
+      }
+      const int agg = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) {
+        // decoupled look-back (single thread; tiles are large)
+        long long excl = 0;
+        if (t == 0) {
+          atomicExch(ws.status, kFlagIncl | (unsigned long long)agg);
+        } else {
+          atomicExch(ws.status + t, kFlagAgg | (unsigned long long)agg);
+          long long p = t - 1;
+          while (true) {
+            unsigned long long w = *((volatile unsigned long long*)(ws.status + p));
+            if ((w >> 62) == 0) { __nanosleep(20); continue; }
+            excl += (long long)(w & kValMask);
+            if ((w >> 62) == 2) break;
+            --p;
+          }
+          atomicExch(ws.status + t, kFlagIncl | (unsigned long long)(excl + agg));
+        }
+        tile_base_sh = excl;
+        if (t == ntiles - 1) out.total[0] = excl + agg;
+      }
+    }
+    __syncthreads();
+    const long long tb = tile_base_sh;
+#pragma unroll
+    for (int k = 0; k < kRows; ++k) {
+      if (pred[k]) {
+        const long long o = tb + cnt[k][warp] + __popc(ball[k] & lanemask_lt());
+        const int j = seg_of[k];
+        const int s = in.spt_ids[j];
+        out.sel_seg[o] = j;
+        out.sel_pos[o] = pos_of[k];
+        out.sel_node[o] = sc.rec_node[sc.spt_offset[s] + pos_of[k]];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+int coop_grid(const void* kernel, int threads) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+  if (per_sm < 1) per_sm = 1;
+  return sms * per_sm;
+}
+
+}  // namespace
+
+size_t select_scratch_bytes(int64_t cap, int32_t S, int grid) {
+  size_t w_nodes = (size_t(cap) + 31) / 32, w_spt = (size_t(S) + 31) / 32;
+  size_t off = align_up(sizeof(unsigned int) * (kMaxLevels + 3));
+  off += 8 * w_nodes + 4 * w_spt;
+  off = align_up(off);
+  off = align_up(off + 4 * size_t(cap) + 4);
+  off = align_up(off + 4 * size_t(cap) + 4);
+  off += 3 * 8 * size_t(grid) + 256;
+  return off;
+}
+
+size_t compact_scratch_bytes(int32_t S, int64_t R, int grid) {
+  return align_up(256 + 8 * max_tiles(R, S)) + 8 * size_t(grid) + 256;
+}
+
+int select_grid() { return coop_grid((const void*)select_kernel, kSelectThreads); }
+int compact_grid() { return coop_grid((const void*)compact_kernel, kCompactThreads); }
+
+cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut& out,
+                          void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  const int grid = select_grid();
+  if (scratch_bytes < select_scratch_bytes(sc.capacity, sc.num_spts, grid)) return cudaErrorInvalidValue;
+  SelectScratch ws = carve_select(scratch, sc.capacity, sc.num_spts, grid);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, ws.zero_bytes, st);
+  if (e != cudaSuccess) return e;
+  LodScene a = sc; LodView b = v; SelectOut c = out; SelectScratch d = ws;
+  void* args[] = {&a, &b, &c, &d};
+  return cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(grid), dim3(kSelectThreads),
+                                     args, 0, st);
+}
+
+cudaError_t launch_compact(const LodScene& sc, const CompactIn& in, const CompactOut& out,
+                           void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  const int grid = compact_grid();
+  if (scratch_bytes < compact_scratch_bytes(sc.num_spts, sc.num_records, grid)) return cudaErrorInvalidValue;
+  CompactScratch ws = carve_compact(scratch, sc.num_spts, sc.num_records, grid);
+  cudaError_t e = cudaMemsetAsync(scratch, 0, ws.zero_bytes, st);
+  if (e != cudaSuccess) return e;
+  LodScene a = sc; CompactIn b = in; CompactOut c = out; CompactScratch d = ws;
+  void* args[] = {&a, &b, &c, &d};
+  return cudaLaunchCooperativeKernel((const void*)compact_kernel, dim3(grid), dim3(kCompactThreads),
+                                     args, 0, st);
+}
+
+}  // namespace glod

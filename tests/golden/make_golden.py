@@ -1,0 +1,336 @@
+"""Generate golden vectors by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+Outputs tests/golden/*.npz (committed).  Nothing at test time reads
+/root/reference: the fixtures carry the reference's inputs and outputs.
+
+Cases mirror the reference's own seeded fixtures (pkg/tests/conftest.py:
+random_hierarchy / random_scale_hierarchy / random_camera / look_at_camera)
+and known-answer tests (test_spt.py:132-149, test_renderer.py:105-114).
+"""
+from __future__ import annotations
+
+import importlib.util
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def _import_ref():
+    sys.dont_write_bytecode = True
+    spec = importlib.util.spec_from_file_location(
+        "glod", REF / "glod" / "__init__.py", submodule_search_locations=[str(REF / "glod")])
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["glod"] = mod
+    spec.loader.exec_module(mod)
+    import glod.core, glod.hierarchy, glod.spt, glod.hspt, glod.renderer, glod.trainer  # noqa
+    import glod.cache, glod.store  # noqa
+    return sys.modules["glod"]
+
+
+glod = _import_ref()
+from glod.core import AttributeArrays, Camera, Frustum, LodConfig, rotmat_to_quat  # noqa: E402
+from glod.hierarchy import bfs_cut, build_hierarchy  # noqa: E402
+from glod.hspt import build_hspt, cut_hspt, default_size_threshold  # noqa: E402
+from glod.renderer import backward, loss, render_forward  # noqa: E402
+from glod.spt import build_spt, cut_spt  # noqa: E402
+
+
+# ---- the reference's own conftest builders (pkg/tests/conftest.py:11-58) ----
+def random_leaves(rng, n, span=10.0, scale_lo=0.05, scale_hi=0.5):
+    leaves = AttributeArrays.zeros(n)
+    leaves.means = rng.uniform(-span, span, (n, 3))
+    leaves.scales = rng.uniform(scale_lo, scale_hi, (n, 3))
+    q = rng.normal(size=(n, 4))
+    leaves.rotations = q / np.linalg.norm(q, axis=1, keepdims=True)
+    leaves.opacities = rng.uniform(0.05, 1.0, n)
+    leaves.base_colors = rng.uniform(0.0, 1.0, (n, 3))
+    return leaves
+
+
+def look_at_camera(position, target, focal=(40.0, 40.0), resolution=(32, 32), near=0.1):
+    position = np.asarray(position, dtype=np.float64)
+    fwd = np.asarray(target, dtype=np.float64) - position
+    fwd = fwd / np.linalg.norm(fwd)
+    up = np.array([0.0, 1.0, 0.0])
+    if abs(fwd @ up) > 0.99:
+        up = np.array([1.0, 0.0, 0.0])
+    right = np.cross(up, fwd)
+    right = right / np.linalg.norm(right)
+    upv = np.cross(fwd, right)
+    rot = np.stack([right, upv, fwd], axis=1)
+    w, h = resolution
+    return Camera(position=position, orientation=rotmat_to_quat(rot), focal=focal,
+                  principal_point=(w / 2.0, h / 2.0), resolution=resolution, near=near)
+
+
+def random_camera(rng, span=10.0, resolution=(32, 32)):
+    pos = rng.uniform(-3 * span, 3 * span, 3)
+    target = rng.uniform(-span, span, 3)
+    while np.linalg.norm(target - pos) < 1e-3:
+        target = rng.uniform(-span, span, 3)
+    focal = tuple(rng.uniform(20.0, 80.0, 2))
+    return look_at_camera(pos, target, focal=focal, resolution=resolution)
+
+
+def cam_arrays(cam, prefix="cam_"):
+    return {prefix + "position": cam.position, prefix + "orientation": cam.orientation,
+            prefix + "focal": np.array(cam.focal, dtype=np.float64),
+            prefix + "pp": np.array(cam.principal_point, dtype=np.float64),
+            prefix + "res": np.array(cam.resolution, dtype=np.int64),
+            prefix + "near": np.float64(cam.near), prefix + "far": np.float64(cam.far),
+            prefix + "planes": Frustum.from_camera(cam).planes}
+
+
+def hier_arrays(h):
+    return {"children": h.children.astype(np.int32), "parent": h.parent.astype(np.int32),
+            "root": np.int64(h.root), "means": h.attrs.means, "scales": h.attrs.scales,
+            "rotations": h.attrs.rotations, "opacities": h.attrs.opacities,
+            "base_colors": h.attrs.base_colors, "sh_rest": h.attrs.sh_rest}
+
+
+def hspt_arrays(hspt):
+    spts = hspt.spts
+    cnt = np.array([s.subtree_size for s in spts], dtype=np.int64)
+    return {"upper_nodes": hspt.upper_nodes.astype(np.int64),
+            "pass_roots": hspt.passthrough_roots.astype(np.int64),
+            "spt_root": np.array([s.root for s in spts], dtype=np.int64),
+            "spt_center": (np.stack([s.root_center for s in spts]) if spts else np.zeros((0, 3))),
+            "spt_count": cnt,
+            "rec_node": (np.concatenate([s.nodes for s in spts]) if spts else np.zeros(0, np.int64)),
+            "key_self": (np.concatenate([s.key_self for s in spts]) if spts else np.zeros(0)),
+            "key_parent": (np.concatenate([s.key_parent for s in spts]) if spts else np.zeros(0)),
+            "lod_threshold": np.float64(hspt.lod.threshold),
+            "lod_metric": np.int64(0 if hspt.lod.metric == "max_scale" else 1),
+            "size_threshold": np.float64(hspt.size_threshold),
+            "min_subtree": np.int64(hspt.min_subtree)}
+
+
+def rs_arrays(rs, prefix="rs_"):
+    sel = [s.selected for s in rs.per_spt]
+    return {prefix + "upper": rs.upper.astype(np.int64),
+            prefix + "pass": rs.passthrough.astype(np.int64),
+            prefix + "spt_id": np.array([s.spt_id for s in rs.per_spt], dtype=np.int64),
+            prefix + "d_root": np.array([s.d_root for s in rs.per_spt], dtype=np.float64),
+            prefix + "prefix_len": np.array([s.prefix_len for s in rs.per_spt], dtype=np.int64),
+            prefix + "sel_count": np.array([x.size for x in sel], dtype=np.int64),
+            prefix + "sel": (np.concatenate(sel).astype(np.int64) if sel else np.zeros(0, np.int64))}
+
+
+def _designed_scales(rng, h, depth_cut):
+    """Upper nodes small (never taken, md > dist), SPT/pass interiors i.i.d.
+    — the bench generator's shape at golden size."""
+    depth = np.full(h.capacity, -1)
+    lv, fr = 0, np.array([h.root])
+    while fr.size:
+        depth[fr] = lv
+        ch = h.children[fr]
+        fr = ch[ch[:, 0] != -1].ravel()
+        lv += 1
+    s = rng.uniform(0.05, 0.6, h.attrs.scales.shape)
+    s[depth < depth_cut] = 0.004
+    s[depth == depth_cut] = 0.003
+    h.attrs.scales = s
+    return 0.004 ** 3 * 0.9
+
+
+def make_lod_cases():
+    """HSPT cuts on merged, re-scaled and "designed" hierarchies, both
+    metrics, cull on/off, runtime thresholds from coarse (root-only) to
+    1e9 (descend to leaves) — the reference's own fixture families
+    (test_hspt.py, test_acceptance.py:98-127, big_scene T=1e9 :282-306)."""
+    rng = np.random.default_rng(20250701)
+    n_files = 0
+    for case in range(24):
+        n = int(rng.choice([40, 90, 200, 700, 1500, 3000]))
+        family = case % 3            # 0 merged, 1 rescaled i.i.d., 2 designed
+        h = build_hierarchy(random_leaves(rng, n))
+        metric = ("max_scale", "surface_area")[case % 2]
+        build_cfg = LodConfig(threshold=float(rng.uniform(0.5, 20.0)), metric=metric)
+        if family == 1:   # random_scale_hierarchy (conftest.py:26-31)
+            h.attrs.scales = rng.uniform(0.05, 2.0, h.attrs.scales.shape)
+            vols = np.prod(h.attrs.scales, axis=1)
+            thr = float(np.quantile(vols, rng.uniform(0.2, 0.8)))
+        elif family == 2:
+            thr = _designed_scales(rng, h, int(rng.integers(2, 6)))
+        else:
+            thr = float(rng.uniform(0.5, 4.0)) * default_size_threshold(h)
+        min_sub = int(rng.choice([1, 4, 8, 16, 32]))
+        if family == 2:
+            min_sub = int(rng.choice([8, 16, 24]))
+        hspt = build_hspt(h, thr, min_sub, build_cfg)
+        d = {"n_leaves": np.int64(n), "family": np.int64(family)}
+        d.update(hier_arrays(h))
+        d.update(hspt_arrays(hspt))
+        views = []
+        for v in range(8):
+            cam = random_camera(rng)
+            if v >= 6:   # look at the scene centre from close by
+                cam = look_at_camera(rng.uniform(-14, 14, 3), np.zeros(3), focal=(30.0, 30.0))
+            if v in (0, 1):
+                T = float(np.exp(rng.uniform(np.log(0.5), np.log(200.0))))
+            elif v in (2, 3):
+                T = float(10.0 ** rng.uniform(2.5, 9.0))
+            else:
+                T = float(rng.uniform(1.0, 60.0)) if family != 2 else float(rng.uniform(0.5, 8.0))
+            cfg = LodConfig(threshold=T, metric=("max_scale", "surface_area")[int(rng.integers(2))])
+            cull = bool(v % 2 == 0)
+            rs = cut_hspt(hspt, h, cam, cfg, cull=cull)
+            fr = Frustum.from_camera(cam)
+            full = bfs_cut(h, cam, cfg, frustum=fr if cull else None)
+            views.append((cam, cfg, cull, rs, full))
+        for i, (cam, cfg, cull, rs, full) in enumerate(views):
+            d.update(cam_arrays(cam, f"v{i}_"))
+            d[f"v{i}_T"] = np.float64(cfg.threshold)
+            d[f"v{i}_metric"] = np.int64(0 if cfg.metric == "max_scale" else 1)
+            d[f"v{i}_cull"] = np.int64(cull)
+            d.update(rs_arrays(rs, f"v{i}_rs_"))
+            d[f"v{i}_bfs"] = full.node_ids.astype(np.int64)
+        d["n_views"] = np.int64(len(views))
+        np.savez_compressed(OUT / f"lod_{case:02d}.npz", **d)
+        n_files += 1
+    return n_files
+
+
+def make_spt_cases():
+    """cut_spt on single SPTs over a sweep of distances (test_spt.py:151-170),
+    plus the hand-made toy SPT (test_spt.py:132-149)."""
+    rng = np.random.default_rng(1234)
+    d = {}
+    k = 0
+    for case in range(40):
+        n = int(rng.integers(2, 400))
+        h = build_hierarchy(random_leaves(rng, n))
+        h.attrs.scales = rng.uniform(0.05, 2.0, h.attrs.scales.shape)
+        cfg = LodConfig(threshold=float(rng.uniform(0.2, 20.0)),
+                        metric=("max_scale", "surface_area")[case % 2])
+        spt = build_spt(h, h.root, cfg)
+        top = float(spt.key_self.max())
+        dists = list(rng.uniform(0.0, 1.5 * top, 8)) + [float(spt.key_self[3 % spt.subtree_size]),
+                                                         float(spt.key_self[0]), 0.0]
+        for dist in dists:
+            pl, sel = cut_spt(spt, float(dist))
+            d[f"c{k}_root"] = np.int64(spt.root)
+            d[f"c{k}_nodes"] = spt.nodes.astype(np.int64)
+            d[f"c{k}_key_self"] = spt.key_self
+            d[f"c{k}_key_parent"] = spt.key_parent
+            d[f"c{k}_d"] = np.float64(dist)
+            d[f"c{k}_prefix"] = np.int64(pl)
+            d[f"c{k}_sel"] = sel.astype(np.int64)
+            k += 1
+    from glod.spt import Spt
+    nodes = np.array([1, 2, 0], dtype=np.int64)
+    ks = np.array([2.0, 3.0, 10.0])
+    kp = np.array([10.0, 10.0, np.inf])
+    o = np.argsort(-kp, kind="stable")
+    toy = Spt(root=0, root_center=np.zeros(3), nodes=nodes[o], key_self=ks[o], key_parent=kp[o])
+    for dist in (5.0, 20.0, 10.0, 2.0, 1.0):
+        pl, sel = cut_spt(toy, dist)
+        d[f"c{k}_root"] = np.int64(0)
+        d[f"c{k}_nodes"] = toy.nodes
+        d[f"c{k}_key_self"] = toy.key_self
+        d[f"c{k}_key_parent"] = toy.key_parent
+        d[f"c{k}_d"] = np.float64(dist)
+        d[f"c{k}_prefix"] = np.int64(pl)
+        d[f"c{k}_sel"] = sel.astype(np.int64)
+        k += 1
+    d["n_cases"] = np.int64(k)
+    np.savez_compressed(OUT / "spt_cases.npz", **d)
+
+
+def _cam_axis(resolution=(16, 16), focal=(40.0, 40.0), z=-10.0):
+    w, h = resolution   # test_renderer.py:_make_camera
+    return Camera(position=np.array([0.0, 0.0, z]), orientation=np.array([1.0, 0.0, 0.0, 0.0]),
+                  focal=focal, principal_point=(w / 2.0, h / 2.0), resolution=resolution,
+                  near=0.1)
+
+
+def attrs_arrays(a, prefix):
+    return {prefix + k: np.array(v, dtype=np.float64, copy=True) for k, v in a.arrays()}
+
+
+def make_render_cases():
+    """Forward image, backward gradients for a random upstream, and the
+    L1+SSIM loss — micro scenes like test_renderer.py plus a denser scene
+    with saturated pixels (exercises the T>1e-4 gate and the 0.99 clamp)."""
+    rng = np.random.default_rng(777)
+    d = {}
+    k = 0
+    specs = []
+    for i in range(10):
+        specs.append(("micro", int(rng.integers(1, 9)), (16, 16), (40.0, 40.0), 0.8))
+    specs += [("mid", 60, (48, 40), (60.0, 55.0), 1.5), ("dense", 300, (64, 48), (70.0, 70.0), 1.2),
+              ("saturate", 400, (40, 40), (50.0, 50.0), 0.6), ("wide", 150, (96, 64), (80.0, 80.0), 2.5)]
+    for kind, n, res, focal, span in specs:
+        a = random_leaves(rng, n, span=span, scale_lo=0.05, scale_hi=0.4)
+        a.sh_rest = rng.normal(0, 0.1, a.sh_rest.shape)
+        if kind == "saturate":
+            a.opacities = rng.uniform(0.7, 1.0, n)
+        cam = _cam_axis(resolution=res, focal=focal)
+        if kind == "wide":
+            cam = look_at_camera(np.array([1.0, -2.0, -9.0]), np.zeros(3), focal=focal,
+                                 resolution=res, near=0.1)
+        ctx = render_forward(a, cam)
+        up = rng.normal(size=(res[1], res[0], 3))
+        g = backward(ctx, up)
+        target = rng.uniform(0, 1, ctx.image.shape)
+        lv, lg = loss(ctx.image, target, 0.2)
+        d.update(attrs_arrays(a, f"r{k}_a_"))
+        d.update(cam_arrays(cam, f"r{k}_"))
+        d[f"r{k}_image"] = ctx.image
+        d[f"r{k}_upstream"] = up
+        for name, arr in [("means", g.means), ("scales", g.scales), ("rotations", g.rotations),
+                          ("opacities", g.opacities), ("base_colors", g.base_colors),
+                          ("sh_rest", g.sh_rest)]:
+            d[f"r{k}_g_{name}"] = arr
+        d[f"r{k}_target"] = target
+        d[f"r{k}_loss"] = np.float64(lv)
+        d[f"r{k}_loss_grad"] = lg
+        k += 1
+    d["n_cases"] = np.int64(k)
+    np.savez_compressed(OUT / "render_cases.npz", **d)
+
+
+def make_adam_cases():
+    from glod.trainer import DEFAULT_LEARNING_RATES, OptimizerState, _adam_update
+    from glod.renderer import GaussianGradients
+    rng = np.random.default_rng(99)
+    n = 50
+    a = random_leaves(rng, n)
+    a.sh_rest = rng.normal(0, 0.1, a.sh_rest.shape)
+    opt = OptimizerState.zeros(a)
+    d = attrs_arrays(a, "p0_")
+    lrs = dict(DEFAULT_LEARNING_RATES)
+    lrs["means"] = lrs["means"] * 17.0
+    for it in range(3):
+        ids = np.sort(rng.choice(n, size=30, replace=False))
+        g = GaussianGradients(means=rng.normal(size=(30, 3)), scales=rng.normal(size=(30, 3)),
+                              rotations=rng.normal(size=(30, 4)), opacities=rng.normal(size=30),
+                              base_colors=rng.normal(size=(30, 3)), sh_rest=rng.normal(size=(30, 9)))
+        _adam_update(a, opt, ids, g, np.arange(30), lrs)
+        d[f"it{it}_ids"] = ids
+        for name in ("means", "scales", "rotations", "opacities", "base_colors", "sh_rest"):
+            d[f"it{it}_g_{name}"] = getattr(g, name)
+        d.update(attrs_arrays(a, f"it{it}_p_"))
+        for name in opt.m:
+            d[f"it{it}_m_{name}"] = opt.m[name].copy()
+            d[f"it{it}_v_{name}"] = opt.v[name].copy()
+        d[f"it{it}_step"] = opt.step.copy()
+    for k, v in lrs.items():
+        d[f"lr_{k}"] = np.float64(v)
+    np.savez_compressed(OUT / "adam_cases.npz", **d)
+
+
+if __name__ == "__main__":
+    print("lod files", make_lod_cases())
+    make_spt_cases()
+    make_render_cases()
+    make_adam_cases()
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, os.path.getsize(f))
