@@ -106,6 +106,70 @@ int glod_spt_compact(const glod_lod_scene* scene, const glod_spt_compact_in* in,
                      const glod_spt_compact_out* out, void* scratch,
                      int64_t scratch_bytes, void* stream);
 
+/* ======================================================================= *
+ * Rasteriser (renderer.py)
+ * ======================================================================= */
+
+/* Pinhole camera, resolved on the host: w2c = Camera.world_to_cam
+ * (quat_to_rotmat(orientation).T, core.py:285-287), row-major. */
+typedef struct glod_camera {
+  double position[3];
+  double w2c[9];
+  double fx, fy, cx, cy;
+  double near_plane;
+  int32_t width, height;
+} glod_camera;
+
+/* Opaque per-device rasteriser context: owns its stream-ordered workspace
+ * and the forward state the backward pass consumes. */
+typedef struct glod_raster glod_raster;
+
+typedef struct glod_render_stats {
+  int64_t n_gaussians;          /* rows in the render set                    */
+  int64_t n_instances;          /* (gaussian, 16x16 tile) pairs              */
+  int32_t tiles_x, tiles_y;
+} glod_render_stats;
+
+int glod_raster_create(glod_raster** out);
+int glod_raster_destroy(glod_raster* r);
+
+/* Replaces render_forward (renderer.py:117-166).  attrs: [dev] packed f64
+ * attribute block of n rows, section-major [means 3n | scales 3n |
+ * rotations 4n | opacities n | base_colors 3n | sh_rest 9n].  image: [dev]
+ * f32 (height, width, 3).  Synchronises once (instance count, finiteness
+ * check: GLOD_ERR_INVALID_INPUT names the first non-finite Gaussian like
+ * renderer._check_finite). */
+int glod_render_forward(glod_raster* r, const double* attrs, int64_t n,
+                        const glod_camera* cam, float* image, void* stream);
+
+/* Replaces backward (renderer.py:197-304) for the last forward call.
+ * dl_dimage: [dev] f32 (height, width, 3).  grads: [dev] packed f64 block
+ * of n rows (same layout as attrs; raw scale/opacity, not log/logit). */
+int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, void* stream);
+
+int glod_render_stats_get(const glod_raster* r, glod_render_stats* out);
+
+/* Replaces loss (renderer.py:322-360): (1-lam)*L1 + lam*(1-SSIM), 11-tap
+ * sigma=1.5 window, zero padding.  rendered/target/grad: [dev] f32
+ * (height, width, 3).  value: [dev] f64[3] = {loss, l1, mean ssim}. */
+int64_t glod_loss_scratch_bytes(int32_t width, int32_t height);
+int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
+                      int32_t height, double lam, double* value, float* grad,
+                      void* scratch, int64_t scratch_bytes, void* stream);
+
+/* ======================================================================= *
+ * Optimiser (trainer._adam_update, trainer.py:253-299)
+ * ======================================================================= */
+
+/* One ADAM step, in place, on params[ids] from grads[rows].  params, m, v:
+ * [dev] packed f64 blocks of `capacity` rows; step: [dev] int64[capacity];
+ * grads: [dev] packed f64 block of `grad_rows` rows; ids/rows: [dev] int32[n]
+ * (rows == NULL means row i).  ids must be unique.  lrs: host double[6] in
+ * section order (means already scaled by the scene extent). */
+int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
+                   const int32_t* ids, const double* grads, const int32_t* rows,
+                   int64_t grad_rows, int64_t n, const double* lrs, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

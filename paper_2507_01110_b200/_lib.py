@@ -46,6 +46,17 @@ class CompactOut(C.Structure):
                 ("sel_pos", P), ("sel_node", P), ("total", P)]
 
 
+class Camera(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("w2c", C.c_double * 9), ("fx", C.c_double),
+                ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("near_plane", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class RenderStats(C.Structure):
+    _fields_ = [("n_gaussians", C.c_int64), ("n_instances", C.c_int64),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "glod_version": (C.c_int, []),
@@ -56,6 +67,15 @@ SIGNATURES = {
     "glod_spt_compact_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int64]),
     "glod_spt_compact": (C.c_int, [C.POINTER(LodScene), C.POINTER(CompactIn),
                                    C.POINTER(CompactOut), P, C.c_int64, P]),
+    "glod_raster_create": (C.c_int, [C.POINTER(P)]),
+    "glod_raster_destroy": (C.c_int, [P]),
+    "glod_render_forward": (C.c_int, [P, P, C.c_int64, C.POINTER(Camera), P, P]),
+    "glod_render_backward": (C.c_int, [P, P, P, P]),
+    "glod_render_stats_get": (C.c_int, [P, C.POINTER(RenderStats)]),
+    "glod_loss_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
+    "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
+    "glod_adam_step": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
+                                 C.POINTER(C.c_double), P]),
 }
 
 _LIB = None

@@ -4,6 +4,20 @@
 
 #include "../../include/glod_b200.h"
 #include "lod.cuh"
+#include "raster.cuh"
+
+namespace glod {
+size_t loss_scratch_bytes(int W, int H);
+cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
+                        float* grad, void* scratch, size_t bytes, cudaStream_t st);
+cudaError_t launch_adam(double* params, double* m, double* v, long long* step, long long cap,
+                        const int* ids, const double* grads, const int* rows, long long grad_rows,
+                        long long n, const double* lrs, cudaStream_t st);
+}  // namespace glod
+
+struct glod_raster {
+  glod::RasterCtx* ctx;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -54,6 +68,75 @@ int glod_spt_compact(const glod_lod_scene* scene, const glod_spt_compact_in* in,
   return check(glod::launch_compact(*scene, *in, *out, scratch, size_t(scratch_bytes),
                                     static_cast<cudaStream_t>(stream)),
                "glod_spt_compact");
+}
+
+int glod_raster_create(glod_raster** out) {
+  if (!out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  *out = new glod_raster{glod::raster_create()};
+  return GLOD_OK;
+}
+
+int glod_raster_destroy(glod_raster* r) {
+  if (r) {
+    glod::raster_destroy(r->ctx);
+    delete r;
+  }
+  return GLOD_OK;
+}
+
+int glod_render_forward(glod_raster* r, const double* attrs, int64_t n, const glod_camera* cam,
+                        float* image, void* stream) {
+  if (!r || !cam || !image || (n > 0 && !attrs)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "camera resolution out of range");
+  if (n < 0 || n > 0x7fffffffll) return fail(GLOD_ERR_INVALID_ARGUMENT, "n out of range");
+  cudaError_t e = glod::raster_forward(r->ctx, attrs, n, *cam, image, static_cast<cudaStream_t>(stream));
+  int sec, idx;
+  if (glod::raster_bad_input(r->ctx, &sec, &idx)) {
+    static const char* names[6] = {"means", "scales", "rotations", "opacities", "base_colors", "sh_rest"};
+    char buf[128];
+    snprintf(buf, sizeof(buf), "non-finite %s on Gaussian %d", names[sec], idx);
+    return fail(GLOD_ERR_INVALID_INPUT, buf);
+  }
+  return check(e, "glod_render_forward");
+}
+
+int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, void* stream) {
+  if (!r || !dl_dimage || !grads) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::raster_backward(r->ctx, dl_dimage, grads, static_cast<cudaStream_t>(stream)),
+               "glod_render_backward");
+}
+
+int glod_render_stats_get(const glod_raster* r, glod_render_stats* out) {
+  if (!r || !out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  glod::raster_stats(r->ctx, out);
+  return GLOD_OK;
+}
+
+int64_t glod_loss_scratch_bytes(int32_t width, int32_t height) {
+  return int64_t(glod::loss_scratch_bytes(width, height));
+}
+
+int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width, int32_t height,
+                      double lam, double* value, float* grad, void* scratch, int64_t scratch_bytes,
+                      void* stream) {
+  if (!rendered || !target || !value || !grad || !scratch)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (!(lam >= 0.0 && lam <= 1.0)) return fail(GLOD_ERR_INVALID_INPUT, "lambda must lie in [0, 1]");
+  if (width < 1 || height < 1) return fail(GLOD_ERR_INVALID_INPUT, "image dimensions differ");
+  return check(glod::launch_loss(rendered, target, width, height, lam, value, grad, scratch,
+                                 size_t(scratch_bytes), static_cast<cudaStream_t>(stream)),
+               "glod_loss_l1_ssim");
+}
+
+int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
+                   const int32_t* ids, const double* grads, const int32_t* rows, int64_t grad_rows,
+                   int64_t n, const double* lrs, void* stream) {
+  if (n > 0 && (!params || !m || !v || !step || !ids || !grads || !lrs))
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_adam(params, m, v, reinterpret_cast<long long*>(step), capacity, ids,
+                                 grads, rows, grad_rows, n, lrs, static_cast<cudaStream_t>(stream)),
+               "glod_adam_step");
 }
 
 }  // extern "C"

@@ -1,0 +1,200 @@
+// K10: (1-λ)·L1 + λ·(1-SSIM) and its gradient (renderer.py:307-360).
+//
+// 11-tap σ=1.5 Gaussian window applied separably per channel plane with
+// zero padding (scipy correlate1d mode="constant").  Two fused tile
+// kernels: pass 1 blurs x, y, x², y², xy from one shared-memory tile and
+// emits the three SSIM derivative maps plus per-block L1/SSIM partial sums;
+// pass 2 blurs the derivative maps and writes the image gradient.  Window
+// arithmetic is fp64 (the variance terms ux2 - mu² cancel).
+#include "common.cuh"
+#include "../../include/glod_b200.h"
+
+namespace glod {
+namespace {
+
+constexpr int R = 5;             // window half width
+constexpr int TW = 32, TH = 16;  // output tile
+constexpr int IW = TW + 2 * R, IH = TH + 2 * R;
+constexpr int NT = 256;
+constexpr double C1 = 1e-4, C2 = 9e-4;
+
+__constant__ double kWin[2 * R + 1];
+
+// image layout (H, W, 3) interleaved
+__device__ __forceinline__ float at(const float* img, int W, int H, int x, int y, int c) {
+  return (x >= 0 && x < W && y >= 0 && y < H) ? img[3 * ((long long)y * W + x) + c] : 0.f;
+}
+
+__global__ void __launch_bounds__(NT)
+ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int H,
+           float* __restrict__ dmu, float* __restrict__ dx2, float* __restrict__ dxy,
+           double* __restrict__ part, double inv_n) {
+  __shared__ float sx[IH][IW], sy[IH][IW];
+  __shared__ double v[5][TH][IW];
+  __shared__ double red[2][NT / 32];
+  const int c = blockIdx.z;
+  const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
+  for (int k = threadIdx.x; k < IH * IW; k += NT) {
+    const int r = k / IW, q = k % IW;
+    sx[r][q] = at(X, W, H, ox + q - R, oy + r - R, c);
+    sy[r][q] = at(Y, W, H, ox + q - R, oy + r - R, c);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < TH * IW; k += NT) {
+    const int r = k / IW, q = k % IW;
+    double a = 0, b = 0, aa = 0, bb = 0, ab = 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * R; ++t) {
+      const double xv = sx[r + t][q], yv = sy[r + t][q], w = kWin[t];
+      a += w * xv; b += w * yv; aa += w * (xv * xv); bb += w * (yv * yv); ab += w * (xv * yv);
+    }
+    v[0][r][q] = a; v[1][r][q] = b; v[2][r][q] = aa; v[3][r][q] = bb; v[4][r][q] = ab;
+  }
+  __syncthreads();
+  double s_sum = 0, l_sum = 0;
+  for (int k = threadIdx.x; k < TH * TW; k += NT) {
+    const int r = k / TW, q = k % TW;
+    const int x = ox + q, y = oy + r;
+    if (x >= W || y >= H) continue;
+    double mx = 0, my = 0, ux2 = 0, uy2 = 0, uxy = 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * R; ++t) {
+      const double w = kWin[t];
+      mx += w * v[0][r][q + t]; my += w * v[1][r][q + t]; ux2 += w * v[2][r][q + t];
+      uy2 += w * v[3][r][q + t]; uxy += w * v[4][r][q + t];
+    }
+    const double vx = ux2 - mx * mx, vy = uy2 - my * my, cv = uxy - mx * my;
+    const double a1 = 2 * mx * my + C1, a2 = 2 * cv + C2;
+    const double b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
+    const double s = (a1 * a2) / (b1 * b2);
+    const double ds_dmu = (2 * my * a2) / (b1 * b2) - s * 2 * mx / b1;
+    const double ds_dvx = -s / b2;
+    const double ds_dcv = 2 * a1 / (b1 * b2);
+    const long long o = 3 * ((long long)y * W + x) + c;
+    dmu[o] = float((ds_dmu - 2 * mx * ds_dvx - my * ds_dcv) * inv_n);
+    dx2[o] = float(ds_dvx * inv_n);
+    dxy[o] = float(ds_dcv * inv_n);
+    s_sum += s;
+    l_sum += fabs(double(sx[r + R][q + R]) - double(sy[r + R][q + R]));
+  }
+  // block reduction → one partial pair per block (deterministic order)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
+    l_sum += __shfl_xor_sync(0xffffffffu, l_sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s_sum; red[1][threadIdx.x >> 5] = l_sum; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; }
+    const long long bid = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    part[2 * bid] = a;
+    part[2 * bid + 1] = b;
+  }
+}
+
+__global__ void __launch_bounds__(NT)
+ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int H,
+           const float* __restrict__ dmu, const float* __restrict__ dx2, const float* __restrict__ dxy,
+           float* __restrict__ grad, double lam, double inv_n) {
+  __shared__ float s0[IH][IW], s1[IH][IW], s2[IH][IW];
+  __shared__ double v[3][TH][IW];
+  const int c = blockIdx.z;
+  const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
+  for (int k = threadIdx.x; k < IH * IW; k += NT) {
+    const int r = k / IW, q = k % IW;
+    s0[r][q] = at(dmu, W, H, ox + q - R, oy + r - R, c);
+    s1[r][q] = at(dx2, W, H, ox + q - R, oy + r - R, c);
+    s2[r][q] = at(dxy, W, H, ox + q - R, oy + r - R, c);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < TH * IW; k += NT) {
+    const int r = k / IW, q = k % IW;
+    double a = 0, b = 0, d = 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * R; ++t) {
+      const double w = kWin[t];
+      a += w * s0[r + t][q]; b += w * s1[r + t][q]; d += w * s2[r + t][q];
+    }
+    v[0][r][q] = a; v[1][r][q] = b; v[2][r][q] = d;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < TH * TW; k += NT) {
+    const int r = k / TW, q = k % TW;
+    const int x = ox + q, y = oy + r;
+    if (x >= W || y >= H) continue;
+    double a = 0, b = 0, d = 0;
+#pragma unroll
+    for (int t = 0; t <= 2 * R; ++t) {
+      const double w = kWin[t];
+      a += w * v[0][r][q + t]; b += w * v[1][r][q + t]; d += w * v[2][r][q + t];
+    }
+    const long long o = 3 * ((long long)y * W + x) + c;
+    const double xv = X[o], yv = Y[o];
+    const double e = xv - yv;
+    const double sgn = (e > 0) - (e < 0);
+    const double dm = a + 2 * xv * b + yv * d;
+    grad[o] = float((1 - lam) * sgn * inv_n - lam * dm);
+  }
+}
+
+__global__ void ssim_finish(const double* __restrict__ part, int nparts, double lam, double inv_n,
+                            double* __restrict__ out) {
+  __shared__ double red[2][32];
+  double a = 0, b = 0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) { a += part[2 * i]; b += part[2 * i + 1]; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = a; red[1][threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0; b = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) { a += red[0][w]; b += red[1][w]; }
+    const double mssim = a * inv_n, l1 = b * inv_n;
+    out[0] = (1 - lam) * l1 + lam * (1 - mssim);
+    out[1] = l1;
+    out[2] = mssim;
+  }
+}
+
+unsigned g_win_ready = 0;   // bit per device that holds the window
+
+}  // namespace
+
+size_t loss_scratch_bytes(int W, int H) {
+  const size_t npix = size_t(W) * H * 3;
+  const size_t nb = size_t((W + TW - 1) / TW) * ((H + TH - 1) / TH) * 3;
+  return 3 * 4 * npix + 16 * nb + 256;
+}
+
+cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
+                        float* grad, void* scratch, size_t bytes, cudaStream_t st) {
+  if (bytes < loss_scratch_bytes(W, H)) return cudaErrorInvalidValue;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(g_win_ready & (1u << dev))) {
+    double w[2 * R + 1], s = 0;
+    for (int t = -R; t <= R; ++t) { w[t + R] = exp(-(double(t) * t) / (2 * 1.5 * 1.5)); s += w[t + R]; }
+    for (int t = 0; t <= 2 * R; ++t) w[t] /= s;
+    cudaError_t e = cudaMemcpyToSymbol(kWin, w, sizeof(w));
+    if (e != cudaSuccess) return e;
+    g_win_ready |= 1u << dev;
+  }
+  const size_t npix = size_t(W) * H * 3;
+  float* dmu = static_cast<float*>(scratch);
+  float* dx2 = dmu + npix;
+  float* dxy = dx2 + npix;
+  double* part = reinterpret_cast<double*>(dxy + npix + (npix & 1));
+  dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
+  const double inv_n = 1.0 / double(npix);
+  ssim_pass1<<<grid, NT, 0, st>>>(X, Y, W, H, dmu, dx2, dxy, part, inv_n);
+  ssim_pass2<<<grid, NT, 0, st>>>(X, Y, W, H, dmu, dx2, dxy, grad, lam, inv_n);
+  ssim_finish<<<1, 1024, 0, st>>>(part, int(grid.x * grid.y * grid.z), lam, inv_n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace glod

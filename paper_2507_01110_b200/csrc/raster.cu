@@ -1,0 +1,698 @@
+// 3DGS tile rasteriser with the reference's exact compositing semantics
+// (renderer.py:75-304), fp64 per-Gaussian setup, fp32 per-pixel alpha,
+// fp64 transmittance.
+//
+//   K5 preprocess_kernel   _projection + footprint  (renderer.py:75-114,132-148)
+//   K6 depth sort + tile binning: global stable (depth, index) order
+//      (renderer.py:127 lexsort) → instances emitted in rank order → stable
+//      sort by tile id, so every tile list is in the global order.
+//   K7 blend_fwd_kernel    compositing loop          (renderer.py:131-165)
+//   K8 blend_bwd_kernel    reverse loop, 2D partials (renderer.py:219-261)
+//   K9 preprocess_bwd_kernel 2D→3D chain rule        (renderer.py:262-303)
+#include <cub/cub.cuh>
+#include <stdio.h>
+#include <string>
+
+#include "common.cuh"
+#include "raster.cuh"
+
+namespace glod {
+
+namespace {
+
+constexpr double kLowpass = 0.3;
+constexpr double kShC1 = 0.4886025119029199;
+constexpr float kAlphaMax = 0.99f;
+constexpr double kTEps = 1e-4;
+constexpr float kQMax = 32.0f;   // 2 * (3 + 1)^2
+
+struct CamD {
+  double p[3], W[9], fx, fy, cx, cy, near_;
+  int w, h, tw, th;
+};
+
+CamD make_cam(const glod_camera& c) {
+  CamD k;
+  for (int i = 0; i < 3; ++i) k.p[i] = c.position[i];
+  for (int i = 0; i < 9; ++i) k.W[i] = c.w2c[i];
+  k.fx = c.fx; k.fy = c.fy; k.cx = c.cx; k.cy = c.cy; k.near_ = c.near_plane;
+  k.w = c.width; k.h = c.height;
+  k.tw = (c.width + kTileW - 1) / kTileW;
+  k.th = (c.height + kTileH - 1) / kTileH;
+  return k;
+}
+
+// Section offsets in a packed attribute block of n rows.
+struct Sec {
+  const double *mean, *scale, *rot, *opac, *base, *sh;
+  GLOD_DEV Sec(const double* a, long long n)
+      : mean(a), scale(a + 3 * n), rot(a + 6 * n), opac(a + 10 * n), base(a + 11 * n), sh(a + 14 * n) {}
+};
+
+// Everything the forward and backward passes derive from one Gaussian.
+struct Proj {
+  double t[3];       // camera-space position
+  double m2[2];      // pixel mean
+  double R[9];       // rotation (normalised quaternion)
+  double qn[4];      // normalised quaternion
+  double qnorm;
+  double M[9];       // W Σ Wᵀ
+  double J[6];       // 2x3 Jacobian
+  double c00, c01, c11;   // cov2d
+  double v[3];       // view direction
+  double rng;        // ‖μ − p‖
+  double col[3];
+};
+
+GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
+  const double m0 = s.mean[3 * i], m1 = s.mean[3 * i + 1], m2 = s.mean[3 * i + 2];
+  const double d0 = sub(m0, c.p[0]), d1 = sub(m1, c.p[1]), d2 = sub(m2, c.p[2]);
+  // t = (μ − p) @ Wᵀ through dgemm: fma(c2,w2,fma(c1,w1,c0*w0))
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    P.t[k] = fma_(d2, c.W[3 * k + 2], fma_(d1, c.W[3 * k + 1], mul(d0, c.W[3 * k])));
+  const double tz = P.t[2];
+  P.m2[0] = add(div(mul(c.fx, P.t[0]), tz), c.cx);
+  P.m2[1] = add(div(mul(c.fy, P.t[1]), tz), c.cy);
+  double q0 = s.rot[4 * i], q1 = s.rot[4 * i + 1], q2 = s.rot[4 * i + 2], q3 = s.rot[4 * i + 3];
+  P.qnorm = sqrt_(add(add(add(mul(q0, q0), mul(q1, q1)), mul(q2, q2)), mul(q3, q3)));
+  const double w = q0 / P.qnorm, x = q1 / P.qnorm, y = q2 / P.qnorm, z = q3 / P.qnorm;
+  P.qn[0] = w; P.qn[1] = x; P.qn[2] = y; P.qn[3] = z;
+  double* R = P.R;
+  R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z); R[2] = 2 * (x * z + w * y);
+  R[3] = 2 * (x * y + w * z); R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
+  R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
+  const double s0 = s.scale[3 * i], s1 = s.scale[3 * i + 1], s2 = s.scale[3 * i + 2];
+  const double ss[3] = {s0 * s0, s1 * s1, s2 * s2};
+  double Sg[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      Sg[3 * a + b] = R[3 * a] * ss[0] * R[3 * b] + R[3 * a + 1] * ss[1] * R[3 * b + 1] +
+                      R[3 * a + 2] * ss[2] * R[3 * b + 2];
+  double WS[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      WS[3 * a + b] = c.W[3 * a] * Sg[b] + c.W[3 * a + 1] * Sg[3 + b] + c.W[3 * a + 2] * Sg[6 + b];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      P.M[3 * a + b] = WS[3 * a] * c.W[3 * b] + WS[3 * a + 1] * c.W[3 * b + 1] + WS[3 * a + 2] * c.W[3 * b + 2];
+  P.J[0] = c.fx / tz; P.J[1] = 0.0; P.J[2] = -c.fx * P.t[0] / (tz * tz);
+  P.J[3] = 0.0; P.J[4] = c.fy / tz; P.J[5] = -c.fy * P.t[1] / (tz * tz);
+  double JM[6];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      JM[3 * a + b] = P.J[3 * a] * P.M[b] + P.J[3 * a + 1] * P.M[3 + b] + P.J[3 * a + 2] * P.M[6 + b];
+  P.c00 = JM[0] * P.J[0] + JM[1] * P.J[1] + JM[2] * P.J[2] + kLowpass;
+  P.c01 = JM[0] * P.J[3] + JM[1] * P.J[4] + JM[2] * P.J[5];
+  P.c11 = JM[3] * P.J[3] + JM[4] * P.J[4] + JM[5] * P.J[5] + kLowpass;
+  P.rng = norm3_plain(d0, d1, d2);
+  const double inv = P.rng > 0 ? P.rng : 1.0;
+  P.v[0] = d0 / inv; P.v[1] = d1 / inv; P.v[2] = d2 / inv;
+  const double* f = s.sh + 9 * i;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    P.col[k] = s.base[3 * i + k] + kShC1 * (-P.v[1] * f[k] + P.v[2] * f[3 + k] - P.v[0] * f[6 + k]);
+}
+
+GLOD_DEV bool finite(double x) { return isfinite(x); }
+
+__global__ void preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam,
+                                  Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
+                                  int* __restrict__ vals, int* __restrict__ tiles,
+                                  int* __restrict__ bad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Sec s(attrs, n);
+  // _check_finite (renderer.py:67-72): first section, then first row
+  const int cols[6] = {3, 3, 4, 1, 3, 9};
+  const double* base[6] = {s.mean, s.scale, s.rot, s.opac, s.base, s.sh};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    bool ok = true;
+    for (int c = 0; c < cols[k]; ++c) ok &= finite(base[k][cols[k] * i + c]);
+    if (!ok) atomicMin(bad + k, int(i));
+  }
+  vals[i] = int(i);
+  keys[i] = ~0ull;
+  tiles[i] = 0;
+  Proj P;
+  project(s, i, cam, P);
+  const double depth = P.t[2];
+  if (!(depth > cam.near_)) return;            // ok = depth > near
+  const double det = P.c00 * P.c11 - P.c01 * P.c01;
+  if (!(det > 0)) return;                      // `if det <= 0: continue`
+  const double half = (P.c00 + P.c11) / 2;
+  const double lmax = half + sqrt(fmax(half * half - det, 0.0));
+  const double rad = 3.0 * sqrt(lmax);
+  // int(np.floor(.)) never overflows in Python; clamp in fp64 first
+  const double big = 1e9;
+  double fx0 = fmin(fmax(floor(P.m2[0] - rad), -big), big);
+  double fx1 = fmin(fmax(ceil(P.m2[0] + rad) + 1, -big), big);
+  double fy0 = fmin(fmax(floor(P.m2[1] - rad), -big), big);
+  double fy1 = fmin(fmax(ceil(P.m2[1] + rad) + 1, -big), big);
+  const int x0 = max(int(fx0), 0), x1 = min(int(fx1), cam.w);
+  const int y0 = max(int(fy0), 0), y1 = min(int(fy1), cam.h);
+  if (x0 >= x1 || y0 >= y1) return;
+  Splat sp;
+  sp.mx = float(P.m2[0] - x0);
+  sp.my = float(P.m2[1] - y0);
+  sp.ca = float(P.c11 / det);
+  sp.cb = float(-P.c01 / det);
+  sp.cc = float(P.c00 / det);
+  sp.opac = float(s.opac[i]);
+  sp.x0 = int16_t(x0); sp.y0 = int16_t(y0); sp.x1 = int16_t(x1); sp.y1 = int16_t(y1);
+  sp.r = float(P.col[0]); sp.g = float(P.col[1]); sp.b = float(P.col[2]);
+  sp.idx = int(i);
+  splats[i] = sp;
+  keys[i] = __double_as_longlong(depth);       // positive doubles order as uint64
+  const int tx0 = x0 / kTileW, tx1 = (x1 - 1) / kTileW;
+  const int ty0 = y0 / kTileH, ty1 = (y1 - 1) / kTileH;
+  tiles[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+}
+
+__global__ void gather_kernel(const int* __restrict__ order, const Splat* __restrict__ splats,
+                              const int* __restrict__ tiles, Splat* __restrict__ sorted,
+                              int* __restrict__ tiles_sorted, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int g = order[r];
+  const int c = tiles[g];
+  tiles_sorted[r] = c;
+  if (c) sorted[r] = splats[g];
+}
+
+__global__ void emit_kernel(const Splat* __restrict__ sorted, const int* __restrict__ tiles_sorted,
+                            const long long* __restrict__ offs, int tw,
+                            unsigned* __restrict__ ikey, int* __restrict__ ival, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n || tiles_sorted[r] == 0) return;
+  const Splat sp = sorted[r];
+  const int tx0 = sp.x0 / kTileW, tx1 = (sp.x1 - 1) / kTileW;
+  const int ty0 = sp.y0 / kTileH, ty1 = (sp.y1 - 1) / kTileH;
+  long long o = offs[r];
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      ikey[o] = unsigned(ty * tw + tx);
+      ival[o] = int(r);
+      ++o;
+    }
+}
+
+__global__ void ranges_kernel(const unsigned* __restrict__ ikey, long long n, int2* __restrict__ range) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned k = ikey[i];
+  if (i == 0 || ikey[i - 1] != k) range[k].x = int(i);
+  if (i == n - 1 || ikey[i + 1] != k) range[k].y = int(i + 1);
+}
+
+// Per-pixel alpha with an explicit rounding sequence so the forward and the
+// backward kernels produce bit-identical values (no contraction variance).
+GLOD_DEV bool pixel_alpha(const Splat& g, int px, int py, float& dx, float& dy, float& q,
+                          float& gauss, float& alpha) {
+  if (px < g.x0 || px >= g.x1 || py < g.y0 || py >= g.y1) return false;
+  dx = __fsub_rn(float(px - g.x0), g.mx);
+  dy = __fsub_rn(float(py - g.y0), g.my);
+  // q = a dx² + c dy² + 2 b dy dx   (renderer.py:151-152)
+  q = __fadd_rn(__fadd_rn(__fmul_rn(g.ca, __fmul_rn(dx, dx)), __fmul_rn(g.cc, __fmul_rn(dy, dy))),
+                __fmul_rn(__fmul_rn(__fmul_rn(2.0f, g.cb), dy), dx));
+  if (!(q <= kQMax)) return false;
+  gauss = __expf(__fmul_rn(-0.5f, q));
+  const float a = __fmul_rn(g.opac, gauss);
+  alpha = fminf(a, kAlphaMax);
+  return alpha > 0.0f;
+}
+
+__global__ void __launch_bounds__(kBlendThreads)
+blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
+                 const int2* __restrict__ range, CamD cam, float* __restrict__ image,
+                 double* __restrict__ t_final, int* __restrict__ last_out) {
+  __shared__ Splat sm[kBlendThreads];
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tw, ty = tile / cam.tw;
+  const int px = tx * kTileW + int(threadIdx.x % kTileW);
+  const int py = ty * kTileH + int(threadIdx.x / kTileW);
+  const bool inside = px < cam.w && py < cam.h;
+  const int2 rg = range[tile];
+  double T = 1.0;
+  float cr = 0.f, cg = 0.f, cb = 0.f;
+  int last = -1;
+  bool done = !inside;
+  for (int base = rg.x; base < rg.y; base += kBlendThreads) {
+    if (__syncthreads_count(!done) == 0) break;
+    const int k = base + int(threadIdx.x);
+    if (k < rg.y) sm[threadIdx.x] = sorted[ival[k]];
+    __syncthreads();
+    const int cnt = min(kBlendThreads, rg.y - base);
+    for (int j = 0; j < cnt && !done; ++j) {
+      float dx, dy, q, gs, al;
+      if (!pixel_alpha(sm[j], px, py, dx, dy, q, gs, al)) continue;
+      const double w = double(al) * T;
+      cr += float(w) * sm[j].r;
+      cg += float(w) * sm[j].g;
+      cb += float(w) * sm[j].b;
+      T = T * (1.0 - double(al));
+      last = base + j;
+      if (T <= kTEps) done = true;           // later alphas are gated to 0
+    }
+  }
+  if (inside) {
+    const long long pix = (long long)py * cam.w + px;
+    image[3 * pix] = cr;
+    image[3 * pix + 1] = cg;
+    image[3 * pix + 2] = cb;
+    t_final[pix] = T;
+    last_out[pix] = last;
+  }
+}
+
+GLOD_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(kBlendThreads)
+blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
+                 const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
+                 const double* __restrict__ t_final, const int* __restrict__ last_in,
+                 double* __restrict__ g2) {
+  __shared__ Splat sm[kBlendThreads];
+  __shared__ int max_last;
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tw, ty = tile / cam.tw;
+  const int px = tx * kTileW + int(threadIdx.x % kTileW);
+  const int py = ty * kTileH + int(threadIdx.x / kTileW);
+  const bool inside = px < cam.w && py < cam.h;
+  const int2 rg = range[tile];
+  const int lane = threadIdx.x & 31;
+  double T = 1.0;
+  int last = -1;
+  float gr = 0.f, gg = 0.f, gb = 0.f;
+  if (inside) {
+    const long long pix = (long long)py * cam.w + px;
+    T = t_final[pix];
+    last = last_in[pix];
+    gr = dimg[3 * pix]; gg = dimg[3 * pix + 1]; gb = dimg[3 * pix + 2];
+  }
+  if (threadIdx.x == 0) max_last = -1;
+  __syncthreads();
+  atomicMax(&max_last, last);
+  __syncthreads();
+  const int end = max_last + 1;   // nothing beyond the last contributor matters
+  double rr = 0.0, rg_ = 0.0, rb = 0.0;   // rear accumulator Σ_behind w·c
+  for (int top = end; top > rg.x; top -= kBlendThreads) {
+    const int lo = max(rg.x, top - kBlendThreads);
+    const int k = top - 1 - int(threadIdx.x);
+    __syncthreads();
+    if (k >= lo) sm[threadIdx.x] = sorted[ival[k]];
+    __syncthreads();
+    const int cnt = top - lo;
+    for (int j = 0; j < cnt; ++j) {
+      const int inst = top - 1 - j;
+      const Splat& g = sm[j];
+      double c[kG2];
+#pragma unroll
+      for (int u = 0; u < kG2; ++u) c[u] = 0.0;
+      float dx, dy, q, gs, al;
+      bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
+      if (hit) {
+        const double a = al;
+        const double Tf = T / (1.0 - a);                   // T before this splat
+        const double w = a * Tf;
+        c[0] = w * gr; c[1] = w * gg; c[2] = w * gb;       // dl_dcolor
+        const double gc = double(gr) * g.r + double(gg) * g.g + double(gb) * g.b;
+        const double grear = double(gr) * rr + double(gg) * rg_ + double(gb) * rb;
+        const double dla = gc * Tf - grear / (1.0 - a);
+        rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
+        T = Tf;
+        if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
+          const double G = gs;
+          c[3] = G * dla;
+          const double dq = -0.5 * double(g.opac) * G * dla;
+          const double X = dx, Y = dy;
+          c[4] = -dq * (2.0 * g.ca * X + 2.0 * g.cb * Y);
+          c[5] = -dq * (2.0 * g.cb * X + 2.0 * g.cc * Y);
+          c[6] = dq * X * X;
+          c[7] = dq * X * Y;
+          c[8] = dq * Y * Y;
+        }
+      }
+      if (__any_sync(0xffffffffu, hit)) {
+#pragma unroll
+        for (int u = 0; u < kG2; ++u) {
+          const double s = warp_sum(c[u]);
+          if (lane == 0 && s != 0.0) atomicAdd(g2 + (long long)kG2 * g.idx + u, s);
+        }
+      }
+    }
+  }
+}
+
+// K9: 2D partials → gradients of the raw attributes (renderer.py:262-303).
+__global__ void preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
+                                      const int* __restrict__ tiles_of, const double* __restrict__ g2,
+                                      double* __restrict__ grads) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Sec s(attrs, n);
+  double* gm = grads;                 // means [3n]
+  double* gsc = grads + 3 * n;        // scales
+  double* grot = grads + 6 * n;       // rotations
+  double* gop = grads + 10 * n;       // opacities
+  double* gbase = grads + 11 * n;     // base colours
+  double* gsh = grads + 14 * n;       // sh_rest
+  const double* a2 = g2 + (long long)kG2 * i;
+  if (tiles_of[i] == 0) {
+    for (int k = 0; k < 3; ++k) { gm[3 * i + k] = 0; gsc[3 * i + k] = 0; gbase[3 * i + k] = 0; }
+    for (int k = 0; k < 4; ++k) grot[4 * i + k] = 0;
+    for (int k = 0; k < 9; ++k) gsh[9 * i + k] = 0;
+    gop[i] = 0;
+    return;
+  }
+  Proj P;
+  project(s, i, cam, P);
+  const double det = P.c00 * P.c11 - P.c01 * P.c01;
+  const double ca = P.c11 / det, cb = -P.c01 / det, cc = P.c00 / det;
+  const double dcol[3] = {a2[0], a2[1], a2[2]};
+  gop[i] = a2[3];
+  const double dmx = a2[4], dmy = a2[5];
+  const double daa = a2[6], dbb = a2[7], dcc = a2[8];
+  // dl_dcov2d = -C dC C with C = [[a,b],[b,c]], dC = [[daa,dbb],[dbb,dcc]]
+  const double t00 = ca * daa + cb * dbb, t01 = ca * dbb + cb * dcc;
+  const double t10 = cb * daa + cc * dbb, t11 = cb * dbb + cc * dcc;
+  const double D00 = -(t00 * ca + t01 * cb), D01 = -(t00 * cb + t01 * cc);
+  const double D10 = -(t10 * ca + t11 * cb), D11 = -(t10 * cb + t11 * cc);
+  const double Dc[4] = {D00, D01, D10, D11};
+  // dl_dm = Jᵀ Dc J (3x3); dl_dsigma = Wᵀ dl_dm W
+  double DJ[6];   // Dc @ J (2x3)
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) DJ[3 * a + b] = Dc[2 * a] * P.J[b] + Dc[2 * a + 1] * P.J[3 + b];
+  double dM[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) dM[3 * a + b] = P.J[a] * DJ[b] + P.J[3 + a] * DJ[3 + b];
+  const double* W = cam.W;
+  double tmp[9], dS[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) tmp[3 * a + b] = dM[3 * a] * W[b] + dM[3 * a + 1] * W[3 + b] + dM[3 * a + 2] * W[6 + b];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) dS[3 * a + b] = W[a] * tmp[b] + W[3 + a] * tmp[3 + b] + W[6 + a] * tmp[6 + b];
+  // dl_dj = (Dc + Dcᵀ) J M  (2x3)
+  const double S00 = 2 * D00, S01 = D01 + D10, S11 = 2 * D11;
+  double JM[6];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      JM[3 * a + b] = P.J[3 * a] * P.M[b] + P.J[3 * a + 1] * P.M[3 + b] + P.J[3 * a + 2] * P.M[6 + b];
+  double dJ[6];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    dJ[b] = S00 * JM[b] + S01 * JM[3 + b];
+    dJ[3 + b] = S01 * JM[b] + S11 * JM[3 + b];
+  }
+  const double tx = P.t[0], ty = P.t[1], tz = P.t[2];
+  const double fx = cam.fx, fy = cam.fy;
+  double dt[3];
+  dt[0] = dmx * fx / tz + dJ[2] * (-fx / (tz * tz));
+  dt[1] = dmy * fy / tz + dJ[5] * (-fy / (tz * tz));
+  dt[2] = dmx * (-fx * tx / (tz * tz)) + dmy * (-fy * ty / (tz * tz)) + dJ[0] * (-fx / (tz * tz)) +
+          dJ[4] * (-fy / (tz * tz)) + dJ[2] * (2 * fx * tx / (tz * tz * tz)) +
+          dJ[5] * (2 * fy * ty / (tz * tz * tz));
+  double dmean[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dmean[k] = W[k] * dt[0] + W[3 + k] * dt[1] + W[6 + k] * dt[2];
+  // colour path (renderer.py:281-291)
+  const double* f = s.sh + 9 * i;
+  const double* v = P.v;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gbase[3 * i + k] = dcol[k];
+    gsh[9 * i + k] = -kShC1 * v[1] * dcol[k];
+    gsh[9 * i + 3 + k] = kShC1 * v[2] * dcol[k];
+    gsh[9 * i + 6 + k] = -kShC1 * v[0] * dcol[k];
+  }
+  const double dv0 = kShC1 * -(f[6] * dcol[0] + f[7] * dcol[1] + f[8] * dcol[2]);
+  const double dv1 = kShC1 * -(f[0] * dcol[0] + f[1] * dcol[1] + f[2] * dcol[2]);
+  const double dv2 = kShC1 * (f[3] * dcol[0] + f[4] * dcol[1] + f[5] * dcol[2]);
+  const double vd = v[0] * dv0 + v[1] * dv1 + v[2] * dv2;
+  dmean[0] += (dv0 - v[0] * vd) / P.rng;
+  dmean[1] += (dv1 - v[1] * vd) / P.rng;
+  dmean[2] += (dv2 - v[2] * vd) / P.rng;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) gm[3 * i + k] = dmean[k];
+  // covariance → scale and normalised quaternion
+  double sym[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) sym[3 * a + b] = 0.5 * (dS[3 * a + b] + dS[3 * b + a]);
+  const double* R = P.R;
+  const double sc[3] = {s.scale[3 * i], s.scale[3 * i + 1], s.scale[3 * i + 2]};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double acc = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) acc += R[3 * a + k] * sym[3 * a + b] * R[3 * b + k];
+    gsc[3 * i + k] = 2 * sc[k] * acc;
+  }
+  // dl_dr = 2 sym R diag(s²)
+  double dR[9];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      dR[3 * a + b] = 2 * (sym[3 * a] * R[b] + sym[3 * a + 1] * R[3 + b] + sym[3 * a + 2] * R[6 + b]) *
+                      (sc[b] * sc[b]);
+  const double w = P.qn[0], x = P.qn[1], y = P.qn[2], z = P.qn[3];
+  // dR/dq for each quaternion component (renderer.py:177-194)
+  const double Dw[9] = {0, -z, y, z, 0, -x, -y, x, 0};
+  const double Dx[9] = {0, y, z, y, -2 * x, -w, z, w, -2 * x};
+  const double Dy[9] = {-2 * y, x, w, x, 0, z, -w, z, -2 * y};
+  const double Dz[9] = {-2 * z, -w, x, w, -2 * z, y, x, y, 0};
+  double dq[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int e = 0; e < 9; ++e) {
+    dq[0] += dR[e] * 2 * Dw[e];
+    dq[1] += dR[e] * 2 * Dx[e];
+    dq[2] += dR[e] * 2 * Dy[e];
+    dq[3] += dR[e] * 2 * Dz[e];
+  }
+  const double qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
+  for (int k = 0; k < 4; ++k) grot[4 * i + k] = (dq[k] - P.qn[k] * qd) / P.qnorm;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Workspace: device buffers grown stream-ordered (cudaMallocAsync).
+// ---------------------------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes, cudaStream_t st) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFreeAsync(p, st);
+    size_t want = bytes + bytes / 4 + 4096;
+    cudaError_t e = cudaMallocAsync(&p, want, st);
+    cap = e == cudaSuccess ? want : 0;
+    return e;
+  }
+  void release(cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct RasterCtx {
+  Buf splats, sorted, keys, keys2, vals, vals2, tiles, tiles_sorted, offs;
+  Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin;
+  CamD cam{};
+  const double* attrs = nullptr;
+  long long n = 0, n_inst = 0, n_visible = 0;
+  int bad_section = -1, bad_index = -1;
+  cudaStream_t stream = nullptr;
+  bool have_forward = false;
+};
+
+static int bits_for(long long v) {
+  int b = 1;
+  while ((1ll << b) < v) ++b;
+  return b;
+}
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t _e = (x);                       \
+    if (_e != cudaSuccess) return _e;           \
+  } while (0)
+
+cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const glod_camera& c,
+                           float* image, cudaStream_t st) {
+  R->cam = make_cam(c);
+  R->attrs = attrs;
+  R->n = n;
+  R->stream = st;
+  R->have_forward = true;
+  R->bad_section = -1;
+  const CamD& cam = R->cam;
+  const long long npix = (long long)cam.w * cam.h;
+  const int ntiles = cam.tw * cam.th;
+  CK(R->tfinal.ensure(8 * npix, st));
+  CK(R->last.ensure(4 * npix, st));
+  CK(R->range.ensure(8 * (size_t)ntiles, st));
+  CK(cudaMemsetAsync(R->range.p, 0, 8 * (size_t)ntiles, st));
+  if (n == 0) {
+    CK(cudaMemsetAsync(image, 0, 12 * npix, st));
+    CK(cudaMemsetAsync(R->tfinal.p, 0, 8 * npix, st));
+    R->n_inst = 0;
+    R->n_visible = 0;
+    // T=1 everywhere, no contributors: the blend kernel writes exactly that
+    blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(nullptr, nullptr, R->range.as<int2>(), cam,
+                                                         image, R->tfinal.as<double>(), R->last.as<int>());
+    return cudaGetLastError();
+  }
+  CK(R->splats.ensure(sizeof(Splat) * n, st));
+  CK(R->sorted.ensure(sizeof(Splat) * n, st));
+  CK(R->keys.ensure(8 * n, st));
+  CK(R->keys2.ensure(8 * n, st));
+  CK(R->vals.ensure(4 * n, st));
+  CK(R->vals2.ensure(4 * n, st));
+  CK(R->tiles.ensure(4 * n, st));
+  CK(R->tiles_sorted.ensure(4 * n + 4, st));
+  CK(R->offs.ensure(8 * (n + 1), st));
+  CK(R->bad.ensure(64, st));
+  CK(R->host_pin.p ? cudaSuccess : cudaMallocHost(&R->host_pin.p, 256));
+  R->host_pin.cap = 256;
+  int init_bad[8];
+  for (int k = 0; k < 8; ++k) init_bad[k] = 0x7fffffff;
+  CK(cudaMemcpyAsync(R->bad.p, init_bad, sizeof(init_bad), cudaMemcpyHostToDevice, st));
+  const int TB = 256;
+  const int nb = int((n + TB - 1) / TB);
+  preprocess_kernel<<<nb, TB, 0, st>>>(attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
+                                       R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>());
+  CK(cudaGetLastError());
+  // global stable sort on fp64 depth bits (ties keep index order)
+  size_t tb_sort = 0, tb_scan = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (int*)nullptr, (int*)nullptr, int(n), 0, 64, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, (int*)nullptr, (long long*)nullptr, int(n + 1), st);
+  CK(R->temp.ensure(std::max(tb_sort, tb_scan), st));
+  size_t tb = R->temp.cap;
+  CK(cub::DeviceRadixSort::SortPairs(R->temp.p, tb, R->keys.as<unsigned long long>(),
+                                     R->keys2.as<unsigned long long>(), R->vals.as<int>(),
+                                     R->vals2.as<int>(), int(n), 0, 64, st));
+  const int* order = R->vals2.as<int>();
+  gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
+                                   R->tiles_sorted.as<int>(), n);
+  CK(cudaGetLastError());
+  CK(cudaMemsetAsync(R->tiles_sorted.as<int>() + n, 0, 4, st));
+  tb = R->temp.cap;
+  CK(cub::DeviceScan::ExclusiveSum(R->temp.p, tb, R->tiles_sorted.as<int>(), R->offs.as<long long>(),
+                                   int(n + 1), st));
+  long long* hp = static_cast<long long*>(R->host_pin.p);
+  CK(cudaMemcpyAsync(hp, R->offs.as<long long>() + n, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hp + 1, R->bad.p, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int* badh = reinterpret_cast<const int*>(hp + 1);
+  for (int k = 0; k < 6; ++k)
+    if (badh[k] != 0x7fffffff) {
+      R->bad_section = k;
+      R->bad_index = badh[k];
+      return cudaErrorInvalidValue;
+    }
+  const long long n_inst = hp[0];
+  R->n_inst = n_inst;
+  if (n_inst > 0x7fffffffll) return cudaErrorMemoryAllocation;
+  CK(R->ikey.ensure(4 * n_inst + 4, st));
+  CK(R->ikey2.ensure(4 * n_inst + 4, st));
+  CK(R->ival.ensure(4 * n_inst + 4, st));
+  CK(R->ival2.ensure(4 * n_inst + 4, st));
+  emit_kernel<<<nb, TB, 0, st>>>(R->sorted.as<Splat>(), R->tiles_sorted.as<int>(), R->offs.as<long long>(),
+                                 cam.tw, R->ikey.as<unsigned>(), R->ival.as<int>(), n);
+  CK(cudaGetLastError());
+  if (n_inst > 0) {
+    const int kb = bits_for(ntiles);
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
+                                    (int*)nullptr, int(n_inst), 0, kb, st);
+    CK(R->temp.ensure(need, st));
+    tb = R->temp.cap;
+    CK(cub::DeviceRadixSort::SortPairs(R->temp.p, tb, R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(),
+                                       R->ival.as<int>(), R->ival2.as<int>(), int(n_inst), 0, kb, st));
+    ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey2.as<unsigned>(), n_inst,
+                                                              R->range.as<int2>());
+    CK(cudaGetLastError());
+  }
+  blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
+                                                       R->range.as<int2>(), cam, image,
+                                                       R->tfinal.as<double>(), R->last.as<int>());
+  return cudaGetLastError();
+}
+
+cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cudaStream_t st) {
+  const CamD& cam = R->cam;
+  const long long n = R->n;
+  if (n == 0) return cudaSuccess;
+  const int ntiles = cam.tw * cam.th;
+  CK(R->g2.ensure(8 * kG2 * (size_t)n, st));
+  CK(cudaMemsetAsync(R->g2.p, 0, 8 * kG2 * (size_t)n, st));
+  if (R->n_inst > 0)
+    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
+                                                         R->range.as<int2>(), cam, dimg,
+                                                         R->tfinal.as<double>(), R->last.as<int>(),
+                                                         R->g2.as<double>());
+  CK(cudaGetLastError());
+  const int TB = 128;
+  preprocess_bwd_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->attrs, n, cam, R->tiles.as<int>(),
+                                                               R->g2.as<double>(), grads);
+  return cudaGetLastError();
+}
+
+RasterCtx* raster_create() { return new RasterCtx(); }
+
+void raster_stats(const RasterCtx* R, glod_render_stats* out) {
+  out->n_gaussians = R->n;
+  out->n_instances = R->n_inst;
+  out->tiles_x = R->cam.tw;
+  out->tiles_y = R->cam.th;
+}
+
+bool raster_bad_input(const RasterCtx* R, int* section, int* index) {
+  if (R->bad_section < 0) return false;
+  *section = R->bad_section;
+  *index = R->bad_index;
+  return true;
+}
+
+void raster_destroy(RasterCtx* R) {
+  cudaStream_t st = R->stream;
+  Buf* all[] = {&R->splats, &R->sorted, &R->keys, &R->keys2, &R->vals, &R->vals2, &R->tiles,
+                &R->tiles_sorted, &R->offs, &R->ikey, &R->ikey2, &R->ival, &R->ival2, &R->range,
+                &R->tfinal, &R->last, &R->g2, &R->temp, &R->bad};
+  for (Buf* b : all) b->release(st);
+  if (R->host_pin.p) cudaFreeHost(R->host_pin.p);
+  delete R;
+}
+
+}  // namespace glod

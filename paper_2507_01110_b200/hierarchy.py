@@ -147,6 +147,14 @@ def _rotmat_to_quat_t(m: torch.Tensor) -> torch.Tensor:
     return q / torch.linalg.norm(q, dim=1, keepdim=True)
 
 
+def _eigh_batched(cov: torch.Tensor, chunk: int = 1 << 15):
+    # cusolver's batched syev rejects very large batches; chunk them
+    if cov.shape[0] <= chunk:
+        return torch.linalg.eigh(cov)
+    parts = [torch.linalg.eigh(cov[i:i + chunk]) for i in range(0, cov.shape[0], chunk)]
+    return torch.cat([p[0] for p in parts]), torch.cat([p[1] for p in parts])
+
+
 def _merge_level(A: dict, dst, a, b):
     """Moment-matched merge of children (a, b) into dst (hierarchy.py:136-176)."""
     wa = A["opacities"][a] * torch.prod(A["scales"][a], 1)
@@ -168,7 +176,7 @@ def _merge_level(A: dict, dst, a, b):
     cov = (fa[..., None] * (ca + da[:, :, None] * da[:, None, :])
            + fb[..., None] * (cb + db[:, :, None] * db[:, None, :]))
     cov = 0.5 * (cov + cov.transpose(1, 2))
-    vals, vecs = torch.linalg.eigh(cov)
+    vals, vecs = _eigh_batched(cov)
     flip = torch.linalg.det(vecs) < 0
     vecs[:, :, 2] = torch.where(flip[:, None], -vecs[:, :, 2], vecs[:, :, 2])
     A["means"][dst] = mean

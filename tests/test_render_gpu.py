@@ -1,0 +1,132 @@
+"""GPU rasteriser / loss / ADAM parity through the C-ABI.
+
+Tolerances (BASELINE north star): images ≤ 1e-4 max-abs per channel;
+gradients ≤ 1e-3 relative, evaluated per attribute array as
+|g − g_ref| ≤ 1e-3 · (|g_ref| + 1e-2 · max|g_ref|)  (the second term keeps
+entries that are ~0 from demanding infinite relative precision).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import glod_oracle as O  # noqa: E402
+from paper_2507_01110_b200 import renderer as Rn  # noqa: E402
+from paper_2507_01110_b200.core import AttributeArrays, SECTIONS  # noqa: E402
+
+from .conftest import golden  # noqa: E402
+from .helpers import camera_of  # noqa: E402
+
+NAMES = [n for n, _ in SECTIONS]
+IMG_TOL = 1e-4
+GRAD_REL = 1e-3
+
+
+def attrs_of(d, p):
+    return AttributeArrays(*(d[p + k] for k in NAMES))
+
+
+def assert_grads_close(got, want, where=""):
+    for k in NAMES:
+        g = np.asarray(getattr(got, k) if not isinstance(got, dict) else got[k], dtype=np.float64)
+        w = np.asarray(want[k], dtype=np.float64)
+        scale = np.max(np.abs(w)) if w.size else 0.0
+        tol = GRAD_REL * (np.abs(w) + 1e-2 * scale) + 1e-300
+        bad = np.abs(g - w) > tol
+        assert not bad.any(), (f"{where} {k}: max rel err "
+                               f"{np.max(np.abs(g - w) / (np.abs(w) + 1e-2 * scale + 1e-300)):.3e}")
+
+
+def test_render_golden_forward_backward_loss():
+    d = golden("render_cases.npz")
+    for k in range(int(d["n_cases"])):
+        cam = camera_of(d, f"r{k}_")
+        a = attrs_of(d, f"r{k}_a_")
+        ctx = Rn.render_forward(a, cam)
+        err = np.max(np.abs(ctx.image - d[f"r{k}_image"]))
+        assert err <= IMG_TOL, (k, err)
+        g = Rn.backward(ctx, d[f"r{k}_upstream"])
+        want = {n: d[f"r{k}_g_{n}"] for n in NAMES}
+        assert_grads_close(g, want, where=f"case {k}")
+        lv, lg = Rn.loss(d[f"r{k}_image"], d[f"r{k}_target"], 0.2)
+        assert abs(lv - float(d[f"r{k}_loss"])) <= 1e-6 * max(1.0, abs(float(d[f"r{k}_loss"])))
+        ref = d[f"r{k}_loss_grad"]
+        assert np.max(np.abs(lg - ref)) <= 1e-4 * np.max(np.abs(ref))
+
+
+def test_render_empty_and_offscreen():
+    d = golden("render_cases.npz")
+    cam = camera_of(d, "r0_")
+    img = Rn.render(AttributeArrays.zeros(0), cam)
+    assert img.shape == (cam.resolution[1], cam.resolution[0], 3) and np.all(img == 0)
+    a = AttributeArrays.zeros(1)
+    a.means[0] = [0, 0, -50]        # behind the camera
+    a.opacities[:] = 1.0
+    a.base_colors[0] = [1, 1, 1]
+    assert np.all(Rn.render(a, cam) == 0)
+
+
+def test_render_rejects_non_finite():
+    d = golden("render_cases.npz")
+    cam = camera_of(d, "r0_")
+    a = AttributeArrays.zeros(3)
+    a.means[1, 2] = np.nan
+    with pytest.raises(Rn.InvalidInputError, match="Gaussian 1"):
+        Rn.render(a, cam)
+
+
+def test_single_opaque_center_kat():
+    """Known answer (test_renderer.py:105-114): centre pixel = 0.99·colour."""
+    d = golden("render_cases.npz")
+    cam = camera_of(d, "r0_")
+    a = AttributeArrays.zeros(1)
+    a.opacities[:] = 1.0
+    a.base_colors[0] = [0.2, 0.5, 0.9]
+    img = Rn.render(a, cam)
+    np.testing.assert_allclose(img[8, 8], 0.99 * a.base_colors[0], rtol=1e-6)
+
+
+@pytest.mark.parametrize("n_leaves,res", [(20_000, (256, 256)), (60_000, (640, 360))])
+def test_render_designed_scene_vs_oracle(n_leaves, res):
+    """Render sets from the LoD cut of a generated scene (thousands of
+    Gaussians, saturated pixels) against the numpy oracle."""
+    from paper_2507_01110_b200 import hspt as H
+    from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene, orbit_views, scene_extent
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=n_leaves, spt_leaves=1024, seed=2))
+    E = scene_extent(n_leaves)
+    cam = orbit_views(1, 1.4 * E, 0.6 * E, resolution=res, seed=4)[0]
+    rs = H.cut_hspt(hs, h, cam, cfg)
+    a = h.attrs.take(rs.nodes)
+    ctx = Rn.render_forward(a, cam)
+    A = {k: getattr(a, k) for k in NAMES}
+    img, octx = O.render_forward(A, O.Cam.of(cam))
+    assert np.max(np.abs(ctx.image - img)) <= IMG_TOL
+    up = np.random.default_rng(0).normal(size=img.shape)
+    assert_grads_close(Rn.backward(ctx, up), O.backward(octx, up), where="designed")
+
+
+def test_adam_golden():
+    from paper_2507_01110_b200 import _lib
+    import ctypes as C
+    d = golden("adam_cases.npz")
+    n = d["p0_means"].shape[0]
+    a = attrs_of(d, "p0_")
+    P = torch.from_numpy(a.packed()).cuda()
+    M = torch.zeros_like(P)
+    V = torch.zeros_like(P)
+    step = torch.zeros(n, dtype=torch.int64, device="cuda")
+    lrs = (C.c_double * 6)(*[float(d["lr_" + k]) for k in NAMES])
+    for it in range(3):
+        ids = torch.from_numpy(d[f"it{it}_ids"].astype(np.int32)).cuda()
+        g = AttributeArrays(*(d[f"it{it}_g_{k}"] for k in NAMES))
+        G = torch.from_numpy(g.packed()).cuda()
+        _lib.check(_lib.lib().glod_adam_step(_lib.ptr(P), _lib.ptr(M), _lib.ptr(V), _lib.ptr(step), n,
+                                             _lib.ptr(ids), _lib.ptr(G), None, ids.numel(), ids.numel(),
+                                             lrs, _lib.stream_ptr()))
+        got = AttributeArrays.from_packed(P.cpu().numpy(), n)
+        for k in NAMES:
+            np.testing.assert_allclose(getattr(got, k), d[f"it{it}_p_{k}"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_array_equal(step.cpu().numpy(), d[f"it{it}_step"])
