@@ -170,6 +170,38 @@ int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t 
                    const int32_t* ids, const double* grads, const int32_t* rows,
                    int64_t grad_rows, int64_t n, const double* lrs, void* stream);
 
+/* ======================================================================= *
+ * Store / cache data movement (trainer.py:325-364, store.py:304-333)
+ * ======================================================================= */
+
+/* Where each render row comes from: rows [0, n_upper+n_pass) are master
+ * rows (h.attrs.take(concat(upper, passthrough))); row n_upper+n_pass+k is
+ * row sel_pos[k] of the cache block of segment sel_seg[k].  Blocks and the
+ * master are packed f64 attribute blocks (seg_rows[j] / capacity rows). */
+typedef struct glod_gather_plan {
+  double* master;               /* [dev] packed f64, capacity rows            */
+  int64_t capacity;
+  const int32_t* upper_ids;     /* [dev] [n_upper]                            */
+  const int32_t* pass_ids;      /* [dev] [n_pass]                             */
+  int32_t n_upper;
+  int32_t n_pass;
+  const int32_t* sel_seg;       /* [dev] [n_sel] (glod_spt_compact output)    */
+  const int32_t* sel_pos;       /* [dev] [n_sel]                              */
+  const int32_t* sel_node;      /* [dev] [n_sel]                              */
+  int64_t n_sel;
+  const uint64_t* seg_block;    /* [dev] [n_spt] device address of each block */
+  const int64_t* seg_rows;      /* [dev] [n_spt] rows (prefix_len) per block  */
+} glod_gather_plan;
+
+/* AttributeArrays.concat of the render set into `out` (packed f64, R =
+ * n_upper+n_pass+n_sel rows); row_node (optional) receives each row's node. */
+int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* row_node,
+                            void* stream);
+/* entry.block.attrs.put(pos, h.attrs.take(node_ids)) for every SPT row. */
+int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream);
+/* Elementwise f32 -> f64 (to_f64=1) or f64 -> f32 (store write-back). */
+int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,12 @@ class RenderStats(C.Structure):
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32)]
 
 
+class GatherPlan(C.Structure):
+    _fields_ = [("master", P), ("capacity", C.c_int64), ("upper_ids", P), ("pass_ids", P),
+                ("n_upper", C.c_int32), ("n_pass", C.c_int32), ("sel_seg", P), ("sel_pos", P),
+                ("sel_node", P), ("n_sel", C.c_int64), ("seg_block", P), ("seg_rows", P)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "glod_version": (C.c_int, []),
@@ -76,6 +82,9 @@ SIGNATURES = {
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
     "glod_adam_step": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
                                  C.POINTER(C.c_double), P]),
+    "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
+    "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
+    "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
 }
 
 _LIB = None

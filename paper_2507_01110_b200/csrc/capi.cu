@@ -13,6 +13,10 @@ cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam
 cudaError_t launch_adam(double* params, double* m, double* v, long long* step, long long cap,
                         const int* ids, const double* grads, const int* rows, long long grad_rows,
                         long long n, const double* lrs, cudaStream_t st);
+cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
+                          cudaStream_t st);
+cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
+cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st);
 }  // namespace glod
 
 struct glod_raster {
@@ -137,6 +141,26 @@ int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t 
   return check(glod::launch_adam(params, m, v, reinterpret_cast<long long*>(step), capacity, ids,
                                  grads, rows, grad_rows, n, lrs, static_cast<cudaStream_t>(stream)),
                "glod_adam_step");
+}
+
+int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* row_node,
+                            void* stream) {
+  if (!plan || !out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  const long long R = (long long)plan->n_upper + plan->n_pass + plan->n_sel;
+  return check(glod::launch_gather(*plan, R, out, row_node, static_cast<cudaStream_t>(stream)),
+               "glod_gather_render_rows");
+}
+
+int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream) {
+  if (!plan) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_scatter_back(*plan, static_cast<cudaStream_t>(stream)),
+               "glod_scatter_to_blocks");
+}
+
+int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* stream) {
+  if (n > 0 && (!in || !out)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_convert(in, out, n, to_f64, static_cast<cudaStream_t>(stream)),
+               "glod_convert");
 }
 
 }  // extern "C"

@@ -1,0 +1,134 @@
+// K4: render-set gather and cache-block maintenance (trainer.py:325-364,
+// store.py:304-333 data movement).
+//
+//  gather_rows   render rows = master[upper ∪ passthrough] then, per selected
+//                SPT, cache-block rows at the cut positions (AttributeArrays
+//                .take + concat, core.py:120-159) — one kernel, 23 f64/row.
+//  scatter_back  after ADAM: block[pos] = master[node] (trainer.py:363)
+//  convert       f32 store prefix ↔ f64 cache block (store.py:334,330)
+#include "common.cuh"
+#include "../../include/glod_b200.h"
+
+namespace glod {
+namespace {
+
+__constant__ int kSecOff[7] = {0, 3, 6, 10, 11, 14, 23};   // column offsets per section
+__constant__ int kSecCols[6] = {3, 3, 4, 1, 3, 9};
+
+struct Src {
+  const double* base;
+  long long rows;
+  long long idx;
+};
+
+GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
+  const long long n_mem = (long long)p.n_upper + p.n_pass;
+  Src s;
+  if (r < p.n_upper) {
+    node = p.upper_ids[r];
+    s = {p.master, p.capacity, node};
+  } else if (r < n_mem) {
+    node = p.pass_ids[r - p.n_upper];
+    s = {p.master, p.capacity, node};
+  } else {
+    const long long k = r - n_mem;
+    const int j = p.sel_seg[k];
+    node = p.sel_node[k];
+    s = {reinterpret_cast<const double*>(p.seg_block[j]), p.seg_rows[j], p.sel_pos[k]};
+  }
+  return s;
+}
+
+// One warp per row: lanes 0..22 each move one of the 23 attribute values.
+__global__ void gather_rows_kernel(glod_gather_plan p, long long R, double* __restrict__ out,
+                                   int* __restrict__ row_node) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= R) return;
+  int node;
+  const Src s = row_source(p, gw, node);
+  if (lane < 23) {
+    int sec = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) sec += lane >= kSecOff[k];
+    const int col = lane - kSecOff[sec], cols = kSecCols[sec];
+    out[kSecOff[sec] * R + gw * cols + col] = s.base[kSecOff[sec] * s.rows + s.idx * cols + col];
+  }
+  if (lane == 0 && row_node) row_node[gw] = node;
+}
+
+__global__ void scatter_back_kernel(glod_gather_plan p, long long n_sel) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= n_sel || lane >= 23) return;
+  const int j = p.sel_seg[gw];
+  double* blk = reinterpret_cast<double*>(p.seg_block[j]);
+  const long long P = p.seg_rows[j], pos = p.sel_pos[gw], node = p.sel_node[gw];
+  int sec = 0;
+#pragma unroll
+  for (int k = 1; k < 6; ++k) sec += lane >= kSecOff[k];
+  const int col = lane - kSecOff[sec], cols = kSecCols[sec];
+  blk[kSecOff[sec] * P + pos * cols + col] = p.master[kSecOff[sec] * p.capacity + node * cols + col];
+}
+
+__global__ void f32_to_f64_kernel(const float4* __restrict__ in, double4* __restrict__ out, long long n4) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = in[i];
+    out[i] = make_double4(v.x, v.y, v.z, v.w);
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double4* __restrict__ in, float4* __restrict__ out, long long n4) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const double4 v = in[i];
+    out[i] = make_float4(float(v.x), float(v.y), float(v.z), float(v.w));
+  }
+}
+
+__global__ void tail_f32_to_f64(const float* in, double* out, long long from, long long n) {
+  const long long i = from + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+__global__ void tail_f64_to_f32(const double* in, float* out, long long from, long long n) {
+  const long long i = from + threadIdx.x;
+  if (i < n) out[i] = float(in[i]);
+}
+
+int grid_for(long long n, int tb) {
+  long long g = (n + tb - 1) / tb;
+  return int(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
+}
+
+}  // namespace
+
+cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
+                          cudaStream_t st) {
+  if (R <= 0) return cudaSuccess;
+  const int TB = 256;
+  gather_rows_kernel<<<int((R * 32 + TB - 1) / TB), TB, 0, st>>>(p, R, out, row_node);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st) {
+  if (p.n_sel <= 0) return cudaSuccess;
+  const int TB = 256;
+  scatter_back_kernel<<<int((p.n_sel * 32 + TB - 1) / TB), TB, 0, st>>>(p, p.n_sel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const long long n4 = n / 4;
+  const int TB = 256;
+  if (to_f64) {
+    if (n4) f32_to_f64_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const float4*)in, (double4*)out, n4);
+    if (n % 4) tail_f32_to_f64<<<1, 4, 0, st>>>((const float*)in, (double*)out, n4 * 4, n);
+  } else {
+    if (n4) f64_to_f32_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const double4*)in, (float4*)out, n4);
+    if (n % 4) tail_f64_to_f32<<<1, 4, 0, st>>>((const double*)in, (float*)out, n4 * 4, n);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace glod

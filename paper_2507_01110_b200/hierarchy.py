@@ -147,12 +147,37 @@ def _rotmat_to_quat_t(m: torch.Tensor) -> torch.Tensor:
     return q / torch.linalg.norm(q, dim=1, keepdim=True)
 
 
-def _eigh_batched(cov: torch.Tensor, chunk: int = 1 << 15):
-    # cusolver's batched syev rejects very large batches; chunk them
-    if cov.shape[0] <= chunk:
-        return torch.linalg.eigh(cov)
-    parts = [torch.linalg.eigh(cov[i:i + chunk]) for i in range(0, cov.shape[0], chunk)]
-    return torch.cat([p[0] for p in parts]), torch.cat([p[1] for p in parts])
+def _eigh_batched(cov: torch.Tensor, sweeps: int = 8):
+    """Symmetric 3x3 eigen-decomposition by cyclic Jacobi rotations,
+    vectorised over the batch (cusolver's batched syev rejects large
+    batches).  Returns ascending eigenvalues and column eigenvectors like
+    torch.linalg.eigh."""
+    A = cov.clone()
+    n = A.shape[0]
+    V = torch.eye(3, dtype=A.dtype, device=A.device).expand(n, 3, 3).clone()
+    for _ in range(sweeps):
+        for p, q in ((0, 1), (0, 2), (1, 2)):
+            apq = A[:, p, q]
+            app, aqq = A[:, p, p], A[:, q, q]
+            nz = apq.abs() > 1e-300
+            tau = (aqq - app) / torch.where(nz, 2.0 * apq, torch.ones_like(apq))
+            t = torch.sign(tau) / (tau.abs() + torch.sqrt(1.0 + tau * tau))
+            t = torch.where(tau == 0, torch.ones_like(t), t)
+            t = torch.where(nz, t, torch.zeros_like(t))
+            c = 1.0 / torch.sqrt(1.0 + t * t)
+            s_ = t * c
+            J = torch.eye(3, dtype=A.dtype, device=A.device).expand(n, 3, 3).clone()
+            J[:, p, p] = c
+            J[:, q, q] = c
+            J[:, p, q] = s_
+            J[:, q, p] = -s_
+            A = J.transpose(1, 2) @ A @ J
+            V = V @ J
+    vals = torch.diagonal(A, dim1=1, dim2=2)
+    order = torch.argsort(vals, dim=1)
+    vals = vals.gather(1, order)
+    vecs = V.gather(2, order[:, None, :].expand(-1, 3, -1))
+    return vals, vecs
 
 
 def _merge_level(A: dict, dst, a, b):

@@ -1,0 +1,140 @@
+"""Out-of-core scene store in pinned host DRAM.
+
+Mirrors the reference store's data model (store.py:143-333): attributes as
+six little-endian f32 sections in *slot* order — every non-SPT node first
+(ascending id), then each SPT's records in record order — so an SPT cut
+prefix is one contiguous range per section.  Where the reference reads
+prefixes from a file/memory backing, this store keeps the sections in
+page-locked host memory and moves prefixes to HBM with cudaMemcpyAsync
+(6 contiguous ranges per prefix, store.py:304-312); write-back is the
+reverse copy.  Byte counters follow the reference exactly
+(`attribute_bytes_read += prefix_len · 92`, store.py:311).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .core import BYTES_PER_GAUSSIAN_F32, SECTIONS, AttributeArrays
+
+
+class NotFoundError(KeyError):
+    pass
+
+
+class InvalidBlockError(ValueError):
+    pass
+
+
+@dataclass
+class AttributeBlock:
+    """Attributes of an SPT record prefix, in record order (store.py:130-140).
+    `attrs` is an AttributeArrays (host) or a packed device tensor."""
+
+    spt_id: int
+    prefix_len: int
+    attrs: object
+
+    def __post_init__(self):
+        if isinstance(self.attrs, AttributeArrays) and len(self.attrs) != self.prefix_len:
+            raise InvalidBlockError("block arrays do not match prefix_len")
+
+
+def slot_order(h, hspt) -> np.ndarray:
+    """slot → node (store.py:143-154)."""
+    flat = hspt.flat_records()
+    in_spt = np.zeros(h.capacity, dtype=bool)
+    in_spt[flat["nodes"]] = True
+    alive = np.ones(h.capacity, dtype=bool)
+    if h.free:
+        alive[np.asarray(h.free, dtype=np.int64)] = False
+    head = np.nonzero(alive & ~in_spt)[0]
+    return np.concatenate([head, flat["nodes"]]).astype(np.int64)
+
+
+class HostStore:
+    """Pinned host store + per-SPT directory, built from (hierarchy, hspt)."""
+
+    bytes_per_gaussian = BYTES_PER_GAUSSIAN_F32
+
+    def __init__(self, h, hspt, pin: bool = True):
+        flat = hspt.flat_records()
+        self.slot_to_node = slot_order(h, hspt)
+        self.nslots = int(self.slot_to_node.size)
+        self.record_offset = flat["offset"].astype(np.int64)
+        self.record_count = flat["count"].astype(np.int64)
+        self.total_records = int(self.record_count.sum())
+        pin = pin and torch.cuda.is_available()
+        self.sections = []
+        for name, cols in SECTIONS:
+            arr = np.asarray(getattr(h.attrs, name))[self.slot_to_node].astype(np.float32)
+            t = torch.from_numpy(np.ascontiguousarray(arr.reshape(self.nslots, cols)))
+            self.sections.append(t.pin_memory() if pin else t)
+        self.attribute_bytes_read = 0
+
+    # -- directory ----------------------------------------------------------
+    def _check(self, spt_id: int):
+        if spt_id < 0 or spt_id >= self.record_count.size:
+            raise NotFoundError(f"unknown spt_id {spt_id}")
+
+    def spt_slot_start(self, spt_id: int) -> int:
+        self._check(spt_id)
+        return self.nslots - self.total_records + int(self.record_offset[spt_id])
+
+    # -- host (drop-in) API -------------------------------------------------
+    def load_spt_prefix(self, spt_id: int, prefix_len: int) -> AttributeBlock:
+        self._check(spt_id)
+        if prefix_len > int(self.record_count[spt_id]):
+            raise InvalidBlockError(f"prefix {prefix_len} exceeds record count "
+                                    f"{int(self.record_count[spt_id])}")
+        s = self.spt_slot_start(spt_id)
+        parts = []
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            a = sec[s:s + prefix_len].numpy().copy()
+            parts.append(a if cols > 1 else a[:, 0])
+        self.attribute_bytes_read += prefix_len * self.bytes_per_gaussian
+        return AttributeBlock(spt_id, int(prefix_len), AttributeArrays(*parts))
+
+    def write_back(self, block: AttributeBlock) -> None:
+        self._check(block.spt_id)
+        if block.prefix_len > int(self.record_count[block.spt_id]):
+            raise InvalidBlockError("block longer than the SPT")
+        if not isinstance(block.attrs, AttributeArrays):
+            raise InvalidBlockError("host write_back needs an AttributeArrays block")
+        s = self.spt_slot_start(block.spt_id)
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            v = np.asarray(getattr(block.attrs, name), dtype=np.float32).reshape(block.prefix_len, cols)
+            sec[s:s + block.prefix_len] = torch.from_numpy(v)
+
+    # -- device path ----------------------------------------------------------
+    def prefix_to_device(self, spt_id: int, prefix_len: int, out_f32: torch.Tensor) -> None:
+        """Six async H2D copies of the prefix into a packed f32 staging block
+        (section-major, prefix_len rows).  Counts bytes like the reference."""
+        s = self.spt_slot_start(spt_id)
+        P = int(prefix_len)
+        off = 0
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            out_f32[off:off + cols * P].view(P, cols).copy_(sec[s:s + P], non_blocking=True)
+            off += cols * P
+        self.attribute_bytes_read += P * self.bytes_per_gaussian
+
+    def device_to_store(self, spt_id: int, prefix_len: int, src_f32: torch.Tensor) -> None:
+        """Async D2H write-back of a packed f32 block (store.py:323-333)."""
+        s = self.spt_slot_start(spt_id)
+        P = int(prefix_len)
+        off = 0
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            sec[s:s + P].copy_(src_f32[off:off + cols * P].view(P, cols), non_blocking=True)
+            off += cols * P
+
+    def memory_report(self, gaussian_count: int | None = None) -> dict:
+        """store.py:395-411 accounting (92 B attrs, 184 B optimiser, 12 B SPT)."""
+        n = self.nslots if gaussian_count is None else gaussian_count
+        attr = self.bytes_per_gaussian
+        return {"attribute_bytes_per_gaussian": attr, "optimizer_bytes_per_gaussian": 2 * attr,
+                "spt_metadata_bytes_per_gaussian": 12, "topology_bytes_per_node": 12,
+                "gaussian_count": int(n), "attribute_total_bytes": int(n) * attr,
+                "optimizer_total_bytes": int(n) * 2 * attr, "spt_metadata_total_bytes": int(n) * 12,
+                "training_bytes_per_gaussian": attr + 2 * attr + 12 + 12}

@@ -1,0 +1,254 @@
+"""Device-resident training step (mirrors trainer.train_step, trainer.py:312-378).
+
+Layout in HBM (per scene):
+  params, m, v   packed f64 attribute blocks of `capacity` rows — the
+                 authoritative `h.attrs` and the ADAM moments
+                 (OptimizerState, trainer.py:93-124); 552 B per node
+  step           int64 [capacity] per-node ADAM step counts
+  LoD tables     DeviceLodScene (means/scales are views into `params`)
+  cache blocks   one packed f64 block per resident SPT prefix (DeviceCache)
+Host: the pinned f32 store (HostStore), cache metadata, scheduler RNG.
+
+One step = scheduler draw → LoD select (K2) → cache decisions on the host
+(one small D2H) → H2D of missed prefixes + f32→f64 upcast → SPT compaction
+at the cached distances (K1) → render-row gather (K4) → rasterise (K5-K7)
+→ L1+SSIM (K10) → backward (K8/K9) → ADAM on the touched nodes (K11) →
+cache blocks refreshed from the master rows → periodic flush.  Every
+counter the reference returns is reproduced exactly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cache import CacheConfig, CacheEntry, DeviceCache
+from .core import BYTES_PER_GAUSSIAN_F32, FLOATS_PER_GAUSSIAN, SECTIONS, AttributeArrays, Camera, LodConfig
+from .device import DeviceLodScene
+from .renderer import Rasterizer
+from .scheduler import DEFAULT_K, DEFAULT_RANDOM_EVERY, build_view_graph, next_view
+from .store import HostStore
+
+DEFAULT_LEARNING_RATES = {
+    "means": 1.6e-4,        # × scene extent
+    "scales": 5e-3,
+    "rotations": 1e-3,
+    "opacities": 5e-2,
+    "base_colors": 2.5e-3,
+    "sh_rest": 2.5e-3 / 20.0,
+}
+
+
+class NonFiniteLossError(RuntimeError):
+    pass
+
+
+@dataclass
+class TrainConfig:
+    """Subset of trainer.TrainConfig (trainer.py:64-90) the step uses."""
+
+    total_iterations: int = 1
+    loss_lambda: float = 0.2
+    learning_rates: dict = field(default_factory=lambda: dict(DEFAULT_LEARNING_RATES))
+    lod: LodConfig = field(default_factory=lambda: LodConfig(threshold=1.0))
+    cache: CacheConfig = field(default_factory=lambda: CacheConfig(budget_bytes=64 << 20))
+    scheduler_k: int = DEFAULT_K
+    scheduler_exploration: float | None = None
+    scheduler_random_every: int = DEFAULT_RANDOM_EVERY
+    seed: int = 0
+
+    def __post_init__(self):
+        for name, lr in self.learning_rates.items():
+            if not lr > 0:
+                raise ValueError(f"learning rate for {name} must be > 0")
+
+
+def _packed(t: torch.Tensor, rows: int, name: str) -> torch.Tensor:
+    off = 0
+    for n, cols in SECTIONS:
+        if n == name:
+            return t[off * rows:(off + cols) * rows]
+        off += cols
+    raise KeyError(name)
+
+
+class DeviceScene:
+    """Master params + ADAM state + LoD tables + host store for one HSPT."""
+
+    def __init__(self, h, hspt, device=None):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.cap = h.capacity
+        self.params = torch.from_numpy(h.attrs.packed(np.float64)).to(dev)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step = torch.zeros(self.cap, dtype=torch.int64, device=dev)
+        self.lod = DeviceLodScene(h, hspt, means=_packed(self.params, self.cap, "means"),
+                                  scales=_packed(self.params, self.cap, "scales"))
+        self.store = HostStore(h, hspt)
+        self.hspt = hspt
+
+    def attrs_host(self) -> AttributeArrays:
+        return AttributeArrays.from_packed(self.params.cpu().numpy(), self.cap)
+
+
+class Trainer:
+    """The per-GPU training engine.  `views` is a list of (Camera, target)
+    with targets (h, w, 3) float images (numpy or pinned torch)."""
+
+    def __init__(self, h, hspt, views, cfg: TrainConfig, extent: float, device_targets: bool = True):
+        self.cfg = cfg
+        self.scene = DeviceScene(h, hspt)
+        dev = self.scene.device
+        self.cache = DeviceCache(config=cfg.cache)
+        self.rast = Rasterizer()
+        self.views = [(Camera.from_any(c), t) for c, t in views]
+        pos = np.stack([c.position for c, _ in self.views])
+        self.graph = build_view_graph(pos, k=cfg.scheduler_k, exploration=cfg.scheduler_exploration,
+                                      random_every=cfg.scheduler_random_every)
+        self.rng = np.random.default_rng(cfg.seed)
+        self.current_view = 0
+        self.iteration = 0
+        self.extent = float(extent)
+        lrs = dict(cfg.learning_rates)
+        lrs["means"] = lrs["means"] * self.extent
+        self.lrs = (C.c_double * 6)(*[float(lrs[n]) for n, _ in SECTIONS])
+        # targets: device-resident f32, or pinned host copied every step (e2e)
+        self.device_targets = device_targets
+        self.targets = []
+        for _, t in self.views:
+            tt = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
+            tt = tt.to(torch.float32)
+            self.targets.append(tt.to(dev) if device_targets else tt.pin_memory())
+        S1 = max(self.scene.lod.S, 1)
+        self._h_sel = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()   # counts | ids | prefix
+        self._h_droot = torch.empty(S1, dtype=torch.float64).pin_memory()
+        self._h_dist = torch.empty(S1, dtype=torch.float64).pin_memory()
+        self._h_blk = torch.empty(2 * S1, dtype=torch.int64).pin_memory()       # ptr | rows
+        self._d_dist = torch.empty(S1, dtype=torch.float64, device=dev)
+        self._d_blk = torch.empty(2 * S1, dtype=torch.int64, device=dev)
+        self._h_total = torch.empty(2, dtype=torch.int64).pin_memory()
+        self._h_loss = torch.empty(3, dtype=torch.float64).pin_memory()
+        self._rows = None
+        self._row_node = None
+        self._target_dev = None
+        self.last_stats = {}
+
+    # ------------------------------------------------------------------
+    def _write_back(self, spt_id: int, blk: torch.Tensor, rows: int):
+        f32 = torch.empty(FLOATS_PER_GAUSSIAN * rows, dtype=torch.float32, device=blk.device)
+        _lib.check(_lib.lib().glod_convert(_lib.ptr(blk), _lib.ptr(f32), f32.numel(), 0,
+                                           _lib.stream_ptr()))
+        self.scene.store.device_to_store(spt_id, rows, f32)
+
+    def _load_prefix(self, spt_id: int, P: int) -> torch.Tensor:
+        dev = self.scene.device
+        f32 = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float32, device=dev)
+        self.scene.store.prefix_to_device(spt_id, P, f32)
+        blk = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().glod_convert(_lib.ptr(f32), _lib.ptr(blk), f32.numel(), 1,
+                                           _lib.stream_ptr()))
+        return blk
+
+    def _ensure(self, name, numel, dtype):
+        t = getattr(self, name)
+        if t is None or t.numel() < numel:
+            t = torch.empty(max(numel, 1) + numel // 4, dtype=dtype, device=self.scene.device)
+            setattr(self, name, t)
+        return t
+
+    # ------------------------------------------------------------------
+    def select(self, cam: Camera):
+        """LoD select + one D2H of the per-SPT table (the step's host sync)."""
+        sc = self.scene
+        sel = sc.lod.select(cam, self.cfg.lod, cull=True)
+        S1 = max(sc.lod.S, 1)
+        h = self._h_sel
+        h[:4].copy_(sel.counts, non_blocking=True)
+        h[4:4 + S1].copy_(sel.spt_ids[:S1], non_blocking=True)
+        h[4 + S1:4 + 2 * S1].copy_(sel.prefix_len[:S1], non_blocking=True)
+        self._h_droot.copy_(sel.d_root[:S1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
+        dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
+        return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
+
+    def train_step(self, iteration: int) -> dict:
+        cfg, sc = self.cfg, self.scene
+        self.current_view = next_view(self.graph, self.current_view, iteration, self.rng)
+        cam, _ = self.views[self.current_view]
+        target = self.targets[self.current_view]
+        if not self.device_targets:
+            self._target_dev = target.to(sc.device, non_blocking=True)
+            target = self._target_dev
+        sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam)
+        spt_ids = sc.lod.spt_perm[dev_ids]
+
+        bytes_before = sc.store.attribute_bytes_read
+        hits_before = self.cache.hits
+        loaded = 0
+        entries = []
+        hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
+        S1 = max(sc.lod.S, 1)
+        for j in range(n_sp):
+            sid, d, P = int(spt_ids[j]), float(d_root[j]), int(prefix[j])
+            e = self.cache.lookup(sid, d)
+            if e is None:
+                blk = self._load_prefix(sid, P)
+                loaded += P
+                e = CacheEntry(spt_id=sid, cached_distance=d, prefix_len=P, block=blk,
+                               nbytes=P * BYTES_PER_GAUSSIAN_F32)
+                for esid, eblk in self.cache.insert(e):
+                    self._write_back(esid, eblk, eblk.numel() // FLOATS_PER_GAUSSIAN)
+            entries.append(e)
+            hd[j] = e.cached_distance
+            hb[j] = e.block.data_ptr()
+            hb[S1 + j] = e.prefix_len
+        dev = sc.device
+        if n_sp:
+            self._d_dist.copy_(self._h_dist, non_blocking=True)
+            self._d_blk.copy_(self._h_blk, non_blocking=True)
+        cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist)
+        self._h_total.copy_(cmp.total, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        n_sel = int(self._h_total[0])
+        n_mem = n_up + n_pa
+        R = n_mem + n_sel
+        rows = self._ensure("_rows", FLOATS_PER_GAUSSIAN * R, torch.float64)[:FLOATS_PER_GAUSSIAN * R]
+        row_node = self._ensure("_row_node", R, torch.int32)[:max(R, 1)]
+        plan = _lib.GatherPlan(
+            master=_lib.ptr(sc.params), capacity=sc.cap, upper_ids=_lib.ptr(sel.upper),
+            pass_ids=_lib.ptr(sel.passthrough), n_upper=n_up, n_pass=n_pa,
+            sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
+            n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]))
+        L = _lib.lib()
+        st = _lib.stream_ptr()
+        _lib.check(L.glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node), st))
+        image = self.rast.forward(rows, R, cam)
+        value, dimg = self.rast.loss(image, target, cfg.loss_lambda)
+        self._h_loss.copy_(value, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss_value = float(self._h_loss[0])
+        if not np.isfinite(loss_value):
+            raise NonFiniteLossError(f"iteration {iteration}: non-finite loss rendering view "
+                                     f"{self.current_view} with {R} gaussians")
+        grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
+        _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v), _lib.ptr(sc.step),
+                                    sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs, st))
+        _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
+        for e in entries:
+            e.dirty = True
+        for esid, eblk in self.cache.tick_and_maybe_flush(iteration):
+            self._write_back(esid, eblk, eblk.numel() // FLOATS_PER_GAUSSIAN)
+        self.iteration = iteration
+        self.last_stats = {"n_upper": n_up, "n_pass": n_pa, "n_spt": n_sp,
+                           "prefix_total": int(prefix.sum()) if n_sp else 0,
+                           "n_instances": self.rast.stats()["n_instances"]}
+        self._last_grads = grads
+        return {"iteration": iteration, "view": self.current_view, "loss": loss_value,
+                "gaussians_rendered": int(R), "gaussians_loaded_from_store": int(loaded),
+                "cache_hits": int(self.cache.hits - hits_before),
+                "bytes_streamed": int(sc.store.attribute_bytes_read - bytes_before)}
