@@ -1,0 +1,134 @@
+"""GPU train_step parity against the oracle's restatement of
+trainer.train_step (store + device-cache semantics included).
+
+Each GPU step is checked from an identical state: the oracle is re-synced
+from a snapshot of the GPU state (params, moments, step counts, pinned
+store, cache entries and blocks) taken just before the step.  Checked:
+scheduled view, every counter (exact), render-set size (exact), loss
+(1e-5 relative), per-row gradients (1e-3 relative, see test_render_gpu),
+and the post-step parameters (ADAM: tight except where a near-zero
+gradient's sign is ambiguous — there the update may differ by ≤ 2·lr).
+"""
+from __future__ import annotations
+
+from collections import OrderedDict
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import glod_oracle as O  # noqa: E402
+from oracle.train_oracle import OracleTrainer  # noqa: E402
+from paper_2507_01110_b200.cache import CacheConfig  # noqa: E402
+from paper_2507_01110_b200.core import SECTIONS, AttributeArrays  # noqa: E402
+from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene, orbit_views, scene_extent  # noqa: E402
+from paper_2507_01110_b200.trainer import TrainConfig, Trainer  # noqa: E402
+
+from .test_render_gpu import assert_grads_close  # noqa: E402
+
+NAMES = [n for n, _ in SECTIONS]
+
+
+def _dict(a: AttributeArrays):
+    return {k: np.array(getattr(a, k), copy=True) for k in NAMES}
+
+
+def snapshot(tr: Trainer):
+    torch.cuda.synchronize()
+    sc = tr.scene
+    cap = sc.cap
+    snap = {"P": _dict(AttributeArrays.from_packed(sc.params.cpu().numpy(), cap)),
+            "M": _dict(AttributeArrays.from_packed(sc.m.cpu().numpy(), cap)),
+            "V": _dict(AttributeArrays.from_packed(sc.v.cpu().numpy(), cap)),
+            "step": sc.step.cpu().numpy().copy(),
+            "store": [s.numpy().copy() for s in sc.store.sections],
+            "cache": OrderedDict(), "resident": tr.cache.resident_bytes}
+    for sid, e in tr.cache.entries.items():
+        blk = _dict(AttributeArrays.from_packed(e.block.cpu().numpy(), e.prefix_len))
+        snap["cache"][sid] = [e.cached_distance, e.prefix_len, blk, e.dirty]
+    return snap
+
+
+def restore(orc: OracleTrainer, snap):
+    orc.P = {k: v.copy() for k, v in snap["P"].items()}
+    orc.M = {k: v.copy() for k, v in snap["M"].items()}
+    orc.V = {k: v.copy() for k, v in snap["V"].items()}
+    orc.step = snap["step"].copy()
+    orc.store = [s.copy() for s in snap["store"]]
+    orc.cache = OrderedDict((k, [e[0], e[1], {n: a.copy() for n, a in e[2].items()}, e[3]])
+                            for k, e in snap["cache"].items())
+    orc.resident = snap["resident"]
+
+
+def make_case(n_leaves=6000, res=(96, 64), n_views=10, budget_frac=0.35, seed=3):
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=n_leaves, spt_leaves=256, seed=seed,
+                                          pass_fraction=0.1))
+    E = scene_extent(n_leaves)
+    cams = orbit_views(n_views, 1.5 * E, 0.6 * E, resolution=res, focal=(70.0, 70.0), seed=seed,
+                       jitter=0.2)
+    rng = np.random.default_rng(seed)
+    targets = [np.clip(rng.normal(0.5, 0.2, (res[1], res[0], 3)), 0, 1) for _ in cams]
+    budget = int(budget_frac * hs.flat_records()["nodes"].size * 92)
+    tcfg = TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=budget, flush_interval=7),
+                       scheduler_k=4, seed=seed)
+    tr = Trainer(h, hs, list(zip(cams, targets)), tcfg, extent=2 * E)
+    flat = hs.flat_records()
+    kind = np.full(h.capacity, -1, np.int32)
+    kind[flat["roots"]] = np.arange(flat["roots"].size)
+    kind[hs.passthrough_roots] = -2
+    st = tr.scene.store
+    lrs = dict(tcfg.learning_rates)
+    lrs["means"] *= 2 * E
+    orc = OracleTrainer(_dict(h.attrs), h.children, h.root, kind, flat,
+                        [s.numpy() for s in st.sections],
+                        [st.spt_slot_start(i) for i in range(len(hs.spts))],
+                        [(O.Cam.of(c), t) for c, t in zip(cams, targets)], cfg.threshold,
+                        cfg.metric_code, budget, flush_interval=7, lrs=lrs)
+    return tr, orc, lrs
+
+
+def test_train_steps_match_oracle():
+    tr, orc, lrs = make_case()
+    saw_miss = saw_hit = saw_evict = False
+    for it in range(1, 13):
+        snap = snapshot(tr)
+        got = tr.train_step(it)
+        restore(orc, snap)
+        want, extra = orc.step(it, view=got["view"])
+        for k in ("view", "gaussians_rendered", "gaussians_loaded_from_store", "cache_hits",
+                  "bytes_streamed"):
+            assert got[k] == want[k], (it, k, got[k], want[k])
+        assert abs(got["loss"] - want["loss"]) <= 1e-5 * abs(want["loss"]), it
+        R = got["gaussians_rendered"]
+        g = AttributeArrays.from_packed(tr._last_grads[:23 * R].cpu().numpy(), R)
+        assert_grads_close(g, extra["grads"], where=f"step {it}")
+        post = AttributeArrays.from_packed(tr.scene.params.cpu().numpy(), tr.scene.cap)
+        for k, (name, _) in enumerate(SECTIONS):
+            a, b = getattr(post, name), orc.P[name]
+            d = np.abs(a - b)
+            lr = lrs[name] if name not in ("scales", "opacities") else 1.0
+            assert np.all(d <= 2.5 * lr * np.maximum(1.0, np.abs(b)) + 1e-12), (it, name, d.max())
+            assert np.mean(d <= 1e-7 * np.maximum(1.0, np.abs(b))) > 0.98, (it, name)
+        saw_miss |= got["gaussians_loaded_from_store"] > 0
+        saw_hit |= got["cache_hits"] > 0
+        saw_evict |= tr.cache.resident_bytes < sum(e.nbytes for e in tr.cache.entries.values()) + 1
+    assert saw_miss and saw_hit
+
+
+def test_warm_cache_zero_loads():
+    """test_trainer.py:154-168: revisiting the same view with a warm cache
+    loads nothing from the store."""
+    tr, _, _ = make_case(budget_frac=2.0)
+    tr.graph.random_every = 1   # uniform draws; then pin the view below
+    first = None
+    for it in range(1, 4):
+        tr.rng = np.random.default_rng(0)
+        r = tr.train_step(it * 1)
+        if first is None:
+            first = r
+        else:
+            assert r["view"] == first["view"]
+            assert r["gaussians_loaded_from_store"] == 0
+            assert r["bytes_streamed"] == 0
