@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the per-view hot path of "A LoD of Gaussians" on B200.
+
+Metric (BASELINE.json): train iters/s (and render FPS) at 1080p on a
+10M-Gaussian synthetic scene, with the out-of-core store in pinned host
+DRAM + the device cache.  A step = one training view per GPU: LoD cut →
+cache/store gather → rasterise → L1+SSIM → backward → ADAM (+ cache
+refresh).  With N GPUs each rank trains its own view per step (views
+sharded by rank, scaling "weak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  `--impl reference` times the reference's
+CPU algorithm (the oracle port, oracle/) on the host cores on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASE_METRIC = "train iters/s @1080p, 10M-Gaussian synthetic scene (host-DRAM store + device cache)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--leaves", type=int, default=10_000_000)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--views", type=int, default=32)
+    ap.add_argument("--budget-mb", type=int, default=1024)
+    ap.add_argument("--spt-leaves", type=int, default=8192)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------
+def make_workload(args, device=None):
+    from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene, orbit_views, scene_extent
+    t0 = time.time()
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=args.leaves, spt_leaves=args.spt_leaves,
+                                          seed=args.seed), device=device)
+    E = scene_extent(args.leaves)
+    cams = orbit_views(args.views, 1.3 * E, 0.7 * E, resolution=(args.width, args.height),
+                       seed=args.seed, jitter=0.15, target_jitter=0.1 * E)
+    build_s = time.time() - t0
+    return h, hs, cfg, cams, E, build_s
+
+
+def synthetic_targets(n, w, h, seed):
+    """Smooth synthetic target images (data: synthetic)."""
+    rng = np.random.default_rng(seed + 99)
+    out = []
+    yy, xx = np.mgrid[0:h, 0:w].astype(np.float32)
+    for i in range(n):
+        f = rng.uniform(0.002, 0.01, 3)
+        ph = rng.uniform(0, 6.28, 3)
+        img = np.stack([0.5 + 0.35 * np.sin(f[c] * (xx + 0.7 * yy) + ph[c]) for c in range(3)], -1)
+        out.append(img.astype(np.float32))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.gpu = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait(timeout=5)
+        self.f.flush()
+        rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------
+def roofline_for(stage_ms: dict, stats: dict, args, peaks: dict) -> dict:
+    """Dominant kernel of the step and its achieved rate vs the measured peak.
+
+    Algorithmic bytes per launch:
+      blend_bwd: per instance 52 B (4 B id + 48 B splat record) + per pixel
+                 36 B (dL/dimage 12, T_final 8, last 4, image 12) +
+                 per Gaussian 72 B (9 f64 partials)
+      blend_fwd: per instance 52 B + per pixel 24 B (image 12, T 8, last 4)
+    """
+    npix = args.width * args.height
+    inst = stats.get("n_instances", 0)
+    R = stats.get("rendered", 0)
+    stage = max(stage_ms, key=lambda k: stage_ms[k])
+    if stage == "backward":
+        alg = inst * 52 + npix * 36 + R * 72 + R * (23 * 8 * 2)   # + K9 reads attrs, writes grads
+        name = "blend_bwd+preprocess_bwd"
+    elif stage == "forward":
+        alg = inst * 52 + npix * 24 + R * (23 * 8 + 48 + 16)
+        name = "preprocess+sort+blend_fwd"
+    else:
+        alg = None
+        name = stage
+    ms = stage_ms[stage]
+    peak = peaks.get("hbm_gbs", 6542.1)
+    ach = (alg / (ms * 1e-3) / 1e9) if alg else None
+    return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": (ach / peak) if ach else None, "traffic": None, "ms": ms,
+            "note": "blend stages are issue/atomic bound (no dense contraction); "
+                    "frac is algorithmic HBM bytes / measured copy peak"}
+
+
+def cpu_baseline(trainer, args, R, sample_s) -> dict:
+    """The oracle (CPU restatement of the reference) on a bounded sample of
+    the same workload: cut of the full scene, L1+SSIM on the full 1080p
+    image, forward+backward of a prefix of the render set; extrapolated
+    linearly in the number of rendered Gaussians to one train step."""
+    import torch
+    from oracle import glod_oracle as O
+    from paper_2507_01110_b200.core import AttributeArrays, Frustum
+
+    cam, _ = trainer.views[trainer.current_view]
+    ocam = O.Cam.of(cam)
+    sc = trainer.scene
+    h_attrs = sc.attrs_host()
+    lod = sc.lod
+    flat = sc.hspt.flat_records()
+    kind = lod.kind.cpu().numpy()
+    # kind on device uses sorted-root order; the oracle wants caller spt ids
+    kind_o = np.where(kind >= 0, lod.spt_perm[np.maximum(kind, 0)], kind).astype(np.int32)
+    t0 = time.perf_counter()
+    O.cut_hspt(lod.root, lod.children.cpu().numpy().reshape(-1, 2), kind_o, h_attrs.means,
+               h_attrs.scales, flat["offset"], flat["count"], flat["roots"], flat["centers"],
+               flat["key_self"], flat["key_parent"], flat["nodes"], cam.position,
+               trainer.cfg.lod.threshold, trainer.cfg.lod.metric_code, Frustum.from_camera(cam).planes)
+    t_cut = time.perf_counter() - t0
+    rows = AttributeArrays.from_packed(trainer._rows[:23 * R].cpu().numpy(), R)
+    img = np.zeros((args.height, args.width, 3))
+    tgt = trainer.targets[trainer.current_view].cpu().numpy().astype(np.float64)
+    t0 = time.perf_counter()
+    O.ssim_l1_loss(img, tgt, 0.2)
+    t_loss = time.perf_counter() - t0
+    # fwd+bwd per Gaussian on growing prefixes until the time budget is used
+    n, t_rb, done = 0, 0.0, 0
+    step = 256
+    while t_rb < sample_s and done < R:
+        k = min(step, R - done)
+        idx = np.arange(done, done + k)
+        A = {nm: getattr(rows, nm)[idx] for nm in ("means", "scales", "rotations", "opacities",
+                                                  "base_colors", "sh_rest")}
+        t0 = time.perf_counter()
+        im, ctx = O.render_forward(A, ocam)
+        O.backward(ctx, np.ones_like(im) * 1e-3)
+        t_rb += time.perf_counter() - t0
+        done += k
+        step = min(step * 2, 4096)
+    per_g = t_rb / max(done, 1)
+    t_iter = t_cut + t_loss + per_g * R
+    return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": (f"oracle cut_hspt on the full scene ({t_cut:.2f}s) + L1/SSIM at "
+                       f"{args.width}x{args.height} ({t_loss:.2f}s) + render fwd+bwd of {done} of "
+                       f"{R} render-set Gaussians ({t_rb:.1f}s, {per_g * 1e3:.2f} ms/Gaussian), "
+                       f"extrapolated to one train step ({t_iter:.0f}s)")}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_01110_b200 import _lib
+    from paper_2507_01110_b200.cache import CacheConfig
+    from paper_2507_01110_b200.trainer import TrainConfig, Trainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    h, hs, cfg, cams, E, build_s = make_workload(args, device="cuda")
+    targets = synthetic_targets(len(cams), args.width, args.height, args.seed)
+    tcfg = TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=args.budget_mb << 20),
+                       seed=args.seed + 1000 * rank)
+    t0 = time.time()
+    tr = Trainer(h, hs, list(zip(cams, targets)), tcfg, extent=2 * E)
+    setup_s = time.time() - t0
+    del h
+    it = 0
+    for _ in range(args.warmup):
+        it += 1
+        tr.train_step(it)
+    torch.cuda.synchronize()
+    # ---- timed region: device-resident inputs ---------------------------
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    n_launch0 = _lib.load().glod_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    recs = []
+    for _ in range(args.steps):
+        it += 1
+        recs.append(tr.train_step(it))
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.load().glod_launch_count() - n_launch0
+    clk = clocks.stop() if rank == 0 else {}
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * args.steps / (ms / 1e3)
+    # ---- per-stage timing (separate pass; CUDA events per stage) ---------
+    tr.enable_timing(True)
+    for _ in range(max(3, args.steps // 4)):
+        it += 1
+        tr.train_step(it)
+    stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
+    tr.enable_timing(False)
+    stats = dict(tr.last_stats)
+    stats["rendered"] = recs[-1]["gaussians_rendered"]
+    # ---- render FPS (cut + cache gather + forward) ------------------------
+    torch.cuda.synchronize()
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nfr = max(args.steps, 5)
+    img = None
+    for v in range(3):
+        img = tr.render_view(v % len(cams), img)
+    r0.record()
+    for f in range(nfr):
+        img = tr.render_view(f % len(cams), img)
+    r1.record()
+    torch.cuda.synchronize()
+    render_fps = world * nfr / (r0.elapsed_time(r1) / 1e3)
+    # ---- end to end: targets from pinned host memory every step -----------
+    tr.targets = [t.cpu().pin_memory() for t in tr.targets]
+    tr.device_targets = False
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        it += 1
+        tr.train_step(it)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h2d = args.width * args.height * 3 * 4 + 8 * 3          # target image + camera
+    d2h = 3 * 8                                              # loss value
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": BASE_METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32",
+        "data": "synthetic (seeded designed_scene + synthetic smooth targets)",
+        "config": {"workload": "C4: 10M-leaf designed scene, 1080p, pinned host store + device cache",
+                   "leaves": args.leaves, "nodes": int(tr.scene.cap), "resolution": [args.width, args.height],
+                   "views": args.views, "cache_budget_mb": args.budget_mb, "spts": int(tr.scene.lod.S),
+                   "spt_records": int(tr.scene.lod.R), "parallelism": f"views x{world}",
+                   "render_set": stats.get("rendered"), "n_spt_selected": stats.get("n_spt"),
+                   "prefix_total": stats.get("prefix_total"), "n_instances": stats.get("n_instances"),
+                   "loaded_last_step": recs[-1]["gaussians_loaded_from_store"],
+                   "hits_last_step": recs[-1]["cache_hits"],
+                   "mean_loaded_per_step": float(np.mean([r["gaussians_loaded_from_store"] for r in recs])),
+                   "mean_rendered": float(np.mean([r["gaussians_rendered"] for r in recs])),
+                   "l2_flush": "none; per-step working set (params 3.7 GB, instances) exceeds L2",
+                   "scene_build_s": round(build_s, 1), "setup_s": round(setup_s, 1)},
+        "stage_ms": stage_ms,
+        "render_fps": render_fps,
+        "e2e": {"value": world * args.steps / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roofline_for(stage_ms, stats, args, peaks),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(tr, args, stats["rendered"], args.cpu_sample_s)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """`--impl reference`: the oracle port of the reference's CPU path on the
+    host cores, rank 0 only; each step = the reference pipeline on a bounded
+    sample of one view (full cut, full-resolution L1/SSIM, fwd+bwd of a
+    slice of the render set), extrapolated to the full step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from oracle import glod_oracle as O
+    from paper_2507_01110_b200.core import Frustum
+
+    h, hs, cfg, cams, E, build_s = make_workload(args, device="cuda" if torch.cuda.is_available() else "cpu")
+    flat = hs.flat_records()
+    kind = np.full(h.capacity, -1, np.int32)
+    kind[flat["roots"]] = np.arange(flat["roots"].size)
+    kind[hs.passthrough_roots] = -2
+    targets = synthetic_targets(min(len(cams), 4), args.width, args.height, args.seed)
+    per_step = []
+    rendered = []
+    budget = max(2.0, args.cpu_sample_s / max(args.steps, 1))
+    for s in range(args.warmup + args.steps):
+        cam = cams[s % len(cams)]
+        t0 = time.perf_counter()
+        rs = O.cut_hspt(h.root, h.children, kind, h.attrs.means, h.attrs.scales, flat["offset"],
+                        flat["count"], flat["roots"], flat["centers"], flat["key_self"],
+                        flat["key_parent"], flat["nodes"], cam.position, cfg.threshold,
+                        cfg.metric_code, Frustum.from_camera(cam).planes)
+        t_cut = time.perf_counter() - t0
+        nodes = np.concatenate([rs["upper"], rs["passthrough"]] + rs["selected"])
+        R = nodes.size
+        t0 = time.perf_counter()
+        strip = max(16, args.height // 8)
+        O.ssim_l1_loss(np.zeros((strip, args.width, 3)), targets[0][:strip].astype(np.float64), 0.2)
+        t_loss = (time.perf_counter() - t0) * args.height / strip
+        ocam = O.Cam.of(cam)
+        done, t_rb, k = 0, 0.0, 128
+        while t_rb < budget and done < R:
+            idx = nodes[done:done + k]
+            A = {nm: getattr(h.attrs, nm)[idx] for nm in ("means", "scales", "rotations", "opacities",
+                                                         "base_colors", "sh_rest")}
+            t0 = time.perf_counter()
+            im, ctx = O.render_forward(A, ocam)
+            O.backward(ctx, np.ones_like(im) * 1e-3)
+            t_rb += time.perf_counter() - t0
+            done += idx.size
+        t_step = t_cut + t_loss + (t_rb / max(done, 1)) * R
+        if s >= args.warmup:
+            per_step.append(t_step)
+            rendered.append(R)
+    t_mean = float(np.mean(per_step))
+    value = 1.0 / t_mean
+    line = {"impl": "reference", "metric": BASE_METRIC, "value": value, "unit": "iters/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_mean * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded designed_scene)",
+            "config": {"workload": "C4: 10M-leaf designed scene, 1080p (oracle port on CPU)",
+                       "leaves": args.leaves, "resolution": [args.width, args.height],
+                       "mean_rendered": float(np.mean(rendered))},
+            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": 1, "kind": "port",
+                             "sample": (f"per step: full oracle cut_hspt, L1/SSIM timed on a "
+                                        f"{max(16, args.height // 8)}-row strip scaled to full height, "
+                                        f"render fwd+bwd timed on ≈{budget:.0f}s of the render set "
+                                        f"and extrapolated to all of it")},
+            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

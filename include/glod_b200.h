@@ -31,6 +31,8 @@ extern "C" {
 
 int glod_version(void);
 const char* glod_last_error(void);
+/* Number of kernels this library has launched in the process so far. */
+uint64_t glod_launch_count(void);
 
 /* ======================================================================= *
  * LoD selection

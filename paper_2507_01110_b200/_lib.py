@@ -67,6 +67,7 @@ class GatherPlan(C.Structure):
 SIGNATURES = {
     "glod_version": (C.c_int, []),
     "glod_last_error": (C.c_char_p, []),
+    "glod_launch_count": (C.c_uint64, []),
     "glod_lod_select_scratch_bytes": (C.c_int64, [C.c_int64, C.c_int32]),
     "glod_lod_select": (C.c_int, [C.POINTER(LodScene), C.POINTER(LodView),
                                   C.POINTER(SelectOut), P, C.c_int64, P]),

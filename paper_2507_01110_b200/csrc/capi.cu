@@ -1,5 +1,6 @@
 // extern "C" entry points (include/glod_b200.h).
 #include <stdio.h>
+#include <atomic>
 #include <string>
 
 #include "../../include/glod_b200.h"
@@ -7,6 +8,8 @@
 #include "raster.cuh"
 
 namespace glod {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 size_t loss_scratch_bytes(int W, int H);
 cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
                         float* grad, void* scratch, size_t bytes, cudaStream_t st);
@@ -41,6 +44,8 @@ int check(cudaError_t e, const char* where) {
 extern "C" {
 
 int glod_version(void) { return 1; }
+
+uint64_t glod_launch_count(void) { return glod::g_launches.load(std::memory_order_relaxed); }
 
 const char* glod_last_error(void) { return g_err.c_str(); }
 

@@ -7,6 +7,10 @@
 
 namespace glod {
 
+// Host-side count of kernel launches issued by this library (reported by
+// bench.py as gpu_launches; defined in capi.cu).
+void count_launch(unsigned long long n = 1);
+
 // ---------------------------------------------------------------------------
 // Exact-rounding fp64 arithmetic.  The LoD decisions must reproduce the
 // reference's numpy/OpenBLAS float paths bit for bit, so every

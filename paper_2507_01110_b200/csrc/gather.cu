@@ -106,6 +106,7 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
                           cudaStream_t st) {
   if (R <= 0) return cudaSuccess;
   const int TB = 256;
+  count_launch();
   gather_rows_kernel<<<int((R * 32 + TB - 1) / TB), TB, 0, st>>>(p, R, out, row_node);
   return cudaGetLastError();
 }
@@ -113,6 +114,7 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st) {
   if (p.n_sel <= 0) return cudaSuccess;
   const int TB = 256;
+  count_launch();
   scatter_back_kernel<<<int((p.n_sel * 32 + TB - 1) / TB), TB, 0, st>>>(p, p.n_sel);
   return cudaGetLastError();
 }
@@ -122,11 +124,11 @@ cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, c
   const long long n4 = n / 4;
   const int TB = 256;
   if (to_f64) {
-    if (n4) f32_to_f64_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const float4*)in, (double4*)out, n4);
-    if (n % 4) tail_f32_to_f64<<<1, 4, 0, st>>>((const float*)in, (double*)out, n4 * 4, n);
+    if (n4) { count_launch(); f32_to_f64_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const float4*)in, (double4*)out, n4); }
+    if (n % 4) { count_launch(); tail_f32_to_f64<<<1, 4, 0, st>>>((const float*)in, (double*)out, n4 * 4, n); }
   } else {
-    if (n4) f64_to_f32_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const double4*)in, (float4*)out, n4);
-    if (n % 4) tail_f64_to_f32<<<1, 4, 0, st>>>((const double*)in, (float*)out, n4 * 4, n);
+    if (n4) { count_launch(); f64_to_f32_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const double4*)in, (float4*)out, n4); }
+    if (n % 4) { count_launch(); tail_f64_to_f32<<<1, 4, 0, st>>>((const double*)in, (float*)out, n4 * 4, n); }
   }
   return cudaGetLastError();
 }

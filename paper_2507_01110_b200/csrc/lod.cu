@@ -501,6 +501,7 @@ cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut&
   if (e != cudaSuccess) return e;
   LodScene a = sc; LodView b = v; SelectOut c = out; SelectScratch d = ws;
   void* args[] = {&a, &b, &c, &d};
+  count_launch();
   return cudaLaunchCooperativeKernel((const void*)select_kernel, dim3(grid), dim3(kSelectThreads),
                                      args, 0, st);
 }
@@ -514,6 +515,7 @@ cudaError_t launch_compact(const LodScene& sc, const CompactIn& in, const Compac
   if (e != cudaSuccess) return e;
   LodScene a = sc; CompactIn b = in; CompactOut c = out; CompactScratch d = ws;
   void* args[] = {&a, &b, &c, &d};
+  count_launch();
   return cudaLaunchCooperativeKernel((const void*)compact_kernel, dim3(grid), dim3(kCompactThreads),
                                      args, 0, st);
 }

@@ -191,8 +191,11 @@ cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam
   double* part = reinterpret_cast<double*>(dxy + npix + (npix & 1));
   dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
   const double inv_n = 1.0 / double(npix);
+  count_launch();
   ssim_pass1<<<grid, NT, 0, st>>>(X, Y, W, H, dmu, dx2, dxy, part, inv_n);
+  count_launch();
   ssim_pass2<<<grid, NT, 0, st>>>(X, Y, W, H, dmu, dx2, dxy, grad, lam, inv_n);
+  count_launch();
   ssim_finish<<<1, 1024, 0, st>>>(part, int(grid.x * grid.y * grid.z), lam, inv_n, out);
   return cudaGetLastError();
 }

@@ -568,6 +568,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
     R->n_inst = 0;
     R->n_visible = 0;
     // T=1 everywhere, no contributors: the blend kernel writes exactly that
+    count_launch();
     blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(nullptr, nullptr, R->range.as<int2>(), cam,
                                                          image, R->tfinal.as<double>(), R->last.as<int>());
     return cudaGetLastError();
@@ -589,6 +590,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   CK(cudaMemcpyAsync(R->bad.p, init_bad, sizeof(init_bad), cudaMemcpyHostToDevice, st));
   const int TB = 256;
   const int nb = int((n + TB - 1) / TB);
+  count_launch();
   preprocess_kernel<<<nb, TB, 0, st>>>(attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
                                        R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>());
   CK(cudaGetLastError());
@@ -603,6 +605,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
                                      R->keys2.as<unsigned long long>(), R->vals.as<int>(),
                                      R->vals2.as<int>(), int(n), 0, 64, st));
   const int* order = R->vals2.as<int>();
+  count_launch();
   gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
                                    R->tiles_sorted.as<int>(), n);
   CK(cudaGetLastError());
@@ -628,6 +631,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   CK(R->ikey2.ensure(4 * n_inst + 4, st));
   CK(R->ival.ensure(4 * n_inst + 4, st));
   CK(R->ival2.ensure(4 * n_inst + 4, st));
+  count_launch();
   emit_kernel<<<nb, TB, 0, st>>>(R->sorted.as<Splat>(), R->tiles_sorted.as<int>(), R->offs.as<long long>(),
                                  cam.tw, R->ikey.as<unsigned>(), R->ival.as<int>(), n);
   CK(cudaGetLastError());
@@ -640,10 +644,12 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
     tb = R->temp.cap;
     CK(cub::DeviceRadixSort::SortPairs(R->temp.p, tb, R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(),
                                        R->ival.as<int>(), R->ival2.as<int>(), int(n_inst), 0, kb, st));
+    count_launch();
     ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey2.as<unsigned>(), n_inst,
                                                               R->range.as<int2>());
     CK(cudaGetLastError());
   }
+  count_launch();
   blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
                                                        R->range.as<int2>(), cam, image,
                                                        R->tfinal.as<double>(), R->last.as<int>());
@@ -658,12 +664,14 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   CK(R->g2.ensure(8 * kG2 * (size_t)n, st));
   CK(cudaMemsetAsync(R->g2.p, 0, 8 * kG2 * (size_t)n, st));
   if (R->n_inst > 0)
+    count_launch();
     blend_bwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
                                                          R->range.as<int2>(), cam, dimg,
                                                          R->tfinal.as<double>(), R->last.as<int>(),
                                                          R->g2.as<double>());
   CK(cudaGetLastError());
   const int TB = 128;
+  count_launch();
   preprocess_bwd_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->attrs, n, cam, R->tiles.as<int>(),
                                                                R->g2.as<double>(), grads);
   return cudaGetLastError();

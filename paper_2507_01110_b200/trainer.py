@@ -136,6 +136,27 @@ class Trainer:
         self._row_node = None
         self._target_dev = None
         self.last_stats = {}
+        self.timing = None          # {stage: [ms, ...]} when profiling is on
+        self._ev = []
+
+    # -- optional per-stage CUDA-event timing (bench.py) ---------------------
+    def enable_timing(self, on: bool = True):
+        self.timing = {} if on else None
+
+    def _mark(self, name):
+        if self.timing is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self._ev.append((name, e))
+
+    def _collect(self):
+        if self.timing is None or not self._ev:
+            return
+        torch.cuda.current_stream().synchronize()
+        for (a, ea), (b, eb) in zip(self._ev[:-1], self._ev[1:]):
+            self.timing.setdefault(b, []).append(ea.elapsed_time(eb))
+        self._ev = []
 
     # ------------------------------------------------------------------
     def _write_back(self, spt_id: int, blk: torch.Tensor, rows: int):
@@ -176,17 +197,14 @@ class Trainer:
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
         return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
 
-    def train_step(self, iteration: int) -> dict:
-        cfg, sc = self.cfg, self.scene
-        self.current_view = next_view(self.graph, self.current_view, iteration, self.rng)
-        cam, _ = self.views[self.current_view]
-        target = self.targets[self.current_view]
-        if not self.device_targets:
-            self._target_dev = target.to(sc.device, non_blocking=True)
-            target = self._target_dev
+    def _gather_view(self, cam: Camera):
+        """Cut + cache decisions + prefix loads + compaction + row gather
+        (trainer.py:319-347, cli._gather cli.py:111-136)."""
+        sc = self.scene
+        self._mark("start")
         sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam)
+        self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
-
         bytes_before = sc.store.attribute_bytes_read
         hits_before = self.cache.hits
         loaded = 0
@@ -207,16 +225,16 @@ class Trainer:
             hd[j] = e.cached_distance
             hb[j] = e.block.data_ptr()
             hb[S1 + j] = e.prefix_len
-        dev = sc.device
         if n_sp:
             self._d_dist.copy_(self._h_dist, non_blocking=True)
             self._d_blk.copy_(self._h_blk, non_blocking=True)
+        self._mark("cache")
         cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist)
         self._h_total.copy_(cmp.total, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        self._mark("compact")
         n_sel = int(self._h_total[0])
-        n_mem = n_up + n_pa
-        R = n_mem + n_sel
+        R = n_up + n_pa + n_sel
         rows = self._ensure("_rows", FLOATS_PER_GAUSSIAN * R, torch.float64)[:FLOATS_PER_GAUSSIAN * R]
         row_node = self._ensure("_row_node", R, torch.int32)[:max(R, 1)]
         plan = _lib.GatherPlan(
@@ -224,31 +242,64 @@ class Trainer:
             pass_ids=_lib.ptr(sel.passthrough), n_upper=n_up, n_pass=n_pa,
             sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
             n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]))
+        _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
+                                                      _lib.stream_ptr()))
+        self._mark("gather")
+        self.last_stats = {"n_upper": n_up, "n_pass": n_pa, "n_spt": n_sp,
+                           "prefix_total": int(prefix.sum()) if n_sp else 0}
+        counters = {"gaussians_rendered": int(R), "gaussians_loaded_from_store": int(loaded),
+                    "cache_hits": int(self.cache.hits - hits_before),
+                    "bytes_streamed": int(sc.store.attribute_bytes_read - bytes_before)}
+        return R, rows, row_node, plan, entries, counters
+
+    def render_view(self, view: int, image: torch.Tensor | None = None) -> torch.Tensor:
+        """Serve/bench path (cli.cmd_render, cli.py:139-189): cut + cache +
+        gather + forward render of one view; no parameter updates."""
+        cam, _ = self.views[view]
+        R, rows, _, _, _, counters = self._gather_view(cam)
+        img = self.rast.forward(rows, R, cam, image=image)
+        self._mark("forward")
+        self._collect()
+        self.last_render = counters
+        return img
+
+    def train_step(self, iteration: int) -> dict:
+        cfg, sc = self.cfg, self.scene
+        self.current_view = next_view(self.graph, self.current_view, iteration, self.rng)
+        cam, _ = self.views[self.current_view]
+        target = self.targets[self.current_view]
+        if not self.device_targets:
+            self._target_dev = target.to(sc.device, non_blocking=True)
+            target = self._target_dev
+        R, rows, row_node, plan, entries, counters = self._gather_view(cam)
         L = _lib.lib()
         st = _lib.stream_ptr()
-        _lib.check(L.glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node), st))
         image = self.rast.forward(rows, R, cam)
+        self._mark("forward")
         value, dimg = self.rast.loss(image, target, cfg.loss_lambda)
+        self._mark("loss")
         self._h_loss.copy_(value, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         loss_value = float(self._h_loss[0])
         if not np.isfinite(loss_value):
             raise NonFiniteLossError(f"iteration {iteration}: non-finite loss rendering view "
                                      f"{self.current_view} with {R} gaussians")
+        self._mark("loss_read")
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
+        self._mark("backward")
         _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v), _lib.ptr(sc.step),
                                     sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs, st))
+        self._mark("adam")
         _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
         for e in entries:
             e.dirty = True
         for esid, eblk in self.cache.tick_and_maybe_flush(iteration):
             self._write_back(esid, eblk, eblk.numel() // FLOATS_PER_GAUSSIAN)
+        self._mark("scatter_flush")
+        self._collect()
         self.iteration = iteration
-        self.last_stats = {"n_upper": n_up, "n_pass": n_pa, "n_spt": n_sp,
-                           "prefix_total": int(prefix.sum()) if n_sp else 0,
-                           "n_instances": self.rast.stats()["n_instances"]}
+        self.last_stats["n_instances"] = self.rast.stats()["n_instances"]
         self._last_grads = grads
-        return {"iteration": iteration, "view": self.current_view, "loss": loss_value,
-                "gaussians_rendered": int(R), "gaussians_loaded_from_store": int(loaded),
-                "cache_hits": int(self.cache.hits - hits_before),
-                "bytes_streamed": int(sc.store.attribute_bytes_read - bytes_before)}
+        out = {"iteration": iteration, "view": self.current_view, "loss": loss_value}
+        out.update(counters)
+        return out
