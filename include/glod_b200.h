@@ -204,6 +204,34 @@ int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream);
 /* Elementwise f32 -> f64 (to_f64=1) or f64 -> f32 (store write-back). */
 int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* stream);
 
+/* The pinned host store (store.py's slot-ordered f32 sections), as device-
+ * accessible addresses of page-locked host memory (glod_host_device_ptr). */
+typedef struct glod_store_view {
+  const float* section[6];      /* [host-mapped] section k: nslots x cols_k   */
+  int64_t nslots;
+} glod_store_view;
+
+/* One SPT prefix transfer: `rows` slots starting at `slot_start` <-> the
+ * packed f64 cache block `block`.  elem_start = 23 * (rows of all earlier
+ * items): the items of one call tile a flat index space of 23*sum(rows). */
+typedef struct glod_prefix_item {
+  int64_t slot_start;
+  int64_t rows;
+  int64_t elem_start;
+  double* block;                /* [dev]                                       */
+} glod_prefix_item;
+
+/* Device address of page-locked host memory (cudaHostGetDevicePointer). */
+int glod_host_device_ptr(void* host, void** dev);
+/* Scene.load_spt_prefix + astype(f64) for a batch of misses (store.py:314-321,
+ * trainer.py:333-334): one zero-copy kernel, f32 -> f64.  items: [dev]. */
+int glod_store_load_prefixes(const glod_store_view* store, const glod_prefix_item* items,
+                             int32_t n_items, int64_t total_elems, void* stream);
+/* Scene.write_back for a batch of evicted/flushed blocks (store.py:323-333):
+ * f64 -> f32 written straight into the pinned store. */
+int glod_store_write_back(const glod_store_view* store, const glod_prefix_item* items,
+                          int32_t n_items, int64_t total_elems, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,7 +118,7 @@ class OracleTrainer:
                           self.spt["key_self"], self.spt["key_parent"], self.spt["nodes"],
                           cam.position, self.T, self.metric, planes)
 
-    def step(self, iteration, view):
+    def train_step(self, iteration, view):
         """trainer.train_step (trainer.py:312-378) for the scheduled `view`
         (scheduler.next_view is host code shared by both sides); returns
         (counters, extras)."""

@@ -63,6 +63,15 @@ class GatherPlan(C.Structure):
                 ("sel_node", P), ("n_sel", C.c_int64), ("seg_block", P), ("seg_rows", P)]
 
 
+class StoreView(C.Structure):
+    _fields_ = [("section", P * 6), ("nslots", C.c_int64)]
+
+
+class PrefixItem(C.Structure):
+    _fields_ = [("slot_start", C.c_int64), ("rows", C.c_int64), ("elem_start", C.c_int64),
+                ("block", P)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "glod_version": (C.c_int, []),
@@ -86,6 +95,9 @@ SIGNATURES = {
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
     "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
+    "glod_host_device_ptr": (C.c_int, [P, C.POINTER(P)]),
+    "glod_store_load_prefixes": (C.c_int, [C.POINTER(StoreView), P, C.c_int32, C.c_int64, P]),
+    "glod_store_write_back": (C.c_int, [C.POINTER(StoreView), P, C.c_int32, C.c_int64, P]),
 }
 
 _LIB = None

@@ -20,6 +20,8 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
 cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st);
+cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
+                              long long total, int load, cudaStream_t st);
 }  // namespace glod
 
 struct glod_raster {
@@ -166,6 +168,27 @@ int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* str
   if (n > 0 && (!in || !out)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_convert(in, out, n, to_f64, static_cast<cudaStream_t>(stream)),
                "glod_convert");
+}
+
+int glod_host_device_ptr(void* host, void** dev) {
+  if (!host || !dev) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(cudaHostGetDevicePointer(dev, host, 0), "glod_host_device_ptr");
+}
+
+int glod_store_load_prefixes(const glod_store_view* store, const glod_prefix_item* items,
+                             int32_t n_items, int64_t total_elems, void* stream) {
+  if (!store || (n_items > 0 && !items)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_store_xfer(*store, items, n_items, total_elems, 1,
+                                       static_cast<cudaStream_t>(stream)),
+               "glod_store_load_prefixes");
+}
+
+int glod_store_write_back(const glod_store_view* store, const glod_prefix_item* items,
+                          int32_t n_items, int64_t total_elems, void* stream) {
+  if (!store || (n_items > 0 && !items)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_store_xfer(*store, items, n_items, total_elems, 0,
+                                       static_cast<cudaStream_t>(stream)),
+               "glod_store_write_back");
 }
 
 }  // extern "C"

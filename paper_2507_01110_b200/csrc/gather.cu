@@ -95,6 +95,55 @@ __global__ void tail_f64_to_f32(const double* in, float* out, long long from, lo
   if (i < n) out[i] = float(in[i]);
 }
 
+// Zero-copy store transfers: the pinned host store is mapped into the
+// device address space (UVA), so one kernel moves every missed prefix of a
+// step across PCIe with coalesced 128-B requests and converts f32 → f64 on
+// the way (and the reverse for write-back) — no staging buffer and no
+// per-range cudaMemcpy calls (a prefix is 6 ranges; a step has hundreds).
+struct ItemRange {
+  int lo, hi;
+};
+
+GLOD_DEV int find_item(const glod_prefix_item* items, int lo, int hi, long long e) {
+  // last item with elem_start <= e
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (items[mid].elem_start <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <bool kLoad>
+__global__ void __launch_bounds__(256)
+store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items, int n_items,
+                  long long total) {
+  __shared__ int s_lo, s_hi;
+  const long long base = (long long)blockIdx.x * blockDim.x;
+  if (base >= total) return;
+  if (threadIdx.x == 0) {
+    const long long last = min(total, base + (long long)blockDim.x) - 1;
+    s_lo = find_item(items, 0, n_items - 1, base);
+    s_hi = find_item(items, s_lo, n_items - 1, last);
+  }
+  __syncthreads();
+  const long long e = base + threadIdx.x;
+  if (e >= total) return;
+  const int it = s_lo == s_hi ? s_lo : find_item(items, s_lo, s_hi, e);
+  const glod_prefix_item I = items[it];
+  const long long local = e - I.elem_start;
+  const long long rows = I.rows;
+  int sec = 0;
+#pragma unroll
+  for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
+  const long long within = local - kSecOff[sec] * rows;
+  float* host = const_cast<float*>(sv.section[sec]) + I.slot_start * kSecCols[sec] + within;
+  if (kLoad) {
+    I.block[local] = double(*host);
+  } else {
+    *host = float(I.block[local]);
+  }
+}
+
 int grid_for(long long n, int tb) {
   long long g = (n + tb - 1) / tb;
   return int(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -130,6 +179,19 @@ cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, c
     if (n4) { count_launch(); f64_to_f32_kernel<<<grid_for(n4, TB), TB, 0, st>>>((const double4*)in, (float4*)out, n4); }
     if (n % 4) { count_launch(); tail_f64_to_f32<<<1, 4, 0, st>>>((const double*)in, (float*)out, n4 * 4, n); }
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
+                              long long total, int load, cudaStream_t st) {
+  if (n_items <= 0 || total <= 0) return cudaSuccess;
+  const int TB = 256;
+  const long long nb = (total + TB - 1) / TB;
+  count_launch();
+  if (load)
+    store_xfer_kernel<true><<<unsigned(nb), TB, 0, st>>>(sv, items, n_items, total);
+  else
+    store_xfer_kernel<false><<<unsigned(nb), TB, 0, st>>>(sv, items, n_items, total);
   return cudaGetLastError();
 }
 

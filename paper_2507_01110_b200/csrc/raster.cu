@@ -274,13 +274,18 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   }
 }
 
-GLOD_DEV double warp_sum(double v) {
+GLOD_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-__global__ void __launch_bounds__(kBlendThreads)
+// Back-to-front per pixel with the reference's rear accumulator
+// (renderer.py:219-261).  Transmittance is recovered in fp64
+// (T_front = T_after / (1 − α)); dl/dα is formed in fp64 (its two terms
+// cancel); the nine per-Gaussian partials are fp32 per pixel, summed across
+// the warp with shuffles and accumulated into fp64 with one atomic per warp.
+__global__ void __launch_bounds__(kBlendThreads, 3)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
@@ -319,38 +324,37 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
     for (int j = 0; j < cnt; ++j) {
       const int inst = top - 1 - j;
       const Splat& g = sm[j];
-      double c[kG2];
+      float c[kG2];
 #pragma unroll
-      for (int u = 0; u < kG2; ++u) c[u] = 0.0;
+      for (int u = 0; u < kG2; ++u) c[u] = 0.f;
       float dx, dy, q, gs, al;
-      bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
+      const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
       if (hit) {
         const double a = al;
         const double Tf = T / (1.0 - a);                   // T before this splat
         const double w = a * Tf;
-        c[0] = w * gr; c[1] = w * gg; c[2] = w * gb;       // dl_dcolor
+        const float wf = float(w);
+        c[0] = wf * gr; c[1] = wf * gg; c[2] = wf * gb;    // dl_dcolor
         const double gc = double(gr) * g.r + double(gg) * g.g + double(gb) * g.b;
         const double grear = double(gr) * rr + double(gg) * rg_ + double(gb) * rb;
-        const double dla = gc * Tf - grear / (1.0 - a);
+        const float dla = float(gc * Tf - grear / (1.0 - a));
         rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
         T = Tf;
         if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
-          const double G = gs;
-          c[3] = G * dla;
-          const double dq = -0.5 * double(g.opac) * G * dla;
-          const double X = dx, Y = dy;
-          c[4] = -dq * (2.0 * g.ca * X + 2.0 * g.cb * Y);
-          c[5] = -dq * (2.0 * g.cb * X + 2.0 * g.cc * Y);
-          c[6] = dq * X * X;
-          c[7] = dq * X * Y;
-          c[8] = dq * Y * Y;
+          c[3] = gs * dla;
+          const float dq = -0.5f * g.opac * gs * dla;
+          c[4] = -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
+          c[5] = -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
+          c[6] = dq * dx * dx;
+          c[7] = dq * dx * dy;
+          c[8] = dq * dy * dy;
         }
       }
       if (__any_sync(0xffffffffu, hit)) {
 #pragma unroll
         for (int u = 0; u < kG2; ++u) {
-          const double s = warp_sum(c[u]);
-          if (lane == 0 && s != 0.0) atomicAdd(g2 + (long long)kG2 * g.idx + u, s);
+          const float s = warp_sum(c[u]);
+          if (lane == 0 && s != 0.f) atomicAdd(g2 + (long long)kG2 * g.idx + u, double(s));
         }
       }
     }

@@ -129,6 +129,20 @@ class HostStore:
             sec[s:s + P].copy_(src_f32[off:off + cols * P].view(P, cols), non_blocking=True)
             off += cols * P
 
+    def device_view(self):
+        """glod_store_view of the pinned sections (device-mapped addresses)."""
+        if getattr(self, "_view", None) is None:
+            import ctypes as C
+            from . import _lib
+            v = _lib.StoreView()
+            for k, sec in enumerate(self.sections):
+                dp = C.c_void_p()
+                _lib.check(_lib.lib().glod_host_device_ptr(C.c_void_p(sec.data_ptr()), C.byref(dp)))
+                v.section[k] = dp.value
+            v.nslots = self.nslots
+            self._view = v
+        return self._view
+
     def memory_report(self, gaussian_count: int | None = None) -> dict:
         """store.py:395-411 accounting (92 B attrs, 184 B optimiser, 12 B SPT)."""
         n = self.nslots if gaussian_count is None else gaussian_count

@@ -134,6 +134,10 @@ class Trainer:
         self._h_loss = torch.empty(3, dtype=torch.float64).pin_memory()
         self._rows = None
         self._row_node = None
+        self._grads = None
+        self._h_items = self._h_items_wb = None
+        self._d_items = self._d_items_wb = None
+        self._inflight = []
         self._target_dev = None
         self.last_stats = {}
         self.timing = None          # {stage: [ms, ...]} when profiling is on
@@ -159,20 +163,31 @@ class Trainer:
         self._ev = []
 
     # ------------------------------------------------------------------
-    def _write_back(self, spt_id: int, blk: torch.Tensor, rows: int):
-        f32 = torch.empty(FLOATS_PER_GAUSSIAN * rows, dtype=torch.float32, device=blk.device)
-        _lib.check(_lib.lib().glod_convert(_lib.ptr(blk), _lib.ptr(f32), f32.numel(), 0,
-                                           _lib.stream_ptr()))
-        self.scene.store.device_to_store(spt_id, rows, f32)
-
-    def _load_prefix(self, spt_id: int, P: int) -> torch.Tensor:
-        dev = self.scene.device
-        f32 = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float32, device=dev)
-        self.scene.store.prefix_to_device(spt_id, P, f32)
-        blk = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float64, device=dev)
-        _lib.check(_lib.lib().glod_convert(_lib.ptr(f32), _lib.ptr(blk), f32.numel(), 1,
-                                           _lib.stream_ptr()))
-        return blk
+    def _xfer(self, items, load: bool):
+        """One zero-copy kernel for a batch of (slot_start, rows, block)
+        store transfers (loads: f32→f64 into blocks; write-backs: f64→f32)."""
+        if not items:
+            return
+        n = len(items)
+        tab = np.empty((n, 4), dtype=np.int64)
+        off = 0
+        for i, (slot, rows, blk) in enumerate(items):
+            tab[i] = (slot, rows, off, blk.data_ptr())
+            off += FLOATS_PER_GAUSSIAN * rows
+        buf = self._h_items if load else self._h_items_wb
+        if buf is None or buf.shape[0] < n:
+            buf = torch.empty((max(n, 64) * 2, 4), dtype=torch.int64).pin_memory()
+            if load:
+                self._h_items = buf
+            else:
+                self._h_items_wb = buf
+        buf[:n].numpy()[:] = tab
+        dev = self._ensure("_d_items" if load else "_d_items_wb", 4 * n, torch.int64)
+        dev[:4 * n].copy_(buf[:n].reshape(-1), non_blocking=True)
+        fn = _lib.lib().glod_store_load_prefixes if load else _lib.lib().glod_store_write_back
+        _lib.check(fn(C.byref(self.scene.store.device_view()), _lib.ptr(dev), n, off, _lib.stream_ptr()))
+        # keep the pinned table and the blocks alive until the kernel ran
+        self._inflight.append((buf, [b for _, _, b in items]))
 
     def _ensure(self, name, numel, dtype):
         t = getattr(self, name)
@@ -211,20 +226,29 @@ class Trainer:
         entries = []
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         S1 = max(sc.lod.S, 1)
+        store = sc.store
+        loads, wbs = [], []
         for j in range(n_sp):
             sid, d, P = int(spt_ids[j]), float(d_root[j]), int(prefix[j])
             e = self.cache.lookup(sid, d)
             if e is None:
-                blk = self._load_prefix(sid, P)
+                blk = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float64, device=sc.device)
+                loads.append((store.spt_slot_start(sid), P, blk))
+                store.attribute_bytes_read += P * BYTES_PER_GAUSSIAN_F32
                 loaded += P
                 e = CacheEntry(spt_id=sid, cached_distance=d, prefix_len=P, block=blk,
                                nbytes=P * BYTES_PER_GAUSSIAN_F32)
                 for esid, eblk in self.cache.insert(e):
-                    self._write_back(esid, eblk, eblk.numel() // FLOATS_PER_GAUSSIAN)
+                    wbs.append((store.spt_slot_start(esid), eblk.numel() // FLOATS_PER_GAUSSIAN, eblk))
             entries.append(e)
             hd[j] = e.cached_distance
             hb[j] = e.block.data_ptr()
             hb[S1 + j] = e.prefix_len
+        # every load precedes every write-back: a replaced entry's prefix is
+        # re-read from the store before its dirty block is written back
+        # (trainer.py:333-341), other evicted SPTs are not loaded this step
+        self._xfer(loads, load=True)
+        self._xfer(wbs, load=False)
         if n_sp:
             self._d_dist.copy_(self._h_dist, non_blocking=True)
             self._d_blk.copy_(self._h_blk, non_blocking=True)
@@ -293,10 +317,11 @@ class Trainer:
         _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
         for e in entries:
             e.dirty = True
-        for esid, eblk in self.cache.tick_and_maybe_flush(iteration):
-            self._write_back(esid, eblk, eblk.numel() // FLOATS_PER_GAUSSIAN)
+        self._xfer([(sc.store.spt_slot_start(esid), eblk.numel() // FLOATS_PER_GAUSSIAN, eblk)
+                    for esid, eblk in self.cache.tick_and_maybe_flush(iteration)], load=False)
         self._mark("scatter_flush")
         self._collect()
+        self._inflight = []      # the step's syncs above ordered every transfer
         self.iteration = iteration
         self.last_stats["n_instances"] = self.rast.stats()["n_instances"]
         self._last_grads = grads

@@ -96,7 +96,7 @@ def test_train_steps_match_oracle():
         snap = snapshot(tr)
         got = tr.train_step(it)
         restore(orc, snap)
-        want, extra = orc.step(it, view=got["view"])
+        want, extra = orc.train_step(it, view=got["view"])
         for k in ("view", "gaussians_rendered", "gaussians_loaded_from_store", "cache_hits",
                   "bytes_streamed"):
             assert got[k] == want[k], (it, k, got[k], want[k])
