@@ -238,6 +238,9 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("GLOD_PROFILE_RANGE") == "1"     # ncu --profile-from-start off
+    if prof:
+        torch.cuda.cudart().cudaProfilerStart()
     e0.record()
     recs = []
     for _ in range(args.steps):
@@ -245,6 +248,8 @@ def run_ours(args):
         recs.append(tr.train_step(it))
     e1.record()
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)

@@ -240,6 +240,7 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   const int tx = tile % cam.tw, ty = tile / cam.tw;
   const int px = tx * kTileW + int(threadIdx.x % kTileW);
   const int py = ty * kTileH + int(threadIdx.x / kTileW);
+  const int wx0 = tx * kTileW, wy0 = ty * kTileH + 2 * int(threadIdx.x >> 5);
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   double T = 1.0;
@@ -253,8 +254,10 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
     __syncthreads();
     const int cnt = min(kBlendThreads, rg.y - base);
     for (int j = 0; j < cnt && !done; ++j) {
+      const Splat& g = sm[j];
+      if (g.x1 <= wx0 || g.x0 >= wx0 + kTileW || g.y1 <= wy0 || g.y0 >= wy0 + 2) continue;
       float dx, dy, q, gs, al;
-      if (!pixel_alpha(sm[j], px, py, dx, dy, q, gs, al)) continue;
+      if (!pixel_alpha(g, px, py, dx, dy, q, gs, al)) continue;
       const double w = double(al) * T;
       cr += float(w) * sm[j].r;
       cg += float(w) * sm[j].g;
@@ -281,63 +284,74 @@ GLOD_DEV float warp_sum(float v) {
 }
 
 // Back-to-front per pixel with the reference's rear accumulator
-// (renderer.py:219-261).  Transmittance is recovered in fp64
-// (T_front = T_after / (1 − α)); dl/dα is formed in fp64 (its two terms
-// cancel); the nine per-Gaussian partials are fp32 per pixel, summed across
-// the warp with shuffles and accumulated into fp64 with one atomic per warp.
+// (renderer.py:219-261).  Per-pixel math is fp32 (T recovered as
+// T_front = T_after / (1 − α) from the fp64 final transmittance).  The nine
+// per-Gaussian partials are summed per batch in shared memory — a warp
+// shuffle-reduces first when many of its lanes hit the splat, otherwise the
+// hitting lanes add directly — and flushed with one fp64 atomic per
+// (splat, tile, partial).  Warps skip splats whose bbox misses their 16x2
+// pixel strip without evaluating any pixel.
 __global__ void __launch_bounds__(kBlendThreads, 3)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
                  double* __restrict__ g2) {
   __shared__ Splat sm[kBlendThreads];
+  __shared__ float acc[kBlendThreads][kG2];
   __shared__ int max_last;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
   const int px = tx * kTileW + int(threadIdx.x % kTileW);
   const int py = ty * kTileH + int(threadIdx.x / kTileW);
+  const int wx0 = tx * kTileW, wy0 = ty * kTileH + 2 * int(threadIdx.x >> 5);
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   const int lane = threadIdx.x & 31;
-  double T = 1.0;
+  float T = 1.f;
   int last = -1;
   float gr = 0.f, gg = 0.f, gb = 0.f;
   if (inside) {
     const long long pix = (long long)py * cam.w + px;
-    T = t_final[pix];
+    T = float(t_final[pix]);
     last = last_in[pix];
     gr = dimg[3 * pix]; gg = dimg[3 * pix + 1]; gb = dimg[3 * pix + 2];
   }
+  int wlast = last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
   if (threadIdx.x == 0) max_last = -1;
   __syncthreads();
-  atomicMax(&max_last, last);
+  if (lane == 0) atomicMax(&max_last, wlast);
   __syncthreads();
   const int end = max_last + 1;   // nothing beyond the last contributor matters
-  double rr = 0.0, rg_ = 0.0, rb = 0.0;   // rear accumulator Σ_behind w·c
+  float rr = 0.f, rg_ = 0.f, rb = 0.f;   // rear accumulator Σ_behind w·c
   for (int top = end; top > rg.x; top -= kBlendThreads) {
     const int lo = max(rg.x, top - kBlendThreads);
     const int k = top - 1 - int(threadIdx.x);
     __syncthreads();
     if (k >= lo) sm[threadIdx.x] = sorted[ival[k]];
+#pragma unroll
+    for (int u = 0; u < kG2; ++u) acc[threadIdx.x][u] = 0.f;
     __syncthreads();
     const int cnt = top - lo;
     for (int j = 0; j < cnt; ++j) {
       const int inst = top - 1 - j;
       const Splat& g = sm[j];
+      if (inst > wlast || g.x1 <= wx0 || g.x0 >= wx0 + kTileW || g.y1 <= wy0 || g.y0 >= wy0 + 2)
+        continue;                                          // warp-uniform skip
       float c[kG2];
 #pragma unroll
       for (int u = 0; u < kG2; ++u) c[u] = 0.f;
       float dx, dy, q, gs, al;
       const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
       if (hit) {
-        const double a = al;
-        const double Tf = T / (1.0 - a);                   // T before this splat
-        const double w = a * Tf;
-        const float wf = float(w);
-        c[0] = wf * gr; c[1] = wf * gg; c[2] = wf * gb;    // dl_dcolor
-        const double gc = double(gr) * g.r + double(gg) * g.g + double(gb) * g.b;
-        const double grear = double(gr) * rr + double(gg) * rg_ + double(gb) * rb;
-        const float dla = float(gc * Tf - grear / (1.0 - a));
+        const float inv = 1.f / (1.f - al);
+        const float Tf = T * inv;                          // T before this splat
+        const float w = al * Tf;
+        c[0] = w * gr; c[1] = w * gg; c[2] = w * gb;       // dl_dcolor
+        const float gc = gr * g.r + gg * g.g + gb * g.b;
+        const float grear = gr * rr + gg * rg_ + gb * rb;
+        const float dla = gc * Tf - grear * inv;
         rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
         T = Tf;
         if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
@@ -350,12 +364,26 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
           c[8] = dq * dy * dy;
         }
       }
-      if (__any_sync(0xffffffffu, hit)) {
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (bal == 0) continue;
+      if (__popc(bal) >= 8) {
 #pragma unroll
         for (int u = 0; u < kG2; ++u) {
           const float s = warp_sum(c[u]);
-          if (lane == 0 && s != 0.f) atomicAdd(g2 + (long long)kG2 * g.idx + u, double(s));
+          if (lane == 0) atomicAdd(&acc[j][u], s);
         }
+      } else if (hit) {
+#pragma unroll
+        for (int u = 0; u < kG2; ++u) atomicAdd(&acc[j][u], c[u]);
+      }
+    }
+    __syncthreads();
+    if (int(threadIdx.x) < cnt) {
+      const int idx = sm[threadIdx.x].idx;
+#pragma unroll
+      for (int u = 0; u < kG2; ++u) {
+        const float v = acc[threadIdx.x][u];
+        if (v != 0.f) atomicAdd(g2 + (long long)kG2 * idx + u, double(v));
       }
     }
   }

@@ -135,8 +135,6 @@ class Trainer:
         self._rows = None
         self._row_node = None
         self._grads = None
-        self._h_items = self._h_items_wb = None
-        self._d_items = self._d_items_wb = None
         self._inflight = []
         self._target_dev = None
         self.last_stats = {}
@@ -174,20 +172,16 @@ class Trainer:
         for i, (slot, rows, blk) in enumerate(items):
             tab[i] = (slot, rows, off, blk.data_ptr())
             off += FLOATS_PER_GAUSSIAN * rows
-        buf = self._h_items if load else self._h_items_wb
-        if buf is None or buf.shape[0] < n:
-            buf = torch.empty((max(n, 64) * 2, 4), dtype=torch.int64).pin_memory()
-            if load:
-                self._h_items = buf
-            else:
-                self._h_items_wb = buf
+        # fresh pinned table per call: torch's caching host allocator keeps it
+        # from being reused until the async copy below has completed
+        buf = torch.empty((n, 4), dtype=torch.int64, pin_memory=True)
         buf[:n].numpy()[:] = tab
-        dev = self._ensure("_d_items" if load else "_d_items_wb", 4 * n, torch.int64)
+        dev = torch.empty(4 * n, dtype=torch.int64, device=self.scene.device)
         dev[:4 * n].copy_(buf[:n].reshape(-1), non_blocking=True)
         fn = _lib.lib().glod_store_load_prefixes if load else _lib.lib().glod_store_write_back
         _lib.check(fn(C.byref(self.scene.store.device_view()), _lib.ptr(dev), n, off, _lib.stream_ptr()))
         # keep the pinned table and the blocks alive until the kernel ran
-        self._inflight.append((buf, [b for _, _, b in items]))
+        self._inflight.append((buf, dev, [b for _, _, b in items]))
 
     def _ensure(self, name, numel, dtype):
         t = getattr(self, name)
@@ -227,11 +221,23 @@ class Trainer:
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         S1 = max(sc.lod.S, 1)
         store = sc.store
-        loads, wbs = [], []
+        # Store transfers are batched: a batch runs all its loads, then all
+        # its write-backs.  The reference interleaves them (load, insert →
+        # write back evictions, next SPT, …), so a batch is closed whenever
+        # an SPT about to be loaded has a write-back pending in it (an SPT
+        # evicted earlier in this step and selected again later must be
+        # re-read *after* its write-back).  A replaced entry (miss on a
+        # resident SPT) is loaded before its dirty block is written back —
+        # the reference's stale-store order (trainer.py:333-341).
+        loads, wbs, wb_ids = [], [], set()
         for j in range(n_sp):
             sid, d, P = int(spt_ids[j]), float(d_root[j]), int(prefix[j])
             e = self.cache.lookup(sid, d)
             if e is None:
+                if sid in wb_ids:
+                    self._xfer(loads, load=True)
+                    self._xfer(wbs, load=False)
+                    loads, wbs, wb_ids = [], [], set()
                 blk = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float64, device=sc.device)
                 loads.append((store.spt_slot_start(sid), P, blk))
                 store.attribute_bytes_read += P * BYTES_PER_GAUSSIAN_F32
@@ -240,13 +246,11 @@ class Trainer:
                                nbytes=P * BYTES_PER_GAUSSIAN_F32)
                 for esid, eblk in self.cache.insert(e):
                     wbs.append((store.spt_slot_start(esid), eblk.numel() // FLOATS_PER_GAUSSIAN, eblk))
+                    wb_ids.add(esid)
             entries.append(e)
             hd[j] = e.cached_distance
             hb[j] = e.block.data_ptr()
             hb[S1 + j] = e.prefix_len
-        # every load precedes every write-back: a replaced entry's prefix is
-        # re-read from the store before its dirty block is written back
-        # (trainer.py:333-341), other evicted SPTs are not loaded this step
         self._xfer(loads, load=True)
         self._xfer(wbs, load=False)
         if n_sp:
