@@ -277,6 +277,30 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   }
 }
 
+// Transposed warp reduction of 8 values (9 shuffles instead of 8x5): after
+// it, lane l holds the warp total of value ((l >> 2) & 7).
+GLOD_DEV float warp_reduce8(const float (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? v[i] : v[i + 4];
+    const float keep = b4 ? v[i + 4] : v[i];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float x[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b3 ? w[i] : w[i + 2];
+    const float keep = b3 ? w[i + 2] : w[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float y = (b2 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
+
 GLOD_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -285,19 +309,17 @@ GLOD_DEV float warp_sum(float v) {
 
 // Back-to-front per pixel with the reference's rear accumulator
 // (renderer.py:219-261).  Per-pixel math is fp32 (T recovered as
-// T_front = T_after / (1 − α) from the fp64 final transmittance).  The nine
-// per-Gaussian partials are summed per batch in shared memory — a warp
-// shuffle-reduces first when many of its lanes hit the splat, otherwise the
-// hitting lanes add directly — and flushed with one fp64 atomic per
-// (splat, tile, partial).  Warps skip splats whose bbox misses their 16x2
-// pixel strip without evaluating any pixel.
-__global__ void __launch_bounds__(kBlendThreads, 3)
+// T_front = T_after / (1 − α) from the fp64 final transmittance).  For each
+// (splat, warp) with at least one hit the nine per-Gaussian partials are
+// warp-reduced (transposed reduction) and nine lanes issue one fp64
+// reduction each.  Warps skip splats whose bbox misses their 16x2 strip or
+// that lie beyond the strip's last contributor.
+__global__ void __launch_bounds__(kBlendThreads, 4)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
                  double* __restrict__ g2) {
-  __shared__ Splat sm[kBlendThreads];
-  __shared__ float acc[kBlendThreads][kG2];
+  __shared__ float4 sm[kBlendThreads][3];
   __shared__ int max_last;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
@@ -325,23 +347,32 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   __syncthreads();
   const int end = max_last + 1;   // nothing beyond the last contributor matters
   float rr = 0.f, rg_ = 0.f, rb = 0.f;   // rear accumulator Σ_behind w·c
+  const float4* src = reinterpret_cast<const float4*>(sorted);
   for (int top = end; top > rg.x; top -= kBlendThreads) {
     const int lo = max(rg.x, top - kBlendThreads);
     const int k = top - 1 - int(threadIdx.x);
     __syncthreads();
-    if (k >= lo) sm[threadIdx.x] = sorted[ival[k]];
-#pragma unroll
-    for (int u = 0; u < kG2; ++u) acc[threadIdx.x][u] = 0.f;
+    if (k >= lo) {
+      const long long s = ival[k];
+      sm[threadIdx.x][0] = src[3 * s];
+      sm[threadIdx.x][1] = src[3 * s + 1];
+      sm[threadIdx.x][2] = src[3 * s + 2];
+    }
     __syncthreads();
     const int cnt = top - lo;
     for (int j = 0; j < cnt; ++j) {
       const int inst = top - 1 - j;
-      const Splat& g = sm[j];
+      const float4 a0 = sm[j][0], a1 = sm[j][1], a2 = sm[j][2];
+      Splat g;
+      *reinterpret_cast<float4*>(&g) = a0;
+      *(reinterpret_cast<float4*>(&g) + 1) = a1;
+      *(reinterpret_cast<float4*>(&g) + 2) = a2;
       if (inst > wlast || g.x1 <= wx0 || g.x0 >= wx0 + kTileW || g.y1 <= wy0 || g.y0 >= wy0 + 2)
         continue;                                          // warp-uniform skip
-      float c[kG2];
+      float c[8];
+      float c8 = 0.f;
 #pragma unroll
-      for (int u = 0; u < kG2; ++u) c[u] = 0.f;
+      for (int u = 0; u < 8; ++u) c[u] = 0.f;
       float dx, dy, q, gs, al;
       const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
       if (hit) {
@@ -361,29 +392,17 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
           c[5] = -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
           c[6] = dq * dx * dx;
           c[7] = dq * dx * dy;
-          c[8] = dq * dy * dy;
+          c8 = dq * dy * dy;
         }
       }
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (bal == 0) continue;
-      if (__popc(bal) >= 8) {
-#pragma unroll
-        for (int u = 0; u < kG2; ++u) {
-          const float s = warp_sum(c[u]);
-          if (lane == 0) atomicAdd(&acc[j][u], s);
-        }
-      } else if (hit) {
-#pragma unroll
-        for (int u = 0; u < kG2; ++u) atomicAdd(&acc[j][u], c[u]);
-      }
-    }
-    __syncthreads();
-    if (int(threadIdx.x) < cnt) {
-      const int idx = sm[threadIdx.x].idx;
-#pragma unroll
-      for (int u = 0; u < kG2; ++u) {
-        const float v = acc[threadIdx.x][u];
-        if (v != 0.f) atomicAdd(g2 + (long long)kG2 * idx + u, double(v));
+      if (!__any_sync(0xffffffffu, hit)) continue;
+      const float t8 = warp_reduce8(c, lane);
+      const float s8 = warp_sum(c8);
+      double* dst = g2 + (long long)kG2 * g.idx;
+      if ((lane & 3) == 0) {
+        if (t8 != 0.f) atomicAdd(dst + (lane >> 2), double(t8));
+      } else if (lane == 1) {
+        if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
       }
     }
   }
