@@ -28,6 +28,7 @@ extern "C" {
 #define GLOD_ERR_INVALID_ARGUMENT 1   /* ValueError / InvalidParameterError */
 #define GLOD_ERR_CUDA 2               /* RuntimeError                        */
 #define GLOD_ERR_INVALID_INPUT 3      /* renderer.InvalidInputError          */
+#define GLOD_ERR_OVER_BUDGET 4        /* cache.OverBudgetError               */
 
 int glod_version(void);
 const char* glod_last_error(void);
@@ -167,10 +168,15 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
  * [dev] packed f64 blocks of `capacity` rows; step: [dev] int64[capacity];
  * grads: [dev] packed f64 block of `grad_rows` rows; ids/rows: [dev] int32[n]
  * (rows == NULL means row i).  ids must be unique.  lrs: host double[6] in
- * section order (means already scaled by the scene extent). */
+ * section order (means already scaled by the scene extent).  refresh
+ * (optional, see glod_gather_plan below): when given, row r is a render row
+ * of that plan and SPT rows also write their updated values into their
+ * cache block (entry.block.attrs.put, trainer.py:363). */
+struct glod_gather_plan;
 int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows,
-                   int64_t grad_rows, int64_t n, const double* lrs, void* stream);
+                   int64_t grad_rows, int64_t n, const double* lrs,
+                   const struct glod_gather_plan* refresh, void* stream);
 
 /* ======================================================================= *
  * Store / cache data movement (trainer.py:325-364, store.py:304-333)
@@ -231,6 +237,45 @@ int glod_store_load_prefixes(const glod_store_view* store, const glod_prefix_ite
  * f64 -> f32 written straight into the pinned store. */
 int glod_store_write_back(const glod_store_view* store, const glod_prefix_item* items,
                           int32_t n_items, int64_t total_elems, void* stream);
+
+/* ======================================================================= *
+ * Device cache table (cache.DeviceCache, cache.py:42-109, driven like the
+ * gather loop of trainer.train_step, trainer.py:329-345)
+ * ======================================================================= */
+typedef struct glod_cache glod_cache;
+
+typedef struct glod_cache_stats_t {
+  int64_t entries, resident_bytes, hits, misses, loaded_rows;
+} glod_cache_stats_t;
+
+/* slot_start: host int64[num_spts], first store slot of each SPT
+ * (Scene.spt_slot_start, store.py:299-302).  bytes_per_row = 92. */
+int glod_cache_create(int64_t budget_bytes, double d_min, double d_max, int64_t flush_interval,
+                      int32_t bytes_per_row, const int64_t* slot_start, int32_t num_spts,
+                      glod_cache** out);
+int glod_cache_destroy(glod_cache* c);
+/* One view's cache pass over the selected SPTs (host arrays, ascending
+ * spt order): lookup, miss → stream-ordered block allocation + prefix load
+ * from the pinned store, insert with LRU eviction and write-back of dirty
+ * victims.  Outputs per SPT the distance its positions are cut at
+ * (cached_distance), its block address and rows.  counters_out[2] =
+ * {rows loaded from the store, cache hits}.  GLOD_ERR_OVER_BUDGET when one
+ * prefix exceeds the budget. */
+int glod_cache_step(glod_cache* c, const glod_store_view* store, int32_t n,
+                    const int32_t* spt_ids, const double* d_root, const int32_t* prefix_len,
+                    double* dist_out, uint64_t* block_out, int64_t* rows_out,
+                    int64_t* counters_out, void* stream);
+/* After the step's kernels are enqueued: mark this step's entries dirty
+ * (training), tick_and_maybe_flush(iteration) (iteration < 0: no flush),
+ * release evicted blocks stream-ordered. */
+int glod_cache_end_step(glod_cache* c, const glod_store_view* store, int64_t iteration,
+                        int32_t mark_dirty, void* stream);
+int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
+/* Resident entries in LRU order (front first), up to `capacity`. */
+int glod_cache_entries(const glod_cache* c, int32_t* spt_id, double* cached_distance,
+                       int64_t* prefix_len, uint64_t* block, int32_t* dirty, int64_t capacity);
+/* Synchronous device→host copy (snapshots / tests). */
+int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,7 @@ GLOD_OK = 0
 GLOD_ERR_INVALID_ARGUMENT = 1
 GLOD_ERR_CUDA = 2
 GLOD_ERR_INVALID_INPUT = 3
+GLOD_ERR_OVER_BUDGET = 4
 
 P = C.c_void_p
 
@@ -72,6 +73,11 @@ class PrefixItem(C.Structure):
                 ("block", P)]
 
 
+class CacheStats(C.Structure):
+    _fields_ = [("entries", C.c_int64), ("resident_bytes", C.c_int64), ("hits", C.c_int64),
+                ("misses", C.c_int64), ("loaded_rows", C.c_int64)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "glod_version": (C.c_int, []),
@@ -91,13 +97,21 @@ SIGNATURES = {
     "glod_loss_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
     "glod_adam_step": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
-                                 C.POINTER(C.c_double), P]),
+                                 C.POINTER(C.c_double), P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
     "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
     "glod_host_device_ptr": (C.c_int, [P, C.POINTER(P)]),
     "glod_store_load_prefixes": (C.c_int, [C.POINTER(StoreView), P, C.c_int32, C.c_int64, P]),
     "glod_store_write_back": (C.c_int, [C.POINTER(StoreView), P, C.c_int32, C.c_int64, P]),
+    "glod_cache_create": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, P,
+                                    C.c_int32, C.POINTER(P)]),
+    "glod_cache_destroy": (C.c_int, [P]),
+    "glod_cache_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, P, P, P, P, P]),
+    "glod_cache_end_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int64, C.c_int32, P]),
+    "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
+    "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
+    "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),
 }
 
 _LIB = None
@@ -139,6 +153,9 @@ def check(code: int):
     if code == GLOD_ERR_INVALID_INPUT:
         from .renderer import InvalidInputError
         raise InvalidInputError(msg)
+    if code == GLOD_ERR_OVER_BUDGET:
+        from .cache import OverBudgetError
+        raise OverBudgetError(msg)
     raise GlodError(msg)
 
 

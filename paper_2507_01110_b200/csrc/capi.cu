@@ -10,12 +10,14 @@
 namespace glod {
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int set_error(int code, const char* what);
 size_t loss_scratch_bytes(int W, int H);
 cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
                         float* grad, void* scratch, size_t bytes, cudaStream_t st);
 cudaError_t launch_adam(double* params, double* m, double* v, long long* step, long long cap,
                         const int* ids, const double* grads, const int* rows, long long grad_rows,
-                        long long n, const double* lrs, cudaStream_t st);
+                        long long n, const double* lrs, const glod_gather_plan* plan,
+                        cudaStream_t st);
 cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
@@ -36,6 +38,14 @@ int fail(int code, const char* what) {
   return code;
 }
 
+}  // namespace
+
+int glod::set_error(int code, const char* what) {
+  g_err = what;
+  return code;
+}
+
+namespace {
 int check(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return GLOD_OK;
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -142,11 +152,12 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
 
 int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows, int64_t grad_rows,
-                   int64_t n, const double* lrs, void* stream) {
+                   int64_t n, const double* lrs, const glod_gather_plan* refresh, void* stream) {
   if (n > 0 && (!params || !m || !v || !step || !ids || !grads || !lrs))
     return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_adam(params, m, v, reinterpret_cast<long long*>(step), capacity, ids,
-                                 grads, rows, grad_rows, n, lrs, static_cast<cudaStream_t>(stream)),
+                                 grads, rows, grad_rows, n, lrs, refresh,
+                                 static_cast<cudaStream_t>(stream)),
                "glod_adam_step");
 }
 

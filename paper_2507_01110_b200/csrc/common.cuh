@@ -10,6 +10,8 @@ namespace glod {
 // Host-side count of kernel launches issued by this library (reported by
 // bench.py as gpu_launches; defined in capi.cu).
 void count_launch(unsigned long long n = 1);
+// Sets the thread-local message returned by glod_last_error(); returns code.
+int set_error(int code, const char* what);
 
 // ---------------------------------------------------------------------------
 // Exact-rounding fp64 arithmetic.  The LoD decisions must reproduce the

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .cache import CacheConfig, CacheEntry, DeviceCache
+from .cache import CacheConfig, NativeCache
 from .core import BYTES_PER_GAUSSIAN_F32, FLOATS_PER_GAUSSIAN, SECTIONS, AttributeArrays, Camera, LodConfig
 from .device import DeviceLodScene
 from .renderer import Rasterizer
@@ -103,7 +103,7 @@ class Trainer:
         self.cfg = cfg
         self.scene = DeviceScene(h, hspt)
         dev = self.scene.device
-        self.cache = DeviceCache(config=cfg.cache)
+        self.cache = NativeCache(cfg.cache, self.scene.store)
         self.rast = Rasterizer()
         self.views = [(Camera.from_any(c), t) for c, t in views]
         pos = np.stack([c.position for c, _ in self.views])
@@ -135,7 +135,6 @@ class Trainer:
         self._rows = None
         self._row_node = None
         self._grads = None
-        self._inflight = []
         self._target_dev = None
         self.last_stats = {}
         self.timing = None          # {stage: [ms, ...]} when profiling is on
@@ -161,28 +160,6 @@ class Trainer:
         self._ev = []
 
     # ------------------------------------------------------------------
-    def _xfer(self, items, load: bool):
-        """One zero-copy kernel for a batch of (slot_start, rows, block)
-        store transfers (loads: f32→f64 into blocks; write-backs: f64→f32)."""
-        if not items:
-            return
-        n = len(items)
-        tab = np.empty((n, 4), dtype=np.int64)
-        off = 0
-        for i, (slot, rows, blk) in enumerate(items):
-            tab[i] = (slot, rows, off, blk.data_ptr())
-            off += FLOATS_PER_GAUSSIAN * rows
-        # fresh pinned table per call: torch's caching host allocator keeps it
-        # from being reused until the async copy below has completed
-        buf = torch.empty((n, 4), dtype=torch.int64, pin_memory=True)
-        buf[:n].numpy()[:] = tab
-        dev = torch.empty(4 * n, dtype=torch.int64, device=self.scene.device)
-        dev[:4 * n].copy_(buf[:n].reshape(-1), non_blocking=True)
-        fn = _lib.lib().glod_store_load_prefixes if load else _lib.lib().glod_store_write_back
-        _lib.check(fn(C.byref(self.scene.store.device_view()), _lib.ptr(dev), n, off, _lib.stream_ptr()))
-        # keep the pinned table and the blocks alive until the kernel ran
-        self._inflight.append((buf, dev, [b for _, _, b in items]))
-
     def _ensure(self, name, numel, dtype):
         t = getattr(self, name)
         if t is None or t.numel() < numel:
@@ -214,45 +191,9 @@ class Trainer:
         sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam)
         self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
-        bytes_before = sc.store.attribute_bytes_read
-        hits_before = self.cache.hits
-        loaded = 0
-        entries = []
-        hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         S1 = max(sc.lod.S, 1)
-        store = sc.store
-        # Store transfers are batched: a batch runs all its loads, then all
-        # its write-backs.  The reference interleaves them (load, insert →
-        # write back evictions, next SPT, …), so a batch is closed whenever
-        # an SPT about to be loaded has a write-back pending in it (an SPT
-        # evicted earlier in this step and selected again later must be
-        # re-read *after* its write-back).  A replaced entry (miss on a
-        # resident SPT) is loaded before its dirty block is written back —
-        # the reference's stale-store order (trainer.py:333-341).
-        loads, wbs, wb_ids = [], [], set()
-        for j in range(n_sp):
-            sid, d, P = int(spt_ids[j]), float(d_root[j]), int(prefix[j])
-            e = self.cache.lookup(sid, d)
-            if e is None:
-                if sid in wb_ids:
-                    self._xfer(loads, load=True)
-                    self._xfer(wbs, load=False)
-                    loads, wbs, wb_ids = [], [], set()
-                blk = torch.empty(FLOATS_PER_GAUSSIAN * P, dtype=torch.float64, device=sc.device)
-                loads.append((store.spt_slot_start(sid), P, blk))
-                store.attribute_bytes_read += P * BYTES_PER_GAUSSIAN_F32
-                loaded += P
-                e = CacheEntry(spt_id=sid, cached_distance=d, prefix_len=P, block=blk,
-                               nbytes=P * BYTES_PER_GAUSSIAN_F32)
-                for esid, eblk in self.cache.insert(e):
-                    wbs.append((store.spt_slot_start(esid), eblk.numel() // FLOATS_PER_GAUSSIAN, eblk))
-                    wb_ids.add(esid)
-            entries.append(e)
-            hd[j] = e.cached_distance
-            hb[j] = e.block.data_ptr()
-            hb[S1 + j] = e.prefix_len
-        self._xfer(loads, load=True)
-        self._xfer(wbs, load=False)
+        hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
+        loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
         if n_sp:
             self._d_dist.copy_(self._h_dist, non_blocking=True)
             self._d_blk.copy_(self._h_blk, non_blocking=True)
@@ -276,9 +217,9 @@ class Trainer:
         self.last_stats = {"n_upper": n_up, "n_pass": n_pa, "n_spt": n_sp,
                            "prefix_total": int(prefix.sum()) if n_sp else 0}
         counters = {"gaussians_rendered": int(R), "gaussians_loaded_from_store": int(loaded),
-                    "cache_hits": int(self.cache.hits - hits_before),
-                    "bytes_streamed": int(sc.store.attribute_bytes_read - bytes_before)}
-        return R, rows, row_node, plan, entries, counters
+                    "cache_hits": int(hits),
+                    "bytes_streamed": int(loaded * sc.store.bytes_per_gaussian)}
+        return R, rows, row_node, plan, None, counters
 
     def render_view(self, view: int, image: torch.Tensor | None = None) -> torch.Tensor:
         """Serve/bench path (cli.cmd_render, cli.py:139-189): cut + cache +
@@ -286,6 +227,7 @@ class Trainer:
         cam, _ = self.views[view]
         R, rows, _, _, _, counters = self._gather_view(cam)
         img = self.rast.forward(rows, R, cam, image=image)
+        self.cache.end_step(-1, mark_dirty=False)
         self._mark("forward")
         self._collect()
         self.last_render = counters
@@ -299,7 +241,7 @@ class Trainer:
         if not self.device_targets:
             self._target_dev = target.to(sc.device, non_blocking=True)
             target = self._target_dev
-        R, rows, row_node, plan, entries, counters = self._gather_view(cam)
+        R, rows, row_node, plan, _, counters = self._gather_view(cam)
         L = _lib.lib()
         st = _lib.stream_ptr()
         image = self.rast.forward(rows, R, cam)
@@ -316,16 +258,12 @@ class Trainer:
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
         self._mark("backward")
         _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v), _lib.ptr(sc.step),
-                                    sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs, st))
+                                    sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs,
+                                    C.byref(plan), st))
         self._mark("adam")
-        _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
-        for e in entries:
-            e.dirty = True
-        self._xfer([(sc.store.spt_slot_start(esid), eblk.numel() // FLOATS_PER_GAUSSIAN, eblk)
-                    for esid, eblk in self.cache.tick_and_maybe_flush(iteration)], load=False)
+        self.cache.end_step(iteration, mark_dirty=True)
         self._mark("scatter_flush")
         self._collect()
-        self._inflight = []      # the step's syncs above ordered every transfer
         self.iteration = iteration
         self.last_stats["n_instances"] = self.rast.stats()["n_instances"]
         self._last_grads = grads
