@@ -168,15 +168,17 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
  * [dev] packed f64 blocks of `capacity` rows; step: [dev] int64[capacity];
  * grads: [dev] packed f64 block of `grad_rows` rows; ids/rows: [dev] int32[n]
  * (rows == NULL means row i).  ids must be unique.  lrs: host double[6] in
- * section order (means already scaled by the scene extent).  refresh
+ * section order (means already scaled by the scene extent).  bias_table:
+ * [dev] f64 [2*bias_len] = {1-0.9^t, 1-0.999^t for t < bias_len} (or NULL /
+ * bias_len 0: computed with pow in the kernel).  refresh
  * (optional, see glod_gather_plan below): when given, row r is a render row
  * of that plan and SPT rows also write their updated values into their
  * cache block (entry.block.attrs.put, trainer.py:363). */
 struct glod_gather_plan;
 int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows,
-                   int64_t grad_rows, int64_t n, const double* lrs,
-                   const struct glod_gather_plan* refresh, void* stream);
+                   int64_t grad_rows, int64_t n, const double* lrs, const double* bias_table,
+                   int64_t bias_len, const struct glod_gather_plan* refresh, void* stream);
 
 /* ======================================================================= *
  * Store / cache data movement (trainer.py:325-364, store.py:304-333)

@@ -97,7 +97,7 @@ SIGNATURES = {
     "glod_loss_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
     "glod_adam_step": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
-                                 C.POINTER(C.c_double), P, P]),
+                                 C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
     "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),

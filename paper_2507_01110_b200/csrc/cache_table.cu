@@ -56,9 +56,34 @@ struct CacheTable {
   std::vector<double*> to_free;           // blocks freed after their write-back
   int device = 0;
   cudaEvent_t items_done = nullptr;       // last H2D from the pinned item table
+  // Write-backs run on a side stream so the D2H PCIe direction overlaps the
+  // rest of the step; the main stream waits for them before anything that
+  // could observe the store (the next loads) or reuse a written-back block.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_wb = nullptr;
+  bool wb_pending = false;
+
+  cudaError_t ensure_side() {
+    if (side) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_wb, cudaEventDisableTiming);
+    return e;
+  }
+
+  // main stream waits for outstanding write-backs
+  cudaError_t join(cudaStream_t st) {
+    if (!wb_pending) return cudaSuccess;
+    wb_pending = false;
+    return cudaStreamWaitEvent(st, ev_wb, 0);
+  }
 
   ~CacheTable() {
+    if (side) cudaStreamSynchronize(side);
     if (items_done) cudaEventDestroy(items_done);
+    if (ev_main) cudaEventDestroy(ev_main);
+    if (ev_wb) cudaEventDestroy(ev_wb);
+    if (side) cudaStreamDestroy(side);
     for (auto& e : lru) cudaFree(e.block);
     if (h_items) cudaFreeHost(h_items);
     if (d_items) cudaFree(d_items);
@@ -93,9 +118,16 @@ struct Xfer {
   double* block;
 };
 
-// Runs one batch: all loads, then all write-backs, from one pinned table.
+// Runs one batch: all loads (main stream), then all write-backs (side
+// stream, after the loads), from one pinned item table.
 cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, std::vector<Xfer>& loads,
                       std::vector<Xfer>& wbs, size_t& table_off, cudaStream_t st) {
+  cudaError_t e = c->ensure_side();
+  if (e != cudaSuccess) return e;
+  // loads observe every earlier write-back, and the device item table is
+  // not rewritten while a write-back kernel may still read it
+  e = c->join(st);
+  if (e != cudaSuccess) return e;
   for (int pass = 0; pass < 2; ++pass) {
     std::vector<Xfer>& v = pass == 0 ? loads : wbs;
     if (v.empty()) continue;
@@ -109,11 +141,20 @@ cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, std::vector<Xfer
       off += kFloats * v[i].rows;
     }
     glod_prefix_item* d = c->d_items + table_off;
-    cudaError_t e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return e;
     e = cudaEventRecord(c->items_done, st);
     if (e != cudaSuccess) return e;
-    e = launch_store_xfer(sv, d, int(v.size()), off, pass == 0, st);
+    if (pass == 0) {
+      e = launch_store_xfer(sv, d, int(v.size()), off, 1, st);
+    } else {
+      // side stream: after this batch's loads and the item-table copy
+      e = cudaEventRecord(c->ev_main, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_main, 0);
+      if (e == cudaSuccess) e = launch_store_xfer(sv, d, int(v.size()), off, 0, c->side);
+      if (e == cudaSuccess) e = cudaEventRecord(c->ev_wb, c->side);
+      c->wb_pending = true;
+    }
     if (e != cudaSuccess) return e;
     table_off += v.size();
     v.clear();
@@ -212,6 +253,9 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
 // reference keeps its `entry` references alive) — release them only once
 // the step's kernels are enqueued.
 cudaError_t cache_release(CacheTable* c, cudaStream_t st) {
+  if (c->to_free.empty()) return cudaSuccess;
+  cudaError_t j = c->join(st);     // a freed block may still be being written back
+  if (j != cudaSuccess) return j;
   for (double* b : c->to_free) {
     cudaError_t e = cudaFreeAsync(b, st);
     if (e != cudaSuccess) return e;

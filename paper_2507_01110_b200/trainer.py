@@ -135,6 +135,8 @@ class Trainer:
         self._rows = None
         self._row_node = None
         self._grads = None
+        self._bias = None
+        self._bias_len = 0
         self._target_dev = None
         self.last_stats = {}
         self.timing = None          # {stage: [ms, ...]} when profiling is on
@@ -160,6 +162,19 @@ class Trainer:
         self._ev = []
 
     # ------------------------------------------------------------------
+    def _bias_table(self, iteration: int):
+        """1-β^t for every step count a node can have after this iteration,
+        computed with numpy's power exactly like the reference
+        (trainer.py:261-263); grown by doubling."""
+        need = iteration + 2
+        if self._bias is None or self._bias_len < need:
+            n = max(1024, 2 * need)
+            t = np.arange(n, dtype=np.float64)
+            tab = np.concatenate([1.0 - 0.9 ** t, 1.0 - 0.999 ** t])
+            self._bias = torch.from_numpy(tab).to(self.scene.device)
+            self._bias_len = n
+        return self._bias, self._bias_len
+
     def _ensure(self, name, numel, dtype):
         t = getattr(self, name)
         if t is None or t.numel() < numel:
@@ -257,9 +272,10 @@ class Trainer:
         self._mark("loss_read")
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
         self._mark("backward")
+        bias, blen = self._bias_table(iteration)
         _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v), _lib.ptr(sc.step),
                                     sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs,
-                                    C.byref(plan), st))
+                                    _lib.ptr(bias), blen, C.byref(plan), st))
         self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
         self._mark("scatter_flush")

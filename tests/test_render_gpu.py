@@ -125,7 +125,7 @@ def test_adam_golden():
         G = torch.from_numpy(g.packed()).cuda()
         _lib.check(_lib.lib().glod_adam_step(_lib.ptr(P), _lib.ptr(M), _lib.ptr(V), _lib.ptr(step), n,
                                              _lib.ptr(ids), _lib.ptr(G), None, ids.numel(), ids.numel(),
-                                             lrs, None, _lib.stream_ptr()))
+                                             lrs, None, 0, None, _lib.stream_ptr()))
         got = AttributeArrays.from_packed(P.cpu().numpy(), n)
         for k in NAMES:
             np.testing.assert_allclose(getattr(got, k), d[f"it{it}_p_{k}"], rtol=1e-12, atol=1e-14)
