@@ -55,6 +55,7 @@ class SceneSpec:
     s_lo: float = 0.03
     s_hi: float = 0.3
     metric: str = "max_scale"
+    relabel: bool = True            # node ids in store slot order (see relabel_slot_order)
 
 
 def scene_extent(n_leaves: int) -> float:
@@ -99,7 +100,33 @@ def designed_scene(spec: SceneSpec, device=None):
     scales[is_cut] = s_cut
     h.attrs.scales = scales
     hspt = build_hspt(h, thr, spec.min_subtree, cfg)
+    if spec.relabel:
+        h = relabel_slot_order(h, hspt)
+        hspt = build_hspt(h, thr, spec.min_subtree, cfg)
     return h, hspt, cfg
+
+
+def relabel_slot_order(h: Hierarchy, hspt: Hspt) -> Hierarchy:
+    """Renumber nodes so that node id == store slot (store.py:143-154: every
+    non-SPT node first in ascending id, then each SPT's records in record
+    order).  A data-layout choice for HBM: SPT cut prefixes become
+    contiguous id ranges, so the render rows a view selects (and the ADAM
+    updates of their master rows) are nearly sequential in memory.  Ties in
+    the SPT record order (siblings share key_parent, broken by node id) keep
+    their order because new ids increase along the records; rebuilding the
+    HSPT on the result reproduces the same partition and record order."""
+    from .store import slot_order
+    order = slot_order(h, hspt)                      # slot -> old id
+    new_of = np.full(h.capacity, -1, dtype=np.int64)
+    new_of[order] = np.arange(order.size)
+    n = order.size
+    attrs = h.attrs.take(order)
+    par = h.parent[order].astype(np.int64)
+    ch = h.children[order].astype(np.int64)
+    par = np.where(par >= 0, new_of[np.maximum(par, 0)], -1)
+    ch = np.where(ch >= 0, new_of[np.maximum(ch, 0)], -1)
+    return Hierarchy(attrs=attrs, parent=par.astype(np.int32), children=ch.astype(np.int32),
+                     root=int(new_of[h.root]))
 
 
 def look_at(position, target, focal, resolution, near=0.1) -> Camera:
