@@ -238,9 +238,11 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   __shared__ Splat sm[kBlendThreads];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  const int px = tx * kTileW + int(threadIdx.x % kTileW);
-  const int py = ty * kTileH + int(threadIdx.x / kTileW);
-  const int wx0 = tx * kTileW, wy0 = ty * kTileH + 2 * int(threadIdx.x >> 5);
+  // each warp owns an 8x4 pixel block of the 16x16 tile (square-ish, so the
+  // warp-uniform bbox test rejects more splats than a 16x2 strip)
+  const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
+  const int wx0 = tx * kTileW + (wid & 1) * 8, wy0 = ty * kTileH + (wid >> 1) * 4;
+  const int px = wx0 + (ln & 7), py = wy0 + (ln >> 3);
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   double T = 1.0;
@@ -255,7 +257,7 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
     const int cnt = min(kBlendThreads, rg.y - base);
     for (int j = 0; j < cnt && !done; ++j) {
       const Splat& g = sm[j];
-      if (g.x1 <= wx0 || g.x0 >= wx0 + kTileW || g.y1 <= wy0 || g.y0 >= wy0 + 2) continue;
+      if (g.x1 <= wx0 || g.x0 >= wx0 + 8 || g.y1 <= wy0 || g.y0 >= wy0 + 4) continue;
       float dx, dy, q, gs, al;
       if (!pixel_alpha(g, px, py, dx, dy, q, gs, al)) continue;
       const double w = double(al) * T;
@@ -323,9 +325,11 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   __shared__ int max_last;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  const int px = tx * kTileW + int(threadIdx.x % kTileW);
-  const int py = ty * kTileH + int(threadIdx.x / kTileW);
-  const int wx0 = tx * kTileW, wy0 = ty * kTileH + 2 * int(threadIdx.x >> 5);
+  // each warp owns an 8x4 pixel block of the 16x16 tile (square-ish, so the
+  // warp-uniform bbox test rejects more splats than a 16x2 strip)
+  const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
+  const int wx0 = tx * kTileW + (wid & 1) * 8, wy0 = ty * kTileH + (wid >> 1) * 4;
+  const int px = wx0 + (ln & 7), py = wy0 + (ln >> 3);
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   const int lane = threadIdx.x & 31;
@@ -367,7 +371,7 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
       *reinterpret_cast<float4*>(&g) = a0;
       *(reinterpret_cast<float4*>(&g) + 1) = a1;
       *(reinterpret_cast<float4*>(&g) + 2) = a2;
-      if (inst > wlast || g.x1 <= wx0 || g.x0 >= wx0 + kTileW || g.y1 <= wy0 || g.y0 >= wy0 + 2)
+      if (inst > wlast || g.x1 <= wx0 || g.x0 >= wx0 + 8 || g.y1 <= wy0 || g.y0 >= wy0 + 4)
         continue;                                          // warp-uniform skip
       float c[8];
       float c8 = 0.f;
