@@ -99,8 +99,16 @@ class Trainer:
     """The per-GPU training engine.  `views` is a list of (Camera, target)
     with targets (h, w, 3) float images (numpy or pinned torch)."""
 
-    def __init__(self, h, hspt, views, cfg: TrainConfig, extent: float, device_targets: bool = True):
+    def __init__(self, h, hspt, views, cfg: TrainConfig, extent: float, device_targets: bool = True,
+                 group=None):
+        import torch.distributed as dist
         self.cfg = cfg
+        # view sharding: with an initialised process group of >1 ranks each
+        # step's gradients are summed over ranks on the union of touched
+        # nodes (parallel.sparse_grad_allreduce) before a replicated ADAM
+        self.group = group
+        self.distributed = dist.is_available() and dist.is_initialized() and \
+            dist.get_world_size(group) > 1
         self.scene = DeviceScene(h, hspt)
         dev = self.scene.device
         self.cache = NativeCache(cfg.cache, self.scene.store)
@@ -273,9 +281,20 @@ class Trainer:
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
         self._mark("backward")
         bias, blen = self._bias_table(iteration)
-        _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v), _lib.ptr(sc.step),
-                                    sc.cap, _lib.ptr(row_node), _lib.ptr(grads), None, R, R, self.lrs,
-                                    _lib.ptr(bias), blen, C.byref(plan), st))
+        if self.distributed:
+            from .parallel import sparse_grad_allreduce
+            U, GU = sparse_grad_allreduce(row_node[:R], grads, R, self.group)
+            ids = U.to(torch.int32)
+            nU = int(ids.numel())
+            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v),
+                                        _lib.ptr(sc.step), sc.cap, _lib.ptr(ids), _lib.ptr(GU), None,
+                                        nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
+            _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
+            self._last_union = (ids, GU)
+        else:
+            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v),
+                                        _lib.ptr(sc.step), sc.cap, _lib.ptr(row_node), _lib.ptr(grads),
+                                        None, R, R, self.lrs, _lib.ptr(bias), blen, C.byref(plan), st))
         self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
         self._mark("scatter_flush")
