@@ -289,23 +289,63 @@ CompactScratch carve_compact(void* base, int32_t S, int64_t R, int grid) {
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
+// Decoupled look-back by one warp over windows of 32 predecessors
+// (aggregates are summed until the nearest inclusive prefix is found).
+GLOD_DEV long long lookback(unsigned long long* status, long long t, int agg, int lane) {
+  if (t == 0) {
+    if (lane == 0) atomicExch(status, kFlagIncl | (unsigned long long)agg);
+    return 0;
+  }
+  if (lane == 0) atomicExch(status + t, kFlagAgg | (unsigned long long)agg);
+  long long excl = 0;
+  long long p = t - 1 - lane;
+  while (true) {
+    unsigned long long w = (2ull << 62);
+    if (p >= 0) w = *((volatile unsigned long long*)(status + p));
+    while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+      if ((w >> 62) == 0) {
+        __nanosleep(16);
+        w = *((volatile unsigned long long*)(status + p));
+      }
+    }
+    const unsigned incl = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    long long v = (long long)(w & kValMask);
+    if (incl) {
+      const int first = __ffs(incl) - 1;      // nearest inclusive predecessor
+      if (lane > first) v = 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (incl) break;
+    p -= 32;
+  }
+  if (lane == 0) atomicExch(status + t, kFlagIncl | (unsigned long long)(excl + agg));
+  return excl;
+}
+
+template <typename K>
 __global__ void __launch_bounds__(kCompactThreads)
 compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   __shared__ long long sm[kCompactThreads / 32 + 1];
   __shared__ int cnt[kRows][kCompactThreads / 32];
   __shared__ long long tile_base_sh;
   __shared__ int seg_lo_sh, seg_hi_sh;
+  __shared__ long long seg_start_sh, seg_off_sh;
+  __shared__ double seg_d_sh;
+  __shared__ int seg_rr_sh, seg_rootrec_sh;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = kCompactThreads / 32;
   const long long gthreads = (long long)gridDim.x * blockDim.x;
   const int n_spt = *in.n_spt;
+  const K* key_self = static_cast<const K*>(sc.key_self);
 
   // phase A: prefix length and root rule per selected SPT (spt.py:70-73)
   for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_spt; j += gthreads) {
     const int s = in.spt_ids[j];
     const double d = in.dist[j];
     const int pl = prefix_len_of(sc, s, d);
-    const int rr = d >= key_self_at(sc, sc.spt_offset[s] + sc.spt_root_rec[s]);
+    const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
     out.prefix_len[j] = pl;
     out.root_rule[j] = rr;
     out.seg_start[j] = rr ? 1 : pl;          // segment length, scanned below
@@ -356,41 +396,68 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       int c = a, e = n_spt;
       while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
       seg_hi_sh = c - 1;
+      const int j = a - 1;
+      const int sp = in.spt_ids[j];
+      seg_start_sh = ld_cg(out.seg_start + j);
+      seg_off_sh = sc.spt_offset[sp];
+      seg_d_sh = in.dist[j];
+      seg_rr_sh = ld_cg(out.root_rule + j);
+      seg_rootrec_sh = sc.spt_root_rec[sp];
     }
     __syncthreads();
     const int jlo = seg_lo_sh, jhi = seg_hi_sh;
     bool pred[kRows];
     int seg_of[kRows], pos_of[kRows];
-    int jcur = jlo;
+    if (jlo == jhi && !seg_rr_sh) {
+      // fast path: the whole tile is inside one SPT prefix — a straight
+      // coalesced stream of key_self compared against one distance
+      const long long s0 = seg_start_sh, off = seg_off_sh;
+      const double d = seg_d_sh;
+      K kv[kRows];
 #pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-      pred[k] = false;
-      seg_of[k] = -1;
-      pos_of[k] = 0;
-      if (vi < tend) {
-        int j = jcur;
-        if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
-          int a = jcur, b = jhi + 1;
-          while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
-          j = a - 1;
-          jcur = j;
+      for (int k = 0; k < kRows; ++k) {
+        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+        kv[k] = vi < tend ? key_self[off + (vi - s0)] : K(0);
+      }
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) {
+        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+        pred[k] = vi < tend && double(kv[k]) <= d;
+        seg_of[k] = jlo;
+        pos_of[k] = int(vi - s0);
+      }
+    } else {
+      int jcur = jlo;
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) {
+        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+        pred[k] = false;
+        seg_of[k] = -1;
+        pos_of[k] = 0;
+        if (vi < tend) {
+          int j = jcur;
+          if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
+            int a = jcur, b = jhi + 1;
+            while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
+            j = a - 1;
+            jcur = j;
+          }
+          const long long local = vi - ld_cg(out.seg_start + j);
+          const int s = in.spt_ids[j];
+          const int64_t off = sc.spt_offset[s];
+          int rec;
+          bool p;
+          if (ld_cg(out.root_rule + j)) {
+            rec = sc.spt_root_rec[s];
+            p = true;
+          } else {
+            rec = int(local);
+            p = double(key_self[off + rec]) <= in.dist[j];
+          }
+          pred[k] = p;
+          seg_of[k] = j;
+          pos_of[k] = rec;
         }
-        const long long local = vi - ld_cg(out.seg_start + j);
-        const int s = in.spt_ids[j];
-        const int64_t off = sc.spt_offset[s];
-        int rec;
-        bool p;
-        if (ld_cg(out.root_rule + j)) {
-          rec = sc.spt_root_rec[s];
-          p = true;
-        } else {
-          rec = int(local);
-          p = key_self_at(sc, off + rec) <= in.dist[j];
-        }
-        pred[k] = p;
-        seg_of[k] = j;
-        pos_of[k] = rec;
       }
     }
     unsigned ball[kRows];
@@ -425,23 +492,8 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
         run += vals[q];
       }
       const int agg = __shfl_sync(0xffffffffu, incl, 31);
+      const long long excl = lookback(ws.status, t, agg, lane);
       if (lane == 0) {
-        // decoupled look-back (single thread; tiles are large)
-        long long excl = 0;
-        if (t == 0) {
-          atomicExch(ws.status, kFlagIncl | (unsigned long long)agg);
-        } else {
-          atomicExch(ws.status + t, kFlagAgg | (unsigned long long)agg);
-          long long p = t - 1;
-          while (true) {
-            unsigned long long w = *((volatile unsigned long long*)(ws.status + p));
-            if ((w >> 62) == 0) { __nanosleep(20); continue; }
-            excl += (long long)(w & kValMask);
-            if ((w >> 62) == 2) break;
-            --p;
-          }
-          atomicExch(ws.status + t, kFlagIncl | (unsigned long long)(excl + agg));
-        }
         tile_base_sh = excl;
         if (t == ntiles - 1) out.total[0] = excl + agg;
       }
@@ -453,10 +505,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       if (pred[k]) {
         const long long o = tb + cnt[k][warp] + __popc(ball[k] & lanemask_lt());
         const int j = seg_of[k];
-        const int s = in.spt_ids[j];
+        const int64_t off = (jlo == jhi) ? seg_off_sh : sc.spt_offset[in.spt_ids[j]];
         out.sel_seg[o] = j;
         out.sel_pos[o] = pos_of[k];
-        out.sel_node[o] = sc.rec_node[sc.spt_offset[s] + pos_of[k]];
+        out.sel_node[o] = sc.rec_node[off + pos_of[k]];
       }
     }
     __syncthreads();
@@ -490,7 +542,7 @@ size_t compact_scratch_bytes(int32_t S, int64_t R, int grid) {
 }
 
 int select_grid() { return coop_grid((const void*)select_kernel, kSelectThreads); }
-int compact_grid() { return coop_grid((const void*)compact_kernel, kCompactThreads); }
+int compact_grid() { return coop_grid((const void*)compact_kernel<float>, kCompactThreads); }
 
 cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut& out,
                           void* scratch, size_t scratch_bytes, cudaStream_t st) {
@@ -516,8 +568,8 @@ cudaError_t launch_compact(const LodScene& sc, const CompactIn& in, const Compac
   LodScene a = sc; CompactIn b = in; CompactOut c = out; CompactScratch d = ws;
   void* args[] = {&a, &b, &c, &d};
   count_launch();
-  return cudaLaunchCooperativeKernel((const void*)compact_kernel, dim3(grid), dim3(kCompactThreads),
-                                     args, 0, st);
+  const void* fn = sc.key_f64 ? (const void*)compact_kernel<double> : (const void*)compact_kernel<float>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kCompactThreads), args, 0, st);
 }
 
 }  // namespace glod

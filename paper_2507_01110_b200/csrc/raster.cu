@@ -124,6 +124,32 @@ GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
 
 GLOD_DEV bool finite(double x) { return isfinite(x); }
 
+// Does any pixel of tile (tx, ty) ∩ bbox lie in the q ≤ 32 ellipse?  Exact
+// minimum of the positive-definite quadratic over the continuous rectangle
+// (a superset of the integer pixels), with a small margin — conservative, so
+// dropping a tile never changes a pixel (its q > 32 pixels have α = 0).
+// Used identically when counting and when emitting instances.
+GLOD_DEV float edge_min(float a, float b, float c, float fixed, float lo, float hi) {
+  // min over t∈[lo,hi] of a·f² + 2b·f·t + c·t²
+  float t = fminf(fmaxf(__fdiv_rn(-__fmul_rn(b, fixed), c), lo), hi);
+  return __fadd_rn(__fadd_rn(__fmul_rn(a, __fmul_rn(fixed, fixed)),
+                             __fmul_rn(__fmul_rn(2.f, b), __fmul_rn(fixed, t))),
+                   __fmul_rn(c, __fmul_rn(t, t)));
+}
+
+GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
+  const int xa = max(tx * kTileW, int(g.x0)), xb = min(tx * kTileW + kTileW - 1, int(g.x1) - 1);
+  const int ya = max(ty * kTileH, int(g.y0)), yb = min(ty * kTileH + kTileH - 1, int(g.y1) - 1);
+  const float dxa = __fsub_rn(float(xa - g.x0), g.mx), dxb = __fsub_rn(float(xb - g.x0), g.mx);
+  const float dya = __fsub_rn(float(ya - g.y0), g.my), dyb = __fsub_rn(float(yb - g.y0), g.my);
+  if (dxa <= 0.f && dxb >= 0.f && dya <= 0.f && dyb >= 0.f) return true;
+  float m = edge_min(g.ca, g.cb, g.cc, dxa, dya, dyb);
+  m = fminf(m, edge_min(g.ca, g.cb, g.cc, dxb, dya, dyb));
+  m = fminf(m, edge_min(g.cc, g.cb, g.ca, dya, dxa, dxb));
+  m = fminf(m, edge_min(g.cc, g.cb, g.ca, dyb, dxa, dxb));
+  return m <= 32.01f;
+}
+
 __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam,
                                   Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
                                   int* __restrict__ vals, int* __restrict__ tiles,
@@ -171,11 +197,15 @@ __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n,
   sp.x0 = int16_t(x0); sp.y0 = int16_t(y0); sp.x1 = int16_t(x1); sp.y1 = int16_t(y1);
   sp.r = float(P.col[0]); sp.g = float(P.col[1]); sp.b = float(P.col[2]);
   sp.idx = int(i);
-  splats[i] = sp;
-  keys[i] = __double_as_longlong(depth);       // positive doubles order as uint64
   const int tx0 = x0 / kTileW, tx1 = (x1 - 1) / kTileW;
   const int ty0 = y0 / kTileH, ty1 = (y1 - 1) / kTileH;
-  tiles[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  int nt = 0;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) nt += tile_hit(sp, tx, ty);
+  if (nt == 0) return;                         // every bbox pixel has q > 32: α = 0
+  splats[i] = sp;
+  keys[i] = __double_as_longlong(depth);       // positive doubles order as uint64
+  tiles[i] = nt;
 }
 
 __global__ void gather_kernel(const int* __restrict__ order, const Splat* __restrict__ splats,
@@ -200,6 +230,7 @@ __global__ void emit_kernel(const Splat* __restrict__ sorted, const int* __restr
   long long o = offs[r];
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
+      if (!tile_hit(sp, tx, ty)) continue;
       ikey[o] = unsigned(ty * tw + tx);
       ival[o] = int(r);
       ++o;
