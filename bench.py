@@ -282,6 +282,11 @@ def run_ours(args):
     r1.record()
     torch.cuda.synchronize()
     render_fps = world * nfr / (r0.elapsed_time(r1) / 1e3)
+    tr.enable_timing(True)
+    for f in range(min(nfr, 8)):
+        tr.render_view(f % len(cams), img)
+    render_stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
+    tr.enable_timing(False)
     # ---- end to end: targets from pinned host memory every step -----------
     tr.targets = [t.cpu().pin_memory() for t in tr.targets]
     tr.device_targets = False
@@ -328,6 +333,7 @@ def run_ours(args):
                    "scene_build_s": round(build_s, 1), "setup_s": round(setup_s, 1)},
         "stage_ms": stage_ms,
         "render_fps": render_fps,
+        "render_stage_ms": render_stage_ms,
         "e2e": {"value": world * args.steps / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),

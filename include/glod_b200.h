@@ -90,6 +90,9 @@ typedef struct glod_spt_compact_in {
   const int32_t* n_spt;         /* [dev] scalar                               */
   const int32_t* spt_ids;       /* [dev] [n_spt]                              */
   const double* dist;           /* [dev] [n_spt] cut distance per SPT         */
+  const int32_t* known_prefix;  /* [dev] [n_spt] #{key_parent > dist} when the
+                                   caller already has it (select output, cache
+                                   entry), or NULL: binary search            */
 } glod_spt_compact_in;
 
 typedef struct glod_spt_compact_out {

@@ -39,7 +39,7 @@ class SelectOut(C.Structure):
 
 
 class CompactIn(C.Structure):
-    _fields_ = [("n_spt", P), ("spt_ids", P), ("dist", P)]
+    _fields_ = [("n_spt", P), ("spt_ids", P), ("dist", P), ("known_prefix", P)]
 
 
 class CompactOut(C.Structure):

@@ -340,15 +340,44 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   const int n_spt = *in.n_spt;
   const K* key_self = static_cast<const K*>(sc.key_self);
 
-  // phase A: prefix length and root rule per selected SPT (spt.py:70-73)
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_spt; j += gthreads) {
-    const int s = in.spt_ids[j];
-    const double d = in.dist[j];
-    const int pl = prefix_len_of(sc, s, d);
-    const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
-    out.prefix_len[j] = pl;
-    out.root_rule[j] = rr;
-    out.seg_start[j] = rr ? 1 : pl;          // segment length, scanned below
+  // phase A: prefix length and root rule per selected SPT (spt.py:70-73);
+  // the prefix comes from the caller when known, else a warp-cooperative
+  // 32-ary search over key_parent (one warp per SPT)
+  {
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = gthreads >> 5;
+    for (long long j = gw; j < n_spt; j += nw) {
+      const int s = in.spt_ids[j];
+      const double d = in.dist[j];
+      int pl;
+      if (in.known_prefix) {
+        pl = in.known_prefix[j];
+      } else {
+        const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
+        long long a = 0, b = sc.spt_count[s];        // answer in [a, b]
+        while (b - a > 32) {
+          const long long step = (b - a + 31) / 32;
+          const long long probe = a + step * lane;    // lane 0 probes a (known > d or start)
+          const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
+          const unsigned m = __ballot_sync(0xffffffffu, gt);
+          const int last = 31 - __clz(m);             // last probe with key_parent > d
+          const long long na = a + step * last;
+          b = min(b, na + step);
+          a = na;
+        }
+        // finish linearly over ≤ 32 candidates
+        const long long probe = a + lane;
+        const bool gt = probe < b && double(kp[probe]) > d;
+        const unsigned m = __ballot_sync(0xffffffffu, gt);
+        pl = int(a + __popc(m));
+      }
+      const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
+      if (lane == 0) {
+        out.prefix_len[j] = pl;
+        out.root_rule[j] = rr;
+        out.seg_start[j] = rr ? 1 : pl;          // segment length, scanned below
+      }
+    }
   }
   grid_sync(ws.bar);
 

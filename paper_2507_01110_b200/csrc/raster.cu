@@ -25,6 +25,7 @@ constexpr double kShC1 = 0.4886025119029199;
 constexpr float kAlphaMax = 0.99f;
 constexpr double kTEps = 1e-4;
 constexpr float kQMax = 32.0f;   // 2 * (3 + 1)^2
+constexpr int kPruneMaxTiles = 64;   // splats spanning more tiles keep their full bbox
 
 struct CamD {
   double p[3], W[9], fx, fy, cx, cy, near_;
@@ -199,9 +200,13 @@ __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n,
   sp.idx = int(i);
   const int tx0 = x0 / kTileW, tx1 = (x1 - 1) / kTileW;
   const int ty0 = y0 / kTileH, ty1 = (y1 - 1) / kTileH;
-  int nt = 0;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) nt += tile_hit(sp, tx, ty);
+  const int nbox = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  int nt = nbox;
+  if (nbox <= kPruneMaxTiles) {                // exact ellipse test for normal splats
+    nt = 0;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) nt += tile_hit(sp, tx, ty);
+  }
   if (nt == 0) return;                         // every bbox pixel has q > 32: α = 0
   splats[i] = sp;
   keys[i] = __double_as_longlong(depth);       // positive doubles order as uint64
@@ -228,9 +233,10 @@ __global__ void emit_kernel(const Splat* __restrict__ sorted, const int* __restr
   const int tx0 = sp.x0 / kTileW, tx1 = (sp.x1 - 1) / kTileW;
   const int ty0 = sp.y0 / kTileH, ty1 = (sp.y1 - 1) / kTileH;
   long long o = offs[r];
+  const bool prune = (tx1 - tx0 + 1) * (ty1 - ty0 + 1) <= kPruneMaxTiles;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
-      if (!tile_hit(sp, tx, ty)) continue;
+      if (prune && !tile_hit(sp, tx, ty)) continue;
       ikey[o] = unsigned(ty * tw + tx);
       ival[o] = int(r);
       ++o;

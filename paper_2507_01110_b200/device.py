@@ -170,8 +170,9 @@ class DeviceLodScene:
                             self.o_counts)
 
     def compact(self, n_spt: torch.Tensor, spt_ids: torch.Tensor, dist: torch.Tensor,
-                stream=None) -> CompactResult:
-        cin = _lib.CompactIn(n_spt=_lib.ptr(n_spt), spt_ids=_lib.ptr(spt_ids), dist=_lib.ptr(dist))
+                known_prefix: torch.Tensor | None = None, stream=None) -> CompactResult:
+        cin = _lib.CompactIn(n_spt=_lib.ptr(n_spt), spt_ids=_lib.ptr(spt_ids), dist=_lib.ptr(dist),
+                             known_prefix=_lib.ptr(known_prefix))
         cout = _lib.CompactOut(prefix_len=_lib.ptr(self.c_prefix), root_rule=_lib.ptr(self.c_rootrule),
                                seg_start=_lib.ptr(self.c_segstart), sel_seg=_lib.ptr(self.c_seg),
                                sel_pos=_lib.ptr(self.c_pos), sel_node=_lib.ptr(self.c_node),
@@ -186,7 +187,7 @@ class DeviceLodScene:
     def cut(self, cam: Camera, cfg: LodConfig, cull: bool = True):
         from .hspt import RenderSet, SptSelection
         sel = self.select(cam, cfg, cull)
-        cmp = self.compact(sel.counts[2:3], sel.spt_ids, sel.d_root)
+        cmp = self.compact(sel.counts[2:3], sel.spt_ids, sel.d_root, known_prefix=sel.prefix_len)
         counts = sel.counts.cpu().numpy()
         n_up, n_pa, n_sp = int(counts[0]), int(counts[1]), int(counts[2])
         total = int(cmp.total[0].item())

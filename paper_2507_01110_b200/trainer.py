@@ -138,6 +138,8 @@ class Trainer:
         self._h_blk = torch.empty(2 * S1, dtype=torch.int64).pin_memory()       # ptr | rows
         self._d_dist = torch.empty(S1, dtype=torch.float64, device=dev)
         self._d_blk = torch.empty(2 * S1, dtype=torch.int64, device=dev)
+        self._h_pref = torch.empty(S1, dtype=torch.int32).pin_memory()
+        self._d_pref = torch.empty(S1, dtype=torch.int32, device=dev)
         self._h_total = torch.empty(2, dtype=torch.int64).pin_memory()
         self._h_loss = torch.empty(3, dtype=torch.float64).pin_memory()
         self._rows = None
@@ -218,10 +220,13 @@ class Trainer:
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
         if n_sp:
+            # the prefix at the cached distance is the entry's prefix_len
+            self._h_pref.numpy()[:n_sp] = hb[S1:S1 + n_sp]
             self._d_dist.copy_(self._h_dist, non_blocking=True)
             self._d_blk.copy_(self._h_blk, non_blocking=True)
+            self._d_pref.copy_(self._h_pref, non_blocking=True)
         self._mark("cache")
-        cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist)
+        cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist, known_prefix=self._d_pref)
         self._h_total.copy_(cmp.total, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         self._mark("compact")
