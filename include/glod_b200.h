@@ -279,6 +279,18 @@ int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
 /* Resident entries in LRU order (front first), up to `capacity`. */
 int glod_cache_entries(const glod_cache* c, int32_t* spt_id, double* cached_distance,
                        int64_t* prefix_len, uint64_t* block, int32_t* dirty, int64_t capacity);
+/* K6 stable LSD radix sort of (key, int32 value) pairs by key bits
+ * [begin_bit, end_bit) — the rasteriser's depth order and tile binning,
+ * exported for direct use/testing.  keys/vals and their *_alt buffers:
+ * [dev] length n; the sorted result ends in the alternates when
+ * *result_in_alt == 1.  scratch: glod_sort_scratch_bytes(n) bytes. */
+int64_t glod_sort_scratch_bytes(int64_t n);
+int glod_sort_pairs_u64(uint64_t* keys, uint64_t* keys_alt, int32_t* vals, int32_t* vals_alt,
+                        int64_t n, int32_t begin_bit, int32_t end_bit, void* scratch,
+                        int64_t scratch_bytes, int32_t* result_in_alt, void* stream);
+int glod_sort_pairs_u32(uint32_t* keys, uint32_t* keys_alt, int32_t* vals, int32_t* vals_alt,
+                        int64_t n, int32_t begin_bit, int32_t end_bit, void* scratch,
+                        int64_t scratch_bytes, int32_t* result_in_alt, void* stream);
 /* Synchronous device→host copy (snapshots / tests). */
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 

@@ -112,6 +112,11 @@ SIGNATURES = {
     "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
     "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
     "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),
+    "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
+    "glod_sort_pairs_u64": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
+                                      C.POINTER(C.c_int32), P]),
+    "glod_sort_pairs_u32": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
+                                      C.POINTER(C.c_int32), P]),
 }
 
 _LIB = None

@@ -289,41 +289,6 @@ CompactScratch carve_compact(void* base, int32_t S, int64_t R, int grid) {
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-// Decoupled look-back by one warp over windows of 32 predecessors
-// (aggregates are summed until the nearest inclusive prefix is found).
-GLOD_DEV long long lookback(unsigned long long* status, long long t, int agg, int lane) {
-  if (t == 0) {
-    if (lane == 0) atomicExch(status, kFlagIncl | (unsigned long long)agg);
-    return 0;
-  }
-  if (lane == 0) atomicExch(status + t, kFlagAgg | (unsigned long long)agg);
-  long long excl = 0;
-  long long p = t - 1 - lane;
-  while (true) {
-    unsigned long long w = (2ull << 62);
-    if (p >= 0) w = *((volatile unsigned long long*)(status + p));
-    while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
-      if ((w >> 62) == 0) {
-        __nanosleep(16);
-        w = *((volatile unsigned long long*)(status + p));
-      }
-    }
-    const unsigned incl = __ballot_sync(0xffffffffu, (w >> 62) == 2);
-    long long v = (long long)(w & kValMask);
-    if (incl) {
-      const int first = __ffs(incl) - 1;      // nearest inclusive predecessor
-      if (lane > first) v = 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    excl += v;
-    if (incl) break;
-    p -= 32;
-  }
-  if (lane == 0) atomicExch(status + t, kFlagIncl | (unsigned long long)(excl + agg));
-  return excl;
-}
-
 template <typename K>
 __global__ void __launch_bounds__(kCompactThreads)
 compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
@@ -407,140 +372,162 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   }
   grid_sync(ws.bar);
 
-  // phase C: tiles of the virtual record space, single pass with look-back
+  // phase C: the virtual record space is split into one contiguous chunk
+  // per block.  C1 counts each chunk's selected records, a grid barrier
+  // and a block-level prefix give every chunk its output offset, C2
+  // re-streams the chunk and writes the selections in order.  (A one-pass
+  // decoupled look-back serialises on the inclusive-prefix chain across the
+  // ~300 concurrently running tiles; the second read of a chunk is mostly
+  // an L2 hit for the prefix sizes a view produces.)
   const long long total = ld_cg(out.total + 1);
   const long long ntiles = (total + kTile - 1) / kTile;
   if (ntiles == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) out.total[0] = 0;
     return;
   }
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const long long tbase = t * kTile;
-    const long long tend = min(total, tbase + kTile);
-    if (threadIdx.x == 0) {
-      // segments overlapping [tbase, tend): upper_bound(seg_start, x) - 1
-      int a = 0, b = n_spt;
-      while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
-      seg_lo_sh = a - 1;
-      int c = a, e = n_spt;
-      while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
-      seg_hi_sh = c - 1;
-      const int j = a - 1;
-      const int sp = in.spt_ids[j];
-      seg_start_sh = ld_cg(out.seg_start + j);
-      seg_off_sh = sc.spt_offset[sp];
-      seg_d_sh = in.dist[j];
-      seg_rr_sh = ld_cg(out.root_rule + j);
-      seg_rootrec_sh = sc.spt_root_rec[sp];
+  const long long t_lo = ntiles * blockIdx.x / gridDim.x, t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
+  long long mine = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    long long run = 0;
+    if (pass == 1) {
+      run = sum_before(ws.block_cnt, blockIdx.x, sm);
+      if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out.total[0] = run + mine;
     }
-    __syncthreads();
-    const int jlo = seg_lo_sh, jhi = seg_hi_sh;
-    bool pred[kRows];
-    int seg_of[kRows], pos_of[kRows];
-    if (jlo == jhi && !seg_rr_sh) {
-      // fast path: the whole tile is inside one SPT prefix — a straight
-      // coalesced stream of key_self compared against one distance
-      const long long s0 = seg_start_sh, off = seg_off_sh;
-      const double d = seg_d_sh;
-      K kv[kRows];
-#pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-        kv[k] = vi < tend ? key_self[off + (vi - s0)] : K(0);
+    long long count = 0;
+    for (long long t = t_lo; t < t_hi; ++t) {
+      const long long tbase = t * kTile;
+      const long long tend = min(total, tbase + kTile);
+      if (threadIdx.x == 0) {
+        // segments overlapping [tbase, tend): upper_bound(seg_start, x) - 1
+        int a = 0, b = n_spt;
+        while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
+        seg_lo_sh = a - 1;
+        int c = a, e = n_spt;
+        while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
+        seg_hi_sh = c - 1;
+        const int j = a - 1;
+        const int sp = in.spt_ids[j];
+        seg_start_sh = ld_cg(out.seg_start + j);
+        seg_off_sh = sc.spt_offset[sp];
+        seg_d_sh = in.dist[j];
+        seg_rr_sh = ld_cg(out.root_rule + j);
       }
+      __syncthreads();
+      const int jlo = seg_lo_sh, jhi = seg_hi_sh;
+      bool pred[kRows];
+      int seg_of[kRows], pos_of[kRows];
+      if (jlo == jhi && !seg_rr_sh) {
+        // fast path: the whole tile is inside one SPT prefix — a straight
+        // coalesced stream of key_self compared against one distance
+        const long long s0 = seg_start_sh, off = seg_off_sh;
+        const double d = seg_d_sh;
+        K kv[kRows];
 #pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-        pred[k] = vi < tend && double(kv[k]) <= d;
-        seg_of[k] = jlo;
-        pos_of[k] = int(vi - s0);
-      }
-    } else {
-      int jcur = jlo;
+        for (int k = 0; k < kRows; ++k) {
+          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+          kv[k] = vi < tend ? key_self[off + (vi - s0)] : K(0);
+        }
 #pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-        pred[k] = false;
-        seg_of[k] = -1;
-        pos_of[k] = 0;
-        if (vi < tend) {
-          int j = jcur;
-          if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
-            int a = jcur, b = jhi + 1;
-            while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
-            j = a - 1;
-            jcur = j;
+        for (int k = 0; k < kRows; ++k) {
+          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+          pred[k] = vi < tend && double(kv[k]) <= d;
+          seg_of[k] = jlo;
+          pos_of[k] = int(vi - s0);
+        }
+      } else {
+        int jcur = jlo;
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
+          pred[k] = false;
+          seg_of[k] = -1;
+          pos_of[k] = 0;
+          if (vi < tend) {
+            int j = jcur;
+            if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
+              int a = jcur, b = jhi + 1;
+              while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
+              j = a - 1;
+              jcur = j;
+            }
+            const long long local = vi - ld_cg(out.seg_start + j);
+            const int s = in.spt_ids[j];
+            const int64_t off = sc.spt_offset[s];
+            int rec;
+            bool p;
+            if (ld_cg(out.root_rule + j)) {
+              rec = sc.spt_root_rec[s];
+              p = true;
+            } else {
+              rec = int(local);
+              p = double(key_self[off + rec]) <= in.dist[j];
+            }
+            pred[k] = p;
+            seg_of[k] = j;
+            pos_of[k] = rec;
           }
-          const long long local = vi - ld_cg(out.seg_start + j);
-          const int s = in.spt_ids[j];
-          const int64_t off = sc.spt_offset[s];
-          int rec;
-          bool p;
-          if (ld_cg(out.root_rule + j)) {
-            rec = sc.spt_root_rec[s];
-            p = true;
-          } else {
-            rec = int(local);
-            p = double(key_self[off + rec]) <= in.dist[j];
-          }
-          pred[k] = p;
-          seg_of[k] = j;
-          pos_of[k] = rec;
         }
       }
+      if (pass == 0) {
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) count += pred[k];
+        __syncthreads();     // segment scalars are rewritten for the next tile
+        continue;
+      }
+      unsigned ball[kRows];
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) {
+        ball[k] = __ballot_sync(0xffffffffu, pred[k]);
+        if (lane == 0) cnt[k][warp] = __popc(ball[k]);
+      }
+      __syncthreads();
+      // exclusive scan over (row, warp) in row-major order: kRows*nwarps = 128 values
+      if (warp == 0) {
+        constexpr int per = kRows * (kCompactThreads / 32) / 32;   // 4
+        int vals[per];
+        int s = 0;
+#pragma unroll
+        for (int q = 0; q < per; ++q) {
+          int idx = lane * per + q;
+          vals[q] = cnt[idx / nwarps][idx % nwarps];
+          s += vals[q];
+        }
+        int incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int rn = incl - s;
+#pragma unroll
+        for (int q = 0; q < per; ++q) {
+          int idx = lane * per + q;
+          cnt[idx / nwarps][idx % nwarps] = rn;
+          rn += vals[q];
+        }
+        if (lane == 31) tile_base_sh = incl;      // tile aggregate
+      }
+      __syncthreads();
+      const long long tb = run;
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) {
+        if (pred[k]) {
+          const long long o = tb + cnt[k][warp] + __popc(ball[k] & lanemask_lt());
+          const int j = seg_of[k];
+          const int64_t off = (jlo == jhi) ? seg_off_sh : sc.spt_offset[in.spt_ids[j]];
+          out.sel_seg[o] = j;
+          out.sel_pos[o] = pos_of[k];
+          out.sel_node[o] = sc.rec_node[off + pos_of[k]];
+        }
+      }
+      run += tile_base_sh;
+      __syncthreads();
     }
-    unsigned ball[kRows];
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      ball[k] = __ballot_sync(0xffffffffu, pred[k]);
-      if (lane == 0) cnt[k][warp] = __popc(ball[k]);
+    if (pass == 0) {
+      mine = block_sum(count, sm);
+      if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = mine;
+      grid_sync(ws.bar);
     }
-    __syncthreads();
-    // exclusive scan over (row, warp) in row-major order: kRows*nwarps = 128 values
-    if (warp == 0) {
-      constexpr int per = kRows * (kCompactThreads / 32) / 32;   // 4
-      int vals[per];
-      int s = 0;
-#pragma unroll
-      for (int q = 0; q < per; ++q) {
-        int idx = lane * per + q;
-        vals[q] = cnt[idx / nwarps][idx % nwarps];
-        s += vals[q];
-      }
-      int incl = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int run = incl - s;
-#pragma unroll
-      for (int q = 0; q < per; ++q) {
-        int idx = lane * per + q;
-        cnt[idx / nwarps][idx % nwarps] = run;
-        run += vals[q];
-      }
-      const int agg = __shfl_sync(0xffffffffu, incl, 31);
-      const long long excl = lookback(ws.status, t, agg, lane);
-      if (lane == 0) {
-        tile_base_sh = excl;
-        if (t == ntiles - 1) out.total[0] = excl + agg;
-      }
-    }
-    __syncthreads();
-    const long long tb = tile_base_sh;
-#pragma unroll
-    for (int k = 0; k < kRows; ++k) {
-      if (pred[k]) {
-        const long long o = tb + cnt[k][warp] + __popc(ball[k] & lanemask_lt());
-        const int j = seg_of[k];
-        const int64_t off = (jlo == jhi) ? seg_off_sh : sc.spt_offset[in.spt_ids[j]];
-        out.sel_seg[o] = j;
-        out.sel_pos[o] = pos_of[k];
-        out.sel_node[o] = sc.rec_node[off + pos_of[k]];
-      }
-    }
-    __syncthreads();
   }
 }
 

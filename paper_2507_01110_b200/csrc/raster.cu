@@ -9,7 +9,6 @@
 //   K7 blend_fwd_kernel    compositing loop          (renderer.py:131-165)
 //   K8 blend_bwd_kernel    reverse loop, 2D partials (renderer.py:219-261)
 //   K9 preprocess_bwd_kernel 2D→3D chain rule        (renderer.py:262-303)
-#include <cub/cub.cuh>
 #include <stdio.h>
 #include <string>
 
@@ -17,6 +16,15 @@
 #include "raster.cuh"
 
 namespace glod {
+
+size_t radix_scratch_bytes(long long n);
+size_t scan_scratch_bytes(long long n);
+template <typename K>
+cudaError_t radix_sort_pairs(K* keys, K* keys_alt, int* vals, int* vals_alt, long long n, int begin_bit,
+                             int end_bit, void* scratch, size_t scratch_bytes, bool range_bits,
+                             int* result_in_alt, cudaStream_t st);
+cudaError_t exclusive_scan_i32(const int* in, long long* out, long long n, void* scratch, size_t bytes,
+                               cudaStream_t st);
 
 namespace {
 
@@ -625,6 +633,8 @@ struct RasterCtx {
   int bad_section = -1, bad_index = -1;
   cudaStream_t stream = nullptr;
   bool have_forward = false;
+  const unsigned* ikey_sorted = nullptr;
+  const int* ival_sorted = nullptr;
 };
 
 static int bits_for(long long v) {
@@ -686,25 +696,19 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   preprocess_kernel<<<nb, TB, 0, st>>>(attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
                                        R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>());
   CK(cudaGetLastError());
-  // global stable sort on fp64 depth bits (ties keep index order)
-  size_t tb_sort = 0, tb_scan = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  (int*)nullptr, (int*)nullptr, int(n), 0, 64, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, (int*)nullptr, (long long*)nullptr, int(n + 1), st);
-  CK(R->temp.ensure(std::max(tb_sort, tb_scan), st));
-  size_t tb = R->temp.cap;
-  CK(cub::DeviceRadixSort::SortPairs(R->temp.p, tb, R->keys.as<unsigned long long>(),
-                                     R->keys2.as<unsigned long long>(), R->vals.as<int>(),
-                                     R->vals2.as<int>(), int(n), 0, 64, st));
-  const int* order = R->vals2.as<int>();
+  // global stable sort on fp64 depth bits (ties keep index order), K6
+  CK(R->temp.ensure(std::max(radix_scratch_bytes(n), scan_scratch_bytes(n + 1)), st));
+  int alt = 0;
+  CK(radix_sort_pairs<unsigned long long>(R->keys.as<unsigned long long>(), R->keys2.as<unsigned long long>(),
+                                          R->vals.as<int>(), R->vals2.as<int>(), n, 0, 64, R->temp.p,
+                                          R->temp.cap, true, &alt, st));
+  const int* order = alt ? R->vals2.as<int>() : R->vals.as<int>();
   count_launch();
   gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
                                    R->tiles_sorted.as<int>(), n);
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(R->tiles_sorted.as<int>() + n, 0, 4, st));
-  tb = R->temp.cap;
-  CK(cub::DeviceScan::ExclusiveSum(R->temp.p, tb, R->tiles_sorted.as<int>(), R->offs.as<long long>(),
-                                   int(n + 1), st));
+  CK(exclusive_scan_i32(R->tiles_sorted.as<int>(), R->offs.as<long long>(), n + 1, R->temp.p, R->temp.cap, st));
   long long* hp = static_cast<long long*>(R->host_pin.p);
   CK(cudaMemcpyAsync(hp, R->offs.as<long long>() + n, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hp + 1, R->bad.p, 32, cudaMemcpyDeviceToHost, st));
@@ -729,20 +733,18 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   CK(cudaGetLastError());
   if (n_inst > 0) {
     const int kb = bits_for(ntiles);
-    size_t need = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, need, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
-                                    (int*)nullptr, int(n_inst), 0, kb, st);
-    CK(R->temp.ensure(need, st));
-    tb = R->temp.cap;
-    CK(cub::DeviceRadixSort::SortPairs(R->temp.p, tb, R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(),
-                                       R->ival.as<int>(), R->ival2.as<int>(), int(n_inst), 0, kb, st));
+    CK(R->temp.ensure(radix_scratch_bytes(n_inst), st));
+    int alt2 = 0;
+    CK(radix_sort_pairs<unsigned>(R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(), R->ival.as<int>(),
+                                  R->ival2.as<int>(), n_inst, 0, kb, R->temp.p, R->temp.cap, false, &alt2, st));
+    R->ikey_sorted = alt2 ? R->ikey2.as<unsigned>() : R->ikey.as<unsigned>();
+    R->ival_sorted = alt2 ? R->ival2.as<int>() : R->ival.as<int>();
     count_launch();
-    ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey2.as<unsigned>(), n_inst,
-                                                              R->range.as<int2>());
+    ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey_sorted, n_inst, R->range.as<int2>());
     CK(cudaGetLastError());
   }
   count_launch();
-  blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
+  blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                        R->range.as<int2>(), cam, image,
                                                        R->tfinal.as<double>(), R->last.as<int>());
   return cudaGetLastError();
@@ -755,12 +757,13 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   const int ntiles = cam.tw * cam.th;
   CK(R->g2.ensure(8 * kG2 * (size_t)n, st));
   CK(cudaMemsetAsync(R->g2.p, 0, 8 * kG2 * (size_t)n, st));
-  if (R->n_inst > 0)
+  if (R->n_inst > 0) {
     count_launch();
-    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival2.as<int>(),
+    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                          R->range.as<int2>(), cam, dimg,
                                                          R->tfinal.as<double>(), R->last.as<int>(),
                                                          R->g2.as<double>());
+  }
   CK(cudaGetLastError());
   const int TB = 128;
   count_launch();
