@@ -13,6 +13,8 @@
 // all selected SPTs at once: the selected prefixes are laid end to end in a
 // virtual index space and compacted by a single order-preserving pass with
 // decoupled look-back, so each key_self is read exactly once.
+#include <climits>
+
 #include "common.cuh"
 #include "lod.cuh"
 
@@ -394,23 +396,52 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out.total[0] = run + mine;
     }
     long long count = 0;
+    if (threadIdx.x == 0) seg_lo_sh = -1;
+    __syncthreads();
     for (long long t = t_lo; t < t_hi; ++t) {
       const long long tbase = t * kTile;
       const long long tend = min(total, tbase + kTile);
-      if (threadIdx.x == 0) {
-        // segments overlapping [tbase, tend): upper_bound(seg_start, x) - 1
-        int a = 0, b = n_spt;
-        while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
-        seg_lo_sh = a - 1;
-        int c = a, e = n_spt;
-        while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
-        seg_hi_sh = c - 1;
-        const int j = a - 1;
-        const int sp = in.spt_ids[j];
-        seg_start_sh = ld_cg(out.seg_start + j);
-        seg_off_sh = sc.spt_offset[sp];
-        seg_d_sh = in.dist[j];
-        seg_rr_sh = ld_cg(out.root_rule + j);
+      if (warp == 0) {
+        // segments overlapping [tbase, tend).  Tiles of a chunk are visited
+        // in order, so the search starts at the previous tile's first
+        // segment: one coalesced probe of 32 seg_start values usually finds
+        // both ends (binary search only after long runs of tiny segments).
+        int jl = seg_lo_sh;
+        if (jl < 0) {          // first tile of the chunk: binary search
+          int a = 0, b = n_spt;
+          while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
+          jl = a - 1;
+        }
+        int jlo_new = -1, jhi_new = -1;
+        while (true) {
+          const int j = jl + lane;
+          const long long st_j = j < n_spt ? ld_cg(out.seg_start + j) : LLONG_MAX;
+          const unsigned le_lo = __ballot_sync(0xffffffffu, st_j <= tbase);
+          const unsigned le_hi = __ballot_sync(0xffffffffu, st_j <= tend - 1);
+          if (le_lo != 0xffffffffu || jl + 32 >= n_spt) {
+            // starts are non-decreasing: the set bits are a prefix of lanes
+            jlo_new = jl + __popc(le_lo) - 1;
+            if (le_hi != 0xffffffffu || jl + 32 >= n_spt) {
+              jhi_new = jl + __popc(le_hi) - 1;
+            } else {
+              int c = jl + 32, e = n_spt;   // tile spans many segments: binary search
+              while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
+              jhi_new = c - 1;
+            }
+            break;
+          }
+          jl += 31;
+        }
+        if (lane == 0) {
+          seg_lo_sh = jlo_new;
+          seg_hi_sh = jhi_new;
+          const int j = jlo_new;
+          const int sp = in.spt_ids[j];
+          seg_start_sh = ld_cg(out.seg_start + j);
+          seg_off_sh = sc.spt_offset[sp];
+          seg_d_sh = in.dist[j];
+          seg_rr_sh = ld_cg(out.root_rule + j);
+        }
       }
       __syncthreads();
       const int jlo = seg_lo_sh, jhi = seg_hi_sh;

@@ -41,21 +41,6 @@ hist_kernel(const K* __restrict__ keys, long long n, long long chunk, int shift,
   for (int d = threadIdx.x; d < kBins; d += kSortThreads) bh[(long long)d * nblocks + blockIdx.x] = h[d];
 }
 
-// single block: exclusive scan of kBins*nblocks counts in digit-major order
-__global__ void __launch_bounds__(1024) scan_kernel(unsigned* __restrict__ bh, long long m) {
-  __shared__ long long sm[1024 / 32 + 1];
-  const long long per = (m + blockDim.x - 1) / blockDim.x;
-  const long long a = per * threadIdx.x, b = min(m, a + per);
-  long long s = 0;
-  for (long long i = a; i < b; ++i) s += bh[i];
-  long long o = block_excl_scan(s, sm);
-  for (long long i = a; i < b; ++i) {
-    const unsigned v = bh[i];
-    bh[i] = unsigned(o);
-    o += v;
-  }
-}
-
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 scatter_kernel(const K* __restrict__ kin, K* __restrict__ kout, const int* __restrict__ vin,
@@ -147,8 +132,9 @@ __global__ void minmax_kernel(const K* __restrict__ keys, long long n, K* __rest
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 8;
 
+template <typename In>
 __global__ void __launch_bounds__(kScanThreads)
-scan_reduce_kernel(const int* __restrict__ in, long long n, long long* __restrict__ bsum) {
+scan_reduce_kernel(const In* __restrict__ in, long long n, long long* __restrict__ bsum) {
   __shared__ long long sm[kScanThreads / 32 + 1];
   const long long base = (long long)blockIdx.x * kScanThreads * kScanItems;
   long long s = 0;
@@ -177,22 +163,23 @@ scan_blocks_kernel(long long* __restrict__ bsum, int nb) {
 }
 
 // blocked arrangement per thread (kScanItems consecutive) for the final scan
+template <typename In, typename Out>
 __global__ void __launch_bounds__(kScanThreads)
-scan_final_kernel(const int* __restrict__ in, long long n, const long long* __restrict__ bsum,
-                  long long* __restrict__ out) {
+scan_final_kernel(const In* __restrict__ in, long long n, const long long* __restrict__ bsum,
+                  Out* __restrict__ out) {
   __shared__ long long sm[kScanThreads / 32 + 1];
   const long long base = (long long)blockIdx.x * kScanThreads * kScanItems + (long long)threadIdx.x * kScanItems;
-  int v[kScanItems];
+  long long v[kScanItems];
   long long s = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    v[k] = base + k < n ? in[base + k] : 0;
+    v[k] = base + k < n ? (long long)in[base + k] : 0;
     s += v[k];
   }
   long long o = bsum[blockIdx.x] + block_excl_scan(s, sm);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) out[base + k] = o;
+    if (base + k < n) out[base + k] = Out(o);
     o += v[k];
   }
 }
@@ -204,21 +191,30 @@ size_t scan_scratch_bytes(long long n) {
   return size_t(nb > 0 ? nb : 1) * 8 + 64;
 }
 
-// out[i] = sum(in[0..i)) for i in [0, n), int32 in → int64 out
-cudaError_t exclusive_scan_i32(const int* in, long long* out, long long n, void* scratch, size_t bytes,
-                               cudaStream_t st) {
+// out[i] = sum(in[0..i)) for i in [0, n): reduce / scan block sums / final
+template <typename In, typename Out>
+cudaError_t exclusive_scan(const In* in, Out* out, long long n, void* scratch, size_t bytes, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (bytes < scan_scratch_bytes(n)) return cudaErrorInvalidValue;
   const int nb = int((n + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems));
   long long* bsum = static_cast<long long*>(scratch);
   count_launch();
-  scan_reduce_kernel<<<nb, kScanThreads, 0, st>>>(in, n, bsum);
+  scan_reduce_kernel<In><<<nb, kScanThreads, 0, st>>>(in, n, bsum);
   count_launch();
   scan_blocks_kernel<<<1, kScanThreads, 0, st>>>(bsum, nb);
   count_launch();
-  scan_final_kernel<<<nb, kScanThreads, 0, st>>>(in, n, bsum, out);
+  scan_final_kernel<In, Out><<<nb, kScanThreads, 0, st>>>(in, n, bsum, out);
   return cudaGetLastError();
 }
+
+cudaError_t exclusive_scan_i32(const int* in, long long* out, long long n, void* scratch, size_t bytes,
+                               cudaStream_t st) {
+  return exclusive_scan<int, long long>(in, out, n, scratch, bytes, st);
+}
+
+size_t scan_scratch_bytes(long long n);
+template <typename In, typename Out>
+cudaError_t exclusive_scan(const In* in, Out* out, long long n, void* scratch, size_t bytes, cudaStream_t st);
 
 // Each block sorts a chunk of whole rounds; ~4 blocks per SM keeps the
 // digit-major histogram scan short.
@@ -228,10 +224,12 @@ long long chunk_for(long long n) {
   return (per < 1 ? 1 : per) * kRound;
 }
 
-// Scratch: histograms (256 × nblocks u32) + 2 × u64 min/max.
+// Scratch: histograms (256 × nblocks u32), their exclusive scan (u32),
+// 2 × u64 min/max, scan block sums.
 size_t radix_scratch_bytes(long long n) {
   const long long nb = (n + chunk_for(n) - 1) / chunk_for(n);
-  return size_t(kBins) * size_t(nb > 0 ? nb : 1) * 4 + 64;
+  const size_t m = size_t(kBins) * size_t(nb > 0 ? nb : 1);
+  return 2 * m * 4 + 64 + scan_scratch_bytes((long long)m) + 256;
 }
 
 // Sorts (keys, vals) of length n stably by key bits [begin_bit, end_bit).
@@ -247,9 +245,13 @@ cudaError_t radix_sort_pairs(K* keys, K* keys_alt, int* vals, int* vals_alt, lon
   if (scratch_bytes < radix_scratch_bytes(n)) return cudaErrorInvalidValue;
   const long long chunk = chunk_for(n);
   const int nblocks = int((n + chunk - 1) / chunk);
+  const size_t m = size_t(kBins) * nblocks;
   unsigned* bh = static_cast<unsigned*>(scratch);
-  unsigned long long* mm = reinterpret_cast<unsigned long long*>(static_cast<char*>(scratch) +
-                                                                   size_t(kBins) * nblocks * 4);
+  unsigned* bo = bh + m;
+  char* tail = static_cast<char*>(scratch) + 2 * m * 4;
+  unsigned long long* mm = reinterpret_cast<unsigned long long*>(tail);
+  void* scan_tmp = tail + 64;
+  const size_t scan_bytes = scratch_bytes - (2 * m * 4 + 64);
   if (range_bits) {
     unsigned long long init[2] = {~0ull, 0ull};
     cudaError_t e = cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
@@ -272,10 +274,10 @@ cudaError_t radix_sort_pairs(K* keys, K* keys_alt, int* vals, int* vals_alt, lon
   for (int shift = begin_bit; shift < end_bit; shift += 8) {
     count_launch();
     hist_kernel<K><<<nblocks, kSortThreads, 0, st>>>(kin, n, chunk, shift, bh, nblocks);
+    cudaError_t e = exclusive_scan<unsigned, unsigned>(bh, bo, (long long)m, scan_tmp, scan_bytes, st);
+    if (e != cudaSuccess) return e;
     count_launch();
-    scan_kernel<<<1, 1024, 0, st>>>(bh, (long long)kBins * nblocks);
-    count_launch();
-    scatter_kernel<K><<<nblocks, kSortThreads, 0, st>>>(kin, kout, vin, vout, n, chunk, shift, bh, nblocks);
+    scatter_kernel<K><<<nblocks, kSortThreads, 0, st>>>(kin, kout, vin, vout, n, chunk, shift, bo, nblocks);
     K* tk = kin; kin = kout; kout = tk;
     int* tv = vin; vin = vout; vout = tv;
     ++flips;
