@@ -26,6 +26,7 @@ constexpr int kSelectThreads = 512;
 constexpr int kCompactThreads = 512;
 constexpr int kRows = 8;                          // items per thread per tile
 constexpr int kTile = kCompactThreads * kRows;    // 4096 virtual records
+constexpr int kUnroll = 8;                        // keys per lane in flight (K1 phase C)
 constexpr int kMaxLevels = 250;
 
 constexpr uint32_t kPass = 1u << 31;   // entry belongs to a passthrough BFS
@@ -374,189 +375,111 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   }
   grid_sync(ws.bar);
 
-  // phase C: the virtual record space is split into one contiguous chunk
-  // per block.  C1 counts each chunk's selected records, a grid barrier
-  // and a block-level prefix give every chunk its output offset, C2
-  // re-streams the chunk and writes the selections in order.  (A one-pass
-  // decoupled look-back serialises on the inclusive-prefix chain across the
-  // ~300 concurrently running tiles; the second read of a chunk is mostly
-  // an L2 hit for the prefix sizes a view produces.)
+  // phase C: every warp owns a contiguous range of the virtual record space
+  // (the selected prefixes laid end to end).  C1 counts each warp range's
+  // selections; after a grid barrier each warp's output offset is the sum
+  // of all earlier ranges; C2 re-streams its range and writes the
+  // selections in order.  Inside a range everything is warp-synchronous:
+  // striped coalesced key loads (kUnroll×32 keys in flight per warp),
+  // ballot + popc for the in-order ranks, no block barriers.
   const long long total = ld_cg(out.total + 1);
-  const long long ntiles = (total + kTile - 1) / kTile;
-  if (ntiles == 0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) out.total[0] = 0;
-    return;
-  }
-  const long long t_lo = ntiles * blockIdx.x / gridDim.x, t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
-  long long mine = 0;
+  const long long nwarps_g = (long long)gridDim.x * nwarps;
+  const long long gwarp = (long long)blockIdx.x * nwarps + warp;
+  const long long r_lo = total * gwarp / nwarps_g, r_hi = total * (gwarp + 1) / nwarps_g;
+  __shared__ long long wcount[kCompactThreads / 32];
+  long long run = 0;
   for (int pass = 0; pass < 2; ++pass) {
-    long long run = 0;
     if (pass == 1) {
-      run = sum_before(ws.block_cnt, blockIdx.x, sm);
-      if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out.total[0] = run + mine;
+      // offset of this warp range = Σ earlier blocks + Σ earlier warps of this block
+      const long long blk = sum_before(ws.block_cnt, blockIdx.x, sm);
+      long long w_before = 0;
+      for (int w = 0; w < warp; ++w) w_before += wcount[w];
+      run = blk + w_before;
+      if (blockIdx.x == gridDim.x - 1 && warp == nwarps - 1 && lane == 0) out.total[0] = run + wcount[warp];
     }
+    // per-lane segment cursor
+    int j = -1;
+    long long s_start = 0, s_end = -1, off = 0;
+    double d = 0.0;
+    int rr = 0, rootrec = 0;
     long long count = 0;
-    if (threadIdx.x == 0) seg_lo_sh = -1;
-    __syncthreads();
-    for (long long t = t_lo; t < t_hi; ++t) {
-      const long long tbase = t * kTile;
-      const long long tend = min(total, tbase + kTile);
-      if (warp == 0) {
-        // segments overlapping [tbase, tend).  Tiles of a chunk are visited
-        // in order, so the search starts at the previous tile's first
-        // segment: one coalesced probe of 32 seg_start values usually finds
-        // both ends (binary search only after long runs of tiny segments).
-        int jl = seg_lo_sh;
-        if (jl < 0) {          // first tile of the chunk: binary search
-          int a = 0, b = n_spt;
-          while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= tbase) a = m + 1; else b = m; }
-          jl = a - 1;
-        }
-        int jlo_new = -1, jhi_new = -1;
-        while (true) {
-          const int j = jl + lane;
-          const long long st_j = j < n_spt ? ld_cg(out.seg_start + j) : LLONG_MAX;
-          const unsigned le_lo = __ballot_sync(0xffffffffu, st_j <= tbase);
-          const unsigned le_hi = __ballot_sync(0xffffffffu, st_j <= tend - 1);
-          if (le_lo != 0xffffffffu || jl + 32 >= n_spt) {
-            // starts are non-decreasing: the set bits are a prefix of lanes
-            jlo_new = jl + __popc(le_lo) - 1;
-            if (le_hi != 0xffffffffu || jl + 32 >= n_spt) {
-              jhi_new = jl + __popc(le_hi) - 1;
-            } else {
-              int c = jl + 32, e = n_spt;   // tile spans many segments: binary search
-              while (c < e) { int m = (c + e) >> 1; if (ld_cg(out.seg_start + m) <= tend - 1) c = m + 1; else e = m; }
-              jhi_new = c - 1;
-            }
-            break;
-          }
-          jl += 31;
-        }
-        if (lane == 0) {
-          seg_lo_sh = jlo_new;
-          seg_hi_sh = jhi_new;
-          const int j = jlo_new;
-          const int sp = in.spt_ids[j];
-          seg_start_sh = ld_cg(out.seg_start + j);
-          seg_off_sh = sc.spt_offset[sp];
-          seg_d_sh = in.dist[j];
-          seg_rr_sh = ld_cg(out.root_rule + j);
-        }
-      }
-      __syncthreads();
-      const int jlo = seg_lo_sh, jhi = seg_hi_sh;
-      bool pred[kRows];
-      int seg_of[kRows], pos_of[kRows];
-      if (jlo == jhi && !seg_rr_sh) {
-        // fast path: the whole tile is inside one SPT prefix — a straight
-        // coalesced stream of key_self compared against one distance
-        const long long s0 = seg_start_sh, off = seg_off_sh;
-        const double d = seg_d_sh;
-        K kv[kRows];
+    for (long long base = r_lo; base < r_hi; base += 32LL * kUnroll) {
+      K kv[kUnroll];
+      int rec[kUnroll];
+      bool ok[kUnroll];
 #pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-          kv[k] = vi < tend ? key_self[off + (vi - s0)] : K(0);
-        }
-#pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-          pred[k] = vi < tend && double(kv[k]) <= d;
-          seg_of[k] = jlo;
-          pos_of[k] = int(vi - s0);
-        }
-      } else {
-        int jcur = jlo;
-#pragma unroll
-        for (int k = 0; k < kRows; ++k) {
-          const long long vi = tbase + (long long)k * kCompactThreads + threadIdx.x;
-          pred[k] = false;
-          seg_of[k] = -1;
-          pos_of[k] = 0;
-          if (vi < tend) {
-            int j = jcur;
-            if (jlo != jhi) {   // advance to the segment containing vi (rows increase)
-              int a = jcur, b = jhi + 1;
-              while (a < b) { int m = (a + b) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else b = m; }
+      for (int k = 0; k < kUnroll; ++k) {
+        const long long vi = base + (long long)k * 32 + lane;
+        ok[k] = vi < r_hi;
+        rec[k] = 0;
+        if (ok[k]) {
+          if (vi >= s_end) {                         // move the cursor (usually 0-1 steps)
+            if (j < 0 || vi >= s_end + 64) {
+              int a = (j < 0 ? 0 : j), bb = n_spt;
+              while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else bb = m; }
               j = a - 1;
-              jcur = j;
-            }
-            const long long local = vi - ld_cg(out.seg_start + j);
-            const int s = in.spt_ids[j];
-            const int64_t off = sc.spt_offset[s];
-            int rec;
-            bool p;
-            if (ld_cg(out.root_rule + j)) {
-              rec = sc.spt_root_rec[s];
-              p = true;
             } else {
-              rec = int(local);
-              p = double(key_self[off + rec]) <= in.dist[j];
+              while (j + 1 < n_spt && ld_cg(out.seg_start + j + 1) <= vi) ++j;
             }
-            pred[k] = p;
-            seg_of[k] = j;
-            pos_of[k] = rec;
+            s_start = ld_cg(out.seg_start + j);
+            s_end = j + 1 < n_spt ? ld_cg(out.seg_start + j + 1) : total;
+            const int sp = in.spt_ids[j];
+            off = sc.spt_offset[sp];
+            d = in.dist[j];
+            rr = ld_cg(out.root_rule + j);
+            rootrec = sc.spt_root_rec[sp];
           }
+          rec[k] = rr ? rootrec : int(vi - s_start);
         }
       }
-      if (pass == 0) {
+      // the cursor state is per lane; the key loads below are independent
 #pragma unroll
-        for (int k = 0; k < kRows; ++k) count += pred[k];
-        __syncthreads();     // segment scalars are rewritten for the next tile
-        continue;
-      }
-      unsigned ball[kRows];
+      for (int k = 0; k < kUnroll; ++k) kv[k] = ok[k] ? key_self[off + rec[k]] : K(0);
+      // (off/d/rr belong to the lane's segment at its last item; items of
+      // one lane can only straddle a boundary within a step, handled below)
 #pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        ball[k] = __ballot_sync(0xffffffffu, pred[k]);
-        if (lane == 0) cnt[k][warp] = __popc(ball[k]);
-      }
-      __syncthreads();
-      // exclusive scan over (row, warp) in row-major order: kRows*nwarps = 128 values
-      if (warp == 0) {
-        constexpr int per = kRows * (kCompactThreads / 32) / 32;   // 4
-        int vals[per];
-        int s = 0;
-#pragma unroll
-        for (int q = 0; q < per; ++q) {
-          int idx = lane * per + q;
-          vals[q] = cnt[idx / nwarps][idx % nwarps];
-          s += vals[q];
+      for (int k = 0; k < kUnroll; ++k) {
+        bool p = false;
+        int seg = j;
+        long long o_k = off;
+        double d_k = d;
+        int rr_k = rr;
+        if (ok[k]) {
+          const long long vi = base + (long long)k * 32 + lane;
+          if (vi < s_start) {                        // this item is in an earlier segment
+            int a = 0, bb = j;
+            while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else bb = m; }
+            seg = a - 1;
+            const int sp = in.spt_ids[seg];
+            o_k = sc.spt_offset[sp];
+            d_k = in.dist[seg];
+            rr_k = ld_cg(out.root_rule + seg);
+            rec[k] = rr_k ? sc.spt_root_rec[sp] : int(vi - ld_cg(out.seg_start + seg));
+            kv[k] = key_self[o_k + rec[k]];
+          }
+          p = rr_k ? true : double(kv[k]) <= d_k;
         }
-        int incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        int rn = incl - s;
-#pragma unroll
-        for (int q = 0; q < per; ++q) {
-          int idx = lane * per + q;
-          cnt[idx / nwarps][idx % nwarps] = rn;
-          rn += vals[q];
-        }
-        if (lane == 31) tile_base_sh = incl;      // tile aggregate
-      }
-      __syncthreads();
-      const long long tb = run;
-#pragma unroll
-      for (int k = 0; k < kRows; ++k) {
-        if (pred[k]) {
-          const long long o = tb + cnt[k][warp] + __popc(ball[k] & lanemask_lt());
-          const int j = seg_of[k];
-          const int64_t off = (jlo == jhi) ? seg_off_sh : sc.spt_offset[in.spt_ids[j]];
-          out.sel_seg[o] = j;
-          out.sel_pos[o] = pos_of[k];
-          out.sel_node[o] = sc.rec_node[off + pos_of[k]];
+        const unsigned bal = __ballot_sync(0xffffffffu, p);
+        if (pass == 0) {
+          count += __popc(bal);
+        } else {
+          if (p) {
+            const long long o = run + __popc(bal & lanemask_lt());
+            out.sel_seg[o] = seg;
+            out.sel_pos[o] = rec[k];
+            out.sel_node[o] = sc.rec_node[o_k + rec[k]];
+          }
+          run += __popc(bal);
         }
       }
-      run += tile_base_sh;
-      __syncthreads();
     }
     if (pass == 0) {
-      mine = block_sum(count, sm);
-      if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = mine;
+      if (lane == 0) wcount[warp] = count;
+      __syncthreads();
+      long long c = 0;
+      if (threadIdx.x < nwarps) c = wcount[threadIdx.x];
+      c = block_sum(c, sm);
+      if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = c;
       grid_sync(ws.bar);
     }
   }
