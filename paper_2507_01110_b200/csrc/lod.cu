@@ -293,7 +293,7 @@ constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 template <typename K>
-__global__ void __launch_bounds__(kCompactThreads)
+__global__ void __launch_bounds__(kCompactThreads, 2)
 compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   __shared__ long long sm[kCompactThreads / 32 + 1];
   __shared__ int cnt[kRows][kCompactThreads / 32];
@@ -437,6 +437,9 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       for (int k = 0; k < kUnroll; ++k) kv[k] = ok[k] ? key_self[off + rec[k]] : K(0);
       // (off/d/rr belong to the lane's segment at its last item; items of
       // one lane can only straddle a boundary within a step, handled below)
+      bool pk[kUnroll];
+      int segk[kUnroll];
+      long long offk[kUnroll];
 #pragma unroll
       for (int k = 0; k < kUnroll; ++k) {
         bool p = false;
@@ -459,18 +462,29 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
           }
           p = rr_k ? true : double(kv[k]) <= d_k;
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, p);
-        if (pass == 0) {
-          count += __popc(bal);
-        } else {
-          if (p) {
-            const long long o = run + __popc(bal & lanemask_lt());
-            out.sel_seg[o] = seg;
-            out.sel_pos[o] = rec[k];
-            out.sel_node[o] = sc.rec_node[o_k + rec[k]];
-          }
-          run += __popc(bal);
+        pk[k] = p;
+        segk[k] = seg;
+        offk[k] = o_k;
+      }
+      if (pass == 0) {
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) count += __popc(__ballot_sync(0xffffffffu, pk[k]));
+        continue;
+      }
+      // all node-id gathers in flight before the ordered stores
+      int node[kUnroll];
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) node[k] = pk[k] ? sc.rec_node[offk[k] + rec[k]] : 0;
+#pragma unroll
+      for (int k = 0; k < kUnroll; ++k) {
+        const unsigned bal = __ballot_sync(0xffffffffu, pk[k]);
+        if (pk[k]) {
+          const long long o = run + __popc(bal & lanemask_lt());
+          out.sel_seg[o] = segk[k];
+          out.sel_pos[o] = rec[k];
+          out.sel_node[o] = node[k];
         }
+        run += __popc(bal);
       }
     }
     if (pass == 0) {
