@@ -385,17 +385,24 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   const long long total = ld_cg(out.total + 1);
   const long long nwarps_g = (long long)gridDim.x * nwarps;
   const long long gwarp = (long long)blockIdx.x * nwarps + warp;
-  const long long r_lo = total * gwarp / nwarps_g, r_hi = total * (gwarp + 1) / nwarps_g;
   __shared__ long long wcount[kCompactThreads / 32];
+  // waves small enough that the second pass re-reads the keys from L2
+  const long long wave = sc.key_f64 ? (8ll << 20) : (16ll << 20);
+  long long wave_base = 0;                      // selections before this wave
+  for (long long w_lo = 0; w_lo < total || (total == 0 && w_lo == 0); w_lo += wave) {
+  const long long w_len = min(wave, total - w_lo);
+  const long long r_lo = w_lo + w_len * gwarp / nwarps_g, r_hi = w_lo + w_len * (gwarp + 1) / nwarps_g;
   long long run = 0;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
-      // offset of this warp range = Σ earlier blocks + Σ earlier warps of this block
+      // offset of this warp range = earlier waves + earlier blocks + earlier warps of this block
       const long long blk = sum_before(ws.block_cnt, blockIdx.x, sm);
+      const long long all = sum_before(ws.block_cnt, gridDim.x, sm);
       long long w_before = 0;
       for (int w = 0; w < warp; ++w) w_before += wcount[w];
-      run = blk + w_before;
-      if (blockIdx.x == gridDim.x - 1 && warp == nwarps - 1 && lane == 0) out.total[0] = run + wcount[warp];
+      run = wave_base + blk + w_before;
+      if (threadIdx.x == 0 && blockIdx.x == 0 && w_lo + w_len >= total) out.total[0] = wave_base + all;
+      wave_base += all;
     }
     // per-lane segment cursor
     int j = -1;
@@ -496,6 +503,9 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = c;
       grid_sync(ws.bar);
     }
+  }
+  grid_sync(ws.bar);            // block_cnt is rewritten by the next wave
+  if (total == 0) break;
   }
 }
 

@@ -444,10 +444,22 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
           c8 = dq * dy * dy;
         }
       }
-      if (!__any_sync(0xffffffffu, hit)) continue;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (bal == 0) continue;
+      double* dst = g2 + (long long)kG2 * g.idx;
+      if (__popc(bal) <= 2) {
+        // one or two hitting lanes: their partials go straight to the
+        // fp64 accumulators (cheaper than a 32-lane reduction)
+        if (hit) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c[u] != 0.f) atomicAdd(dst + u, double(c[u]));
+          if (c8 != 0.f) atomicAdd(dst + 8, double(c8));
+        }
+        continue;
+      }
       const float t8 = warp_reduce8(c, lane);
       const float s8 = warp_sum(c8);
-      double* dst = g2 + (long long)kG2 * g.idx;
       if ((lane & 3) == 0) {
         if (t8 != 0.f) atomicAdd(dst + (lane >> 2), double(t8));
       } else if (lane == 1) {
