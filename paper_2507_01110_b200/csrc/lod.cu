@@ -411,15 +411,16 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
     int rr = 0, rootrec = 0;
     long long count = 0;
     for (long long base = r_lo; base < r_hi; base += 32LL * kUnroll) {
-      K kv[kUnroll];
+      int segk[kUnroll];
       int rec[kUnroll];
-      bool ok[kUnroll];
+      long long addr[kUnroll];
 #pragma unroll
       for (int k = 0; k < kUnroll; ++k) {
         const long long vi = base + (long long)k * 32 + lane;
-        ok[k] = vi < r_hi;
+        segk[k] = -1;
         rec[k] = 0;
-        if (ok[k]) {
+        addr[k] = 0;
+        if (vi < r_hi) {
           if (vi >= s_end) {                         // move the cursor (usually 0-1 steps)
             if (j < 0 || vi >= s_end + 64) {
               int a = (j < 0 ? 0 : j), bb = n_spt;
@@ -436,42 +437,27 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
             rr = ld_cg(out.root_rule + j);
             rootrec = sc.spt_root_rec[sp];
           }
+          segk[k] = j;
           rec[k] = rr ? rootrec : int(vi - s_start);
+          addr[k] = off + rec[k];
         }
       }
-      // the cursor state is per lane; the key loads below are independent
+      K kv[kUnroll];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) kv[k] = ok[k] ? key_self[off + rec[k]] : K(0);
-      // (off/d/rr belong to the lane's segment at its last item; items of
-      // one lane can only straddle a boundary within a step, handled below)
+      for (int k = 0; k < kUnroll; ++k) kv[k] = segk[k] >= 0 ? key_self[addr[k]] : K(0);
       bool pk[kUnroll];
-      int segk[kUnroll];
-      long long offk[kUnroll];
 #pragma unroll
       for (int k = 0; k < kUnroll; ++k) {
         bool p = false;
-        int seg = j;
-        long long o_k = off;
-        double d_k = d;
-        int rr_k = rr;
-        if (ok[k]) {
-          const long long vi = base + (long long)k * 32 + lane;
-          if (vi < s_start) {                        // this item is in an earlier segment
-            int a = 0, bb = j;
-            while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else bb = m; }
-            seg = a - 1;
-            const int sp = in.spt_ids[seg];
-            o_k = sc.spt_offset[sp];
-            d_k = in.dist[seg];
-            rr_k = ld_cg(out.root_rule + seg);
-            rec[k] = rr_k ? sc.spt_root_rec[sp] : int(vi - ld_cg(out.seg_start + seg));
-            kv[k] = key_self[o_k + rec[k]];
-          }
+        if (segk[k] >= 0) {
+          // the cursor's segment is the common case; earlier items of a
+          // lane that crossed a boundary fetch their own (cached) scalars
+          const bool cur = segk[k] == j;
+          const int rr_k = cur ? rr : ld_cg(out.root_rule + segk[k]);
+          const double d_k = cur ? d : in.dist[segk[k]];
           p = rr_k ? true : double(kv[k]) <= d_k;
         }
         pk[k] = p;
-        segk[k] = seg;
-        offk[k] = o_k;
       }
       if (pass == 0) {
 #pragma unroll
@@ -481,7 +467,7 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       // all node-id gathers in flight before the ordered stores
       int node[kUnroll];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) node[k] = pk[k] ? sc.rec_node[offk[k] + rec[k]] : 0;
+      for (int k = 0; k < kUnroll; ++k) node[k] = pk[k] ? sc.rec_node[addr[k]] : 0;
 #pragma unroll
       for (int k = 0; k < kUnroll; ++k) {
         const unsigned bal = __ballot_sync(0xffffffffu, pk[k]);
