@@ -26,7 +26,8 @@ constexpr int kSelectThreads = 512;
 constexpr int kCompactThreads = 512;
 constexpr int kRows = 8;                          // items per thread per tile
 constexpr int kTile = kCompactThreads * kRows;    // 4096 virtual records
-constexpr int kUnroll = 8;                        // keys per lane in flight (K1 phase C)
+constexpr int kAlign = 4;                         // records per lane group (16-B vector loads)
+constexpr int kGroups = 4;                        // groups per lane in flight (K1 phase C)
 constexpr int kMaxLevels = 250;
 
 constexpr uint32_t kPass = 1u << 31;   // entry belongs to a passthrough BFS
@@ -292,6 +293,20 @@ CompactScratch carve_compact(void* base, int32_t S, int64_t R, int grid) {
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
+// 4 consecutive keys, aligned by the record layout (device.pad_records)
+GLOD_DEV void load4(const float* p, long long a, float (&v)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p + a);
+  v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+}
+GLOD_DEV void load4(const double* p, long long a, double (&v)[4]) {
+  const double2 x = *reinterpret_cast<const double2*>(p + a);
+  const double2 y = *reinterpret_cast<const double2*>(p + a + 2);
+  v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+}
+GLOD_DEV int rootrec_of(const LodScene& sc, const CompactIn& in, int j) {
+  return sc.spt_root_rec[in.spt_ids[j]];
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kCompactThreads, 2)
 compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
@@ -343,7 +358,9 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       if (lane == 0) {
         out.prefix_len[j] = pl;
         out.root_rule[j] = rr;
-        out.seg_start[j] = rr ? 1 : pl;          // segment length, scanned below
+        // virtual segment length, padded to the record alignment so every
+        // segment (and every lane's 4-item group) starts 16-B aligned
+        out.seg_start[j] = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;
       }
     }
   }
@@ -391,7 +408,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   long long wave_base = 0;                      // selections before this wave
   for (long long w_lo = 0; w_lo < total || (total == 0 && w_lo == 0); w_lo += wave) {
   const long long w_len = min(wave, total - w_lo);
-  const long long r_lo = w_lo + w_len * gwarp / nwarps_g, r_hi = w_lo + w_len * (gwarp + 1) / nwarps_g;
+  // warp ranges in whole kAlign groups (virtual segments are padded to kAlign)
+  const long long g_len = w_len / kAlign;
+  const long long r_lo = w_lo + kAlign * (g_len * gwarp / nwarps_g);
+  const long long r_hi = w_lo + kAlign * (g_len * (gwarp + 1) / nwarps_g);
   long long run = 0;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1) {
@@ -408,26 +428,30 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
     int j = -1;
     long long s_start = 0, s_end = -1, off = 0;
     double d = 0.0;
-    int rr = 0, rootrec = 0;
+    int rr = 0, rootrec = 0, seglen = 0;
     long long count = 0;
-    for (long long base = r_lo; base < r_hi; base += 32LL * kUnroll) {
-      int segk[kUnroll];
-      int rec[kUnroll];
-      long long addr[kUnroll];
+    for (long long base = r_lo; base < r_hi; base += 32LL * kAlign * kGroups) {
+      // lane-owned groups of kAlign consecutive virtual records; a group
+      // never straddles a segment (segments are padded to kAlign)
+      int segk[kGroups], loc[kGroups], len[kGroups];
+      long long addr[kGroups];
+      bool isrr[kGroups];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        const long long vi = base + (long long)k * 32 + lane;
+      for (int k = 0; k < kGroups; ++k) {
+        const long long vg = base + ((long long)k * 32 + lane) * kAlign;
         segk[k] = -1;
-        rec[k] = 0;
+        loc[k] = 0;
+        len[k] = 0;
         addr[k] = 0;
-        if (vi < r_hi) {
-          if (vi >= s_end) {                         // move the cursor (usually 0-1 steps)
-            if (j < 0 || vi >= s_end + 64) {
+        isrr[k] = false;
+        if (vg < r_hi) {
+          if (vg >= s_end) {                         // move the cursor (usually 0-1 steps)
+            if (j < 0 || vg >= s_end + 64 * kAlign) {
               int a = (j < 0 ? 0 : j), bb = n_spt;
-              while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vi) a = m + 1; else bb = m; }
+              while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vg) a = m + 1; else bb = m; }
               j = a - 1;
             } else {
-              while (j + 1 < n_spt && ld_cg(out.seg_start + j + 1) <= vi) ++j;
+              while (j + 1 < n_spt && ld_cg(out.seg_start + j + 1) <= vg) ++j;
             }
             s_start = ld_cg(out.seg_start + j);
             s_end = j + 1 < n_spt ? ld_cg(out.seg_start + j + 1) : total;
@@ -436,48 +460,67 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
             d = in.dist[j];
             rr = ld_cg(out.root_rule + j);
             rootrec = sc.spt_root_rec[sp];
+            seglen = rr ? 1 : ld_cg(out.prefix_len + j);
           }
           segk[k] = j;
-          rec[k] = rr ? rootrec : int(vi - s_start);
-          addr[k] = off + rec[k];
+          loc[k] = int(vg - s_start);
+          len[k] = seglen;
+          isrr[k] = rr;
+          addr[k] = off + (rr ? rootrec : loc[k]);
         }
       }
-      K kv[kUnroll];
+      unsigned mask[kGroups];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) kv[k] = segk[k] >= 0 ? key_self[addr[k]] : K(0);
-      bool pk[kUnroll];
-#pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        bool p = false;
+      for (int k = 0; k < kGroups; ++k) {
+        mask[k] = 0;
         if (segk[k] >= 0) {
-          // the cursor's segment is the common case; earlier items of a
-          // lane that crossed a boundary fetch their own (cached) scalars
-          const bool cur = segk[k] == j;
-          const int rr_k = cur ? rr : ld_cg(out.root_rule + segk[k]);
-          const double d_k = cur ? d : in.dist[segk[k]];
-          p = rr_k ? true : double(kv[k]) <= d_k;
+          if (isrr[k]) {
+            mask[k] = 1u;                            // [root] (spt.py:72-73)
+          } else {
+            K kv[kAlign];
+            load4(key_self, addr[k], kv);
+            const double d_k = segk[k] == j ? d : in.dist[segk[k]];
+#pragma unroll
+            for (int e = 0; e < kAlign; ++e)
+              if (loc[k] + e < len[k] && double(kv[e]) <= d_k) mask[k] |= 1u << e;
+          }
         }
-        pk[k] = p;
       }
       if (pass == 0) {
 #pragma unroll
-        for (int k = 0; k < kUnroll; ++k) count += __popc(__ballot_sync(0xffffffffu, pk[k]));
+        for (int k = 0; k < kGroups; ++k) count += __popc(mask[k]);
         continue;
       }
-      // all node-id gathers in flight before the ordered stores
-      int node[kUnroll];
+      int4 node[kGroups];
 #pragma unroll
-      for (int k = 0; k < kUnroll; ++k) node[k] = pk[k] ? sc.rec_node[addr[k]] : 0;
-#pragma unroll
-      for (int k = 0; k < kUnroll; ++k) {
-        const unsigned bal = __ballot_sync(0xffffffffu, pk[k]);
-        if (pk[k]) {
-          const long long o = run + __popc(bal & lanemask_lt());
-          out.sel_seg[o] = segk[k];
-          out.sel_pos[o] = rec[k];
-          out.sel_node[o] = node[k];
+      for (int k = 0; k < kGroups; ++k) {
+        node[k] = make_int4(0, 0, 0, 0);
+        if (mask[k]) {
+          if (isrr[k]) node[k].x = sc.rec_node[addr[k]];
+          else node[k] = *reinterpret_cast<const int4*>(sc.rec_node + addr[k]);
         }
-        run += __popc(bal);
+      }
+#pragma unroll
+      for (int k = 0; k < kGroups; ++k) {
+        const int c = __popc(mask[k]);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        long long o = run + incl - c;
+        const int nd[4] = {node[k].x, node[k].y, node[k].z, node[k].w};
+#pragma unroll
+        for (int e = 0; e < kAlign; ++e) {
+          if (mask[k] & (1u << e)) {
+            out.sel_seg[o] = segk[k];
+            out.sel_pos[o] = isrr[k] ? rootrec_of(sc, in, segk[k]) : loc[k] + e;
+            out.sel_node[o] = nd[e];
+            ++o;
+          }
+        }
+        run += __shfl_sync(0xffffffffu, incl, 31);
       }
     }
     if (pass == 0) {

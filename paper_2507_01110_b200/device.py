@@ -32,6 +32,38 @@ def _t(a, dtype, device):
     return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
 
 
+RECORD_ALIGN = 4   # each SPT's records start on a 16-B boundary (K1 vector loads)
+
+
+def pad_records(flat: dict) -> dict:
+    """Device record layout: every SPT's records start at a multiple of
+    RECORD_ALIGN (padding: key_self NaN, key_parent -inf, node -1), so the
+    compaction kernel streams keys with aligned 16-B vector loads.  Only
+    the offsets change; per-SPT record order and counts are untouched."""
+    counts = np.asarray(flat["count"], dtype=np.int64)
+    offs = np.asarray(flat["offset"], dtype=np.int64)
+    S = counts.size
+    padded = (counts + RECORD_ALIGN - 1) // RECORD_ALIGN * RECORD_ALIGN
+    new_off = np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64) if S else offs
+    total = int(padded.sum()) if S else 0
+    out = dict(flat)
+    ks = np.full(max(total, 1), np.nan)
+    kp = np.full(max(total, 1), -np.inf)
+    nd = np.full(max(total, 1), -1, dtype=np.int64)
+    if S and counts.sum():
+        spt_of = np.repeat(np.arange(S), counts)
+        src = np.concatenate([np.arange(o, o + c) for o, c in zip(offs, counts)]) if S < 64 else \
+            (np.arange(int(counts.sum())) - np.repeat(np.cumsum(counts) - counts, counts)
+             + np.repeat(offs, counts))
+        dst = new_off[spt_of] + (np.arange(int(counts.sum())) - np.repeat(np.cumsum(counts) - counts, counts))
+        ks[dst] = np.asarray(flat["key_self"])[src]
+        kp[dst] = np.asarray(flat["key_parent"])[src]
+        nd[dst] = np.asarray(flat["nodes"])[src]
+    out.update(key_self=ks[:total] if total else ks[:0], key_parent=kp[:total] if total else kp[:0],
+               nodes=nd[:total] if total else nd[:0], offset=new_off)
+    return out
+
+
 def keys_are_f32_exact(*arrs) -> bool:
     for a in arrs:
         fin = np.isfinite(a)
@@ -74,7 +106,7 @@ class DeviceLodScene:
         self.children = _t(h.children.reshape(-1), torch.int32, dev)
         kind = np.full(self.cap, -1, dtype=np.int32)
         if hspt is not None:
-            flat = dict(hspt.flat_records())
+            flat = pad_records(hspt.flat_records())
             # Device SPT index k enumerates SPT roots in ascending node id
             # (cut_hspt visits sorted(selected_spts), hspt.py:147); spt_perm
             # maps k back to the caller's spt_id.
