@@ -524,6 +524,8 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
       }
     }
     if (pass == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
       if (lane == 0) wcount[warp] = count;
       __syncthreads();
       long long c = 0;
