@@ -469,6 +469,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
           addr[k] = off + (rr ? rootrec : loc[k]);
         }
       }
+      // every group's key vector is requested before any is used
+      K kv[kGroups][kAlign];
+#pragma unroll
+      for (int k = 0; k < kGroups; ++k) load4(key_self, (segk[k] >= 0 && !isrr[k]) ? addr[k] : 0, kv[k]);
       unsigned mask[kGroups];
 #pragma unroll
       for (int k = 0; k < kGroups; ++k) {
@@ -477,12 +481,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
           if (isrr[k]) {
             mask[k] = 1u;                            // [root] (spt.py:72-73)
           } else {
-            K kv[kAlign];
-            load4(key_self, addr[k], kv);
             const double d_k = segk[k] == j ? d : in.dist[segk[k]];
 #pragma unroll
             for (int e = 0; e < kAlign; ++e)
-              if (loc[k] + e < len[k] && double(kv[e]) <= d_k) mask[k] |= 1u << e;
+              if (loc[k] + e < len[k] && double(kv[k][e]) <= d_k) mask[k] |= 1u << e;
           }
         }
       }

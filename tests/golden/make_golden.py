@@ -334,3 +334,80 @@ if __name__ == "__main__":
     make_adam_cases()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, os.path.getsize(f))
+
+
+def make_scheduler_cases():
+    """View sequences from scheduler.build_view_graph/next_view (scheduler.py:38-77)."""
+    from glod.scheduler import build_view_graph, next_view
+    rng = np.random.default_rng(5)
+    d = {}
+    for c in range(4):
+        n = int(rng.integers(5, 40))
+        pos = rng.normal(size=(n, 3)) * 10
+        if c == 3:
+            pos[1] = pos[0]          # duplicate positions: ties broken by index
+        k = int(rng.integers(1, 20))
+        g = build_view_graph(pos, k=k, random_every=int(rng.integers(2, 15)))
+        r = np.random.default_rng(100 + c)
+        cur, seq = 0, []
+        for it in range(1, 200):
+            cur = next_view(g, cur, it, r)
+            seq.append(cur)
+        d[f"s{c}_pos"] = pos
+        d[f"s{c}_k"] = np.int64(k)
+        d[f"s{c}_random_every"] = np.int64(g.random_every)
+        d[f"s{c}_neighbors"] = g.neighbors
+        d[f"s{c}_weights"] = g.weights
+        d[f"s{c}_seq"] = np.array(seq, dtype=np.int64)
+    d["n_cases"] = np.int64(4)
+    np.savez_compressed(OUT / "scheduler_cases.npz", **d)
+
+
+def make_cache_cases():
+    """Random operation traces on the reference DeviceCache (cache.py:42-109)
+    with the resulting hit/miss/evicted/resident sequences."""
+    from glod.cache import CacheConfig, CacheEntry, DeviceCache
+    from glod.store import AttributeBlock
+    rng = np.random.default_rng(1007)
+    d = {}
+    for c in range(5):
+        budget = int(rng.integers(500, 5000))
+        flush = int(rng.integers(5, 50))
+        cache = DeviceCache(config=CacheConfig(budget_bytes=budget, flush_interval=flush))
+        ops, res = [], []
+        for op in range(1, 1501):
+            kind = rng.uniform()
+            sid = int(rng.integers(0, 30))
+            if kind < 0.5:
+                dd = float(rng.uniform(0.0, 3.0))
+                hit = cache.lookup(sid, dd) is not None
+                ops.append((0, sid, dd, 0, 0))
+                res.append([int(hit)])
+            elif kind < 0.9:
+                dd = float(rng.uniform(0.5, 2.0))
+                nb = int(rng.integers(1, budget + 1))
+                dirty = int(rng.integers(2))
+                blk = AttributeBlock(spt_id=sid, prefix_len=0, attrs=AttributeArrays.zeros(0))
+                ev = cache.insert(CacheEntry(spt_id=sid, cached_distance=dd, prefix_len=0, block=blk,
+                                             nbytes=nb, dirty=bool(dirty)))
+                ops.append((1, sid, dd, nb, dirty))
+                res.append([e[0] for e in ev])
+            else:
+                fl = cache.tick_and_maybe_flush(op)
+                ops.append((2, op, 0.0, 0, 0))
+                res.append([e[0] for e in fl])
+            res[-1] = res[-1] + [-7] + list(cache.resident_ids()) + [-8, cache.resident_bytes,
+                                                                      cache.hits, cache.misses]
+        d[f"c{c}_budget"] = np.int64(budget)
+        d[f"c{c}_flush"] = np.int64(flush)
+        d[f"c{c}_ops"] = np.array(ops, dtype=np.float64)
+        lens = np.array([len(r) for r in res], dtype=np.int64)
+        d[f"c{c}_reslen"] = lens
+        d[f"c{c}_res"] = np.concatenate([np.array(r, dtype=np.int64) for r in res])
+    d["n_cases"] = np.int64(5)
+    np.savez_compressed(OUT / "cache_cases.npz", **d)
+
+
+if __name__ == "__main__":
+    make_scheduler_cases()
+    make_cache_cases()

@@ -1,0 +1,90 @@
+"""The native cache (csrc/cache_table.cu) against the Python mirror of
+cache.DeviceCache, which itself is pinned to the reference's traces
+(tests/test_host_golden.py).  Random per-view step sequences; after every
+step the LRU order, cached distances, prefixes, dirty flags, counters and
+the per-item outputs must agree exactly, and every freshly loaded block
+must hold the store's rows."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2507_01110_b200.cache import CacheConfig, CacheEntry, DeviceCache, NativeCache, OverBudgetError  # noqa: E402
+from paper_2507_01110_b200.core import SECTIONS, AttributeArrays  # noqa: E402
+from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene  # noqa: E402
+from paper_2507_01110_b200.store import HostStore  # noqa: E402
+
+
+def _py_step(c: DeviceCache, ids, d, P):
+    out = []
+    loaded = 0
+    for sid, dd, pp in zip(ids, d, P):
+        e = c.lookup(int(sid), float(dd))
+        if e is None:
+            e = CacheEntry(int(sid), float(dd), int(pp), None, int(pp) * 92)
+            c.insert(e)
+            loaded += int(pp)
+        out.append((e.cached_distance, e.prefix_len))
+    return out, loaded
+
+
+@pytest.mark.parametrize("seed,budget_frac,flush", [(0, 0.2, 5), (1, 0.6, 3), (2, 1.5, 100)])
+def test_native_cache_matches_mirror(seed, budget_frac, flush):
+    h, hs, _ = designed_scene(SceneSpec(n_leaves=4000, spt_leaves=128, seed=seed, relabel=False))
+    st = HostStore(h, hs)
+    S = len(hs.spts)
+    counts = hs.flat_records()["count"]
+    budget = int(budget_frac * counts.sum() * 92 / 4)
+    cfg = CacheConfig(budget_bytes=max(budget, int(counts.max()) * 92), flush_interval=flush)
+    nat, py = NativeCache(cfg, st), DeviceCache(config=cfg)
+    rng = np.random.default_rng(seed)
+    base = rng.uniform(5, 50, S)
+    for it in range(1, 40):
+        k = int(rng.integers(1, S + 1))
+        ids = np.sort(rng.choice(S, k, replace=False)).astype(np.int32)
+        d = base[ids] * rng.choice([1.0, 1.1, 1.3, 1.6, 0.7], k)
+        if it % 9 == 0:
+            d[0] = 0.0
+        P = np.maximum(1, (counts[ids] * rng.uniform(0.2, 1.0, k)).astype(np.int32))
+        dist = np.zeros(k, np.float64)
+        blk = np.zeros(k, np.uint64)
+        rows = np.zeros(k, np.int64)
+        loaded, hits = nat.step(ids, d, P, dist, blk, rows)
+        want, want_loaded = _py_step(py, ids, d, P)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(dist, [w[0] for w in want])
+        np.testing.assert_array_equal(rows, [w[1] for w in want])
+        assert loaded == want_loaded
+        # a block handed out this step holds the store's rows (nothing written yet)
+        j = int(rng.integers(k))
+        got = nat.read_block(int(blk[j]), int(rows[j]))
+        ga = AttributeArrays.from_packed(got, int(rows[j]))
+        ref = st.load_spt_prefix(int(ids[j]), int(rows[j])).attrs
+        for name, _ in SECTIONS:
+            np.testing.assert_array_equal(getattr(ga, name), np.asarray(getattr(ref, name), np.float64))
+        nat.end_step(it, mark_dirty=True)
+        for sid in ids:
+            e = py.entries.get(int(sid))
+            if e is not None:
+                e.dirty = True
+        py.tick_and_maybe_flush(it)
+        ents = nat.entries()
+        assert [e[0] for e in ents] == py.resident_ids()
+        assert [(e[1], e[2], e[4]) for e in ents] == \
+            [(e.cached_distance, e.prefix_len, e.dirty) for e in py.entries.values()]
+        s = nat.stats()
+        assert (s["hits"], s["misses"], s["resident_bytes"]) == (py.hits, py.misses, py.resident_bytes)
+    torch.cuda.synchronize()
+
+
+def test_native_cache_over_budget():
+    h, hs, _ = designed_scene(SceneSpec(n_leaves=2000, spt_leaves=128, seed=5, relabel=False))
+    st = HostStore(h, hs)
+    nat = NativeCache(CacheConfig(budget_bytes=92 * 3), st)
+    z = np.zeros(1)
+    with pytest.raises(OverBudgetError):
+        nat.step(np.array([0], np.int32), np.array([1.0]), np.array([4], np.int32), z,
+                 np.zeros(1, np.uint64), np.zeros(1, np.int64))
