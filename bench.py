@@ -33,7 +33,7 @@ sys.path.insert(0, str(ROOT))
 BASE_METRIC = "train iters/s @1080p, 10M-Gaussian synthetic scene (host-DRAM store + device cache)"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -48,7 +48,15 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def parse_args_for_tools(leaves=None):
+    """Default workload arguments (tools/)."""
+    a = parse([])
+    if leaves:
+        a.leaves = leaves
+    return a
 
 
 # --------------------------------------------------------------------------

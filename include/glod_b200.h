@@ -230,6 +230,13 @@ typedef struct glod_prefix_item {
   int64_t rows;
   int64_t elem_start;
   double* block;                /* [dev]                                       */
+  /* loads only: rows [0, min(rows, overlay_rows)) are taken as
+   * f64(f32(overlay row)) from this packed f64 block of overlay_rows rows
+   * instead of the store —
+   * a block evicted earlier in the same step whose write-back is in flight
+   * (store.py:323-333 then :314-321).  NULL / 0 for a plain load. */
+  const double* overlay;        /* [dev]                                       */
+  int64_t overlay_rows;
 } glod_prefix_item;
 
 /* Device address of page-locked host memory (cudaHostGetDevicePointer). */
@@ -291,6 +298,11 @@ int glod_sort_pairs_u64(uint64_t* keys, uint64_t* keys_alt, int32_t* vals, int32
 int glod_sort_pairs_u32(uint32_t* keys, uint32_t* keys_alt, int32_t* vals, int32_t* vals_alt,
                         int64_t n, int32_t begin_bit, int32_t end_bit, void* scratch,
                         int64_t scratch_bytes, int32_t* result_in_alt, void* stream);
+/* Stream-ordered small device→host read-back into page-locked host memory,
+ * written by a kernel through the mapped address (no copy engine, so it
+ * never queues behind bulk D2H DMA).  The caller synchronises the stream
+ * before reading host_pinned. */
+int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream);
 /* Synchronous device→host copy (snapshots / tests). */
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 

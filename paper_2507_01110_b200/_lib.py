@@ -70,7 +70,7 @@ class StoreView(C.Structure):
 
 class PrefixItem(C.Structure):
     _fields_ = [("slot_start", C.c_int64), ("rows", C.c_int64), ("elem_start", C.c_int64),
-                ("block", P)]
+                ("block", P), ("overlay", P), ("overlay_rows", C.c_int64)]
 
 
 class CacheStats(C.Structure):
@@ -112,6 +112,7 @@ SIGNATURES = {
     "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
     "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
     "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),
+    "glod_readback": (C.c_int, [P, P, C.c_int64, P]),
     "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
     "glod_sort_pairs_u64": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
                                       C.POINTER(C.c_int32), P]),
@@ -173,3 +174,11 @@ def stream_ptr(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def readback(host_pinned, src, nbytes: int | None = None, stream=None):
+    """Stream-ordered read-back of a device tensor into a pinned host tensor
+    (kernel-written through the mapped address; see glod_readback)."""
+    n = src.numel() * src.element_size() if nbytes is None else nbytes
+    check(lib().glod_readback(ptr(host_pinned), ptr(src), int(n), stream_ptr(stream)))
+

@@ -5,10 +5,10 @@
 // byte budget counted as prefix_len·92, replacement returns the old dirty
 // block, flush every flush_interval iterations) over cache blocks that live
 // in HBM.  Blocks are packed f64 attribute blocks allocated stream-ordered
-// (cudaMallocAsync) and released stream-ordered after their write-back, so
-// a whole step's cache work is one C call: decisions, then batched
-// zero-copy store transfers (loads before write-backs, a batch closed
-// whenever an SPT about to be loaded has a write-back pending).
+// (from a private pool) and released stream-ordered after their write-back, so
+// a whole step's cache work is one C call: decisions, then one batch of
+// zero-copy store transfers (loads on the main stream, write-backs on a
+// side stream).
 #include <stdint.h>
 #include <string.h>
 
@@ -23,6 +23,8 @@ namespace glod {
 
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
+cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
+                            cudaStream_t st);
 
 namespace {
 
@@ -48,63 +50,81 @@ struct CacheTable {
   std::list<Entry> lru;                   // front = least recently used
   std::unordered_map<int32_t, std::list<Entry>::iterator> map;
   int64_t resident = 0, hits = 0, misses = 0, loaded_rows = 0;
-  // transfer staging
-  glod_prefix_item* h_items = nullptr;    // pinned
-  glod_prefix_item* d_items = nullptr;
+  // transfer staging: one pinned host item table, rewritten once its last
+  // H2D copy (event items_done) has run
+  glod_prefix_item* h_items = nullptr;
   size_t items_cap = 0;
+  cudaEvent_t items_done = nullptr;
   std::vector<int32_t> step_ids;          // SPTs rendered this step (dirty at end)
-  std::vector<double*> to_free;           // blocks freed after their write-back
+  std::vector<double*> to_free;           // blocks dropped this step
   int device = 0;
-  cudaEvent_t items_done = nullptr;       // last H2D from the pinned item table
-  // Write-backs run on a side stream so the D2H PCIe direction overlaps the
-  // rest of the step; the main stream waits for them before anything that
-  // could observe the store (the next loads) or reuse a written-back block.
+  // Write-back copies run on a side stream so the D2H PCIe direction
+  // overlaps the rest of the step.  The main stream waits for them only
+  // when a load reads store rows a not-yet-finished write-back of an
+  // earlier step writes (wb_prev); a block evicted and re-requested within
+  // one step is reloaded from the evicted block itself (overlay, below).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_main = nullptr, ev_wb = nullptr;
-  bool wb_pending = false;
+  std::unordered_map<int32_t, int> wb_prev;   // SPT ids with write-backs in flight
+
+  // Blocks and item tables: a private stream-ordered pool (all allocations
+  // and frees on the main stream).  Write-back staging: two persistent f32
+  // buffers used alternately; the main stream reuses one only after the
+  // side stream's copies out of it (ev_stage) — two batches earlier.
+  cudaMemPool_t pool = nullptr;
+  float* stage[2] = {nullptr, nullptr};
+  size_t stage_cap[2] = {0, 0};
+  cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  int stage_next = 0;
 
   cudaError_t ensure_side() {
     if (side) return cudaSuccess;
-    cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaError_t e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    unsigned long long thr = ~0ull;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (e != cudaSuccess) return e;
+    for (int k = 0; k < 2; ++k) {
+      e = cudaEventCreateWithFlags(&ev_stage[k], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_wb, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&items_done, cudaEventDisableTiming);
     return e;
-  }
-
-  // main stream waits for outstanding write-backs
-  cudaError_t join(cudaStream_t st) {
-    if (!wb_pending) return cudaSuccess;
-    wb_pending = false;
-    return cudaStreamWaitEvent(st, ev_wb, 0);
   }
 
   ~CacheTable() {
     if (side) cudaStreamSynchronize(side);
+    cudaDeviceSynchronize();
     if (items_done) cudaEventDestroy(items_done);
     if (ev_main) cudaEventDestroy(ev_main);
     if (ev_wb) cudaEventDestroy(ev_wb);
     if (side) cudaStreamDestroy(side);
     for (auto& e : lru) cudaFree(e.block);
+    for (double* b : to_free) cudaFree(b);
     if (h_items) cudaFreeHost(h_items);
-    if (d_items) cudaFree(d_items);
+    for (int k = 0; k < 2; ++k) {
+      if (stage[k]) cudaFree(stage[k]);
+      if (ev_stage[k]) cudaEventDestroy(ev_stage[k]);
+    }
+    if (pool) cudaMemPoolDestroy(pool);
   }
 
+  // pinned item table of at least n entries, safe to rewrite
   cudaError_t ensure_items(size_t n) {
-    if (!items_done) {
-      cudaError_t e = cudaEventCreateWithFlags(&items_done, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    // the pinned table is rewritten below: its previous copies must be done
+    cudaError_t e = ensure_side();
+    if (e != cudaSuccess) return e;
     cudaEventSynchronize(items_done);
     if (n <= items_cap) return cudaSuccess;
-    size_t want = n * 2 + 64;
-    // outstanding copies from the old pinned table must finish first
-    cudaDeviceSynchronize();
     if (h_items) cudaFreeHost(h_items);
-    if (d_items) cudaFree(d_items);
-    cudaError_t e = cudaMallocHost(&h_items, want * sizeof(glod_prefix_item));
-    if (e != cudaSuccess) return e;
-    e = cudaMalloc(&d_items, want * sizeof(glod_prefix_item));
+    const size_t want = n * 2 + 64;
+    e = cudaMallocHost(&h_items, want * sizeof(glod_prefix_item));
     if (e != cudaSuccess) return e;
     items_cap = want;
     return cudaSuccess;
@@ -114,52 +134,129 @@ struct CacheTable {
 namespace {
 
 struct Xfer {
+  int32_t spt_id;
   int64_t slot, rows;
   double* block;
+  const double* overlay;       // loads: rows [0, overlay_rows) come from here
+  int64_t overlay_rows;
 };
 
-// Runs one batch: all loads (main stream), then all write-backs (side
-// stream, after the loads), from one pinned item table.
-cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, std::vector<Xfer>& loads,
-                      std::vector<Xfer>& wbs, size_t& table_off, cudaStream_t st) {
-  cudaError_t e = c->ensure_side();
-  if (e != cudaSuccess) return e;
-  // loads observe every earlier write-back, and the device item table is
-  // not rewritten while a write-back kernel may still read it
-  e = c->join(st);
-  if (e != cudaSuccess) return e;
-  for (int pass = 0; pass < 2; ++pass) {
-    std::vector<Xfer>& v = pass == 0 ? loads : wbs;
-    if (v.empty()) continue;
-    glod_prefix_item* h = c->h_items + table_off;
-    int64_t off = 0;
-    for (size_t i = 0; i < v.size(); ++i) {
-      h[i].slot_start = v[i].slot;
-      h[i].rows = v[i].rows;
-      h[i].elem_start = off;
-      h[i].block = v[i].block;
-      off += kFloats * v[i].rows;
-    }
-    glod_prefix_item* d = c->d_items + table_off;
-    e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return e;
-    e = cudaEventRecord(c->items_done, st);
-    if (e != cudaSuccess) return e;
-    if (pass == 0) {
-      e = launch_store_xfer(sv, d, int(v.size()), off, 1, st);
-    } else {
-      // side stream: after this batch's loads and the item-table copy
-      e = cudaEventRecord(c->ev_main, st);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_main, 0);
-      if (e == cudaSuccess) e = launch_store_xfer(sv, d, int(v.size()), off, 0, c->side);
-      if (e == cudaSuccess) e = cudaEventRecord(c->ev_wb, c->side);
-      c->wb_pending = true;
-    }
-    if (e != cudaSuccess) return e;
-    table_off += v.size();
-    v.clear();
+// Copies `v` into the pinned table at `off` and then to a stream-ordered
+// device table; returns the device table (freed by the caller's stream
+// order) and the element total.
+cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, cudaStream_t st,
+                        glod_prefix_item** d_out, long long* total) {
+  glod_prefix_item* h = c->h_items + off;
+  long long acc = 0;
+  for (size_t i = 0; i < v.size(); ++i) {
+    h[i].slot_start = v[i].slot;
+    h[i].rows = v[i].rows;
+    h[i].elem_start = acc;
+    h[i].block = v[i].block;
+    h[i].overlay = v[i].overlay;
+    h[i].overlay_rows = v[i].overlay_rows;
+    acc += kFloats * v[i].rows;
   }
+  glod_prefix_item* d = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&d, v.size() * sizeof(glod_prefix_item), c->pool, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  *d_out = d;
+  *total = acc;
   return cudaSuccess;
+}
+
+// Host address of a store section (the view holds device-mapped
+// addresses; the copy engines take the host side under UVA).
+cudaError_t host_section(const glod_store_view& sv, int k, float** out) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, sv.section[k]);
+  if (e != cudaSuccess) return e;
+  *out = static_cast<float*>(at.hostPointer ? at.hostPointer : const_cast<float*>(sv.section[k]));
+  return cudaSuccess;
+}
+
+// One step's transfers.  Loads: one zero-copy kernel on the main stream.
+// Write-backs: the blocks are packed to f32 on the main stream right after
+// the loads (so a replaced dirty entry is written back after its stale
+// reload, and every written-back block is read before this step's ADAM
+// refresh rewrites it — the reference writes back at eviction), then the
+// copy engines move the f32 rows into the pinned store on the side stream
+// (cudaMemcpyBatchAsync, 6 section ranges per block): no SM time, so the
+// D2H direction overlaps the rest of the step without slowing its kernels.
+cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, const std::vector<Xfer>& loads,
+                      const std::vector<Xfer>& wbs, bool join, cudaStream_t st) {
+  cudaError_t e = c->ensure_items(loads.size() + wbs.size() + 1);
+  if (e != cudaSuccess) return e;
+  if (join) {
+    e = cudaStreamWaitEvent(st, c->ev_wb, 0);
+    if (e != cudaSuccess) return e;
+    c->wb_prev.clear();
+  }
+  if (!loads.empty()) {
+    glod_prefix_item* d = nullptr;
+    long long total = 0;
+    e = stage_items(c, loads, 0, st, &d, &total);
+    if (e == cudaSuccess) e = launch_store_xfer(sv, d, int(loads.size()), total, 1, st);
+    if (e == cudaSuccess) e = cudaFreeAsync(d, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (!wbs.empty()) {
+    glod_prefix_item* d = nullptr;
+    long long total = 0;
+    e = stage_items(c, wbs, loads.size(), st, &d, &total);
+    if (e != cudaSuccess) return e;
+    const int sb = c->stage_next;
+    c->stage_next ^= 1;
+    const size_t need = size_t(total) * sizeof(float);
+    if (need > c->stage_cap[sb]) {
+      e = cudaEventSynchronize(c->ev_stage[sb]);          // copies out of the old buffer
+      if (c->stage[sb]) cudaFree(c->stage[sb]);
+      c->stage[sb] = nullptr;
+      c->stage_cap[sb] = 0;
+      if (e == cudaSuccess) e = cudaMalloc(&c->stage[sb], need + need / 2);
+      if (e != cudaSuccess) return e;
+      c->stage_cap[sb] = need + need / 2;
+    }
+    float* staging = c->stage[sb];
+    e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
+    if (e == cudaSuccess) e = launch_pack_f32(d, int(wbs.size()), total, staging, st);
+    if (e == cudaSuccess) e = cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_main, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_main, 0);
+    if (e != cudaSuccess) return e;
+    float* hsec[6];
+    for (int k = 0; k < 6; ++k) {
+      e = host_section(sv, k, &hsec[k]);
+      if (e != cudaSuccess) return e;
+    }
+    static const int off[7] = {0, 3, 6, 10, 11, 14, 23};
+    std::vector<void*> dst, src;
+    std::vector<size_t> size;
+    dst.reserve(6 * wbs.size()); src.reserve(6 * wbs.size()); size.reserve(6 * wbs.size());
+    long long acc = 0;
+    for (const Xfer& x : wbs) {
+      for (int k = 0; k < 6; ++k) {
+        const int cols = off[k + 1] - off[k];
+        dst.push_back(hsec[k] + x.slot * cols);
+        src.push_back(staging + acc + (long long)off[k] * x.rows);
+        size.push_back(size_t(cols) * size_t(x.rows) * sizeof(float));
+      }
+      acc += kFloats * x.rows;
+    }
+    cudaMemcpyAttributes attr = {};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail = 0;
+    e = cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1, &fail,
+                             c->side);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_stage[sb], c->side);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_wb, c->side);
+    if (e != cudaSuccess) return e;
+    for (const Xfer& x : wbs) c->wb_prev[x.spt_id] = 1;
+  }
+  return cudaEventRecord(c->items_done, st);
 }
 
 }  // namespace
@@ -168,14 +265,23 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
                        const double* d_root, const int32_t* prefix_len, double* dist_out,
                        uint64_t* block_out, int64_t* rows_out, int64_t* loaded_rows,
                        int64_t* hits, cudaStream_t st) {
-  // worst case: one load + every resident entry written back per selected SPT
-  cudaError_t e = c->ensure_items(2 * size_t(n) + c->lru.size() + 1);
+  cudaError_t e = c->ensure_side();
   if (e != cudaSuccess) return e;
+  // write-backs of earlier steps already finished: nothing to wait for
+  if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
   std::vector<Xfer> loads, wbs;
-  std::vector<int32_t> wb_ids;
-  size_t table_off = 0;
+  std::unordered_map<int32_t, std::pair<const double*, int64_t>> evicted;   // dirty, this step
+  bool join = false;
   const int64_t hits0 = c->hits, loaded0 = c->loaded_rows;
   c->step_ids.assign(spt_ids, spt_ids + n);
+  auto drop = [&](const Entry& v) {
+    c->resident -= v.nbytes;
+    if (v.dirty) {
+      wbs.push_back({v.spt_id, c->slot_start[v.spt_id], v.prefix_len, v.block, nullptr, 0});
+      evicted[v.spt_id] = {v.block, v.prefix_len};
+    }
+    c->to_free.push_back(v.block);
+  };
   for (int32_t j = 0; j < n; ++j) {
     const int32_t sid = spt_ids[j];
     const double d = d_root[j];
@@ -197,29 +303,30 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
       const int64_t P = prefix_len[j];
       const int64_t nbytes = P * c->bytes_per_row;
       if (nbytes > c->budget) return cudaErrorNotPermitted;   // OverBudgetError
-      bool pending = false;
-      for (int32_t w : wb_ids) pending |= (w == sid);
-      if (pending) {
-        e = run_batch(c, sv, loads, wbs, table_off, st);
-        if (e != cudaSuccess) return e;
-        wb_ids.clear();
-      }
       double* blk = nullptr;
-      e = cudaMallocAsync(&blk, size_t(kFloats) * size_t(P > 0 ? P : 1) * sizeof(double), st);
+      e = cudaMallocFromPoolAsync(&blk, size_t(kFloats) * size_t(P > 0 ? P : 1) * sizeof(double), c->pool, st);
       if (e != cudaSuccess) return e;
-      loads.push_back({c->slot_start[sid], P, blk});
+      Xfer ld{sid, c->slot_start[sid], P, blk, nullptr, 0};
+      auto ev = evicted.find(sid);
+      if (ev != evicted.end()) {
+        // evicted (dirty) earlier in this step: the reference writes it back
+        // and then reads the store, i.e. rows below the old prefix are the
+        // f32 rounding of the evicted block, the rest the untouched store
+        ld.overlay = ev->second.first;
+        ld.overlay_rows = ev->second.second;      // its row count = its section stride
+      } else if (c->wb_prev.count(sid)) {
+        join = true;                 // store rows still being written back
+      }
+      loads.push_back(ld);
       c->loaded_rows += P;
-      // insert: replace (old dirty block written back), append, evict LRU front
+      // insert: replace (old dirty block written back after the load),
+      // append, evict from the LRU front
       if (it != c->map.end()) {
         Entry old = *it->second;
         c->lru.erase(it->second);
         c->map.erase(sid);
-        c->resident -= old.nbytes;
-        if (old.dirty) {
-          wbs.push_back({c->slot_start[old.spt_id], old.prefix_len, old.block});
-          wb_ids.push_back(old.spt_id);
-        }
-        c->to_free.push_back(old.block);
+        drop(old);
+        evicted.erase(sid);          // never requested again this step
       }
       c->lru.push_back({sid, d, P, blk, nbytes, false});
       c->map[sid] = std::prev(c->lru.end());
@@ -228,34 +335,26 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
         Entry v = c->lru.front();
         c->lru.pop_front();
         c->map.erase(v.spt_id);
-        c->resident -= v.nbytes;
-        if (v.dirty) {
-          wbs.push_back({c->slot_start[v.spt_id], v.prefix_len, v.block});
-          wb_ids.push_back(v.spt_id);
-        }
-        c->to_free.push_back(v.block);
+        drop(v);
       }
-      it = c->map.find(sid);
     }
     const Entry& en = *c->map.find(sid)->second;
     dist_out[j] = en.cached_distance;
     block_out[j] = reinterpret_cast<uint64_t>(en.block);
     rows_out[j] = en.prefix_len;
   }
-  e = run_batch(c, sv, loads, wbs, table_off, st);
+  e = run_batch(c, sv, loads, wbs, join, st);
   if (e != cudaSuccess) return e;
   *loaded_rows = c->loaded_rows - loaded0;
   *hits = c->hits - hits0;
   return cudaSuccess;
 }
 
-// Blocks evicted this step are still read by this step's render (the
-// reference keeps its `entry` references alive) — release them only once
-// the step's kernels are enqueued.
+// Blocks dropped this step are still read by this step's kernels (the
+// reference keeps its `entry` references alive): free them in main-stream
+// order once the step is enqueued (their write-backs read the f32 staging
+// copy, not the block).
 cudaError_t cache_release(CacheTable* c, cudaStream_t st) {
-  if (c->to_free.empty()) return cudaSuccess;
-  cudaError_t j = c->join(st);     // a freed block may still be being written back
-  if (j != cudaSuccess) return j;
   for (double* b : c->to_free) {
     cudaError_t e = cudaFreeAsync(b, st);
     if (e != cudaSuccess) return e;
@@ -274,18 +373,15 @@ cudaError_t cache_end_step(CacheTable* c, const glod_store_view& sv, int64_t ite
   c->step_ids.clear();
   cudaError_t e = cudaSuccess;
   if (iteration >= 0 && iteration % c->flush_interval == 0) {
-    e = c->ensure_items(c->lru.size() + 1);
-    if (e != cudaSuccess) return e;
     std::vector<Xfer> none, wbs;
     for (auto& en : c->lru) {
-      if (en.dirty) wbs.push_back({c->slot_start[en.spt_id], en.prefix_len, en.block});
+      if (en.dirty) wbs.push_back({en.spt_id, c->slot_start[en.spt_id], en.prefix_len, en.block, nullptr, 0});
       c->to_free.push_back(en.block);
     }
     c->lru.clear();
     c->map.clear();
     c->resident = 0;
-    size_t off = 0;
-    e = run_batch(c, sv, none, wbs, off, st);
+    e = run_batch(c, sv, none, wbs, false, st);
     if (e != cudaSuccess) return e;
   }
   return cache_release(c, st);
@@ -314,6 +410,7 @@ int glod_cache_create(int64_t budget_bytes, double d_min, double d_max, int64_t 
   c->t.bytes_per_row = bytes_per_row;
   c->t.slot_start.assign(slot_start, slot_start + num_spts);
   cudaGetDevice(&c->t.device);
+  glod::retain_pool_memory();
   *out = c;
   return GLOD_OK;
 }

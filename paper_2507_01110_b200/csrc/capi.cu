@@ -11,6 +11,7 @@ namespace glod {
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int set_error(int code, const char* what);
+void retain_pool_memory();
 size_t loss_scratch_bytes(int W, int H);
 cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
                         float* grad, void* scratch, size_t bytes, cudaStream_t st);
@@ -22,6 +23,7 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
 cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st);
+cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
 }  // namespace glod
@@ -39,6 +41,19 @@ int fail(int code, const char* what) {
 }
 
 }  // namespace
+
+// Workspaces and cache blocks come from the device's default stream-ordered
+// pool.  Its default release threshold (0) hands memory back to the driver
+// at every synchronisation, so the next step's cudaMallocAsync re-maps
+// pages; keep what was reserved instead (HBM is sized for it).
+void glod::retain_pool_memory() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  unsigned long long thr = ~0ull;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+}
 
 int glod::set_error(int code, const char* what) {
   g_err = what;
@@ -93,6 +108,7 @@ int glod_spt_compact(const glod_lod_scene* scene, const glod_spt_compact_in* in,
 
 int glod_raster_create(glod_raster** out) {
   if (!out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  glod::retain_pool_memory();
   *out = new glod_raster{glod::raster_create()};
   return GLOD_OK;
 }
@@ -180,6 +196,12 @@ int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* str
   if (n > 0 && (!in || !out)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_convert(in, out, n, to_f64, static_cast<cudaStream_t>(stream)),
                "glod_convert");
+}
+
+int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream) {
+  if ((!host_pinned || !src) && bytes > 0) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_readback(host_pinned, src, bytes, static_cast<cudaStream_t>(stream)),
+               "glod_readback");
 }
 
 int glod_host_device_ptr(void* host, void** dev) {

@@ -12,6 +12,8 @@ namespace glod {
 void count_launch(unsigned long long n = 1);
 // Sets the thread-local message returned by glod_last_error(); returns code.
 int set_error(int code, const char* what);
+// Keep the default stream-ordered pool's reservations (capi.cu).
+void retain_pool_memory();
 
 // ---------------------------------------------------------------------------
 // Exact-rounding fp64 arithmetic.  The LoD decisions must reproduce the

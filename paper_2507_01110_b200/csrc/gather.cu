@@ -113,10 +113,53 @@ GLOD_DEV int find_item(const glod_prefix_item* items, int lo, int hi, long long 
   return lo;
 }
 
+// Grid-stride over 256-element chunks: the write-back runs on a side stream
+// beside the main step, so its grid is capped (a few CTAs keep the posted
+// PCIe writes saturated) instead of flooding every SM with long-latency
+// blocks that would starve the main stream's kernels.
 template <bool kLoad>
 __global__ void __launch_bounds__(256)
 store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items, int n_items,
                   long long total) {
+  __shared__ int s_lo, s_hi;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < total;
+       base += (long long)gridDim.x * blockDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long last = min(total, base + (long long)blockDim.x) - 1;
+      s_lo = find_item(items, 0, n_items - 1, base);
+      s_hi = find_item(items, s_lo, n_items - 1, last);
+    }
+    __syncthreads();
+    const long long e = base + threadIdx.x;
+    if (e >= total) continue;
+    const int it = s_lo == s_hi ? s_lo : find_item(items, s_lo, s_hi, e);
+    const glod_prefix_item I = items[it];
+    const long long local = e - I.elem_start;
+    const long long rows = I.rows;
+    int sec = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
+    const long long within = local - kSecOff[sec] * rows;
+    float* host = const_cast<float*>(sv.section[sec]) + I.slot_start * kSecCols[sec] + within;
+    if (kLoad) {
+      // overlay: rows below overlay_rows are the f32 rounding of a block whose
+      // write-back to these store rows is still in flight (cache_table.cu)
+      const long long row = within / kSecCols[sec];
+      I.block[local] = row < I.overlay_rows
+                           ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
+                           : double(*host);
+    } else {
+      *host = float(I.block[local]);
+    }
+  }
+}
+
+// Write-back staging: every block of the batch → f32, packed in the items'
+// flat element order (section ranges then go to the store by DMA).
+__global__ void __launch_bounds__(256)
+pack_f32_kernel(const glod_prefix_item* __restrict__ items, int n_items, long long total,
+                float* __restrict__ out) {
   __shared__ int s_lo, s_hi;
   const long long base = (long long)blockIdx.x * blockDim.x;
   if (base >= total) return;
@@ -129,19 +172,21 @@ store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items
   const long long e = base + threadIdx.x;
   if (e >= total) return;
   const int it = s_lo == s_hi ? s_lo : find_item(items, s_lo, s_hi, e);
-  const glod_prefix_item I = items[it];
-  const long long local = e - I.elem_start;
-  const long long rows = I.rows;
-  int sec = 0;
-#pragma unroll
-  for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
-  const long long within = local - kSecOff[sec] * rows;
-  float* host = const_cast<float*>(sv.section[sec]) + I.slot_start * kSecCols[sec] + within;
-  if (kLoad) {
-    I.block[local] = double(*host);
-  } else {
-    *host = float(I.block[local]);
-  }
+  out[e] = float(items[it].block[e - items[it].elem_start]);
+}
+
+// Small device→host read-backs written by a kernel straight into mapped
+// pinned memory: no copy-engine queueing behind the cache's bulk D2H
+// write-back DMA (which would delay the step's host synchronisations).
+__global__ void readback_kernel(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                                long long bytes) {
+  const long long words = bytes >> 2;
+  const unsigned* s4 = reinterpret_cast<const unsigned*>(src);
+  unsigned* d4 = reinterpret_cast<unsigned*>(dst);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x)
+    d4[i] = s4[i];
+  if (blockIdx.x == 0 && threadIdx.x < (bytes & 3)) dst[(words << 2) + threadIdx.x] = src[(words << 2) + threadIdx.x];
 }
 
 int grid_for(long long n, int tb) {
@@ -182,16 +227,45 @@ cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, c
   return cudaGetLastError();
 }
 
+cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  void* dst = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dst, host_pinned, 0);
+  if (e != cudaSuccess) return e;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3) {
+    return cudaMemcpyAsync(host_pinned, src, size_t(bytes), cudaMemcpyDeviceToHost, st);
+  }
+  const long long words = (bytes + 3) >> 2;
+  const int grid = int(words > 256 * 64 ? 64 : (words + 255) / 256);
+  count_launch();
+  readback_kernel<<<grid, 256, 0, st>>>(static_cast<const unsigned char*>(src),
+                                        static_cast<unsigned char*>(dst), bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
+                            cudaStream_t st) {
+  if (n_items <= 0 || total <= 0) return cudaSuccess;
+  const int TB = 256;
+  count_launch();
+  pack_f32_kernel<<<unsigned((total + TB - 1) / TB), TB, 0, st>>>(items, n_items, total, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st) {
   if (n_items <= 0 || total <= 0) return cudaSuccess;
   const int TB = 256;
   const long long nb = (total + TB - 1) / TB;
+  // loads: 8 CTAs/SM in flight hide the PCIe read latency; write-backs
+  // (posted writes, side stream): one CTA per SM
+  const long long cap = load ? 148 * 8 : 148;
+  const unsigned grid = unsigned(nb < cap ? nb : cap);
   count_launch();
   if (load)
-    store_xfer_kernel<true><<<unsigned(nb), TB, 0, st>>>(sv, items, n_items, total);
+    store_xfer_kernel<true><<<grid, TB, 0, st>>>(sv, items, n_items, total);
   else
-    store_xfer_kernel<false><<<unsigned(nb), TB, 0, st>>>(sv, items, n_items, total);
+    store_xfer_kernel<false><<<grid, TB, 0, st>>>(sv, items, n_items, total);
   return cudaGetLastError();
 }
 

@@ -159,12 +159,11 @@ GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
   return m <= 32.01f;
 }
 
-__global__ void preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam,
-                                  Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
-                                  int* __restrict__ vals, int* __restrict__ tiles,
-                                  int* __restrict__ bad) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// One Gaussian; returns its tile count (0 = contributes nothing) and sets
+// its depth key.
+GLOD_DEV int preprocess_one(const double* __restrict__ attrs, long long n, long long i, const CamD& cam,
+                            Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
+                            int* __restrict__ vals, int* __restrict__ tiles, int* __restrict__ bad) {
   Sec s(attrs, n);
   // _check_finite (renderer.py:67-72): first section, then first row
   const int cols[6] = {3, 3, 4, 1, 3, 9};
@@ -181,9 +180,9 @@ __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n,
   Proj P;
   project(s, i, cam, P);
   const double depth = P.t[2];
-  if (!(depth > cam.near_)) return;            // ok = depth > near
+  if (!(depth > cam.near_)) return 0;            // ok = depth > near
   const double det = P.c00 * P.c11 - P.c01 * P.c01;
-  if (!(det > 0)) return;                      // `if det <= 0: continue`
+  if (!(det > 0)) return 0;                      // `if det <= 0: continue`
   const double half = (P.c00 + P.c11) / 2;
   const double lmax = half + sqrt(fmax(half * half - det, 0.0));
   const double rad = 3.0 * sqrt(lmax);
@@ -195,7 +194,7 @@ __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n,
   double fy1 = fmin(fmax(ceil(P.m2[1] + rad) + 1, -big), big);
   const int x0 = max(int(fx0), 0), x1 = min(int(fx1), cam.w);
   const int y0 = max(int(fy0), 0), y1 = min(int(fy1), cam.h);
-  if (x0 >= x1 || y0 >= y1) return;
+  if (x0 >= x1 || y0 >= y1) return 0;
   Splat sp;
   sp.mx = float(P.m2[0] - x0);
   sp.my = float(P.m2[1] - y0);
@@ -215,10 +214,54 @@ __global__ void preprocess_kernel(const double* __restrict__ attrs, long long n,
     for (int ty = ty0; ty <= ty1; ++ty)
       for (int tx = tx0; tx <= tx1; ++tx) nt += tile_hit(sp, tx, ty);
   }
-  if (nt == 0) return;                         // every bbox pixel has q > 32: α = 0
+  if (nt == 0) return 0;                       // every bbox pixel has q > 32: α = 0
   splats[i] = sp;
   keys[i] = __double_as_longlong(depth);       // positive doubles order as uint64
   tiles[i] = nt;
+  return nt;
+}
+
+// K5 over all Gaussians.  Also reduces, for the one host read-back of the
+// forward pass, stats = {Σ tile instances, min key, max key} over the
+// contributing splats (the depth sort only needs the bits where they differ).
+__global__ void __launch_bounds__(256)
+preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat* __restrict__ splats,
+                  unsigned long long* __restrict__ keys, int* __restrict__ vals, int* __restrict__ tiles,
+                  int* __restrict__ bad, unsigned long long* __restrict__ stats) {
+  __shared__ unsigned long long red[3][8];
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int nt = 0;
+  if (i < n) nt = preprocess_one(attrs, n, i, cam, splats, keys, vals, tiles, bad);
+  unsigned long long cnt = (unsigned long long)nt;
+  unsigned long long kmn = ~0ull, kmx = 0;
+  if (nt) kmn = kmx = keys[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmn, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmx, o);
+    kmn = a < kmn ? a : kmn;
+    kmx = b > kmx ? b : kmx;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][w] = cnt;
+    red[1][w] = kmn;
+    red[2][w] = kmx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      cnt += red[0][k];
+      kmn = red[1][k] < kmn ? red[1][k] : kmn;
+      kmx = red[2][k] > kmx ? red[2][k] : kmx;
+    }
+    if (cnt) {
+      atomicAdd(stats, cnt);
+      atomicMin(stats + 1, kmn);
+      atomicMax(stats + 2, kmx);
+    }
+  }
 }
 
 __global__ void gather_kernel(const int* __restrict__ order, const Splat* __restrict__ splats,
@@ -699,21 +742,47 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   CK(R->bad.ensure(64, st));
   CK(R->host_pin.p ? cudaSuccess : cudaMallocHost(&R->host_pin.p, 256));
   R->host_pin.cap = 256;
-  int init_bad[8];
-  for (int k = 0; k < 8; ++k) init_bad[k] = 0x7fffffff;
-  CK(cudaMemcpyAsync(R->bad.p, init_bad, sizeof(init_bad), cudaMemcpyHostToDevice, st));
+  // bad[0..7]: first non-finite row per section; then u64 stats {Σ tile
+  // instances, min key, max key} — one 56-B read-back, the forward's only
+  // host synchronisation.
+  unsigned char init[64];
+  int* ib = reinterpret_cast<int*>(init);
+  for (int k = 0; k < 8; ++k) ib[k] = 0x7fffffff;
+  unsigned long long* is = reinterpret_cast<unsigned long long*>(init + 32);
+  is[0] = 0; is[1] = ~0ull; is[2] = 0; is[3] = 0;
+  CK(cudaMemcpyAsync(R->bad.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  unsigned long long* stats = reinterpret_cast<unsigned long long*>(static_cast<char*>(R->bad.p) + 32);
   const int TB = 256;
   const int nb = int((n + TB - 1) / TB);
   count_launch();
   preprocess_kernel<<<nb, TB, 0, st>>>(attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
-                                       R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>());
+                                       R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>(), stats);
   CK(cudaGetLastError());
-  // global stable sort on fp64 depth bits (ties keep index order), K6
+  unsigned char* hp = static_cast<unsigned char*>(R->host_pin.p);
+  CK(launch_readback(hp, R->bad.p, 64, st));
+  CK(cudaStreamSynchronize(st));
+  const int* badh = reinterpret_cast<const int*>(hp);
+  for (int k = 0; k < 6; ++k)
+    if (badh[k] != 0x7fffffff) {
+      R->bad_section = k;
+      R->bad_index = badh[k];
+      return cudaErrorInvalidValue;
+    }
+  const unsigned long long* hs = reinterpret_cast<const unsigned long long*>(hp + 32);
+  const long long n_inst = (long long)hs[0];
+  R->n_inst = n_inst;
+  if (n_inst > 0x7fffffffll) return cudaErrorMemoryAllocation;
+  // global stable sort on fp64 depth bits (ties keep index order), K6, over
+  // the bits where the contributing keys differ (non-contributing splats
+  // emit no instances, so their relative order is irrelevant)
+  int end_bit = 0;
+  if (n_inst > 0 && hs[1] != hs[2]) end_bit = 64 - __builtin_clzll(hs[1] ^ hs[2]);
   CK(R->temp.ensure(std::max(radix_scratch_bytes(n), scan_scratch_bytes(n + 1)), st));
   int alt = 0;
-  CK(radix_sort_pairs<unsigned long long>(R->keys.as<unsigned long long>(), R->keys2.as<unsigned long long>(),
-                                          R->vals.as<int>(), R->vals2.as<int>(), n, 0, 64, R->temp.p,
-                                          R->temp.cap, true, &alt, st));
+  if (end_bit > 0)
+    CK(radix_sort_pairs<unsigned long long>(R->keys.as<unsigned long long>(), R->keys2.as<unsigned long long>(),
+                                            R->vals.as<int>(), R->vals2.as<int>(), n, 0, end_bit, R->temp.p,
+                                            R->temp.cap, false, &alt, st));
   const int* order = alt ? R->vals2.as<int>() : R->vals.as<int>();
   count_launch();
   gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
@@ -721,20 +790,6 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   CK(cudaGetLastError());
   CK(cudaMemsetAsync(R->tiles_sorted.as<int>() + n, 0, 4, st));
   CK(exclusive_scan_i32(R->tiles_sorted.as<int>(), R->offs.as<long long>(), n + 1, R->temp.p, R->temp.cap, st));
-  long long* hp = static_cast<long long*>(R->host_pin.p);
-  CK(cudaMemcpyAsync(hp, R->offs.as<long long>() + n, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hp + 1, R->bad.p, 32, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const int* badh = reinterpret_cast<const int*>(hp + 1);
-  for (int k = 0; k < 6; ++k)
-    if (badh[k] != 0x7fffffff) {
-      R->bad_section = k;
-      R->bad_index = badh[k];
-      return cudaErrorInvalidValue;
-    }
-  const long long n_inst = hp[0];
-  R->n_inst = n_inst;
-  if (n_inst > 0x7fffffffll) return cudaErrorMemoryAllocation;
   CK(R->ikey.ensure(4 * n_inst + 4, st));
   CK(R->ikey2.ensure(4 * n_inst + 4, st));
   CK(R->ival.ensure(4 * n_inst + 4, st));

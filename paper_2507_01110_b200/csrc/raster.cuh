@@ -34,6 +34,7 @@ void raster_destroy(RasterCtx* r);
 cudaError_t raster_forward(RasterCtx* r, const double* attrs, long long n, const glod_camera& cam,
                            float* image, cudaStream_t st);
 cudaError_t raster_backward(RasterCtx* r, const float* dimg, double* grads, cudaStream_t st);
+cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 void raster_stats(const RasterCtx* r, glod_render_stats* out);
 bool raster_bad_input(const RasterCtx* r, int* section, int* index);
 

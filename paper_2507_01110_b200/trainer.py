@@ -199,10 +199,11 @@ class Trainer:
         sel = sc.lod.select(cam, self.cfg.lod, cull=True)
         S1 = max(sc.lod.S, 1)
         h = self._h_sel
-        h[:4].copy_(sel.counts, non_blocking=True)
-        h[4:4 + S1].copy_(sel.spt_ids[:S1], non_blocking=True)
-        h[4 + S1:4 + 2 * S1].copy_(sel.prefix_len[:S1], non_blocking=True)
-        self._h_droot.copy_(sel.d_root[:S1], non_blocking=True)
+        rb = _lib.readback      # kernel-written: never queues behind the write-back DMA
+        rb(h[:4], sel.counts[:4])
+        rb(h[4:4 + S1], sel.spt_ids[:S1])
+        rb(h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1])
+        rb(self._h_droot, sel.d_root[:S1])
         torch.cuda.current_stream().synchronize()
         n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
@@ -227,7 +228,7 @@ class Trainer:
             self._d_pref.copy_(self._h_pref, non_blocking=True)
         self._mark("cache")
         cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist, known_prefix=self._d_pref)
-        self._h_total.copy_(cmp.total, non_blocking=True)
+        _lib.readback(self._h_total[:1], cmp.total[:1])
         torch.cuda.current_stream().synchronize()
         self._mark("compact")
         n_sel = int(self._h_total[0])
@@ -276,7 +277,7 @@ class Trainer:
         self._mark("forward")
         value, dimg = self.rast.loss(image, target, cfg.loss_lambda)
         self._mark("loss")
-        self._h_loss.copy_(value, non_blocking=True)
+        _lib.readback(self._h_loss[:value.numel()], value)
         torch.cuda.current_stream().synchronize()
         loss_value = float(self._h_loss[0])
         if not np.isfinite(loss_value):

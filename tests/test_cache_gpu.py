@@ -88,3 +88,97 @@ def test_native_cache_over_budget():
     with pytest.raises(OverBudgetError):
         nat.step(np.array([0], np.int32), np.array([1.0]), np.array([4], np.int32), z,
                  np.zeros(1, np.uint64), np.zeros(1, np.int64))
+
+
+def _write_block(address: int, values: np.ndarray):
+    from cuda.bindings import runtime as rt
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    err, = rt.cudaMemcpy(address, v.ctypes.data, v.nbytes, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+    assert int(err) == 0
+
+
+def _write_block_async(address: int, values: np.ndarray):
+    """cudaMemcpyAsync on torch's current stream (the one the cache uses)."""
+    from cuda.bindings import runtime as rt
+    err, = rt.cudaMemcpyAsync(address, values.ctypes.data, values.nbytes,
+                              rt.cudaMemcpyKind.cudaMemcpyHostToDevice,
+                              torch.cuda.current_stream().cuda_stream)
+    assert int(err) == 0
+
+
+@pytest.mark.parametrize("seed,budget_frac", [(3, 0.15), (4, 0.4)])
+def test_native_cache_block_contents(seed, budget_frac):
+    """Block and store *contents* through evictions, write-backs, reloads of
+    blocks evicted earlier in the same step (overlay path) and flushes,
+    against a numpy mirror of the reference's load → insert → write_back
+    order (trainer.py:329-345, store.py:314-333).  Blocks rendered in a step
+    are modified between steps (the ADAM refresh) so every write-back
+    carries new values."""
+    h, hs, _ = designed_scene(SceneSpec(n_leaves=4000, spt_leaves=128, seed=seed, relabel=False))
+    st = HostStore(h, hs)
+    S = len(hs.spts)
+    counts = hs.flat_records()["count"]
+    cfg = CacheConfig(budget_bytes=max(int(budget_frac * counts.sum() * 92 / 3), int(counts.max()) * 92),
+                      flush_interval=11)
+    nat, py = NativeCache(cfg, st), DeviceCache(config=cfg)
+    store = [s.numpy().copy() for s in st.sections]
+    cols = [c for _, c in SECTIONS]
+
+    def load(sid, P):
+        sl = st.spt_slot_start(sid)
+        return np.concatenate([sec[sl:sl + P].reshape(-1).astype(np.float64) for sec in store])
+
+    def write_back(sid, blk):
+        sl = st.spt_slot_start(sid)
+        P = blk.size // 23
+        off = 0
+        for k, c in enumerate(cols):
+            store[k][sl:sl + P] = blk[off:off + c * P].reshape(store[k][sl:sl + P].shape).astype(np.float32)
+            off += c * P
+
+    rng = np.random.default_rng(seed)
+    base = rng.uniform(5, 50, S)
+    for it in range(1, 30):
+        k = int(rng.integers(S // 2, S + 1))
+        ids = np.sort(rng.choice(S, k, replace=False)).astype(np.int32)
+        d = base[ids] * rng.choice([1.0, 1.2, 1.6, 0.6], k)
+        P = np.maximum(1, (counts[ids] * rng.uniform(0.3, 1.0, k)).astype(np.int32))
+        dist = np.zeros(k, np.float64)
+        blk = np.zeros(k, np.uint64)
+        rows = np.zeros(k, np.int64)
+        nat.step(ids, d, P, dist, blk, rows)
+        for sid, dd, pp in zip(ids, d, P):
+            e = py.lookup(int(sid), float(dd))
+            if e is None:
+                e = CacheEntry(int(sid), float(dd), int(pp), load(int(sid), int(pp)), int(pp) * 92)
+                for esid, eblk in py.insert(e):
+                    write_back(esid, eblk)
+        # blocks rendered this step but evicted later in it are still
+        # refreshed by this step's ADAM (main stream, no host sync): their
+        # write-back must have read them first (the mirror keeps the old values)
+        keep = []
+        for j, sid in enumerate(ids):
+            if py.entries.get(int(sid)) is None:
+                junk = np.full(23 * int(rows[j]), 7.0)
+                keep.append(junk)
+                _write_block_async(int(blk[j]), junk)
+        torch.cuda.synchronize()
+        for j, sid in enumerate(ids):
+            e = py.entries.get(int(sid))
+            if e is None:
+                continue
+            np.testing.assert_array_equal(nat.read_block(int(blk[j]), int(rows[j])), e.block,
+                                          err_msg=f"step {it} spt {sid}")
+            # the step's ADAM refresh: new values in every rendered block
+            e.block = e.block + rng.normal(0, 1e-3, e.block.size)
+            _write_block(int(blk[j]), e.block)
+        nat.end_step(it, mark_dirty=True)
+        for sid in ids:
+            e = py.entries.get(int(sid))
+            if e is not None:
+                e.dirty = True
+        for esid, eblk in py.tick_and_maybe_flush(it):
+            write_back(esid, eblk)
+        torch.cuda.synchronize()
+        for k_, sec in enumerate(st.sections):
+            np.testing.assert_array_equal(sec.numpy(), store[k_], err_msg=f"store after step {it}")

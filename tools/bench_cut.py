@@ -35,6 +35,7 @@ def make_spts(n, S, rng):
         kp = np.sort(ks)[::-1].copy()
         kp[0] = np.inf
         nodes = (s * per + rng.permutation(per)).astype(np.int64)
+        ks[0] = ks.max()        # root = record 0 holds the max key: the filter path runs
         spts.append(Spt(root=int(nodes[0]), root_center=np.zeros(3), nodes=nodes, key_self=ks,
                         key_parent=kp))
     return spts
