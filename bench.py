@@ -36,8 +36,8 @@ BASE_METRIC = "train iters/s @1080p, 10M-Gaussian synthetic scene (host-DRAM sto
 def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--leaves", type=int, default=10_000_000)
     ap.add_argument("--width", type=int, default=1920)
@@ -86,9 +86,14 @@ def synthetic_targets(n, w, h, seed):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    nvidia-smi is started before the warm-up (its NVML initialisation
+    stalls the driver for a moment, which must not land in the timed
+    region); only samples taken between mark_start() and mark_stop() are
+    reported."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -96,6 +101,7 @@ class ClockSampler:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.gpu = gpu_index
         self.p = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -105,6 +111,20 @@ class ClockSampler:
         except Exception:
             self.p = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
+
+    @staticmethod
+    def _ts(s):
+        import datetime
+        try:
+            return datetime.datetime.strptime(s.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def stop(self) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -112,18 +132,24 @@ class ClockSampler:
         self.p.wait(timeout=5)
         self.f.flush()
         rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        rows = [r for r in rows if len(r) >= 10]
+        inside = [r for r in rows if self.t0 is not None and self._ts(r[0]) is not None
+                  and self.t0 - 0.05 <= self._ts(r[0]) <= (self.t1 or 1e300) + 0.05]
+        # a timed region shorter than the sampling period: the nearest samples
+        if not inside and rows and self.t0 is not None:
+            stamped = [(abs(self._ts(r[0]) - self.t0), r) for r in rows if self._ts(r[0]) is not None]
+            inside = [r for _, r in sorted(stamped, key=lambda x: x[0])[:2]]
+        isnum = lambda x: x.strip().replace(".", "").isdigit()
+        sm = [float(r[2]) for r in inside if isnum(r[2])]
+        mx = [float(r[3]) for r in inside if isnum(r[3])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in rows:
-            if len(r) < 9:
-                continue
+        for r in inside:
             for k, nm in enumerate(names):
-                if r[5 + k].strip().lower() == "active":
+                if r[6 + k].strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(inside)}
 
 
 # --------------------------------------------------------------------------
@@ -232,15 +258,16 @@ def run_ours(args):
     tr = Trainer(h, hs, list(zip(cams, targets)), tcfg, extent=2 * E)
     setup_s = time.time() - t0
     del h
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
     it = 0
     for _ in range(args.warmup):
         it += 1
         tr.train_step(it)
     torch.cuda.synchronize()
     # ---- timed region: device-resident inputs ---------------------------
-    clocks = ClockSampler(local)
-    if rank == 0:
-        clocks.start()
+    clocks.mark_start()
     n_launch0 = _lib.load().glod_launch_count()
     if world > 1:
         dist.barrier()
@@ -256,6 +283,7 @@ def run_ours(args):
         recs.append(tr.train_step(it))
     e1.record()
     torch.cuda.synchronize()
+    clocks.mark_stop()
     if prof:
         torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
@@ -268,6 +296,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = world * args.steps / (ms / 1e3)
+    cst = tr.cache.stats()
     # ---- per-stage timing (separate pass; CUDA events per stage) ---------
     tr.enable_timing(True)
     for _ in range(max(3, args.steps // 4)):
@@ -337,6 +366,11 @@ def run_ours(args):
                    "hits_last_step": recs[-1]["cache_hits"],
                    "mean_loaded_per_step": float(np.mean([r["gaussians_loaded_from_store"] for r in recs])),
                    "mean_rendered": float(np.mean([r["gaussians_rendered"] for r in recs])),
+                   "prefetch": {"prefetched_rows": cst["prefetched_rows"],
+                                "used_rows": cst["prefetch_used_rows"],
+                                "loaded_rows": cst["loaded_rows"],
+                                "note": "cumulative incl. warm-up; used rows were read from an HBM "
+                                        "copy made by the copy engines during the previous step"},
                    "l2_flush": "none; per-step working set (params 3.7 GB, instances) exceeds L2",
                    "scene_build_s": round(build_s, 1), "setup_s": round(setup_s, 1)},
         "stage_ms": stage_ms,

@@ -237,6 +237,10 @@ typedef struct glod_prefix_item {
    * (store.py:323-333 then :314-321).  NULL / 0 for a plain load. */
   const double* overlay;        /* [dev]                                       */
   int64_t overlay_rows;
+  /* loads only: when non-NULL the prefix is read from this packed f32
+   * section-major copy in HBM (a prefetch, glod_cache_prefetch) instead of
+   * the store; overlay is then unused. */
+  const float* src;             /* [dev]                                       */
 } glod_prefix_item;
 
 /* Device address of page-locked host memory (cudaHostGetDevicePointer). */
@@ -258,6 +262,7 @@ typedef struct glod_cache glod_cache;
 
 typedef struct glod_cache_stats_t {
   int64_t entries, resident_bytes, hits, misses, loaded_rows;
+  int64_t prefetched_rows, prefetch_used_rows;
 } glod_cache_stats_t;
 
 /* slot_start: host int64[num_spts], first store slot of each SPT
@@ -282,6 +287,19 @@ int glod_cache_step(glod_cache* c, const glod_store_view* store, int32_t n,
  * release evicted blocks stream-ordered. */
 int glod_cache_end_step(glod_cache* c, const glod_store_view* store, int64_t iteration,
                         int32_t mark_dirty, void* stream);
+/* Prefetch for a predicted view (no reference counterpart: the reference
+ * reads the store synchronously inside train_step, trainer.py:333-334).
+ * Host arrays as for glod_cache_step.  Every SPT the table would miss
+ * right now (lookup semantics of cache.py:56-73, no LRU update) is copied
+ * store → f32 HBM buffer by the copy engines on a prefetch stream, after
+ * all write-backs issued so far; at most max_rows rows (< 0: no cap).
+ * The next glod_cache_step uses a prefetch for a miss with the same prefix
+ * length whose store rows were not written back since; the others are
+ * freed.  Counters and cache decisions are unaffected.  rows_out: rows
+ * issued. */
+int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n,
+                        const int32_t* spt_ids, const double* d_root, const int32_t* prefix_len,
+                        int64_t max_rows, int64_t* rows_out, void* stream);
 int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
 /* Resident entries in LRU order (front first), up to `capacity`. */
 int glod_cache_entries(const glod_cache* c, int32_t* spt_id, double* cached_distance,

@@ -70,12 +70,13 @@ class StoreView(C.Structure):
 
 class PrefixItem(C.Structure):
     _fields_ = [("slot_start", C.c_int64), ("rows", C.c_int64), ("elem_start", C.c_int64),
-                ("block", P), ("overlay", P), ("overlay_rows", C.c_int64)]
+                ("block", P), ("overlay", P), ("overlay_rows", C.c_int64), ("src", P)]
 
 
 class CacheStats(C.Structure):
     _fields_ = [("entries", C.c_int64), ("resident_bytes", C.c_int64), ("hits", C.c_int64),
-                ("misses", C.c_int64), ("loaded_rows", C.c_int64)]
+                ("misses", C.c_int64), ("loaded_rows", C.c_int64), ("prefetched_rows", C.c_int64),
+                ("prefetch_used_rows", C.c_int64)]
 
 
 # name -> (restype, argtypes)
@@ -109,6 +110,7 @@ SIGNATURES = {
     "glod_cache_destroy": (C.c_int, [P]),
     "glod_cache_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, P, P, P, P, P]),
     "glod_cache_end_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int64, C.c_int32, P]),
+    "glod_cache_prefetch": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, C.c_int64, P, P]),
     "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
     "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
     "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),

@@ -13,6 +13,8 @@
 #include <string.h>
 
 #include <list>
+#include <map>
+#include <set>
 #include <unordered_map>
 #include <vector>
 
@@ -29,6 +31,7 @@ cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long lon
 namespace {
 
 constexpr int kFloats = 23;
+constexpr int kSecOffH[7] = {0, 3, 6, 10, 11, 14, 23};
 
 struct Entry {
   int32_t spt_id;
@@ -37,6 +40,83 @@ struct Entry {
   double* block;
   int64_t nbytes;
   bool dirty;
+};
+
+// A device region sub-allocated on the host (best fit, coalescing free
+// list).  Frees take effect at host time, which is safe because every
+// device user of an arena is ordered on one stream (blocks: the main
+// stream; prefetch buffers: see CacheTable) — it replaces hundreds of
+// cudaMallocFromPoolAsync/cudaFreeAsync driver calls per step that sat on
+// the step's critical path while the GPU waited for the cache decisions.
+class Arena {
+ public:
+  ~Arena() {
+    if (base_) cudaFree(base_);
+  }
+  cudaError_t init(size_t bytes) {
+    bytes = (bytes + kAlign - 1) / kAlign * kAlign;
+    cudaError_t e = cudaMalloc(&base_, bytes);
+    if (e != cudaSuccess) {
+      base_ = nullptr;
+      return e;
+    }
+    cap_ = bytes;
+    put(0, bytes);
+    return cudaSuccess;
+  }
+  bool ready() const { return base_ != nullptr; }
+  void* alloc(size_t bytes) {
+    if (!base_) return nullptr;
+    bytes = bytes ? (bytes + kAlign - 1) / kAlign * kAlign : kAlign;
+    auto it = by_size_.lower_bound({bytes, 0});
+    if (it == by_size_.end()) return nullptr;
+    const size_t off = it->second, sz = it->first;
+    take(off, sz);
+    if (sz > bytes) put(off + bytes, sz - bytes);
+    live_[off] = bytes;
+    return base_ + off;
+  }
+  bool release(void* p) {
+    char* c = static_cast<char*>(p);
+    if (!base_ || c < base_ || c >= base_ + cap_) return false;
+    const size_t off = size_t(c - base_);
+    auto lv = live_.find(off);
+    if (lv == live_.end()) return false;
+    size_t o = off, sz = lv->second;
+    live_.erase(lv);
+    auto nx = free_.lower_bound(o);
+    if (nx != free_.end() && nx->first == o + sz) {
+      sz += nx->second;
+      take(nx->first, nx->second);
+    }
+    auto pv = free_.lower_bound(o);
+    if (pv != free_.begin()) {
+      --pv;
+      if (pv->first + pv->second == o) {
+        o = pv->first;
+        sz += pv->second;
+        take(pv->first, pv->second);
+      }
+    }
+    put(o, sz);
+    return true;
+  }
+
+ private:
+  static constexpr size_t kAlign = 256;
+  void put(size_t off, size_t sz) {
+    free_[off] = sz;
+    by_size_.insert({sz, off});
+  }
+  void take(size_t off, size_t sz) {
+    free_.erase(off);
+    by_size_.erase({sz, off});
+  }
+  char* base_ = nullptr;
+  size_t cap_ = 0;
+  std::map<size_t, size_t> free_;                 // offset -> size
+  std::set<std::pair<size_t, size_t>> by_size_;   // (size, offset)
+  std::unordered_map<size_t, size_t> live_;       // offset -> size
 };
 
 }  // namespace
@@ -58,27 +138,64 @@ struct CacheTable {
   std::vector<int32_t> step_ids;          // SPTs rendered this step (dirty at end)
   std::vector<double*> to_free;           // blocks dropped this step
   int device = 0;
-  // Write-back copies run on a side stream so the D2H PCIe direction
-  // overlaps the rest of the step.  The main stream waits for them only
-  // when a load reads store rows a not-yet-finished write-back of an
-  // earlier step writes (wb_prev); a block evicted and re-requested within
-  // one step is reloaded from the evicted block itself (overlay, below).
+  bool ready = false;
+
+  // Memory.  Blocks and item tables: `blocks` arena (every user on the main
+  // stream), falling back to a private stream-ordered pool when full.
+  // Prefetch buffers: `pfmem` arena; their users are the prefetch stream
+  // (DMA in) and one load kernel on the main stream, after which ev_pf_free
+  // is recorded and the next prefetch DMA waits for it.
+  Arena blocks, pfmem;
+  cudaMemPool_t pool = nullptr;
+
+  // Write-back: the blocks are packed to f32 on the main stream inside the
+  // step (so a replaced dirty entry is written back after its stale reload,
+  // and every written-back block is read before this step's ADAM refresh
+  // rewrites it — the reference writes back at eviction); the copy engines
+  // then move the f32 rows into the pinned store on the side stream
+  // (cudaMemcpyBatchAsync, 6 section ranges per block).  The DMA is issued
+  // at end_step, when the step's kernels are queued and the host is idle
+  // (the batch call costs ~0.3 µs per range of host time).  Two persistent
+  // f32 staging buffers used alternately; the main stream reuses one only
+  // after the side stream's copies out of it (ev_stage).  The main stream
+  // waits for write-backs only when a load reads store rows a not yet
+  // finished write-back of an earlier step writes (wb_prev); a block
+  // evicted and re-requested within one step is reloaded from the evicted
+  // block itself (overlay).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_main = nullptr, ev_wb = nullptr;
   std::unordered_map<int32_t, int> wb_prev;   // SPT ids with write-backs in flight
-
-  // Blocks and item tables: a private stream-ordered pool (all allocations
-  // and frees on the main stream).  Write-back staging: two persistent f32
-  // buffers used alternately; the main stream reuses one only after the
-  // side stream's copies out of it (ev_stage) — two batches earlier.
-  cudaMemPool_t pool = nullptr;
   float* stage[2] = {nullptr, nullptr};
   size_t stage_cap[2] = {0, 0};
   cudaEvent_t ev_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_packed[2] = {nullptr, nullptr};
   int stage_next = 0;
+  struct PendingWb {
+    int sb = -1;
+    std::vector<void*> dst, src;
+    std::vector<size_t> size;
+    std::vector<int32_t> sids;
+  };
+  std::vector<PendingWb> pending;
+  float* hsec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
-  cudaError_t ensure_side() {
-    if (side) return cudaSuccess;
+  // Prefetch (glod_cache_prefetch): the predicted misses of the next view
+  // are copied store → f32 HBM buffers by the copy engines on `pf_st`
+  // while the current step computes; the next cache_step converts a
+  // prefetched prefix from HBM instead of reading it over PCIe.  A prefetch
+  // lives for one step and is used only when its prefix length matches and
+  // no write-back of its store rows was ordered after it.
+  struct Prefetch {
+    int64_t rows;
+    float* buf;
+  };
+  std::unordered_map<int32_t, Prefetch> pf;
+  cudaStream_t pf_st = nullptr;
+  cudaEvent_t ev_pf = nullptr, ev_pf_free = nullptr;
+  int64_t pf_issued_rows = 0, pf_used_rows = 0;
+
+  cudaError_t init(const glod_store_view& sv) {
+    if (ready) return cudaSuccess;
     cudaMemPoolProps props = {};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -89,42 +206,107 @@ struct CacheTable {
     e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     if (e != cudaSuccess) return e;
     for (int k = 0; k < 2; ++k) {
-      e = cudaEventCreateWithFlags(&ev_stage[k], cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_stage[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_packed[k], cudaEventDisableTiming);
     }
-    e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_wb, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&items_done, cudaEventDisableTiming);
-    return e;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pf_st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_pf_free, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    // host addresses of the store sections (the view holds device-mapped
+    // addresses; the copy engines take the host side under UVA)
+    for (int k = 0; k < 6; ++k) {
+      cudaPointerAttributes at;
+      e = cudaPointerGetAttributes(&at, sv.section[k]);
+      if (e != cudaSuccess) return e;
+      hsec[k] = static_cast<float*>(at.hostPointer ? at.hostPointer : const_cast<float*>(sv.section[k]));
+    }
+    // Arenas sized from the budget (counted in f32 store bytes): resident
+    // f64 blocks ≤ 2·budget, blocks dropped within a step ≤ 2·budget more;
+    // prefetch copies ≤ budget.  Capped by free HBM; a failed reservation
+    // just leaves the pool path.
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t want_blocks = size_t(4) * size_t(budget) + (size_t(64) << 20);
+    const size_t want_pf = size_t(budget) + (size_t(16) << 20);
+    if (want_blocks + want_pf < fr / 2) {
+      if (blocks.init(want_blocks) != cudaSuccess || pfmem.init(want_pf) != cudaSuccess) cudaGetLastError();
+    }
+    ready = true;
+    return cudaSuccess;
+  }
+
+  cudaError_t dalloc(void** p, size_t bytes, cudaStream_t st) {
+    *p = blocks.alloc(bytes);
+    if (*p) return cudaSuccess;
+    return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, st);
+  }
+  cudaError_t dfree(void* p, cudaStream_t st) {
+    if (blocks.release(p)) return cudaSuccess;
+    return cudaFreeAsync(p, st);
+  }
+
+  // Prefetch buffers go back to their arena once the main stream has
+  // passed their last use (the caller recorded ev_pf_free on it).
+  void release_prefetches(std::unordered_map<int32_t, Prefetch>& m) {
+    for (auto& kv : m) pfmem.release(kv.second.buf);
+    m.clear();
+  }
+
+  // Issue the queued write-back DMA (side stream).
+  cudaError_t issue_pending() {
+    for (PendingWb& w : pending) {
+      cudaError_t e = cudaStreamWaitEvent(side, ev_packed[w.sb], 0);
+      if (e != cudaSuccess) return e;
+      cudaMemcpyAttributes attr = {};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+      size_t attr_idx = 0, fail = 0;
+      e = cudaMemcpyBatchAsync(w.dst.data(), w.src.data(), w.size.data(), w.dst.size(), &attr, &attr_idx,
+                               1, &fail, side);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_stage[w.sb], side);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_wb, side);
+      if (e != cudaSuccess) return e;
+      for (int32_t sid : w.sids) wb_prev[sid] = 1;
+    }
+    pending.clear();
+    return cudaSuccess;
   }
 
   ~CacheTable() {
     if (side) cudaStreamSynchronize(side);
+    if (pf_st) cudaStreamSynchronize(pf_st);
+    cudaDeviceSynchronize();
+    for (auto& e : lru) dfree(e.block, 0);
+    for (double* b : to_free) dfree(b, 0);
     cudaDeviceSynchronize();
     if (items_done) cudaEventDestroy(items_done);
     if (ev_main) cudaEventDestroy(ev_main);
     if (ev_wb) cudaEventDestroy(ev_wb);
+    if (ev_pf) cudaEventDestroy(ev_pf);
+    if (ev_pf_free) cudaEventDestroy(ev_pf_free);
     if (side) cudaStreamDestroy(side);
-    for (auto& e : lru) cudaFree(e.block);
-    for (double* b : to_free) cudaFree(b);
+    if (pf_st) cudaStreamDestroy(pf_st);
     if (h_items) cudaFreeHost(h_items);
     for (int k = 0; k < 2; ++k) {
       if (stage[k]) cudaFree(stage[k]);
       if (ev_stage[k]) cudaEventDestroy(ev_stage[k]);
+      if (ev_packed[k]) cudaEventDestroy(ev_packed[k]);
     }
     if (pool) cudaMemPoolDestroy(pool);
   }
 
   // pinned item table of at least n entries, safe to rewrite
   cudaError_t ensure_items(size_t n) {
-    cudaError_t e = ensure_side();
-    if (e != cudaSuccess) return e;
     cudaEventSynchronize(items_done);
     if (n <= items_cap) return cudaSuccess;
     if (h_items) cudaFreeHost(h_items);
     const size_t want = n * 2 + 64;
-    e = cudaMallocHost(&h_items, want * sizeof(glod_prefix_item));
+    cudaError_t e = cudaMallocHost(&h_items, want * sizeof(glod_prefix_item));
     if (e != cudaSuccess) return e;
     items_cap = want;
     return cudaSuccess;
@@ -139,11 +321,12 @@ struct Xfer {
   double* block;
   const double* overlay;       // loads: rows [0, overlay_rows) come from here
   int64_t overlay_rows;
+  const float* src = nullptr;  // loads: prefetched f32 copy of the prefix (HBM)
 };
 
-// Copies `v` into the pinned table at `off` and then to a stream-ordered
-// device table; returns the device table (freed by the caller's stream
-// order) and the element total.
+// Copies `v` into the pinned table at `off` and then to a device table
+// (main-stream ordered; freed by the caller after its kernel); returns the
+// device table and the element total.
 cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, cudaStream_t st,
                         glod_prefix_item** d_out, long long* total) {
   glod_prefix_item* h = c->h_items + off;
@@ -155,38 +338,25 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
     h[i].block = v[i].block;
     h[i].overlay = v[i].overlay;
     h[i].overlay_rows = v[i].overlay_rows;
+    h[i].src = v[i].src;
     acc += kFloats * v[i].rows;
   }
-  glod_prefix_item* d = nullptr;
-  cudaError_t e = cudaMallocFromPoolAsync(&d, v.size() * sizeof(glod_prefix_item), c->pool, st);
+  void* d = nullptr;
+  cudaError_t e = c->dalloc(&d, v.size() * sizeof(glod_prefix_item), st);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
-  *d_out = d;
+  *d_out = static_cast<glod_prefix_item*>(d);
   *total = acc;
   return cudaSuccess;
 }
 
-// Host address of a store section (the view holds device-mapped
-// addresses; the copy engines take the host side under UVA).
-cudaError_t host_section(const glod_store_view& sv, int k, float** out) {
-  cudaPointerAttributes at;
-  cudaError_t e = cudaPointerGetAttributes(&at, sv.section[k]);
-  if (e != cudaSuccess) return e;
-  *out = static_cast<float*>(at.hostPointer ? at.hostPointer : const_cast<float*>(sv.section[k]));
-  return cudaSuccess;
-}
-
-// One step's transfers.  Loads: one zero-copy kernel on the main stream.
-// Write-backs: the blocks are packed to f32 on the main stream right after
-// the loads (so a replaced dirty entry is written back after its stale
-// reload, and every written-back block is read before this step's ADAM
-// refresh rewrites it — the reference writes back at eviction), then the
-// copy engines move the f32 rows into the pinned store on the side stream
-// (cudaMemcpyBatchAsync, 6 section ranges per block): no SM time, so the
-// D2H direction overlaps the rest of the step without slowing its kernels.
-cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, const std::vector<Xfer>& loads,
-                      const std::vector<Xfer>& wbs, bool join, cudaStream_t st) {
+// One batch of transfers.  Loads: one kernel on the main stream (zero-copy
+// PCIe reads of the pinned store, or HBM reads of prefetched copies).
+// Write-backs: packed to f32 staging on the main stream; the DMA into the
+// store is queued (CacheTable::pending) and issued at end_step.
+cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::vector<Xfer>& wbs,
+                      bool join, bool wait_pf, const glod_store_view& sv, cudaStream_t st) {
   cudaError_t e = c->ensure_items(loads.size() + wbs.size() + 1);
   if (e != cudaSuccess) return e;
   if (join) {
@@ -194,12 +364,16 @@ cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, const std::vecto
     if (e != cudaSuccess) return e;
     c->wb_prev.clear();
   }
+  if (wait_pf) {
+    e = cudaStreamWaitEvent(st, c->ev_pf, 0);
+    if (e != cudaSuccess) return e;
+  }
   if (!loads.empty()) {
     glod_prefix_item* d = nullptr;
     long long total = 0;
     e = stage_items(c, loads, 0, st, &d, &total);
     if (e == cudaSuccess) e = launch_store_xfer(sv, d, int(loads.size()), total, 1, st);
-    if (e == cudaSuccess) e = cudaFreeAsync(d, st);
+    if (e == cudaSuccess) e = c->dfree(d, st);
     if (e != cudaSuccess) return e;
   }
   if (!wbs.empty()) {
@@ -209,6 +383,12 @@ cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, const std::vecto
     if (e != cudaSuccess) return e;
     const int sb = c->stage_next;
     c->stage_next ^= 1;
+    for (const auto& w : c->pending)          // staging buffer still queued: issue first
+      if (w.sb == sb) {
+        e = c->issue_pending();
+        if (e != cudaSuccess) return e;
+        break;
+      }
     const size_t need = size_t(total) * sizeof(float);
     if (need > c->stage_cap[sb]) {
       e = cudaEventSynchronize(c->ev_stage[sb]);          // copies out of the old buffer
@@ -222,39 +402,24 @@ cudaError_t run_batch(CacheTable* c, const glod_store_view& sv, const std::vecto
     float* staging = c->stage[sb];
     e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
     if (e == cudaSuccess) e = launch_pack_f32(d, int(wbs.size()), total, staging, st);
-    if (e == cudaSuccess) e = cudaFreeAsync(d, st);
-    if (e == cudaSuccess) e = cudaEventRecord(c->ev_main, st);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->side, c->ev_main, 0);
+    if (e == cudaSuccess) e = c->dfree(d, st);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_packed[sb], st);
     if (e != cudaSuccess) return e;
-    float* hsec[6];
-    for (int k = 0; k < 6; ++k) {
-      e = host_section(sv, k, &hsec[k]);
-      if (e != cudaSuccess) return e;
-    }
-    static const int off[7] = {0, 3, 6, 10, 11, 14, 23};
-    std::vector<void*> dst, src;
-    std::vector<size_t> size;
-    dst.reserve(6 * wbs.size()); src.reserve(6 * wbs.size()); size.reserve(6 * wbs.size());
+    CacheTable::PendingWb w;
+    w.sb = sb;
+    w.dst.reserve(6 * wbs.size()); w.src.reserve(6 * wbs.size()); w.size.reserve(6 * wbs.size());
     long long acc = 0;
     for (const Xfer& x : wbs) {
       for (int k = 0; k < 6; ++k) {
-        const int cols = off[k + 1] - off[k];
-        dst.push_back(hsec[k] + x.slot * cols);
-        src.push_back(staging + acc + (long long)off[k] * x.rows);
-        size.push_back(size_t(cols) * size_t(x.rows) * sizeof(float));
+        const int cols = kSecOffH[k + 1] - kSecOffH[k];
+        w.dst.push_back(c->hsec[k] + x.slot * cols);
+        w.src.push_back(staging + acc + (long long)kSecOffH[k] * x.rows);
+        w.size.push_back(size_t(cols) * size_t(x.rows) * sizeof(float));
       }
       acc += kFloats * x.rows;
+      w.sids.push_back(x.spt_id);
     }
-    cudaMemcpyAttributes attr = {};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail = 0;
-    e = cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1, &fail,
-                             c->side);
-    if (e == cudaSuccess) e = cudaEventRecord(c->ev_stage[sb], c->side);
-    if (e == cudaSuccess) e = cudaEventRecord(c->ev_wb, c->side);
-    if (e != cudaSuccess) return e;
-    for (const Xfer& x : wbs) c->wb_prev[x.spt_id] = 1;
+    c->pending.push_back(std::move(w));
   }
   return cudaEventRecord(c->items_done, st);
 }
@@ -265,13 +430,16 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
                        const double* d_root, const int32_t* prefix_len, double* dist_out,
                        uint64_t* block_out, int64_t* rows_out, int64_t* loaded_rows,
                        int64_t* hits, cudaStream_t st) {
-  cudaError_t e = c->ensure_side();
+  cudaError_t e = c->init(sv);
+  if (e == cudaSuccess) e = c->issue_pending();       // end_step was skipped
   if (e != cudaSuccess) return e;
   // write-backs of earlier steps already finished: nothing to wait for
   if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
   std::vector<Xfer> loads, wbs;
   std::unordered_map<int32_t, std::pair<const double*, int64_t>> evicted;   // dirty, this step
-  bool join = false;
+  bool join = false, wait_pf = false;
+  std::unordered_map<int32_t, CacheTable::Prefetch> avail;   // issued last step
+  avail.swap(c->pf);
   const int64_t hits0 = c->hits, loaded0 = c->loaded_rows;
   c->step_ids.assign(spt_ids, spt_ids + n);
   auto drop = [&](const Entry& v) {
@@ -303,12 +471,19 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
       const int64_t P = prefix_len[j];
       const int64_t nbytes = P * c->bytes_per_row;
       if (nbytes > c->budget) return cudaErrorNotPermitted;   // OverBudgetError
-      double* blk = nullptr;
-      e = cudaMallocFromPoolAsync(&blk, size_t(kFloats) * size_t(P > 0 ? P : 1) * sizeof(double), c->pool, st);
+      void* blk = nullptr;
+      e = c->dalloc(&blk, size_t(kFloats) * size_t(P > 0 ? P : 1) * sizeof(double), st);
       if (e != cudaSuccess) return e;
-      Xfer ld{sid, c->slot_start[sid], P, blk, nullptr, 0};
+      Xfer ld{sid, c->slot_start[sid], P, static_cast<double*>(blk), nullptr, 0};
       auto ev = evicted.find(sid);
-      if (ev != evicted.end()) {
+      auto pv = avail.find(sid);
+      if (pv != avail.end() && pv->second.rows == P && ev == evicted.end()) {
+        // prefetched after every write-back of these rows so far: the store
+        // contents the reference would read now
+        ld.src = pv->second.buf;
+        c->pf_used_rows += P;
+        wait_pf = true;
+      } else if (ev != evicted.end()) {
         // evicted (dirty) earlier in this step: the reference writes it back
         // and then reads the store, i.e. rows below the old prefix are the
         // f32 rounding of the evicted block, the rest the untouched store
@@ -328,7 +503,7 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
         drop(old);
         evicted.erase(sid);          // never requested again this step
       }
-      c->lru.push_back({sid, d, P, blk, nbytes, false});
+      c->lru.push_back({sid, d, P, static_cast<double*>(blk), nbytes, false});
       c->map[sid] = std::prev(c->lru.end());
       c->resident += nbytes;
       while (c->resident > c->budget) {
@@ -343,20 +518,26 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
     block_out[j] = reinterpret_cast<uint64_t>(en.block);
     rows_out[j] = en.prefix_len;
   }
-  e = run_batch(c, sv, loads, wbs, join, st);
+  e = run_batch(c, loads, wbs, join, wait_pf, sv, st);
   if (e != cudaSuccess) return e;
+  // every prefetch of the last step is done with once the load kernel ran
+  if (!avail.empty()) {
+    e = cudaEventRecord(c->ev_pf_free, st);
+    if (e != cudaSuccess) return e;
+    c->release_prefetches(avail);
+  }
   *loaded_rows = c->loaded_rows - loaded0;
   *hits = c->hits - hits0;
   return cudaSuccess;
 }
 
 // Blocks dropped this step are still read by this step's kernels (the
-// reference keeps its `entry` references alive): free them in main-stream
-// order once the step is enqueued (their write-backs read the f32 staging
-// copy, not the block).
+// reference keeps its `entry` references alive): release them in
+// main-stream order once the step is enqueued (their write-backs read the
+// f32 staging copy, not the block).
 cudaError_t cache_release(CacheTable* c, cudaStream_t st) {
   for (double* b : c->to_free) {
-    cudaError_t e = cudaFreeAsync(b, st);
+    cudaError_t e = c->dfree(b, st);
     if (e != cudaSuccess) return e;
   }
   c->to_free.clear();
@@ -365,13 +546,14 @@ cudaError_t cache_release(CacheTable* c, cudaStream_t st) {
 
 cudaError_t cache_end_step(CacheTable* c, const glod_store_view& sv, int64_t iteration,
                            int mark_dirty, cudaStream_t st) {
+  cudaError_t e = c->init(sv);
+  if (e != cudaSuccess) return e;
   if (mark_dirty)
     for (int32_t sid : c->step_ids) {
       auto it = c->map.find(sid);
       if (it != c->map.end()) it->second->dirty = true;
     }
   c->step_ids.clear();
-  cudaError_t e = cudaSuccess;
   if (iteration >= 0 && iteration % c->flush_interval == 0) {
     std::vector<Xfer> none, wbs;
     for (auto& en : c->lru) {
@@ -381,10 +563,100 @@ cudaError_t cache_end_step(CacheTable* c, const glod_store_view& sv, int64_t ite
     c->lru.clear();
     c->map.clear();
     c->resident = 0;
-    e = run_batch(c, sv, none, wbs, false, st);
+    // prefetched store rows may be rewritten now: drop them (no main-stream
+    // user, so the arena takes them back at once)
+    c->release_prefetches(c->pf);
+    e = run_batch(c, none, wbs, false, false, sv, st);
     if (e != cudaSuccess) return e;
   }
+  e = c->issue_pending();
+  if (e != cudaSuccess) return e;
   return cache_release(c, st);
+}
+
+// Prefetch of a predicted view (the scheduler's next draw): every selected
+// SPT the table would miss now is copied store → f32 HBM buffer on the
+// prefetch stream by the copy engines (6 section ranges per prefix, one
+// cudaMemcpyBatchAsync), ordered after every write-back issued so far.
+// Read-only on the table; correctness never depends on the prediction
+// (cache_step checks the prefix length and same-step evictions before
+// using one, and a flush drops them).
+cudaError_t cache_prefetch(CacheTable* c, const glod_store_view& sv, int32_t n, const int32_t* spt_ids,
+                           const double* d_root, const int32_t* prefix_len, int64_t max_rows,
+                           int64_t* rows_out, cudaStream_t st) {
+  (void)st;
+  cudaError_t e = c->init(sv);
+  if (e == cudaSuccess) e = c->issue_pending();
+  if (e != cudaSuccess) return e;
+  *rows_out = 0;
+  if (!c->pfmem.ready()) return cudaSuccess;
+  if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
+  struct Want {
+    int32_t sid;
+    int64_t rows;
+    float* buf;
+  };
+  std::vector<Want> now, after_wb;
+  int64_t total = 0;
+  for (int32_t j = 0; j < n; ++j) {
+    const int32_t sid = spt_ids[j];
+    const int64_t P = prefix_len[j];
+    if (P <= 0 || c->pf.count(sid)) continue;
+    auto it = c->map.find(sid);
+    if (it != c->map.end()) {
+      const double cd = it->second->cached_distance, d = d_root[j];
+      bool hit;
+      if (cd == 0.0) hit = d == 0.0;
+      else {
+        const double ratio = d / cd;
+        hit = c->d_min <= ratio && ratio <= c->d_max;
+      }
+      if (hit) continue;
+    }
+    if (P * c->bytes_per_row > c->budget) continue;
+    if (max_rows >= 0 && total + P > max_rows) break;
+    float* buf = static_cast<float*>(c->pfmem.alloc(size_t(kFloats) * size_t(P) * sizeof(float)));
+    if (!buf) break;                                  // prefetch memory full
+    c->pf[sid] = {P, buf};
+    (c->wb_prev.count(sid) ? after_wb : now).push_back({sid, P, buf});
+    total += P;
+  }
+  if (now.empty() && after_wb.empty()) return cudaSuccess;
+  // the buffers' previous users: the last load kernel on the main stream
+  e = cudaStreamWaitEvent(c->pf_st, c->ev_pf_free, 0);
+  if (e != cudaSuccess) return e;
+  auto issue = [&](const std::vector<Want>& v) -> cudaError_t {
+    if (v.empty()) return cudaSuccess;
+    std::vector<void*> dst, src;
+    std::vector<size_t> size;
+    dst.reserve(6 * v.size()); src.reserve(6 * v.size()); size.reserve(6 * v.size());
+    for (const Want& w : v) {
+      const int64_t slot = c->slot_start[w.sid];
+      for (int k = 0; k < 6; ++k) {
+        const int cols = kSecOffH[k + 1] - kSecOffH[k];
+        dst.push_back(w.buf + (int64_t)kSecOffH[k] * w.rows);
+        src.push_back(c->hsec[k] + slot * cols);
+        size.push_back(size_t(cols) * size_t(w.rows) * sizeof(float));
+      }
+    }
+    cudaMemcpyAttributes attr = {};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail = 0;
+    return cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1,
+                                &fail, c->pf_st);
+  };
+  e = issue(now);
+  if (e == cudaSuccess && !after_wb.empty()) {
+    // store rows with a write-back in flight: copy them after it lands
+    e = cudaStreamWaitEvent(c->pf_st, c->ev_wb, 0);
+    if (e == cudaSuccess) e = issue(after_wb);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(c->ev_pf, c->pf_st);
+  if (e != cudaSuccess) return e;
+  c->pf_issued_rows += total;
+  *rows_out = total;
+  return cudaSuccess;
 }
 
 }  // namespace glod
@@ -445,6 +717,17 @@ int glod_cache_end_step(glod_cache* c, const glod_store_view* store, int64_t ite
   return GLOD_OK;
 }
 
+int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n, const int32_t* spt_ids,
+                        const double* d_root, const int32_t* prefix_len, int64_t max_rows,
+                        int64_t* rows_out, void* stream) {
+  if (!c || !store || !rows_out || (n > 0 && (!spt_ids || !d_root || !prefix_len)))
+    return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  cudaError_t e = glod::cache_prefetch(&c->t, *store, n, spt_ids, d_root, prefix_len, max_rows, rows_out,
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
+  return GLOD_OK;
+}
+
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes) {
   if (!dst || !src) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   cudaError_t e = cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDeviceToHost);
@@ -459,6 +742,8 @@ int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out) {
   out->hits = c->t.hits;
   out->misses = c->t.misses;
   out->loaded_rows = c->t.loaded_rows;
+  out->prefetched_rows = c->t.pf_issued_rows;
+  out->prefetch_used_rows = c->t.pf_used_rows;
   return GLOD_OK;
 }
 

@@ -142,7 +142,9 @@ store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items
     for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
     const long long within = local - kSecOff[sec] * rows;
     float* host = const_cast<float*>(sv.section[sec]) + I.slot_start * kSecCols[sec] + within;
-    if (kLoad) {
+    if (kLoad && I.src) {
+      I.block[local] = double(I.src[local]);    // prefetched copy in HBM
+    } else if (kLoad) {
       // overlay: rows below overlay_rows are the f32 rounding of a block whose
       // write-back to these store rows is still in flight (cache_table.cu)
       const long long row = within / kSecCols[sec];

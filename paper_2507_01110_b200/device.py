@@ -182,8 +182,20 @@ class DeviceLodScene:
         self.scales.copy_(torch.from_numpy(np.ascontiguousarray(h.attrs.scales, dtype=np.float64).reshape(-1)))
 
     # ---- kernels ----------------------------------------------------------
+    def _alt_outputs(self):
+        """A second output set (speculative selects of a predicted view)."""
+        if getattr(self, "_alt", None) is None:
+            dev, S1 = self.device, max(self.S, 1)
+            self._alt = (torch.empty(self.cap, dtype=torch.int32, device=dev),
+                         torch.empty(self.cap, dtype=torch.int32, device=dev),
+                         torch.empty(S1, dtype=torch.int32, device=dev),
+                         torch.empty(S1, dtype=torch.float64, device=dev),
+                         torch.empty(S1, dtype=torch.int32, device=dev),
+                         torch.zeros(4, dtype=torch.int32, device=dev))
+        return self._alt
+
     def select(self, cam: Camera, cfg: LodConfig, cull: bool = True,
-               frustum: Frustum | None = None, stream=None) -> SelectResult:
+               frustum: Frustum | None = None, stream=None, alt: bool = False) -> SelectResult:
         v = _lib.LodView()
         v.position[:] = [float(x) for x in cam.position]
         if cull:
@@ -192,14 +204,13 @@ class DeviceLodScene:
         v.cull = int(bool(cull))
         v.metric = cfg.metric_code if hasattr(cfg, "metric_code") else (0 if cfg.metric == "max_scale" else 1)
         v.threshold = float(cfg.threshold)
-        out = _lib.SelectOut(upper_ids=_lib.ptr(self.o_upper), pass_ids=_lib.ptr(self.o_pass),
-                             spt_ids=_lib.ptr(self.o_spt), d_root=_lib.ptr(self.o_droot),
-                             prefix_len=_lib.ptr(self.o_prefix), counts=_lib.ptr(self.o_counts))
+        bufs = self._alt_outputs() if alt else (self.o_upper, self.o_pass, self.o_spt, self.o_droot,
+                                                 self.o_prefix, self.o_counts)
+        out = _lib.SelectOut(*[_lib.ptr(b) for b in bufs])
         _lib.check(_lib.lib().glod_lod_select(C.byref(self._struct), C.byref(v), C.byref(out),
                                               _lib.ptr(self.sel_scratch), self.sel_scratch.numel(),
                                               _lib.stream_ptr(stream)))
-        return SelectResult(self.o_upper, self.o_pass, self.o_spt, self.o_droot, self.o_prefix,
-                            self.o_counts)
+        return SelectResult(*bufs)
 
     def compact(self, n_spt: torch.Tensor, spt_ids: torch.Tensor, dist: torch.Tensor,
                 known_prefix: torch.Tensor | None = None, stream=None) -> CompactResult:

@@ -59,6 +59,9 @@ class TrainConfig:
     scheduler_exploration: float | None = None
     scheduler_random_every: int = DEFAULT_RANDOM_EVERY
     seed: int = 0
+    # copy-engine prefetch of the scheduler's next view's cache misses
+    # (not in the reference; decisions and counters are unchanged)
+    prefetch: bool = True
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -149,6 +152,13 @@ class Trainer:
         self._bias_len = 0
         self._target_dev = None
         self.last_stats = {}
+        # prefetch: last selection per view (host) and the predicted next view
+        self._hist = {}
+        self._next_view = None
+        self._pred = None
+        self._pf_rows_cap = cfg.cache.budget_bytes // BYTES_PER_GAUSSIAN_F32
+        self._h_sel2 = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()
+        self._h_droot2 = torch.empty(S1, dtype=torch.float64).pin_memory()
         self.timing = None          # {stage: [ms, ...]} when profiling is on
         self._ev = []
 
@@ -193,33 +203,62 @@ class Trainer:
         return t
 
     # ------------------------------------------------------------------
-    def select(self, cam: Camera):
-        """LoD select + one D2H of the per-SPT table (the step's host sync)."""
+    def select(self, cam: Camera, spec_cam: Camera | None = None):
+        """LoD select + one D2H of the per-SPT table (the step's host sync).
+        With `spec_cam`, a speculative select of that (predicted next) view
+        runs into the alternate outputs and is read back under the same
+        sync; its per-SPT table lands in self._spec."""
         sc = self.scene
         sel = sc.lod.select(cam, self.cfg.lod, cull=True)
         S1 = max(sc.lod.S, 1)
-        h = self._h_sel
         rb = _lib.readback      # kernel-written: never queues behind the write-back DMA
-        rb(h[:4], sel.counts[:4])
-        rb(h[4:4 + S1], sel.spt_ids[:S1])
-        rb(h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1])
-        rb(self._h_droot, sel.d_root[:S1])
+
+        def read(sel, h, hd):
+            rb(h[:4], sel.counts[:4])
+            rb(h[4:4 + S1], sel.spt_ids[:S1])
+            rb(h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1])
+            rb(hd, sel.d_root[:S1])
+
+        read(sel, self._h_sel, self._h_droot)
+        if spec_cam is not None:
+            read(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True), self._h_sel2, self._h_droot2)
         torch.cuda.current_stream().synchronize()
+        h = self._h_sel
         n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
+        self._spec = None
+        if spec_cam is not None:
+            h2 = self._h_sel2
+            k = int(h2[2])
+            self._spec = (sc.lod.spt_perm[h2[4:4 + k].numpy().astype(np.int64)],
+                          self._h_droot2[:k].numpy().copy(), h2[4 + S1:4 + S1 + k].numpy().copy())
         return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
 
-    def _gather_view(self, cam: Camera):
+    def _predict_next(self, iteration: int):
+        """The scheduler's draw for iteration+1, from a copy of the RNG
+        (the real sequence is untouched)."""
+        g = np.random.Generator(type(self.rng.bit_generator)())
+        g.bit_generator.state = self.rng.bit_generator.state
+        return next_view(self.graph, self.current_view, iteration + 1, g)
+
+    def _gather_view(self, cam: Camera, view: int | None = None):
         """Cut + cache decisions + prefix loads + compaction + row gather
         (trainer.py:319-347, cli._gather cli.py:111-136)."""
         sc = self.scene
         self._mark("start")
-        sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam)
+        nv = self._next_view
+        spec_cam = self.views[nv][0] if nv is not None and nv != view and nv not in self._hist else None
+        sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam, spec_cam)
         self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
         S1 = max(sc.lod.S, 1)
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
+        if view is not None:
+            self._hist[view] = (spt_ids.copy(), d_root.copy(), prefix.copy())
+        # the next view's predicted selection; its misses are prefetched
+        # once this step's kernels are queued (train_step)
+        self._pred = self._hist.get(nv, self._spec) if nv is not None else None
         if n_sp:
             # the prefix at the cached distance is the entry's prefix_len
             self._h_pref.numpy()[:n_sp] = hb[S1:S1 + n_sp]
@@ -254,7 +293,8 @@ class Trainer:
         """Serve/bench path (cli.cmd_render, cli.py:139-189): cut + cache +
         gather + forward render of one view; no parameter updates."""
         cam, _ = self.views[view]
-        R, rows, _, _, _, counters = self._gather_view(cam)
+        self._next_view = None
+        R, rows, _, _, _, counters = self._gather_view(cam, view)
         img = self.rast.forward(rows, R, cam, image=image)
         self.cache.end_step(-1, mark_dirty=False)
         self._mark("forward")
@@ -265,12 +305,13 @@ class Trainer:
     def train_step(self, iteration: int) -> dict:
         cfg, sc = self.cfg, self.scene
         self.current_view = next_view(self.graph, self.current_view, iteration, self.rng)
+        self._next_view = self._predict_next(iteration) if cfg.prefetch else None
         cam, _ = self.views[self.current_view]
         target = self.targets[self.current_view]
         if not self.device_targets:
             self._target_dev = target.to(sc.device, non_blocking=True)
             target = self._target_dev
-        R, rows, row_node, plan, _, counters = self._gather_view(cam)
+        R, rows, row_node, plan, _, counters = self._gather_view(cam, self.current_view)
         L = _lib.lib()
         st = _lib.stream_ptr()
         image = self.rast.forward(rows, R, cam)
@@ -303,6 +344,10 @@ class Trainer:
                                         None, R, R, self.lrs, _lib.ptr(bias), blen, C.byref(plan), st))
         self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
+        if self._pred is not None:
+            # the copy engines fetch the next view's misses while this
+            # step's backward and ADAM run
+            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
         self._mark("scatter_flush")
         self._collect()
         self.iteration = iteration

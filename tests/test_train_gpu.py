@@ -131,3 +131,29 @@ def test_warm_cache_zero_loads():
             assert r["view"] == first["view"]
             assert r["gaussians_loaded_from_store"] == 0
             assert r["bytes_streamed"] == 0
+
+
+def test_prefetch_is_invisible():
+    """The copy-engine prefetch of the predicted next view changes where a
+    missed prefix is read from (an HBM copy made during the previous step),
+    never what: 20 steps with misses, evictions, same-step re-misses and
+    flushes leave params, moments, step counts, the pinned store and every
+    cache block bit-identical to a run without prefetch."""
+    a, _, _ = make_case()
+    b, _, _ = make_case()
+    b.cfg.prefetch = False
+    for it in range(1, 21):
+        ra, rb = a.train_step(it), b.train_step(it)
+        assert ra == rb, it
+    torch.cuda.synchronize()
+    st = a.cache.stats()
+    assert st["prefetch_used_rows"] > 0 and b.cache.stats()["prefetched_rows"] == 0
+    assert torch.equal(a.scene.params, b.scene.params)
+    assert torch.equal(a.scene.m, b.scene.m) and torch.equal(a.scene.v, b.scene.v)
+    assert torch.equal(a.scene.step, b.scene.step)
+    for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
+        assert torch.equal(sa, sb)
+    ea, eb = a.cache.entries(), b.cache.entries()
+    assert [e[:3] + e[4:] for e in ea] == [e[:3] + e[4:] for e in eb]
+    for x, y in zip(ea, eb):
+        assert np.array_equal(a.cache.read_block(x[3], x[2]), b.cache.read_block(y[3], y[2]))

@@ -23,9 +23,9 @@ rng = np.random.default_rng(0)
 for n_items, rows_each in [(120, 8000), (600, 1600), (30, 32000)]:
     starts = np.sort(rng.choice(N // rows_each - 1, n_items, replace=False)) * rows_each
     blocks = [torch.empty(23 * rows_each, dtype=torch.float64, device="cuda") for _ in range(n_items)]
-    tab = np.zeros((n_items, 6), np.int64)     # glod_prefix_item incl. overlay, overlay_rows
+    tab = np.zeros((n_items, 7), np.int64)     # glod_prefix_item incl. overlay, overlay_rows, src
     for i in range(n_items):
-        tab[i] = (starts[i], rows_each, 23 * rows_each * i, blocks[i].data_ptr(), 0, 0)
+        tab[i] = (starts[i], rows_each, 23 * rows_each * i, blocks[i].data_ptr(), 0, 0, 0)
     dtab = torch.from_numpy(tab).cuda()
     total = 23 * rows_each * n_items
     mb = total * 4 / 1e6
