@@ -259,7 +259,7 @@ def run_ours(args):
     setup_s = time.time() - t0
     del h
     clocks = ClockSampler(local)
-    if rank == 0:
+    if rank == 0 and os.environ.get("GLOD_BENCH_NO_CLOCKS") != "1":
         clocks.start()
     it = 0
     for _ in range(args.warmup):
@@ -278,9 +278,12 @@ def run_ours(args):
         torch.cuda.cudart().cudaProfilerStart()
     e0.record()
     recs = []
+    host_t = []
     for _ in range(args.steps):
         it += 1
+        t_h = time.perf_counter()
         recs.append(tr.train_step(it))
+        host_t.append(time.perf_counter() - t_h)
     e1.record()
     torch.cuda.synchronize()
     clocks.mark_stop()
@@ -289,6 +292,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    if os.environ.get("GLOD_BENCH_STEP_TIMES") == "1":
+        print("host ms per timed step:", " ".join(f"{1e3 * x:.1f}" for x in host_t), file=sys.stderr)
     launches = _lib.load().glod_launch_count() - n_launch0
     clk = clocks.stop() if rank == 0 else {}
     if world > 1:

@@ -167,18 +167,22 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
  * Optimiser (trainer._adam_update, trainer.py:253-299)
  * ======================================================================= */
 
-/* One ADAM step, in place, on params[ids] from grads[rows].  params, m, v:
- * [dev] packed f64 blocks of `capacity` rows; step: [dev] int64[capacity];
- * grads: [dev] packed f64 block of `grad_rows` rows; ids/rows: [dev] int32[n]
- * (rows == NULL means row i).  ids must be unique.  lrs: host double[6] in
- * section order (means already scaled by the scene extent).  bias_table:
- * [dev] f64 [2*bias_len] = {1-0.9^t, 1-0.999^t for t < bias_len} (or NULL /
- * bias_len 0: computed with pow in the kernel).  refresh
- * (optional, see glod_gather_plan below): when given, row r is a render row
- * of that plan and SPT rows also write their updated values into their
- * cache block (entry.block.attrs.put, trainer.py:363). */
+/* One ADAM step, in place, on params[ids] from grads[rows]
+ * (trainer._adam_update, trainer.py:253-299).  params: [dev] packed f64
+ * block of `capacity` rows (section-major, as h.attrs).  mv: [dev] the ADAM
+ * moments (OptimizerState m/v, trainer.py:93-124) row-major and
+ * interleaved: f64 [capacity][23][2] = {m, v} per attribute value, so one
+ * node's moments are 368 contiguous bytes.  step: [dev] int64[capacity];
+ * grads: [dev] packed f64 block of `grad_rows` rows; ids/rows: [dev]
+ * int32[n] (rows == NULL means row i).  ids must be unique.  lrs: host
+ * double[6] in section order (means already scaled by the scene extent).
+ * bias_table: [dev] f64 [2*bias_len] = {1-0.9^t, 1-0.999^t for t <
+ * bias_len} (or NULL / bias_len 0: computed with pow in the kernel).
+ * refresh (optional, see glod_gather_plan below): when given, row r is a
+ * render row of that plan and SPT rows also write their updated values
+ * into their cache block (entry.block.attrs.put, trainer.py:363). */
 struct glod_gather_plan;
-int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
+int glod_adam_step(double* params, double* mv, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows,
                    int64_t grad_rows, int64_t n, const double* lrs, const double* bias_table,
                    int64_t bias_len, const struct glod_gather_plan* refresh, void* stream);
@@ -263,6 +267,7 @@ typedef struct glod_cache glod_cache;
 typedef struct glod_cache_stats_t {
   int64_t entries, resident_bytes, hits, misses, loaded_rows;
   int64_t prefetched_rows, prefetch_used_rows;
+  int64_t pool_allocs, grow_events;   /* block-arena misses, staging re-allocations */
 } glod_cache_stats_t;
 
 /* slot_start: host int64[num_spts], first store slot of each SPT

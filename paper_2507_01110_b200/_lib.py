@@ -76,7 +76,7 @@ class PrefixItem(C.Structure):
 class CacheStats(C.Structure):
     _fields_ = [("entries", C.c_int64), ("resident_bytes", C.c_int64), ("hits", C.c_int64),
                 ("misses", C.c_int64), ("loaded_rows", C.c_int64), ("prefetched_rows", C.c_int64),
-                ("prefetch_used_rows", C.c_int64)]
+                ("prefetch_used_rows", C.c_int64), ("pool_allocs", C.c_int64), ("grow_events", C.c_int64)]
 
 
 # name -> (restype, argtypes)
@@ -97,7 +97,7 @@ SIGNATURES = {
     "glod_render_stats_get": (C.c_int, [P, C.POINTER(RenderStats)]),
     "glod_loss_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
-    "glod_adam_step": (C.c_int, [P, P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
+    "glod_adam_step": (C.c_int, [P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
                                  C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),

@@ -12,6 +12,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <list>
 #include <map>
 #include <set>
@@ -193,6 +194,7 @@ struct CacheTable {
   cudaStream_t pf_st = nullptr;
   cudaEvent_t ev_pf = nullptr, ev_pf_free = nullptr;
   int64_t pf_issued_rows = 0, pf_used_rows = 0;
+  int64_t pool_allocs = 0, grow_events = 0;     // arena misses, staging re-allocations
 
   cudaError_t init(const glod_store_view& sv) {
     if (ready) return cudaSuccess;
@@ -235,6 +237,14 @@ struct CacheTable {
     const size_t want_pf = size_t(budget) + (size_t(16) << 20);
     if (want_blocks + want_pf < fr / 2) {
       if (blocks.init(want_blocks) != cudaSuccess || pfmem.init(want_pf) != cudaSuccess) cudaGetLastError();
+      // write-back staging: a batch is at most the resident set (budget
+      // bytes of f32) plus the step's replacements; reserve it up front
+      // (a re-allocation synchronises the device)
+      for (int k = 0; k < 2; ++k) {
+        const size_t want = size_t(budget) + size_t(budget) / 2;
+        if (cudaMalloc(&stage[k], want) == cudaSuccess) stage_cap[k] = want;
+        else { stage[k] = nullptr; cudaGetLastError(); }
+      }
     }
     ready = true;
     return cudaSuccess;
@@ -243,6 +253,7 @@ struct CacheTable {
   cudaError_t dalloc(void** p, size_t bytes, cudaStream_t st) {
     *p = blocks.alloc(bytes);
     if (*p) return cudaSuccess;
+    ++pool_allocs;
     return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, st);
   }
   cudaError_t dfree(void* p, cudaStream_t st) {
@@ -395,9 +406,11 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
       if (c->stage[sb]) cudaFree(c->stage[sb]);
       c->stage[sb] = nullptr;
       c->stage_cap[sb] = 0;
-      if (e == cudaSuccess) e = cudaMalloc(&c->stage[sb], need + need / 2);
+      const size_t want = std::max(need + need / 2, 2 * c->stage_cap[sb]);
+      if (e == cudaSuccess) e = cudaMalloc(&c->stage[sb], want);
       if (e != cudaSuccess) return e;
-      c->stage_cap[sb] = need + need / 2;
+      c->stage_cap[sb] = want;
+      ++c->grow_events;
     }
     float* staging = c->stage[sb];
     e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
@@ -744,6 +757,8 @@ int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out) {
   out->loaded_rows = c->t.loaded_rows;
   out->prefetched_rows = c->t.pf_issued_rows;
   out->prefetch_used_rows = c->t.pf_used_rows;
+  out->pool_allocs = c->t.pool_allocs;
+  out->grow_events = c->t.grow_events;
   return GLOD_OK;
 }
 

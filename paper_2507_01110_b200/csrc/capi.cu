@@ -15,7 +15,7 @@ void retain_pool_memory();
 size_t loss_scratch_bytes(int W, int H);
 cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam, double* out,
                         float* grad, void* scratch, size_t bytes, cudaStream_t st);
-cudaError_t launch_adam(double* params, double* m, double* v, long long* step, long long cap,
+cudaError_t launch_adam(double* params, double* mv, long long* step, long long cap,
                         const int* ids, const double* grads, const int* rows, long long grad_rows,
                         long long n, const double* lrs, const double* bias, long long bias_len,
                         const glod_gather_plan* plan, cudaStream_t st);
@@ -166,13 +166,13 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
                "glod_loss_l1_ssim");
 }
 
-int glod_adam_step(double* params, double* m, double* v, int64_t* step, int64_t capacity,
+int glod_adam_step(double* params, double* mv, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows, int64_t grad_rows,
                    int64_t n, const double* lrs, const double* bias_table, int64_t bias_len,
                    const glod_gather_plan* refresh, void* stream) {
-  if (n > 0 && (!params || !m || !v || !step || !ids || !grads || !lrs))
+  if (n > 0 && (!params || !mv || !step || !ids || !grads || !lrs))
     return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
-  return check(glod::launch_adam(params, m, v, reinterpret_cast<long long*>(step), capacity, ids,
+  return check(glod::launch_adam(params, mv, reinterpret_cast<long long*>(step), capacity, ids,
                                  grads, rows, grad_rows, n, lrs, bias_table, bias_len, refresh,
                                  static_cast<cudaStream_t>(stream)),
                "glod_adam_step");

@@ -39,22 +39,55 @@ GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
   return s;
 }
 
-// One warp per row: lanes 0..22 each move one of the 23 attribute values.
-__global__ void gather_rows_kernel(glod_gather_plan p, long long R, double* __restrict__ out,
-                                   int* __restrict__ row_node) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= R) return;
-  int node;
-  const Src s = row_source(p, gw, node);
-  if (lane < 23) {
-    int sec = 0;
+// One thread per (row, column) of one section (blockIdx.y = section):
+// section-major, so the writes are fully coalesced and a warp reads runs of
+// consecutive source rows; compile-time column counts.  Latency-bound
+// (plan lookups → source row), so each thread handles kGatherIlp values
+// (strided by the block size) and issues all its loads before its stores.
+constexpr int kGatherTB = 256, kGatherIlp = 4;
+
+template <int SEC>
+GLOD_DEV void gather_sec(const glod_gather_plan& p, unsigned R, double* __restrict__ out,
+                         int* __restrict__ row_node) {
+  constexpr int OFFS[7] = {0, 3, 6, 10, 11, 14, 23};
+  constexpr int COLS = OFFS[SEC + 1] - OFFS[SEC];
+  constexpr long long OFF = OFFS[SEC];
+  const unsigned base = blockIdx.x * (kGatherTB * kGatherIlp) + threadIdx.x;
+  if (base >= R * COLS) return;
+  double v[kGatherIlp];
+  int node[kGatherIlp];
 #pragma unroll
-    for (int k = 1; k < 6; ++k) sec += lane >= kSecOff[k];
-    const int col = lane - kSecOff[sec], cols = kSecCols[sec];
-    out[kSecOff[sec] * R + gw * cols + col] = s.base[kSecOff[sec] * s.rows + s.idx * cols + col];
+  for (int k = 0; k < kGatherIlp; ++k) {
+    const unsigned local = base + k * kGatherTB;
+    if (local < R * COLS) {
+      const unsigned r = local / COLS;
+      const int col = int(local - r * COLS);
+      const Src s = row_source(p, r, node[k]);
+      v[k] = s.base[OFF * s.rows + s.idx * COLS + col];
+    }
   }
-  if (lane == 0 && row_node) row_node[gw] = node;
+#pragma unroll
+  for (int k = 0; k < kGatherIlp; ++k) {
+    const unsigned local = base + k * kGatherTB;
+    if (local < R * COLS) {
+      out[OFF * R + local] = v[k];
+      const unsigned r = local / COLS;
+      if (SEC == 0 && local == r * COLS && row_node) row_node[r] = node[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kGatherTB)
+gather_rows_kernel(glod_gather_plan p, long long R, double* __restrict__ out, int* __restrict__ row_node) {
+  const unsigned n = unsigned(R);
+  switch (blockIdx.y) {
+    case 0: gather_sec<0>(p, n, out, row_node); break;
+    case 1: gather_sec<1>(p, n, out, row_node); break;
+    case 2: gather_sec<2>(p, n, out, row_node); break;
+    case 3: gather_sec<3>(p, n, out, row_node); break;
+    case 4: gather_sec<4>(p, n, out, row_node); break;
+    case 5: gather_sec<5>(p, n, out, row_node); break;
+  }
 }
 
 __global__ void scatter_back_kernel(glod_gather_plan p, long long n_sel) {
@@ -203,7 +236,9 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
   if (R <= 0) return cudaSuccess;
   const int TB = 256;
   count_launch();
-  gather_rows_kernel<<<int((R * 32 + TB - 1) / TB), TB, 0, st>>>(p, R, out, row_node);
+  const long long per_block = (long long)kGatherTB * kGatherIlp;
+  const dim3 grid(unsigned((9 * R + per_block - 1) / per_block), 6);
+  gather_rows_kernel<<<grid, kGatherTB, 0, st>>>(p, R, out, row_node);
   return cudaGetLastError();
 }
 

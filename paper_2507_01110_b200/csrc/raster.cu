@@ -10,6 +10,7 @@
 //   K8 blend_bwd_kernel    reverse loop, 2D partials (renderer.py:219-261)
 //   K9 preprocess_bwd_kernel 2D→3D chain rule        (renderer.py:262-303)
 #include <stdio.h>
+#include <algorithm>
 #include <string>
 
 #include "common.cuh"
@@ -146,9 +147,9 @@ GLOD_DEV float edge_min(float a, float b, float c, float fixed, float lo, float 
                    __fmul_rn(c, __fmul_rn(t, t)));
 }
 
-GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
-  const int xa = max(tx * kTileW, int(g.x0)), xb = min(tx * kTileW + kTileW - 1, int(g.x1) - 1);
-  const int ya = max(ty * kTileH, int(g.y0)), yb = min(ty * kTileH + kTileH - 1, int(g.y1) - 1);
+// Does any integer pixel of [xa, xb] × [ya, yb] (inclusive, already
+// clipped to the bbox) lie in the q ≤ 32 ellipse?  Conservative (see above).
+GLOD_DEV bool rect_hit(const Splat& g, int xa, int xb, int ya, int yb) {
   const float dxa = __fsub_rn(float(xa - g.x0), g.mx), dxb = __fsub_rn(float(xb - g.x0), g.mx);
   const float dya = __fsub_rn(float(ya - g.y0), g.my), dyb = __fsub_rn(float(yb - g.y0), g.my);
   if (dxa <= 0.f && dxb >= 0.f && dya <= 0.f && dyb >= 0.f) return true;
@@ -157,6 +158,30 @@ GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
   m = fminf(m, edge_min(g.cc, g.cb, g.ca, dya, dxa, dxb));
   m = fminf(m, edge_min(g.cc, g.cb, g.ca, dyb, dxa, dxb));
   return m <= 32.01f;
+}
+
+GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
+  const int xa = max(tx * kTileW, int(g.x0)), xb = min(tx * kTileW + kTileW - 1, int(g.x1) - 1);
+  const int ya = max(ty * kTileH, int(g.y0)), yb = min(ty * kTileH + kTileH - 1, int(g.y1) - 1);
+  return rect_hit(g, xa, xb, ya, yb);
+}
+
+// The blend kernels give each warp an 8x4 pixel block of the 16x16 tile
+// (warp w: x ∈ ox + 8(w&1) + [0,8), y ∈ oy + 4(w>>1) + [0,4)).  Bit w of
+// the mask: the splat can reach a pixel of warp w's block (bbox overlap
+// and the conservative ellipse test), so warps iterate only over their
+// own splats — a warp skipping a splat changes none of its pixels.
+GLOD_DEV unsigned warp_block_mask(const Splat& g, int ox, int oy) {
+  unsigned m = 0;
+#pragma unroll
+  for (int w = 0; w < kBlendThreads / 32; ++w) {
+    const int xa = ox + (w & 1) * 8, ya = oy + (w >> 1) * 4;
+    if (g.x1 <= xa || g.x0 >= xa + 8 || g.y1 <= ya || g.y0 >= ya + 4) continue;
+    if (rect_hit(g, max(xa, int(g.x0)), min(xa + 7, int(g.x1) - 1), max(ya, int(g.y0)),
+                 min(ya + 3, int(g.y1) - 1)))
+      m |= 1u << w;
+  }
+  return m;
 }
 
 // One Gaussian; returns its tile count (0 = contributes nothing) and sets
@@ -324,13 +349,14 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, float* __restrict__ image,
                  double* __restrict__ t_final, int* __restrict__ last_out) {
   __shared__ Splat sm[kBlendThreads];
+  __shared__ unsigned smask[kBlendThreads];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  // each warp owns an 8x4 pixel block of the 16x16 tile (square-ish, so the
-  // warp-uniform bbox test rejects more splats than a 16x2 strip)
+  const int ox = tx * kTileW, oy = ty * kTileH;
+  // each warp owns an 8x4 pixel block of the 16x16 tile
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
-  const int wx0 = tx * kTileW + (wid & 1) * 8, wy0 = ty * kTileH + (wid >> 1) * 4;
-  const int px = wx0 + (ln & 7), py = wy0 + (ln >> 3);
+  const int px = ox + (wid & 1) * 8 + (ln & 7), py = oy + (wid >> 1) * 4 + (ln >> 3);
+  const unsigned mybit = 1u << wid;
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   double T = 1.0;
@@ -340,21 +366,31 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   for (int base = rg.x; base < rg.y; base += kBlendThreads) {
     if (__syncthreads_count(!done) == 0) break;
     const int k = base + int(threadIdx.x);
-    if (k < rg.y) sm[threadIdx.x] = sorted[ival[k]];
+    if (k < rg.y) {
+      const Splat g = sorted[ival[k]];
+      sm[threadIdx.x] = g;
+      smask[threadIdx.x] = warp_block_mask(g, ox, oy);
+    }
     __syncthreads();
     const int cnt = min(kBlendThreads, rg.y - base);
-    for (int j = 0; j < cnt && !done; ++j) {
-      const Splat& g = sm[j];
-      if (g.x1 <= wx0 || g.x0 >= wx0 + 8 || g.y1 <= wy0 || g.y0 >= wy0 + 4) continue;
-      float dx, dy, q, gs, al;
-      if (!pixel_alpha(g, px, py, dx, dy, q, gs, al)) continue;
-      const double w = double(al) * T;
-      cr += float(w) * sm[j].r;
-      cg += float(w) * sm[j].g;
-      cb += float(w) * sm[j].b;
-      T = T * (1.0 - double(al));
-      last = base + j;
-      if (T <= kTEps) done = true;           // later alphas are gated to 0
+    for (int c = 0; c < cnt; c += 32) {
+      if (__all_sync(0xffffffffu, done)) break;
+      unsigned bits = __ballot_sync(0xffffffffu, c + ln < cnt && (smask[c + ln] & mybit));
+      while (bits) {
+        const int j = c + __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (done) continue;
+        const Splat& g = sm[j];
+        float dx, dy, q, gs, al;
+        if (!pixel_alpha(g, px, py, dx, dy, q, gs, al)) continue;
+        const double w = double(al) * T;
+        cr += float(w) * g.r;
+        cg += float(w) * g.g;
+        cb += float(w) * g.b;
+        T = T * (1.0 - double(al));
+        last = base + j;
+        if (T <= kTEps) done = true;           // later alphas are gated to 0
+      }
     }
   }
   if (inside) {
@@ -410,17 +446,18 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
                  double* __restrict__ g2) {
   __shared__ float4 sm[kBlendThreads][3];
+  __shared__ unsigned smask[kBlendThreads];
   __shared__ int max_last;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  // each warp owns an 8x4 pixel block of the 16x16 tile (square-ish, so the
-  // warp-uniform bbox test rejects more splats than a 16x2 strip)
+  const int ox = tx * kTileW, oy = ty * kTileH;
+  // each warp owns an 8x4 pixel block of the 16x16 tile
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
-  const int wx0 = tx * kTileW + (wid & 1) * 8, wy0 = ty * kTileH + (wid >> 1) * 4;
-  const int px = wx0 + (ln & 7), py = wy0 + (ln >> 3);
+  const int px = ox + (wid & 1) * 8 + (ln & 7), py = oy + (wid >> 1) * 4 + (ln >> 3);
+  const unsigned mybit = 1u << wid;
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
-  const int lane = threadIdx.x & 31;
+  const int lane = ln;
   float T = 1.f;
   int last = -1;
   float gr = 0.f, gg = 0.f, gb = 0.f;
@@ -442,71 +479,80 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   const float4* src = reinterpret_cast<const float4*>(sorted);
   for (int top = end; top > rg.x; top -= kBlendThreads) {
     const int lo = max(rg.x, top - kBlendThreads);
-    const int k = top - 1 - int(threadIdx.x);
+    const int k = top - 1 - int(threadIdx.x);      // slot t holds instance top-1-t
     __syncthreads();
     if (k >= lo) {
       const long long s = ival[k];
-      sm[threadIdx.x][0] = src[3 * s];
-      sm[threadIdx.x][1] = src[3 * s + 1];
-      sm[threadIdx.x][2] = src[3 * s + 2];
+      Splat g;
+      float4* gv = reinterpret_cast<float4*>(&g);
+      gv[0] = src[3 * s];
+      gv[1] = src[3 * s + 1];
+      gv[2] = src[3 * s + 2];
+      sm[threadIdx.x][0] = gv[0];
+      sm[threadIdx.x][1] = gv[1];
+      sm[threadIdx.x][2] = gv[2];
+      smask[threadIdx.x] = warp_block_mask(g, ox, oy);
     }
     __syncthreads();
     const int cnt = top - lo;
-    for (int j = 0; j < cnt; ++j) {
-      const int inst = top - 1 - j;
-      const float4 a0 = sm[j][0], a1 = sm[j][1], a2 = sm[j][2];
-      Splat g;
-      *reinterpret_cast<float4*>(&g) = a0;
-      *(reinterpret_cast<float4*>(&g) + 1) = a1;
-      *(reinterpret_cast<float4*>(&g) + 2) = a2;
-      if (inst > wlast || g.x1 <= wx0 || g.x0 >= wx0 + 8 || g.y1 <= wy0 || g.y0 >= wy0 + 4)
-        continue;                                          // warp-uniform skip
-      float c[8];
-      float c8 = 0.f;
+    for (int c = 0; c < cnt; c += 32) {
+      const int jl = c + ln;
+      unsigned bits = __ballot_sync(0xffffffffu, jl < cnt && top - 1 - jl <= wlast && (smask[jl] & mybit));
+      while (bits) {
+        const int j = c + __ffs(bits) - 1;           // ascending slot = back to front
+        bits &= bits - 1;
+        const int inst = top - 1 - j;
+        Splat g;
+        *reinterpret_cast<float4*>(&g) = sm[j][0];
+        *(reinterpret_cast<float4*>(&g) + 1) = sm[j][1];
+        *(reinterpret_cast<float4*>(&g) + 2) = sm[j][2];
+        float c8 = 0.f;
+        float cv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) c[u] = 0.f;
-      float dx, dy, q, gs, al;
-      const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
-      if (hit) {
-        const float inv = 1.f / (1.f - al);
-        const float Tf = T * inv;                          // T before this splat
-        const float w = al * Tf;
-        c[0] = w * gr; c[1] = w * gg; c[2] = w * gb;       // dl_dcolor
-        const float gc = gr * g.r + gg * g.g + gb * g.b;
-        const float grear = gr * rr + gg * rg_ + gb * rb;
-        const float dla = gc * Tf - grear * inv;
-        rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
-        T = Tf;
-        if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
-          c[3] = gs * dla;
-          const float dq = -0.5f * g.opac * gs * dla;
-          c[4] = -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
-          c[5] = -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
-          c[6] = dq * dx * dx;
-          c[7] = dq * dx * dy;
-          c8 = dq * dy * dy;
-        }
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (bal == 0) continue;
-      double* dst = g2 + (long long)kG2 * g.idx;
-      if (__popc(bal) <= 2) {
-        // one or two hitting lanes: their partials go straight to the
-        // fp64 accumulators (cheaper than a 32-lane reduction)
+        for (int u = 0; u < 8; ++u) cv[u] = 0.f;
+        float dx, dy, q, gs, al;
+        const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
         if (hit) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (c[u] != 0.f) atomicAdd(dst + u, double(c[u]));
-          if (c8 != 0.f) atomicAdd(dst + 8, double(c8));
+          const float inv = __frcp_rn(1.f - al);
+          const float Tf = T * inv;                          // T before this splat
+          const float w = al * Tf;
+          cv[0] = w * gr; cv[1] = w * gg; cv[2] = w * gb;    // dl_dcolor
+          const float gc = gr * g.r + gg * g.g + gb * g.b;
+          const float grear = gr * rr + gg * rg_ + gb * rb;
+          const float dla = gc * Tf - grear * inv;
+          rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
+          T = Tf;
+          if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
+            cv[3] = gs * dla;
+            const float dq = -0.5f * g.opac * gs * dla;
+            cv[4] = -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
+            cv[5] = -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
+            cv[6] = dq * dx * dx;
+            cv[7] = dq * dx * dy;
+            c8 = dq * dy * dy;
+          }
         }
-        continue;
-      }
-      const float t8 = warp_reduce8(c, lane);
-      const float s8 = warp_sum(c8);
-      if ((lane & 3) == 0) {
-        if (t8 != 0.f) atomicAdd(dst + (lane >> 2), double(t8));
-      } else if (lane == 1) {
-        if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        if (bal == 0) continue;
+        double* dst = g2 + (long long)kG2 * g.idx;
+        if (__popc(bal) <= 2) {
+          // one or two hitting lanes: their partials go straight to the
+          // fp64 accumulators (cheaper than a 32-lane reduction)
+          if (hit) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              if (cv[u] != 0.f) atomicAdd(dst + u, double(cv[u]));
+            if (c8 != 0.f) atomicAdd(dst + 8, double(c8));
+          }
+          continue;
+        }
+        const float t8 = warp_reduce8(cv, lane);
+        const float s8 = warp_sum(c8);
+        if ((lane & 3) == 0) {
+          if (t8 != 0.f) atomicAdd(dst + (lane >> 2), double(t8));
+        } else if (lane == 1) {
+          if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
+        }
       }
     }
   }
@@ -666,7 +712,9 @@ struct Buf {
   cudaError_t ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap && p) return cudaSuccess;
     if (p) cudaFreeAsync(p, st);
-    size_t want = bytes + bytes / 4 + 4096;
+    // geometric growth: a view with a larger render set than any before
+    // costs one re-allocation, not one per few-% increase
+    size_t want = std::max(bytes + bytes / 4, 2 * cap) + 4096;
     cudaError_t e = cudaMallocAsync(&p, want, st);
     cap = e == cudaSuccess ? want : 0;
     return e;

@@ -86,13 +86,26 @@ class DeviceScene:
         self.device = dev
         self.cap = h.capacity
         self.params = torch.from_numpy(h.attrs.packed(np.float64)).to(dev)
-        self.m = torch.zeros_like(self.params)
-        self.v = torch.zeros_like(self.params)
+        # ADAM moments, row-major interleaved [cap][23][m, v] (glod_adam_step)
+        self.mv = torch.zeros(self.cap * FLOATS_PER_GAUSSIAN * 2, dtype=torch.float64, device=dev)
         self.step = torch.zeros(self.cap, dtype=torch.int64, device=dev)
         self.lod = DeviceLodScene(h, hspt, means=_packed(self.params, self.cap, "means"),
                                   scales=_packed(self.params, self.cap, "scales"))
         self.store = HostStore(h, hspt)
         self.hspt = hspt
+
+    def moments_packed(self):
+        """(m, v) as packed section-major f64 blocks (the h.attrs layout)."""
+        mv = self.mv.view(self.cap, FLOATS_PER_GAUSSIAN, 2)
+        out = []
+        for k in range(2):
+            x = mv[:, :, k]
+            parts, off = [], 0
+            for _, cols in SECTIONS:
+                parts.append(x[:, off:off + cols].reshape(-1))
+                off += cols
+            out.append(torch.cat(parts))
+        return out[0], out[1]
 
     def attrs_host(self) -> AttributeArrays:
         return AttributeArrays.from_packed(self.params.cpu().numpy(), self.cap)
@@ -198,7 +211,8 @@ class Trainer:
     def _ensure(self, name, numel, dtype):
         t = getattr(self, name)
         if t is None or t.numel() < numel:
-            t = torch.empty(max(numel, 1) + numel // 4, dtype=dtype, device=self.scene.device)
+            grow = 2 * t.numel() if t is not None else 0
+            t = torch.empty(max(numel + numel // 4, grow, 1), dtype=dtype, device=self.scene.device)
             setattr(self, name, t)
         return t
 
@@ -333,13 +347,13 @@ class Trainer:
             U, GU = sparse_grad_allreduce(row_node[:R], grads, R, self.group)
             ids = U.to(torch.int32)
             nU = int(ids.numel())
-            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v),
+            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),
                                         _lib.ptr(sc.step), sc.cap, _lib.ptr(ids), _lib.ptr(GU), None,
                                         nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
             _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
             self._last_union = (ids, GU)
         else:
-            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.m), _lib.ptr(sc.v),
+            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),
                                         _lib.ptr(sc.step), sc.cap, _lib.ptr(row_node), _lib.ptr(grads),
                                         None, R, R, self.lrs, _lib.ptr(bias), blen, C.byref(plan), st))
         self._mark("adam")

@@ -115,18 +115,24 @@ def test_adam_golden():
     n = d["p0_means"].shape[0]
     a = attrs_of(d, "p0_")
     P = torch.from_numpy(a.packed()).cuda()
-    M = torch.zeros_like(P)
-    V = torch.zeros_like(P)
+    MV = torch.zeros(2 * P.numel(), dtype=torch.float64, device="cuda")   # [n][23][m, v]
     step = torch.zeros(n, dtype=torch.int64, device="cuda")
     lrs = (C.c_double * 6)(*[float(d["lr_" + k]) for k in NAMES])
     for it in range(3):
         ids = torch.from_numpy(d[f"it{it}_ids"].astype(np.int32)).cuda()
         g = AttributeArrays(*(d[f"it{it}_g_{k}"] for k in NAMES))
         G = torch.from_numpy(g.packed()).cuda()
-        _lib.check(_lib.lib().glod_adam_step(_lib.ptr(P), _lib.ptr(M), _lib.ptr(V), _lib.ptr(step), n,
+        _lib.check(_lib.lib().glod_adam_step(_lib.ptr(P), _lib.ptr(MV), _lib.ptr(step), n,
                                              _lib.ptr(ids), _lib.ptr(G), None, ids.numel(), ids.numel(),
                                              lrs, None, 0, None, _lib.stream_ptr()))
         got = AttributeArrays.from_packed(P.cpu().numpy(), n)
         for k in NAMES:
             np.testing.assert_allclose(getattr(got, k), d[f"it{it}_p_{k}"], rtol=1e-12, atol=1e-14)
         np.testing.assert_array_equal(step.cpu().numpy(), d[f"it{it}_step"])
+        mv = MV.view(n, 23, 2).cpu().numpy()
+        off = 0
+        for k, (_, cols) in zip(NAMES, SECTIONS):
+            for j, tag in enumerate("mv"):
+                want = d[f"it{it}_{tag}_{k}"].reshape(n, cols)
+                np.testing.assert_allclose(mv[:, off:off + cols, j], want, rtol=1e-12, atol=1e-300)
+            off += cols

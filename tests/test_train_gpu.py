@@ -39,9 +39,10 @@ def snapshot(tr: Trainer):
     torch.cuda.synchronize()
     sc = tr.scene
     cap = sc.cap
+    m, v = sc.moments_packed()
     snap = {"P": _dict(AttributeArrays.from_packed(sc.params.cpu().numpy(), cap)),
-            "M": _dict(AttributeArrays.from_packed(sc.m.cpu().numpy(), cap)),
-            "V": _dict(AttributeArrays.from_packed(sc.v.cpu().numpy(), cap)),
+            "M": _dict(AttributeArrays.from_packed(m.cpu().numpy(), cap)),
+            "V": _dict(AttributeArrays.from_packed(v.cpu().numpy(), cap)),
             "step": sc.step.cpu().numpy().copy(),
             "store": [s.numpy().copy() for s in sc.store.sections],
             "cache": OrderedDict(), "resident": tr.cache.resident_bytes}
@@ -149,7 +150,7 @@ def test_prefetch_is_invisible():
     st = a.cache.stats()
     assert st["prefetch_used_rows"] > 0 and b.cache.stats()["prefetched_rows"] == 0
     assert torch.equal(a.scene.params, b.scene.params)
-    assert torch.equal(a.scene.m, b.scene.m) and torch.equal(a.scene.v, b.scene.v)
+    assert torch.equal(a.scene.mv, b.scene.mv)
     assert torch.equal(a.scene.step, b.scene.step)
     for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
         assert torch.equal(sa, sb)
