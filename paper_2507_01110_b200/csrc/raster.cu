@@ -166,19 +166,35 @@ GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
   return rect_hit(g, xa, xb, ya, yb);
 }
 
-// The blend kernels give each warp an 8x4 pixel block of the 16x16 tile
-// (warp w: x ∈ ox + 8(w&1) + [0,8), y ∈ oy + 4(w>>1) + [0,4)).  Bit w of
-// the mask: the splat can reach a pixel of warp w's block (bbox overlap
-// and the conservative ellipse test), so warps iterate only over their
-// own splats — a warp skipping a splat changes none of its pixels.
+// Blend kernel layout: a 16x16 tile per block of kBlendWarps warps; warp w
+// owns the 8x8 pixel block at (8(w&1), 8(w>>1)) and lane l the two pixels
+// (l&7, l>>3) and (l&7, (l>>3)+4) of it.  Two pixels per lane halve the
+// per-pixel share of every per-splat cost (the splat read from shared
+// memory, the loop, and in the backward the warp reduction and the fp64
+// atomics).  Bit w of a splat's mask: it can reach a pixel of warp w's
+// block (bbox overlap and the conservative ellipse test), so each warp
+// iterates only over its own splats — skipping one changes none of its
+// pixels.
+constexpr int kBlendWarps = 4;
+constexpr int kBlendTB = 32 * kBlendWarps;
+constexpr int kBatch = 256;                 // splats staged per round
+// The forward keeps one pixel per lane (8 warps, 8x4 blocks): its per-pixel
+// state is a sequential fp64 chain, so it wants more warps in flight more
+// than it wants the shared per-splat cost halved.
+constexpr int kFwdWarps = 8;
+constexpr int kFwdTB = 32 * kFwdWarps;
+
+// Mask of the warps (NW warps, 8 x BH pixel blocks, two per block row) a
+// splat can reach.
+template <int NW, int BH>
 GLOD_DEV unsigned warp_block_mask(const Splat& g, int ox, int oy) {
   unsigned m = 0;
 #pragma unroll
-  for (int w = 0; w < kBlendThreads / 32; ++w) {
-    const int xa = ox + (w & 1) * 8, ya = oy + (w >> 1) * 4;
-    if (g.x1 <= xa || g.x0 >= xa + 8 || g.y1 <= ya || g.y0 >= ya + 4) continue;
+  for (int w = 0; w < NW; ++w) {
+    const int xa = ox + (w & 1) * 8, ya = oy + (w >> 1) * BH;
+    if (g.x1 <= xa || g.x0 >= xa + 8 || g.y1 <= ya || g.y0 >= ya + BH) continue;
     if (rect_hit(g, max(xa, int(g.x0)), min(xa + 7, int(g.x1) - 1), max(ya, int(g.y0)),
-                 min(ya + 3, int(g.y1) - 1)))
+                 min(ya + BH - 1, int(g.y1) - 1)))
       m |= 1u << w;
   }
   return m;
@@ -344,16 +360,30 @@ GLOD_DEV bool pixel_alpha(const Splat& g, int px, int py, float& dx, float& dy, 
   return alpha > 0.0f;
 }
 
-__global__ void __launch_bounds__(kBlendThreads)
+// Front-to-back compositing of one pixel with one splat (renderer.py:149-164).
+GLOD_DEV void fwd_pixel(const Splat& g, int px, int py, int inst, double& T, float& cr, float& cg, float& cb,
+                        int& last, bool& done) {
+  float dx, dy, q, gs, al;
+  if (done || !pixel_alpha(g, px, py, dx, dy, q, gs, al)) return;
+  const double w = double(al) * T;
+  cr += float(w) * g.r;
+  cg += float(w) * g.g;
+  cb += float(w) * g.b;
+  T = T * (1.0 - double(al));
+  last = inst;
+  if (T <= kTEps) done = true;           // later alphas are gated to 0
+}
+
+__global__ void __launch_bounds__(kFwdTB)
 blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, float* __restrict__ image,
                  double* __restrict__ t_final, int* __restrict__ last_out) {
-  __shared__ Splat sm[kBlendThreads];
-  __shared__ unsigned smask[kBlendThreads];
+  __shared__ Splat sm[kBatch];
+  __shared__ unsigned smask[kBatch];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
   const int ox = tx * kTileW, oy = ty * kTileH;
-  // each warp owns an 8x4 pixel block of the 16x16 tile
+  // warp w owns the 8x4 pixel block at (8(w&1), 4(w>>1))
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
   const int px = ox + (wid & 1) * 8 + (ln & 7), py = oy + (wid >> 1) * 4 + (ln >> 3);
   const unsigned mybit = 1u << wid;
@@ -363,33 +393,25 @@ blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
   float cr = 0.f, cg = 0.f, cb = 0.f;
   int last = -1;
   bool done = !inside;
-  for (int base = rg.x; base < rg.y; base += kBlendThreads) {
+  for (int base = rg.x; base < rg.y; base += kBatch) {
     if (__syncthreads_count(!done) == 0) break;
-    const int k = base + int(threadIdx.x);
-    if (k < rg.y) {
-      const Splat g = sorted[ival[k]];
-      sm[threadIdx.x] = g;
-      smask[threadIdx.x] = warp_block_mask(g, ox, oy);
+    for (int t = threadIdx.x; t < kBatch; t += kFwdTB) {
+      const int k = base + t;
+      if (k < rg.y) {
+        const Splat g = sorted[ival[k]];
+        sm[t] = g;
+        smask[t] = warp_block_mask<kFwdWarps, 4>(g, ox, oy);
+      }
     }
     __syncthreads();
-    const int cnt = min(kBlendThreads, rg.y - base);
+    const int cnt = min(kBatch, rg.y - base);
     for (int c = 0; c < cnt; c += 32) {
       if (__all_sync(0xffffffffu, done)) break;
       unsigned bits = __ballot_sync(0xffffffffu, c + ln < cnt && (smask[c + ln] & mybit));
       while (bits) {
         const int j = c + __ffs(bits) - 1;
         bits &= bits - 1;
-        if (done) continue;
-        const Splat& g = sm[j];
-        float dx, dy, q, gs, al;
-        if (!pixel_alpha(g, px, py, dx, dy, q, gs, al)) continue;
-        const double w = double(al) * T;
-        cr += float(w) * g.r;
-        cg += float(w) * g.g;
-        cb += float(w) * g.b;
-        T = T * (1.0 - double(al));
-        last = base + j;
-        if (T <= kTEps) done = true;           // later alphas are gated to 0
+        fwd_pixel(sm[j], px, py, base + j, T, cr, cg, cb, last, done);
       }
     }
   }
@@ -435,63 +457,99 @@ GLOD_DEV float warp_sum(float v) {
 
 // Back-to-front per pixel with the reference's rear accumulator
 // (renderer.py:219-261).  Per-pixel math is fp32 (T recovered as
-// T_front = T_after / (1 − α) from the fp64 final transmittance).  For each
-// (splat, warp) with at least one hit the nine per-Gaussian partials are
-// warp-reduced (transposed reduction) and nine lanes issue one fp64
-// reduction each.  Warps skip splats whose bbox misses their 16x2 strip or
-// that lie beyond the strip's last contributor.
-__global__ void __launch_bounds__(kBlendThreads, 4)
+// T_front = T_after / (1 − α) from the fp64 final transmittance); a lane's
+// two pixels add into one set of nine partials.
+struct BwdPix {
+  float T, gr, gg, gb, rr, rg, rb;
+  int last;
+  bool inside;
+};
+
+GLOD_DEV bool bwd_pixel(const Splat& g, int px, int py, int inst, BwdPix& s, float (&cv)[9]) {
+  float dx, dy, q, gs, al;
+  if (!(s.inside && inst <= s.last && pixel_alpha(g, px, py, dx, dy, q, gs, al))) return false;
+  const float inv = __frcp_rn(1.f - al);
+  const float Tf = s.T * inv;                          // T before this splat
+  const float w = al * Tf;
+  cv[0] += w * s.gr; cv[1] += w * s.gg; cv[2] += w * s.gb;   // dl_dcolor
+  const float gc = s.gr * g.r + s.gg * g.g + s.gb * g.b;
+  const float grear = s.gr * s.rr + s.gg * s.rg + s.gb * s.rb;
+  const float dla = gc * Tf - grear * inv;
+  s.rr += w * g.r; s.rg += w * g.g; s.rb += w * g.b;
+  s.T = Tf;
+  if (__fmul_rn(g.opac, gs) < kAlphaMax) {             // live: unclamped
+    cv[3] += gs * dla;
+    const float dq = -0.5f * g.opac * gs * dla;
+    cv[4] += -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
+    cv[5] += -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
+    cv[6] += dq * dx * dx;
+    cv[7] += dq * dx * dy;
+    cv[8] += dq * dy * dy;
+  }
+  return true;
+}
+
+GLOD_DEV BwdPix bwd_init(const CamD& cam, int px, int py, const float* __restrict__ dimg,
+                         const double* __restrict__ t_final, const int* __restrict__ last_in) {
+  BwdPix s{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, -1, px < cam.w && py < cam.h};
+  if (s.inside) {
+    const long long pix = (long long)py * cam.w + px;
+    s.T = float(t_final[pix]);
+    s.last = last_in[pix];
+    s.gr = dimg[3 * pix]; s.gg = dimg[3 * pix + 1]; s.gb = dimg[3 * pix + 2];
+  }
+  return s;
+}
+
+// For each (splat, warp) with at least one hit the nine per-Gaussian
+// partials are warp-reduced (transposed reduction) and nine lanes issue one
+// fp64 reduction each (or, with one or two hitting lanes, those lanes issue
+// theirs directly).  Warps skip splats outside their block (mask) or beyond
+// their last contributor.
+__global__ void __launch_bounds__(kBlendTB, 8)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
                  double* __restrict__ g2) {
-  __shared__ float4 sm[kBlendThreads][3];
-  __shared__ unsigned smask[kBlendThreads];
+  __shared__ float4 sm[kBatch][3];
+  __shared__ unsigned smask[kBatch];
   __shared__ int max_last;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
   const int ox = tx * kTileW, oy = ty * kTileH;
-  // each warp owns an 8x4 pixel block of the 16x16 tile
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
-  const int px = ox + (wid & 1) * 8 + (ln & 7), py = oy + (wid >> 1) * 4 + (ln >> 3);
+  const int px = ox + (wid & 1) * 8 + (ln & 7);
+  const int py0 = oy + (wid >> 1) * 8 + (ln >> 3), py1 = py0 + 4;
   const unsigned mybit = 1u << wid;
-  const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
-  const int lane = ln;
-  float T = 1.f;
-  int last = -1;
-  float gr = 0.f, gg = 0.f, gb = 0.f;
-  if (inside) {
-    const long long pix = (long long)py * cam.w + px;
-    T = float(t_final[pix]);
-    last = last_in[pix];
-    gr = dimg[3 * pix]; gg = dimg[3 * pix + 1]; gb = dimg[3 * pix + 2];
-  }
-  int wlast = last;
+  BwdPix s0 = bwd_init(cam, px, py0, dimg, t_final, last_in);
+  BwdPix s1 = bwd_init(cam, px, py1, dimg, t_final, last_in);
+  int wlast = max(s0.last, s1.last);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
   if (threadIdx.x == 0) max_last = -1;
   __syncthreads();
-  if (lane == 0) atomicMax(&max_last, wlast);
+  if (ln == 0) atomicMax(&max_last, wlast);
   __syncthreads();
   const int end = max_last + 1;   // nothing beyond the last contributor matters
-  float rr = 0.f, rg_ = 0.f, rb = 0.f;   // rear accumulator Σ_behind w·c
   const float4* src = reinterpret_cast<const float4*>(sorted);
-  for (int top = end; top > rg.x; top -= kBlendThreads) {
-    const int lo = max(rg.x, top - kBlendThreads);
-    const int k = top - 1 - int(threadIdx.x);      // slot t holds instance top-1-t
+  for (int top = end; top > rg.x; top -= kBatch) {
+    const int lo = max(rg.x, top - kBatch);
     __syncthreads();
-    if (k >= lo) {
-      const long long s = ival[k];
-      Splat g;
-      float4* gv = reinterpret_cast<float4*>(&g);
-      gv[0] = src[3 * s];
-      gv[1] = src[3 * s + 1];
-      gv[2] = src[3 * s + 2];
-      sm[threadIdx.x][0] = gv[0];
-      sm[threadIdx.x][1] = gv[1];
-      sm[threadIdx.x][2] = gv[2];
-      smask[threadIdx.x] = warp_block_mask(g, ox, oy);
+    for (int t = threadIdx.x; t < kBatch; t += kBlendTB) {
+      const int k = top - 1 - t;                   // slot t holds instance top-1-t
+      if (k >= lo) {
+        const long long si = ival[k];
+        Splat g;
+        float4* gv = reinterpret_cast<float4*>(&g);
+        gv[0] = src[3 * si];
+        gv[1] = src[3 * si + 1];
+        gv[2] = src[3 * si + 2];
+        sm[t][0] = gv[0];
+        sm[t][1] = gv[1];
+        sm[t][2] = gv[2];
+        smask[t] = warp_block_mask<kBlendWarps, 8>(g, ox, oy);
+      }
     }
     __syncthreads();
     const int cnt = top - lo;
@@ -506,32 +564,12 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
         *reinterpret_cast<float4*>(&g) = sm[j][0];
         *(reinterpret_cast<float4*>(&g) + 1) = sm[j][1];
         *(reinterpret_cast<float4*>(&g) + 2) = sm[j][2];
-        float c8 = 0.f;
-        float cv[8];
+        float cv[9];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) cv[u] = 0.f;
-        float dx, dy, q, gs, al;
-        const bool hit = inside && inst <= last && pixel_alpha(g, px, py, dx, dy, q, gs, al);
-        if (hit) {
-          const float inv = __frcp_rn(1.f - al);
-          const float Tf = T * inv;                          // T before this splat
-          const float w = al * Tf;
-          cv[0] = w * gr; cv[1] = w * gg; cv[2] = w * gb;    // dl_dcolor
-          const float gc = gr * g.r + gg * g.g + gb * g.b;
-          const float grear = gr * rr + gg * rg_ + gb * rb;
-          const float dla = gc * Tf - grear * inv;
-          rr += w * g.r; rg_ += w * g.g; rb += w * g.b;
-          T = Tf;
-          if (__fmul_rn(g.opac, gs) < kAlphaMax) {           // live: unclamped
-            cv[3] = gs * dla;
-            const float dq = -0.5f * g.opac * gs * dla;
-            cv[4] = -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
-            cv[5] = -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
-            cv[6] = dq * dx * dx;
-            cv[7] = dq * dx * dy;
-            c8 = dq * dy * dy;
-          }
-        }
+        for (int u = 0; u < 9; ++u) cv[u] = 0.f;
+        const bool h0 = bwd_pixel(g, px, py0, inst, s0, cv);
+        const bool h1 = bwd_pixel(g, px, py1, inst, s1, cv);
+        const bool hit = h0 || h1;
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
         if (bal == 0) continue;
         double* dst = g2 + (long long)kG2 * g.idx;
@@ -540,17 +578,16 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
           // fp64 accumulators (cheaper than a 32-lane reduction)
           if (hit) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 9; ++u)
               if (cv[u] != 0.f) atomicAdd(dst + u, double(cv[u]));
-            if (c8 != 0.f) atomicAdd(dst + 8, double(c8));
           }
           continue;
         }
-        const float t8 = warp_reduce8(cv, lane);
-        const float s8 = warp_sum(c8);
-        if ((lane & 3) == 0) {
-          if (t8 != 0.f) atomicAdd(dst + (lane >> 2), double(t8));
-        } else if (lane == 1) {
+        const float t8 = warp_reduce8(*reinterpret_cast<const float(*)[8]>(cv), ln);
+        const float s8 = warp_sum(cv[8]);
+        if ((ln & 3) == 0) {
+          if (t8 != 0.f) atomicAdd(dst + (ln >> 2), double(t8));
+        } else if (ln == 1) {
           if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
         }
       }
@@ -774,7 +811,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
     R->n_visible = 0;
     // T=1 everywhere, no contributors: the blend kernel writes exactly that
     count_launch();
-    blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(nullptr, nullptr, R->range.as<int2>(), cam,
+    blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(nullptr, nullptr, R->range.as<int2>(), cam,
                                                          image, R->tfinal.as<double>(), R->last.as<int>());
     return cudaGetLastError();
   }
@@ -859,7 +896,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
     CK(cudaGetLastError());
   }
   count_launch();
-  blend_fwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
+  blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                        R->range.as<int2>(), cam, image,
                                                        R->tfinal.as<double>(), R->last.as<int>());
   return cudaGetLastError();
@@ -874,7 +911,7 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   CK(cudaMemsetAsync(R->g2.p, 0, 8 * kG2 * (size_t)n, st));
   if (R->n_inst > 0) {
     count_launch();
-    blend_bwd_kernel<<<ntiles, kBlendThreads, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
+    blend_bwd_kernel<<<ntiles, kBlendTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                          R->range.as<int2>(), cam, dimg,
                                                          R->tfinal.as<double>(), R->last.as<int>(),
                                                          R->g2.as<double>());
