@@ -153,35 +153,51 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
-def roofline_for(stage_ms: dict, stats: dict, args, peaks: dict) -> dict:
-    """Dominant kernel of the step and its achieved rate vs the measured peak.
+def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
+    """Dominant kernel of the step (blend_bwd_kernel: 27% of the step in
+    profiles/round01_launches_summary.txt) and its achieved HBM rate:
+    ALGORITHMIC bytes per launch ÷ its mean launch duration,
+    both measured here over the stage-timing pass (CUDA events recorded on
+    the launching stream around each launch, glod_render_blend_timing).
 
-    Algorithmic bytes per launch:
-      blend_bwd: per instance 52 B (4 B id + 48 B splat record) + per pixel
-                 36 B (dL/dimage 12, T_final 8, last 4, image 12) +
-                 per Gaussian 72 B (9 f64 partials)
-      blend_fwd: per instance 52 B + per pixel 24 B (image 12, T 8, last 4)
-    """
-    npix = args.width * args.height
-    inst = stats.get("n_instances", 0)
-    R = stats.get("rendered", 0)
-    stage = max(stage_ms, key=lambda k: stage_ms[k])
-    if stage == "backward":
-        alg = inst * 52 + npix * 36 + R * 72 + R * (23 * 8 * 2)   # + K9 reads attrs, writes grads
-        name = "blend_bwd+preprocess_bwd"
-    elif stage == "forward":
-        alg = inst * 52 + npix * 24 + R * (23 * 8 + 48 + 16)
-        name = "preprocess+sort+blend_fwd"
-    else:
-        alg = None
-        name = stage
-    ms = stage_ms[stage]
+      blend_bwd: 52 B per tile instance (4 B instance id + 48 B splat
+                 record) + 24 B per pixel (dL/dimage 12, T_final 8, last
+                 contributor 4) + 144 B per rendered Gaussian (9 fp64
+                 accumulators, read-modify-write)
+      blend_fwd: 52 B per instance + 24 B per pixel (image 12, T 8, last 4)
+      adam:      1300 B per row (params r/w 368, moments r/w 736, grads 184,
+                 step 8, id 4) + 184 B per SPT row (cache-block refresh)
+      gather:    372 B per row (184 read, 184 write, 4 node id)
+
+    `traffic` is the ncu-measured DRAM bytes per launch of the same kernel
+    (profiles/ncu_traffic.json, from the committed --set full capture)."""
     peak = peaks.get("hbm_gbs", 6542.1)
-    ach = (alg / (ms * 1e-3) / 1e9) if alg else None
-    return {"bound": "hbm", "kernel": name, "achieved": ach, "peak": peak, "unit": "GB/s",
-            "frac": (ach / peak) if ach else None, "traffic": None, "ms": ms,
-            "note": "blend stages are issue/atomic bound (no dense contraction); "
-                    "frac is algorithmic HBM bytes / measured copy peak"}
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    traffic = {}
+    try:
+        traffic = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+    except Exception:
+        pass
+
+    def line(name, alg_bytes, ms, bound_note):
+        ach = alg_bytes / (ms * 1e-3) / 1e9 if ms else None
+        t = traffic.get(name, {}).get("dram_bytes_per_launch")
+        return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak if ach else None, "traffic": t,
+                "alg_bytes_per_launch": alg_bytes, "ms": ms, "note": bound_note}
+
+    main = line("blend_bwd_kernel", kt["bwd_alg"], kt["bwd_ms"],
+                "issue-bound (no dense contraction: per-pixel fp32 math, warp shuffles, fp64 "
+                "atomics); frac is algorithmic HBM bytes / measured copy peak — see "
+                "profiles/round01.md for issue utilisation")
+    main["peak_source"] = peak_src
+    main["others"] = [
+        line("blend_fwd_kernel", kt["fwd_alg"], kt["fwd_ms"], "issue-bound (per-pixel compositing)"),
+        line("adam_kernel", kt["adam_alg"], stage_ms.get("adam"), "HBM (sparse rows); ms = adam stage"),
+        line("gather_rows_kernel", kt["gather_alg"], stage_ms.get("gather"),
+             "HBM (sparse rows); ms = gather stage"),
+    ]
+    return main
 
 
 def cpu_baseline(trainer, args, R, sample_s) -> dict:
@@ -304,11 +320,25 @@ def run_ours(args):
     cst = tr.cache.stats()
     # ---- per-stage timing (separate pass; CUDA events per stage) ---------
     tr.enable_timing(True)
-    for _ in range(max(3, args.steps // 4)):
+    tr.rast.blend_timing(True)
+    npix = args.width * args.height
+    alg = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0, "gather": 0.0}
+    n_t = max(3, args.steps // 4)
+    for _ in range(n_t):
         it += 1
-        tr.train_step(it)
+        r = tr.train_step(it)
+        R, inst = r["gaussians_rendered"], tr.last_stats["n_instances"]
+        n_spt_rows = R - tr.last_stats["n_upper"] - tr.last_stats["n_pass"]
+        alg["fwd"] += inst * 52 + npix * 24
+        alg["bwd"] += inst * 52 + npix * 24 + R * 144
+        alg["adam"] += R * 1300 + n_spt_rows * 184
+        alg["gather"] += R * 372
+    bt = tr.rast.blend_timing(False)
     stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
     tr.enable_timing(False)
+    kt = {"fwd_ms": bt["fwd_ms"] / max(bt["fwd_launches"], 1), "bwd_ms": bt["bwd_ms"] / max(bt["bwd_launches"], 1),
+          "fwd_alg": alg["fwd"] / n_t, "bwd_alg": alg["bwd"] / n_t, "adam_alg": alg["adam"] / n_t,
+          "gather_alg": alg["gather"] / n_t}
     stats = dict(tr.last_stats)
     stats["rendered"] = recs[-1]["gaussians_rendered"]
     # ---- render FPS (cut + cache gather + forward) ------------------------
@@ -385,7 +415,7 @@ def run_ours(args):
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk,
-        "roofline": roofline_for(stage_ms, stats, args, peaks),
+        "roofline": roofline_for(kt, stage_ms, args, peaks),
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(tr, args, stats["rendered"], args.cpu_sample_s)

@@ -154,6 +154,12 @@ int glod_render_forward(glod_raster* r, const double* attrs, int64_t n,
 int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, void* stream);
 
 int glod_render_stats_get(const glod_raster* r, glod_render_stats* out);
+/* Optional CUDA-event timing of the blend kernels (measurement only; no
+ * reference counterpart).  Collects finished launches into
+ * ms_out[2] = {Σ forward blend ms, Σ backward blend ms} and
+ * launches_out[2]; then enable >= 0 resets the sums and turns timing on
+ * (1) or off (0); enable < 0 leaves both as they are. */
+int glod_render_blend_timing(glod_raster* r, int32_t enable, double* ms_out, int64_t* launches_out);
 
 /* Replaces loss (renderer.py:322-360): (1-lam)*L1 + lam*(1-SSIM), 11-tap
  * sigma=1.5 window, zero padding.  rendered/target/grad: [dev] f32

@@ -775,7 +775,48 @@ struct RasterCtx {
   bool have_forward = false;
   const unsigned* ikey_sorted = nullptr;
   const int* ival_sorted = nullptr;
+  // optional CUDA-event timing of the two blend kernels (bench.py roofline)
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double blend_ms[2] = {0.0, 0.0};
+  long long blend_n[2] = {0, 0};
+  bool pending[2] = {false, false};
 };
+
+static void timing_begin(RasterCtx* R, int k, cudaStream_t st) {
+  if (!R->timing) return;
+  if (!R->ev[0])
+    for (int i = 0; i < 4; ++i) cudaEventCreate(&R->ev[i]);
+  cudaEventRecord(R->ev[2 * k], st);
+}
+
+static void timing_end(RasterCtx* R, int k, cudaStream_t st) {
+  if (!R->timing) return;
+  cudaEventRecord(R->ev[2 * k + 1], st);
+  R->pending[k] = true;
+}
+
+// Accumulate the finished launches' durations (synchronises on the events).
+void raster_timing_collect(RasterCtx* R, int enable, double* fwd_ms, double* bwd_ms, long long* n) {
+  for (int k = 0; k < 2; ++k)
+    if (R->pending[k]) {
+      float ms = 0.f;
+      cudaEventSynchronize(R->ev[2 * k + 1]);
+      if (cudaEventElapsedTime(&ms, R->ev[2 * k], R->ev[2 * k + 1]) == cudaSuccess) {
+        R->blend_ms[k] += ms;
+        R->blend_n[k] += 1;
+      }
+      R->pending[k] = false;
+    }
+  if (fwd_ms) *fwd_ms = R->blend_ms[0];
+  if (bwd_ms) *bwd_ms = R->blend_ms[1];
+  if (n) { n[0] = R->blend_n[0]; n[1] = R->blend_n[1]; }
+  if (enable >= 0) {
+    R->timing = enable != 0;
+    R->blend_ms[0] = R->blend_ms[1] = 0.0;
+    R->blend_n[0] = R->blend_n[1] = 0;
+  }
+}
 
 static int bits_for(long long v) {
   int b = 1;
@@ -896,9 +937,11 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
     CK(cudaGetLastError());
   }
   count_launch();
+  timing_begin(R, 0, st);
   blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                        R->range.as<int2>(), cam, image,
                                                        R->tfinal.as<double>(), R->last.as<int>());
+  timing_end(R, 0, st);
   return cudaGetLastError();
 }
 
@@ -911,10 +954,12 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   CK(cudaMemsetAsync(R->g2.p, 0, 8 * kG2 * (size_t)n, st));
   if (R->n_inst > 0) {
     count_launch();
+    timing_begin(R, 1, st);
     blend_bwd_kernel<<<ntiles, kBlendTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
                                                          R->range.as<int2>(), cam, dimg,
                                                          R->tfinal.as<double>(), R->last.as<int>(),
                                                          R->g2.as<double>());
+    timing_end(R, 1, st);
   }
   CK(cudaGetLastError());
   const int TB = 128;
@@ -947,6 +992,8 @@ void raster_destroy(RasterCtx* R) {
                 &R->tfinal, &R->last, &R->g2, &R->temp, &R->bad};
   for (Buf* b : all) b->release(st);
   if (R->host_pin.p) cudaFreeHost(R->host_pin.p);
+  for (int i = 0; i < 4; ++i)
+    if (R->ev[i]) cudaEventDestroy(R->ev[i]);
   delete R;
 }
 
