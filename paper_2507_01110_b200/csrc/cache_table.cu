@@ -28,6 +28,11 @@ cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item*
                               long long total, int load, cudaStream_t st);
 cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
                             cudaStream_t st);
+long long transfer_chunks(long long rows);
+cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
+                               long long nblocks, cudaStream_t st);
+cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
+                               cudaStream_t st);
 
 namespace {
 
@@ -133,8 +138,8 @@ struct CacheTable {
   int64_t resident = 0, hits = 0, misses = 0, loaded_rows = 0;
   // transfer staging: one pinned host item table, rewritten once its last
   // H2D copy (event items_done) has run
-  glod_prefix_item* h_items = nullptr;
-  size_t items_cap = 0;
+  glod_prefix_item* h_items = nullptr;   // items, then the int2 block map
+  size_t items_cap = 0;                   // bytes
   cudaEvent_t items_done = nullptr;
   std::vector<int32_t> step_ids;          // SPTs rendered this step (dirty at end)
   std::vector<double*> to_free;           // blocks dropped this step
@@ -311,13 +316,13 @@ struct CacheTable {
     if (pool) cudaMemPoolDestroy(pool);
   }
 
-  // pinned item table of at least n entries, safe to rewrite
-  cudaError_t ensure_items(size_t n) {
+  // pinned item table of at least `bytes`, safe to rewrite
+  cudaError_t ensure_items(size_t bytes) {
     cudaEventSynchronize(items_done);
-    if (n <= items_cap) return cudaSuccess;
+    if (bytes <= items_cap) return cudaSuccess;
     if (h_items) cudaFreeHost(h_items);
-    const size_t want = n * 2 + 64;
-    cudaError_t e = cudaMallocHost(&h_items, want * sizeof(glod_prefix_item));
+    const size_t want = bytes * 2 + 4096;
+    cudaError_t e = cudaMallocHost(&h_items, want);
     if (e != cudaSuccess) return e;
     items_cap = want;
     return cudaSuccess;
@@ -335,13 +340,23 @@ struct Xfer {
   const float* src = nullptr;  // loads: prefetched f32 copy of the prefix (HBM)
 };
 
-// Copies `v` into the pinned table at `off` and then to a device table
-// (main-stream ordered; freed by the caller after its kernel); returns the
-// device table and the element total.
+// Host bytes of one batch's table: items + int2 block map.
+size_t table_bytes(const std::vector<Xfer>& v) {
+  long long nb = 0;
+  for (const Xfer& x : v) nb += transfer_chunks(x.rows);
+  return (v.size() * sizeof(glod_prefix_item) + 15) / 16 * 16 + size_t(nb) * sizeof(int2);
+}
+
+// Writes `v` and its block map into the pinned table at byte offset `off`
+// and uploads both (main-stream ordered; the caller frees the device copy
+// after its kernel).  Returns the device items, block map and block count.
 cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, cudaStream_t st,
-                        glod_prefix_item** d_out, long long* total) {
-  glod_prefix_item* h = c->h_items + off;
-  long long acc = 0;
+                        glod_prefix_item** d_items, const int2** d_bmap, long long* nblocks) {
+  char* base = reinterpret_cast<char*>(c->h_items) + off;
+  glod_prefix_item* h = reinterpret_cast<glod_prefix_item*>(base);
+  const size_t items_bytes = (v.size() * sizeof(glod_prefix_item) + 15) / 16 * 16;
+  int2* bm = reinterpret_cast<int2*>(base + items_bytes);
+  long long acc = 0, nb = 0;
   for (size_t i = 0; i < v.size(); ++i) {
     h[i].slot_start = v[i].slot;
     h[i].rows = v[i].rows;
@@ -351,14 +366,18 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
     h[i].overlay_rows = v[i].overlay_rows;
     h[i].src = v[i].src;
     acc += kFloats * v[i].rows;
+    const long long nc = transfer_chunks(v[i].rows);
+    for (long long k = 0; k < nc; ++k) bm[nb++] = make_int2(int(i), int(k));
   }
+  const size_t bytes = items_bytes + size_t(nb) * sizeof(int2);
   void* d = nullptr;
-  cudaError_t e = c->dalloc(&d, v.size() * sizeof(glod_prefix_item), st);
+  cudaError_t e = c->dalloc(&d, bytes, st);
   if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(d, h, v.size() * sizeof(glod_prefix_item), cudaMemcpyHostToDevice, st);
+  e = cudaMemcpyAsync(d, base, bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
-  *d_out = static_cast<glod_prefix_item*>(d);
-  *total = acc;
+  *d_items = static_cast<glod_prefix_item*>(d);
+  *d_bmap = reinterpret_cast<const int2*>(static_cast<char*>(d) + items_bytes);
+  *nblocks = nb;
   return cudaSuccess;
 }
 
@@ -368,7 +387,8 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
 // store is queued (CacheTable::pending) and issued at end_step.
 cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::vector<Xfer>& wbs,
                       bool join, bool wait_pf, const glod_store_view& sv, cudaStream_t st) {
-  cudaError_t e = c->ensure_items(loads.size() + wbs.size() + 1);
+  const size_t load_bytes = table_bytes(loads);
+  cudaError_t e = c->ensure_items(load_bytes + table_bytes(wbs) + 64);
   if (e != cudaSuccess) return e;
   if (join) {
     e = cudaStreamWaitEvent(st, c->ev_wb, 0);
@@ -381,16 +401,19 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
   }
   if (!loads.empty()) {
     glod_prefix_item* d = nullptr;
-    long long total = 0;
-    e = stage_items(c, loads, 0, st, &d, &total);
-    if (e == cudaSuccess) e = launch_store_xfer(sv, d, int(loads.size()), total, 1, st);
+    const int2* bm = nullptr;
+    long long nb = 0;
+    e = stage_items(c, loads, 0, st, &d, &bm, &nb);
+    if (e == cudaSuccess) e = launch_load_blocks(sv, d, bm, nb, st);
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e != cudaSuccess) return e;
   }
   if (!wbs.empty()) {
     glod_prefix_item* d = nullptr;
-    long long total = 0;
-    e = stage_items(c, wbs, loads.size(), st, &d, &total);
+    const int2* bm = nullptr;
+    long long nb = 0, total = 0;
+    for (const Xfer& x : wbs) total += kFloats * x.rows;
+    e = stage_items(c, wbs, (load_bytes + 15) / 16 * 16, st, &d, &bm, &nb);
     if (e != cudaSuccess) return e;
     const int sb = c->stage_next;
     c->stage_next ^= 1;
@@ -414,7 +437,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     }
     float* staging = c->stage[sb];
     e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
-    if (e == cudaSuccess) e = launch_pack_f32(d, int(wbs.size()), total, staging, st);
+    if (e == cudaSuccess) e = launch_pack_blocks(d, bm, nb, staging, st);
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e == cudaSuccess) e = cudaEventRecord(c->ev_packed[sb], st);
     if (e != cudaSuccess) return e;

@@ -210,6 +210,58 @@ pack_f32_kernel(const glod_prefix_item* __restrict__ items, int n_items, long lo
   out[e] = float(items[it].block[e - items[it].elem_start]);
 }
 
+// Cache-path transfers driven by a block map: block b moves elements
+// [chunk·kChunk, (chunk+1)·kChunk) of item bmap[b].x (chunk = bmap[b].y),
+// so no thread searches the item table and every block streams one
+// contiguous span of one prefix.
+constexpr int kChunk = 2048;
+
+// sv.section[sec] without a local-memory copy of the parameter array
+GLOD_DEV const float* section_of(const glod_store_view& sv, int sec) {
+  const float* p = sv.section[0];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) p = sec == k ? sv.section[k] : p;
+  return p;
+}
+
+__global__ void __launch_bounds__(256)
+load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items,
+                   const int2* __restrict__ bmap) {
+  const int2 bm = bmap[blockIdx.x];
+  const glod_prefix_item I = items[bm.x];
+  const long long n = 23LL * I.rows;
+  const long long c0 = (long long)bm.y * kChunk;
+  const long long c1 = min(n, c0 + kChunk);
+  if (I.src) {                                   // prefetched f32 copy in HBM
+    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
+    return;
+  }
+  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {
+    int sec = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) sec += l >= kSecOff[k] * I.rows;
+    const long long within = l - kSecOff[sec] * I.rows;
+    const long long row = within / kSecCols[sec];
+    // overlay: rows below overlay_rows are the f32 rounding of a block whose
+    // write-back to these store rows is still in flight (cache_table.cu)
+    I.block[l] = row < I.overlay_rows
+                     ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
+                     : double(section_of(sv, sec)[I.slot_start * kSecCols[sec] + within]);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __restrict__ bmap,
+                   float* __restrict__ out) {
+  const int2 bm = bmap[blockIdx.x];
+  const glod_prefix_item I = items[bm.x];
+  const long long n = 23LL * I.rows;
+  const long long c0 = (long long)bm.y * kChunk;
+  const long long c1 = min(n, c0 + kChunk);
+  float* o = out + I.elem_start;
+  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[l]);
+}
+
 // Small device→host read-backs written by a kernel straight into mapped
 // pinned memory: no copy-engine queueing behind the cache's bulk D2H
 // write-back DMA (which would delay the step's host synchronisations).
@@ -286,6 +338,24 @@ cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long lon
   const int TB = 256;
   count_launch();
   pack_f32_kernel<<<unsigned((total + TB - 1) / TB), TB, 0, st>>>(items, n_items, total, out);
+  return cudaGetLastError();
+}
+
+long long transfer_chunks(long long rows) { return (23 * rows + kChunk - 1) / kChunk; }
+
+cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
+                               long long nblocks, cudaStream_t st) {
+  if (nblocks <= 0) return cudaSuccess;
+  count_launch();
+  load_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(sv, items, bmap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
+                               cudaStream_t st) {
+  if (nblocks <= 0) return cudaSuccess;
+  count_launch();
+  pack_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(items, bmap, out);
   return cudaGetLastError();
 }
 

@@ -468,7 +468,8 @@ struct BwdPix {
 GLOD_DEV bool bwd_pixel(const Splat& g, int px, int py, int inst, BwdPix& s, float (&cv)[9]) {
   float dx, dy, q, gs, al;
   if (!(s.inside && inst <= s.last && pixel_alpha(g, px, py, dx, dy, q, gs, al))) return false;
-  const float inv = __frcp_rn(1.f - al);
+  float inv;                                           // 1/(1-α), 1-α ≥ 0.01: approx rcp
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.f - al));
   const float Tf = s.T * inv;                          // T before this splat
   const float w = al * Tf;
   cv[0] += w * s.gr; cv[1] += w * s.gg; cv[2] += w * s.gb;   // dl_dcolor
@@ -596,7 +597,7 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
 }
 
 // K9: 2D partials → gradients of the raw attributes (renderer.py:262-303).
-__global__ void preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
+__global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
                                       const int* __restrict__ tiles_of, const double* __restrict__ g2,
                                       double* __restrict__ grads) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
