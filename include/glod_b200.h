@@ -222,6 +222,18 @@ int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* 
                             void* stream);
 /* entry.block.attrs.put(pos, h.attrs.take(node_ids)) for every SPT row. */
 int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream);
+/* View-sharded training (no single-view counterpart): after the replicated
+ * ADAM on the union `ids` of every rank's touched nodes, copy each updated
+ * master row into this rank's resident cache block holding it — the rule of
+ * trainer.py:363 applied to the union.  spt_of_node/rec_of_node: [dev]
+ * int32[capacity] (SPT id / record position of each node, -1 if none);
+ * res_block/res_rows: [dev] per SPT id, the resident block and its rows
+ * (0 if not resident; glod_cache_resident); touched: [dev] int32 per SPT id,
+ * set to 1 for every block written (feed to glod_cache_mark_dirty). */
+int glod_refresh_resident_blocks(const double* master, int64_t capacity, const int32_t* ids, int64_t n,
+                                 const int32_t* spt_of_node, const int32_t* rec_of_node,
+                                 const uint64_t* res_block, const int64_t* res_rows, int32_t* touched,
+                                 void* stream);
 /* Elementwise f32 -> f64 (to_f64=1) or f64 -> f32 (store write-back). */
 int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* stream);
 
@@ -312,6 +324,11 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n,
                         const int32_t* spt_ids, const double* d_root, const int32_t* prefix_len,
                         int64_t max_rows, int64_t* rows_out, void* stream);
 int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
+/* Host tables of the resident blocks per SPT id (block address, rows; 0 if
+ * not resident), for glod_refresh_resident_blocks. */
+int glod_cache_resident(const glod_cache* c, uint64_t* block, int64_t* rows, int32_t num_spts);
+/* Mark the resident entries whose flag is set dirty (host int32 per SPT id). */
+int glod_cache_mark_dirty(glod_cache* c, const int32_t* flags, int32_t num_spts);
 /* Resident entries in LRU order (front first), up to `capacity`. */
 int glod_cache_entries(const glod_cache* c, int32_t* spt_id, double* cached_distance,
                        int64_t* prefix_len, uint64_t* block, int32_t* dirty, int64_t capacity);

@@ -102,6 +102,9 @@ SIGNATURES = {
                                  C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
+    "glod_refresh_resident_blocks": (C.c_int, [P, C.c_int64, P, C.c_int64, P, P, P, P, P, P]),
+    "glod_cache_resident": (C.c_int, [P, P, P, C.c_int32]),
+    "glod_cache_mark_dirty": (C.c_int, [P, P, C.c_int32]),
     "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),
     "glod_host_device_ptr": (C.c_int, [P, C.POINTER(P)]),
     "glod_store_load_prefixes": (C.c_int, [C.POINTER(StoreView), P, C.c_int32, C.c_int64, P]),

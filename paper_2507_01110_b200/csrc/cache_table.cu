@@ -764,6 +764,27 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n, 
   return GLOD_OK;
 }
 
+int glod_cache_resident(const glod_cache* c, uint64_t* block, int64_t* rows, int32_t num_spts) {
+  if (!c || (num_spts > 0 && (!block || !rows))) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  for (int32_t s = 0; s < num_spts; ++s) {
+    block[s] = 0;
+    rows[s] = 0;
+  }
+  for (const auto& e : c->t.lru)
+    if (e.spt_id >= 0 && e.spt_id < num_spts) {
+      block[e.spt_id] = reinterpret_cast<uint64_t>(e.block);
+      rows[e.spt_id] = e.prefix_len;
+    }
+  return GLOD_OK;
+}
+
+int glod_cache_mark_dirty(glod_cache* c, const int32_t* flags, int32_t num_spts) {
+  if (!c || (num_spts > 0 && !flags)) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  for (auto& e : c->t.lru)
+    if (e.spt_id >= 0 && e.spt_id < num_spts && flags[e.spt_id]) e.dirty = true;
+  return GLOD_OK;
+}
+
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes) {
   if (!dst || !src) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   cudaError_t e = cudaMemcpy(dst, src, size_t(bytes), cudaMemcpyDeviceToHost);

@@ -22,6 +22,10 @@ cudaError_t launch_adam(double* params, double* mv, long long* step, long long c
 cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
+cudaError_t launch_refresh_resident(const double* master, long long cap, const int* ids, long long n,
+                                    const int* spt_of_node, const int* rec_of_node,
+                                    const unsigned long long* res_block, const long long* res_rows, int* touched,
+                                    cudaStream_t st);
 cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st);
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
@@ -195,6 +199,19 @@ int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* 
   const long long R = (long long)plan->n_upper + plan->n_pass + plan->n_sel;
   return check(glod::launch_gather(*plan, R, out, row_node, static_cast<cudaStream_t>(stream)),
                "glod_gather_render_rows");
+}
+
+int glod_refresh_resident_blocks(const double* master, int64_t capacity, const int32_t* ids, int64_t n,
+                                 const int32_t* spt_of_node, const int32_t* rec_of_node,
+                                 const uint64_t* res_block, const int64_t* res_rows, int32_t* touched,
+                                 void* stream) {
+  if (n > 0 && (!master || !ids || !spt_of_node || !rec_of_node || !res_block || !res_rows || !touched))
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_refresh_resident(master, capacity, ids, n, spt_of_node, rec_of_node,
+                                             reinterpret_cast<const unsigned long long*>(res_block),
+                                             reinterpret_cast<const long long*>(res_rows), touched,
+                                             static_cast<cudaStream_t>(stream)),
+               "glod_refresh_resident_blocks");
 }
 
 int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream) {

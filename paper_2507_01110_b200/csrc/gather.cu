@@ -210,6 +210,36 @@ pack_f32_kernel(const glod_prefix_item* __restrict__ items, int n_items, long lo
   out[e] = float(items[it].block[e - items[it].elem_start]);
 }
 
+// View-sharded training: after the replicated ADAM on the union U of every
+// rank's touched nodes, each rank's resident cache blocks must hold the new
+// master values of every row any rank updated (the single-view rule
+// entry.block.attrs.put(pos, h.attrs.take(node_ids)), trainer.py:363,
+// applied to the union).  One thread per (node, column); a touched SPT is
+// flagged so the host marks its entry dirty.
+__global__ void refresh_resident_kernel(const double* __restrict__ master, long long cap,
+                                        const int* __restrict__ ids, long long n,
+                                        const int* __restrict__ spt_of_node, const int* __restrict__ rec_of_node,
+                                        const unsigned long long* __restrict__ res_block,
+                                        const long long* __restrict__ res_rows, int* __restrict__ touched) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 23 * n) return;
+  const long long w = e / 23;
+  const int col = int(e - w * 23);
+  const long long id = ids[w];
+  const int s = spt_of_node[id];
+  if (s < 0) return;
+  const long long rows = res_rows[s];
+  const long long pos = rec_of_node[id];
+  if (pos >= rows) return;                 // not resident / outside the cached prefix
+  int sec = 0;
+#pragma unroll
+  for (int k = 1; k < 6; ++k) sec += col >= kSecOff[k];
+  const int c = col - kSecOff[sec], cols = kSecCols[sec];
+  double* blk = reinterpret_cast<double*>(res_block[s]);
+  blk[kSecOff[sec] * rows + pos * cols + c] = master[kSecOff[sec] * cap + id * cols + c];
+  if (col == 0) touched[s] = 1;
+}
+
 // Cache-path transfers driven by a block map: block b moves elements
 // [chunk·kChunk, (chunk+1)·kChunk) of item bmap[b].x (chunk = bmap[b].y),
 // so no thread searches the item table and every block streams one
@@ -338,6 +368,17 @@ cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long lon
   const int TB = 256;
   count_launch();
   pack_f32_kernel<<<unsigned((total + TB - 1) / TB), TB, 0, st>>>(items, n_items, total, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_refresh_resident(const double* master, long long cap, const int* ids, long long n,
+                                    const int* spt_of_node, const int* rec_of_node,
+                                    const unsigned long long* res_block, const long long* res_rows, int* touched,
+                                    cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  count_launch();
+  refresh_resident_kernel<<<unsigned((23 * n + 255) / 256), 256, 0, st>>>(master, cap, ids, n, spt_of_node,
+                                                                           rec_of_node, res_block, res_rows, touched);
   return cudaGetLastError();
 }
 

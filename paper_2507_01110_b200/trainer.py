@@ -217,6 +217,41 @@ class Trainer:
         return t
 
     # ------------------------------------------------------------------
+    def _refresh_union(self, ids: torch.Tensor):
+        """View-sharded step: every resident cache block of this rank takes
+        the new master values of the rows any rank updated (the union `ids`);
+        touched SPTs are marked dirty before the next step's decisions."""
+        sc, dev = self.scene, self.scene.device
+        hs = sc.hspt
+        S = len(hs.spts)
+        if getattr(self, "_spt_of_node", None) is None:
+            flat = hs.flat_records()
+            spt_of = np.full(sc.cap, -1, dtype=np.int32)
+            rec_of = np.full(sc.cap, -1, dtype=np.int32)
+            for k in range(S):
+                o, c = int(flat["offset"][k]), int(flat["count"][k])
+                nodes = flat["nodes"][o:o + c]
+                spt_of[nodes] = k
+                rec_of[nodes] = np.arange(c, dtype=np.int32)
+            self._spt_of_node = torch.from_numpy(spt_of).to(dev)
+            self._rec_of_node = torch.from_numpy(rec_of).to(dev)
+            S1 = max(S, 1)
+            self._h_res = torch.empty(2 * S1, dtype=torch.int64).pin_memory()
+            self._d_res = torch.empty(2 * S1, dtype=torch.int64, device=dev)
+            self._d_touched = torch.zeros(S1, dtype=torch.int32, device=dev)
+            self._h_touched = torch.zeros(S1, dtype=torch.int32).pin_memory()
+        S1 = max(S, 1)
+        hr = self._h_res.numpy()
+        self.cache.resident(hr[:S1].view(np.uint64), hr[S1:])
+        self._d_res.copy_(self._h_res, non_blocking=True)
+        self._d_touched.zero_()
+        _lib.check(_lib.lib().glod_refresh_resident_blocks(
+            _lib.ptr(sc.params), sc.cap, _lib.ptr(ids), int(ids.numel()), _lib.ptr(self._spt_of_node),
+            _lib.ptr(self._rec_of_node), _lib.ptr(self._d_res), _lib.ptr(self._d_res[S1:]),
+            _lib.ptr(self._d_touched), _lib.stream_ptr()))
+        _lib.readback(self._h_touched, self._d_touched)
+        self._touched_pending = True
+
     def select(self, cam: Camera, spec_cam: Camera | None = None):
         """LoD select + one D2H of the per-SPT table (the step's host sync).
         With `spec_cam`, a speculative select of that (predicted next) view
@@ -266,6 +301,10 @@ class Trainer:
         self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
         S1 = max(sc.lod.S, 1)
+        if getattr(self, "_touched_pending", False):
+            # last step's union refresh (read back under this step's sync)
+            self.cache.mark_dirty(self._h_touched.numpy())
+            self._touched_pending = False
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
         if view is not None:
@@ -350,7 +389,7 @@ class Trainer:
             _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),
                                         _lib.ptr(sc.step), sc.cap, _lib.ptr(ids), _lib.ptr(GU), None,
                                         nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
-            _lib.check(L.glod_scatter_to_blocks(C.byref(plan), st))
+            self._refresh_union(ids)
             self._last_union = (ids, GU)
         else:
             _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),

@@ -51,3 +51,39 @@ def test_union_allreduce_path_matches_local():
         assert torch.equal(a.scene.step, b.scene.step)
     finally:
         dist.destroy_process_group()
+
+
+def test_union_refresh_updates_resident_blocks():
+    """View sharding: rows another rank updated reach this rank's resident
+    cache blocks (and mark those entries dirty for write-back)."""
+    from paper_2507_01110_b200 import _lib
+    tr, _, _ = make_case()
+    for it in range(1, 4):
+        tr.train_step(it)
+    torch.cuda.synchronize()
+    sc = tr.scene
+    flat = sc.hspt.flat_records()
+    entries = tr.cache.entries()
+    assert entries
+    sid, _, P, addr, _ = entries[0]
+    o = int(flat["offset"][sid])
+    nodes = flat["nodes"][o:o + P]
+    pick = nodes[::max(1, P // 7)].astype(np.int64)
+    rng = np.random.default_rng(5)
+    view = sc.params.view(-1)
+    off = 0
+    for name, cols in SECTIONS:      # new master values for the picked rows
+        sec = view[off * sc.cap:(off + cols) * sc.cap].view(sc.cap, cols)
+        sec[torch.from_numpy(pick).cuda()] = torch.from_numpy(rng.normal(size=(pick.size, cols))).cuda()
+        off += cols
+    ids = torch.from_numpy(pick.astype(np.int32)).cuda()
+    tr._refresh_union(ids)
+    torch.cuda.synchronize()
+    blk = AttributeArrays.from_packed(tr.cache.read_block(addr, P), P)
+    master = AttributeArrays.from_packed(sc.params.cpu().numpy(), sc.cap)
+    pos = np.array([np.nonzero(nodes == n)[0][0] for n in pick])
+    for name, _ in SECTIONS:
+        np.testing.assert_array_equal(getattr(blk, name)[pos], getattr(master, name)[pick])
+    assert tr._h_touched.numpy()[sid] == 1
+    tr.cache.mark_dirty(tr._h_touched.numpy())
+    assert [e for e in tr.cache.entries() if e[0] == sid][0][4]
