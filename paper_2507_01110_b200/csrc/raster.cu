@@ -350,11 +350,14 @@ GLOD_DEV bool pixel_alpha(const Splat& g, int px, int py, float& dx, float& dy, 
   if (px < g.x0 || px >= g.x1 || py < g.y0 || py >= g.y1) return false;
   dx = __fsub_rn(float(px - g.x0), g.mx);
   dy = __fsub_rn(float(py - g.y0), g.my);
-  // q = a dx² + c dy² + 2 b dy dx   (renderer.py:151-152)
-  q = __fadd_rn(__fadd_rn(__fmul_rn(g.ca, __fmul_rn(dx, dx)), __fmul_rn(g.cc, __fmul_rn(dy, dy))),
-                __fmul_rn(__fmul_rn(__fmul_rn(2.0f, g.cb), dy), dx));
+  // q = a dx² + c dy² + 2 b dy dx   (renderer.py:151-152), explicit FMAs
+  // (the forward and backward kernels evaluate the identical sequence)
+  q = __fmaf_rn(__fmul_rn(g.ca, dx), dx,
+                __fmaf_rn(__fmul_rn(g.cc, dy), dy, __fmul_rn(__fmul_rn(__fmul_rn(2.0f, g.cb), dx), dy)));
   if (!(q <= kQMax)) return false;
-  gauss = __expf(__fmul_rn(-0.5f, q));
+  // exp(-q/2) = 2^(q · (-log2(e)/2)): one multiply + MUFU.EX2
+  // (q ≤ 32: the argument is ≥ -23.1, far from the denormal range)
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gauss) : "f"(__fmul_rn(q, -0.72134752044448170368f)));
   const float a = __fmul_rn(g.opac, gauss);
   alpha = fminf(a, kAlphaMax);
   return alpha > 0.0f;

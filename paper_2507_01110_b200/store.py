@@ -55,11 +55,18 @@ def slot_order(h, hspt) -> np.ndarray:
 
 
 class HostStore:
-    """Pinned host store + per-SPT directory, built from (hierarchy, hspt)."""
+    """Pinned host store + per-SPT directory, built from (hierarchy, hspt).
+
+    `location="device"` keeps the same sections in HBM instead (config C2,
+    a fully device-resident scene): every transfer path is unchanged, the
+    copies just become device-to-device."""
 
     bytes_per_gaussian = BYTES_PER_GAUSSIAN_F32
 
-    def __init__(self, h, hspt, pin: bool = True):
+    def __init__(self, h, hspt, pin: bool = True, location: str = "host"):
+        if location not in ("host", "device"):
+            raise ValueError("location must be 'host' or 'device'")
+        self.location = location
         flat = hspt.flat_records()
         self.slot_to_node = slot_order(h, hspt)
         self.nslots = int(self.slot_to_node.size)
@@ -71,7 +78,10 @@ class HostStore:
         for name, cols in SECTIONS:
             arr = np.asarray(getattr(h.attrs, name))[self.slot_to_node].astype(np.float32)
             t = torch.from_numpy(np.ascontiguousarray(arr.reshape(self.nslots, cols)))
-            self.sections.append(t.pin_memory() if pin else t)
+            if location == "device":
+                self.sections.append(t.to("cuda"))
+            else:
+                self.sections.append(t.pin_memory() if pin else t)
         self.attribute_bytes_read = 0
 
     # -- directory ----------------------------------------------------------
@@ -92,7 +102,7 @@ class HostStore:
         s = self.spt_slot_start(spt_id)
         parts = []
         for (name, cols), sec in zip(SECTIONS, self.sections):
-            a = sec[s:s + prefix_len].numpy().copy()
+            a = sec[s:s + prefix_len].cpu().numpy().copy()
             parts.append(a if cols > 1 else a[:, 0])
         self.attribute_bytes_read += prefix_len * self.bytes_per_gaussian
         return AttributeBlock(spt_id, int(prefix_len), AttributeArrays(*parts))
@@ -106,7 +116,7 @@ class HostStore:
         s = self.spt_slot_start(block.spt_id)
         for (name, cols), sec in zip(SECTIONS, self.sections):
             v = np.asarray(getattr(block.attrs, name), dtype=np.float32).reshape(block.prefix_len, cols)
-            sec[s:s + block.prefix_len] = torch.from_numpy(v)
+            sec[s:s + block.prefix_len] = torch.from_numpy(v).to(sec.device)
 
     # -- device path ----------------------------------------------------------
     def prefix_to_device(self, spt_id: int, prefix_len: int, out_f32: torch.Tensor) -> None:
@@ -136,6 +146,9 @@ class HostStore:
             from . import _lib
             v = _lib.StoreView()
             for k, sec in enumerate(self.sections):
+                if sec.is_cuda:
+                    v.section[k] = sec.data_ptr()
+                    continue
                 dp = C.c_void_p()
                 _lib.check(_lib.lib().glod_host_device_ptr(C.c_void_p(sec.data_ptr()), C.byref(dp)))
                 v.section[k] = dp.value

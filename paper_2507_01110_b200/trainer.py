@@ -62,6 +62,9 @@ class TrainConfig:
     # copy-engine prefetch of the scheduler's next view's cache misses
     # (not in the reference; decisions and counters are unchanged)
     prefetch: bool = True
+    # where the f32 scene store lives: "host" (pinned DRAM, out-of-core) or
+    # "device" (HBM, config C2 — fully device-resident)
+    store_location: str = "host"
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -81,7 +84,7 @@ def _packed(t: torch.Tensor, rows: int, name: str) -> torch.Tensor:
 class DeviceScene:
     """Master params + ADAM state + LoD tables + host store for one HSPT."""
 
-    def __init__(self, h, hspt, device=None):
+    def __init__(self, h, hspt, device=None, store_location: str = "host"):
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.cap = h.capacity
@@ -91,7 +94,7 @@ class DeviceScene:
         self.step = torch.zeros(self.cap, dtype=torch.int64, device=dev)
         self.lod = DeviceLodScene(h, hspt, means=_packed(self.params, self.cap, "means"),
                                   scales=_packed(self.params, self.cap, "scales"))
-        self.store = HostStore(h, hspt)
+        self.store = HostStore(h, hspt, location=store_location)
         self.hspt = hspt
 
     def moments_packed(self):
@@ -125,7 +128,7 @@ class Trainer:
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized() and \
             dist.get_world_size(group) > 1
-        self.scene = DeviceScene(h, hspt)
+        self.scene = DeviceScene(h, hspt, store_location=cfg.store_location)
         dev = self.scene.device
         self.cache = NativeCache(cfg.cache, self.scene.store)
         self.rast = Rasterizer()

@@ -63,7 +63,7 @@ def restore(orc: OracleTrainer, snap):
     orc.resident = snap["resident"]
 
 
-def make_case(n_leaves=6000, res=(96, 64), n_views=10, budget_frac=0.35, seed=3):
+def make_case(n_leaves=6000, res=(96, 64), n_views=10, budget_frac=0.35, seed=3, store_location="host"):
     h, hs, cfg = designed_scene(SceneSpec(n_leaves=n_leaves, spt_leaves=256, seed=seed,
                                           pass_fraction=0.1))
     E = scene_extent(n_leaves)
@@ -73,7 +73,7 @@ def make_case(n_leaves=6000, res=(96, 64), n_views=10, budget_frac=0.35, seed=3)
     targets = [np.clip(rng.normal(0.5, 0.2, (res[1], res[0], 3)), 0, 1) for _ in cams]
     budget = int(budget_frac * hs.flat_records()["nodes"].size * 92)
     tcfg = TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=budget, flush_interval=7),
-                       scheduler_k=4, seed=seed)
+                       scheduler_k=4, seed=seed, store_location=store_location)
     tr = Trainer(h, hs, list(zip(cams, targets)), tcfg, extent=2 * E)
     flat = hs.flat_records()
     kind = np.full(h.capacity, -1, np.int32)
@@ -83,7 +83,7 @@ def make_case(n_leaves=6000, res=(96, 64), n_views=10, budget_frac=0.35, seed=3)
     lrs = dict(tcfg.learning_rates)
     lrs["means"] *= 2 * E
     orc = OracleTrainer(_dict(h.attrs), h.children, h.root, kind, flat,
-                        [s.numpy() for s in st.sections],
+                        [s.cpu().numpy() for s in st.sections],
                         [st.spt_slot_start(i) for i in range(len(hs.spts))],
                         [(O.Cam.of(c), t) for c, t in zip(cams, targets)], cfg.threshold,
                         cfg.metric_code, budget, flush_interval=7, lrs=lrs)
@@ -158,3 +158,16 @@ def test_prefetch_is_invisible():
     assert [e[:3] + e[4:] for e in ea] == [e[:3] + e[4:] for e in eb]
     for x, y in zip(ea, eb):
         assert np.array_equal(a.cache.read_block(x[3], x[2]), b.cache.read_block(y[3], y[2]))
+
+
+def test_device_store_matches_host_store():
+    """C2's device-resident store (sections in HBM) runs the same transfer
+    paths device-to-device: identical counters, parameters and store."""
+    a, _, _ = make_case()
+    b, _, _ = make_case(store_location="device")
+    for it in range(1, 11):
+        assert a.train_step(it) == b.train_step(it), it
+    torch.cuda.synchronize()
+    assert torch.equal(a.scene.params, b.scene.params)
+    for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
+        assert torch.equal(sa, sb.cpu())
