@@ -42,6 +42,28 @@ def city_leaves(rng, n, extent=100.0, height=20.0, sh_sigma=0.05) -> AttributeAr
     return a
 
 
+def city_block_leaves(rng, n, extent=100.0, height=20.0, blocks=8, street=0.15,
+                      sh_sigma=0.05) -> AttributeArrays:
+    """G-city (test_acceptance.py:180-193 `_city_scene` style):
+    leaves on a blocks × blocks grid of city blocks separated by streets
+    (`street` = street width / block pitch), each block a random-height
+    building footprint, plus a thin ground layer in the streets."""
+    a = city_leaves(rng, n, extent, height, sh_sigma)
+    pitch = 2.0 * extent / blocks
+    half = 0.5 * pitch * (1.0 - street)
+    bx = rng.integers(0, blocks, n)
+    bz = rng.integers(0, blocks, n)
+    cx = -extent + (bx + 0.5) * pitch
+    cz = -extent + (bz + 0.5) * pitch
+    bh = rng.uniform(0.3, 1.0, (blocks, blocks)) * height
+    ground = rng.uniform(size=n) < 0.1
+    x = np.where(ground, rng.uniform(-extent, extent, n), cx + rng.uniform(-half, half, n))
+    z = np.where(ground, rng.uniform(-extent, extent, n), cz + rng.uniform(-half, half, n))
+    y = np.where(ground, rng.uniform(0.0, 0.02 * height, n), rng.uniform(0.0, 1.0, n) * bh[bx, bz])
+    a.means = np.stack([x, y, z], axis=1)
+    return a
+
+
 @dataclass
 class SceneSpec:
     n_leaves: int
@@ -56,6 +78,7 @@ class SceneSpec:
     s_hi: float = 0.3
     metric: str = "max_scale"
     relabel: bool = True            # node ids in store slot order (see relabel_slot_order)
+    layout: str = "slab"            # "slab" (city_leaves) or "blocks" (G-city, city_block_leaves)
 
 
 def scene_extent(n_leaves: int) -> float:
@@ -67,7 +90,10 @@ def designed_scene(spec: SceneSpec, device=None):
     rng = np.random.default_rng(spec.seed)
     extent = spec.extent if spec.extent is not None else scene_extent(spec.n_leaves)
     height = spec.height if spec.height is not None else 0.2 * extent
-    h = build_hierarchy(city_leaves(rng, spec.n_leaves, extent, height), device=device)
+    leaves = (city_block_leaves(rng, spec.n_leaves, extent, height) if spec.layout == "blocks"
+              else city_leaves(rng, spec.n_leaves, extent, height))
+    h = build_hierarchy(leaves, device=device)
+    del leaves
     depth = node_depths(h)
     max_depth = int(depth.max())
     D = max(1, int(round(math.log2(max(spec.n_leaves / spec.spt_leaves, 1.0)))))
@@ -159,4 +185,25 @@ def orbit_views(n, radius, height, resolution=(1920, 1080), focal=None, seed=0,
         pos += rng.normal(0.0, jitter * radius * 0.05, 3)
         tgt = rng.normal(0.0, target_jitter, 3)
         cams.append(look_at(pos, tgt, f, resolution))
+    return cams
+
+
+def street_views(n, extent, resolution=(1920, 1080), blocks=8, eye=1.7, seed=0):
+    """Street-level cameras (test_acceptance.py:216-219 style): eye height
+    `eye`, walking along the streets between the city blocks and looking
+    down the street."""
+    rng = np.random.default_rng(seed)
+    w, hh = resolution
+    pitch = 2.0 * extent / blocks
+    cams = []
+    for i in range(n):
+        k = rng.integers(1, blocks)
+        t = rng.uniform(-0.9 * extent, 0.9 * extent)
+        along_x = i % 2 == 0
+        street = -extent + k * pitch
+        pos = np.array([t, eye, street]) if along_x else np.array([street, eye, t])
+        d = np.array([1.0, 0.0, 0.0]) if along_x else np.array([0.0, 0.0, 1.0])
+        d = d * (1 if rng.uniform() < 0.5 else -1)
+        cams.append(look_at(pos, pos + 10.0 * d + np.array([0.0, 0.3, 0.0]), (0.6 * w, 0.6 * w),
+                            resolution, near=0.1))
     return cams
