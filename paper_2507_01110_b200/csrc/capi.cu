@@ -195,8 +195,9 @@ int glod_adam_step(double* params, double* mv, int64_t* step, int64_t capacity,
 
 int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* row_node,
                             void* stream) {
-  if (!plan || !out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (!plan) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   const long long R = (long long)plan->n_upper + plan->n_pass + plan->n_sel;
+  if (R > 0 && !out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_gather(*plan, R, out, row_node, static_cast<cudaStream_t>(stream)),
                "glod_gather_render_rows");
 }

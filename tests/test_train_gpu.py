@@ -171,3 +171,21 @@ def test_device_store_matches_host_store():
     assert torch.equal(a.scene.params, b.scene.params)
     for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
         assert torch.equal(sa, sb.cpu())
+
+
+def test_empty_view_trains():
+    """A view whose cut is empty (camera facing away from the scene) renders
+    the black background, has a finite loss and updates nothing."""
+    from paper_2507_01110_b200.scenegen import look_at
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=4000, spt_leaves=256, seed=2))
+    E = scene_extent(4000)
+    cams = [look_at([3 * E, E, 0.0], [6 * E, E, 0.0], (70.0, 70.0), (64, 48)) for _ in range(3)]
+    cams[1] = look_at([3 * E, E, 1.0], [6 * E, 2 * E, 1.0], (70.0, 70.0), (64, 48))
+    targets = [np.full((48, 64, 3), 0.5) for _ in cams]
+    tr = Trainer(h, hs, list(zip(cams, targets)), TrainConfig(lod=cfg, scheduler_k=2), extent=2 * E)
+    before = tr.scene.params.clone()
+    for it in range(1, 4):
+        r = tr.train_step(it)
+        assert r["gaussians_rendered"] == 0 and np.isfinite(r["loss"])
+    torch.cuda.synchronize()
+    assert torch.equal(before, tr.scene.params)

@@ -13,6 +13,7 @@ HBM footprint.
 """
 import argparse
 import json
+import resource
 import sys
 import time
 from pathlib import Path
@@ -108,6 +109,7 @@ def main():
         "render": fps, "hbm_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
         "hbm_reserved_gb_incl_arenas": round((torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9, 1),
         "scene_build_s": round(build_s, 1), "setup_s": round(setup_s, 1),
+        "host_peak_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 1),
         "data": "synthetic G-city (seeded), synthetic smooth targets"}), flush=True)
 
 
