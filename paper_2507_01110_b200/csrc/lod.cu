@@ -403,6 +403,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   const long long nwarps_g = (long long)gridDim.x * nwarps;
   const long long gwarp = (long long)blockIdx.x * nwarps + warp;
   __shared__ long long wcount[kCompactThreads / 32];
+  // per-warp staging of one lane-group step's selections (≤ 32·kAlign)
+  __shared__ int st_seg[kCompactThreads / 32][32 * kAlign];
+  __shared__ int st_pos[kCompactThreads / 32][32 * kAlign];
+  __shared__ int st_node[kCompactThreads / 32][32 * kAlign];
   // waves small enough that the second pass re-reads the keys from L2
   const long long wave = sc.key_f64 ? (8ll << 20) : (16ll << 20);
   long long wave_base = 0;                      // selections before this wave
@@ -511,18 +515,28 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
           if (lane >= o) incl += y;
         }
-        long long o = run + incl - c;
+        // stage the group's selections in order in shared memory, then the
+        // warp writes them out as coalesced runs of the three arrays
+        int o = incl - c;
         const int nd[4] = {node[k].x, node[k].y, node[k].z, node[k].w};
 #pragma unroll
         for (int e = 0; e < kAlign; ++e) {
           if (mask[k] & (1u << e)) {
-            out.sel_seg[o] = segk[k];
-            out.sel_pos[o] = isrr[k] ? rootrec_of(sc, in, segk[k]) : loc[k] + e;
-            out.sel_node[o] = nd[e];
+            st_seg[warp][o] = segk[k];
+            st_pos[warp][o] = isrr[k] ? rootrec_of(sc, in, segk[k]) : loc[k] + e;
+            st_node[warp][o] = nd[e];
             ++o;
           }
         }
-        run += __shfl_sync(0xffffffffu, incl, 31);
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        for (int i = lane; i < tot; i += 32) {
+          out.sel_seg[run + i] = st_seg[warp][i];
+          out.sel_pos[run + i] = st_pos[warp][i];
+          out.sel_node[run + i] = st_node[warp][i];
+        }
+        __syncwarp();
+        run += tot;
       }
     }
     if (pass == 0) {

@@ -2,7 +2,8 @@
 //
 // 11-tap σ=1.5 Gaussian window applied separably per channel plane with
 // zero padding (scipy correlate1d mode="constant").  Two fused tile
-// kernels: pass 1 blurs x, y, x², y², xy from one shared-memory tile and
+// kernels (a block per 32x16 tile, all three channels in turn): pass 1
+// blurs x, y, x², y², xy from one shared-memory tile and
 // emits the three SSIM derivative maps plus per-block L1/SSIM partial sums;
 // pass 2 blurs the derivative maps and writes the image gradient.  Window
 // arithmetic is fp64 (the variance terms ux2 - mu² cancel).
@@ -32,8 +33,13 @@ ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
   __shared__ float sx[IH][IW], sy[IH][IW];
   __shared__ double v[5][TH][IW];
   __shared__ double red[2][NT / 32];
-  const int c = blockIdx.z;
   const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
+  double s_sum = 0, l_sum = 0;
+  // all three channels of the tile in one block: the interleaved (H, W, 3)
+  // sectors are read from DRAM once (the other channels hit L1/L2) and the
+  // three channels' writes merge in L2
+  for (int c = 0; c < 3; ++c) {
+  __syncthreads();
   for (int k = threadIdx.x; k < IH * IW; k += NT) {
     const int r = k / IW, q = k % IW;
     sx[r][q] = at(X, W, H, ox + q - R, oy + r - R, c);
@@ -51,7 +57,6 @@ ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
     v[0][r][q] = a; v[1][r][q] = b; v[2][r][q] = aa; v[3][r][q] = bb; v[4][r][q] = ab;
   }
   __syncthreads();
-  double s_sum = 0, l_sum = 0;
   for (int k = threadIdx.x; k < TH * TW; k += NT) {
     const int r = k / TW, q = k % TW;
     const int x = ox + q, y = oy + r;
@@ -77,6 +82,7 @@ ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
     s_sum += s;
     l_sum += fabs(double(sx[r + R][q + R]) - double(sy[r + R][q + R]));
   }
+  }
   // block reduction → one partial pair per block (deterministic order)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -88,7 +94,7 @@ ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
   if (threadIdx.x == 0) {
     double a = 0, b = 0;
     for (int w = 0; w < NT / 32; ++w) { a += red[0][w]; b += red[1][w]; }
-    const long long bid = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const long long bid = (long long)blockIdx.y * gridDim.x + blockIdx.x;
     part[2 * bid] = a;
     part[2 * bid + 1] = b;
   }
@@ -100,8 +106,9 @@ ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
            float* __restrict__ grad, double lam, double inv_n) {
   __shared__ float s0[IH][IW], s1[IH][IW], s2[IH][IW];
   __shared__ double v[3][TH][IW];
-  const int c = blockIdx.z;
   const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
+  for (int c = 0; c < 3; ++c) {
+  __syncthreads();
   for (int k = threadIdx.x; k < IH * IW; k += NT) {
     const int r = k / IW, q = k % IW;
     s0[r][q] = at(dmu, W, H, ox + q - R, oy + r - R, c);
@@ -137,6 +144,7 @@ ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
     const double dm = a + 2 * xv * b + yv * d;
     grad[o] = float((1 - lam) * sgn * inv_n - lam * dm);
   }
+  }
 }
 
 __global__ void ssim_finish(const double* __restrict__ part, int nparts, double lam, double inv_n,
@@ -167,7 +175,7 @@ unsigned g_win_ready = 0;   // bit per device that holds the window
 
 size_t loss_scratch_bytes(int W, int H) {
   const size_t npix = size_t(W) * H * 3;
-  const size_t nb = size_t((W + TW - 1) / TW) * ((H + TH - 1) / TH) * 3;
+  const size_t nb = size_t((W + TW - 1) / TW) * ((H + TH - 1) / TH);
   return 3 * 4 * npix + 16 * nb + 256;
 }
 
@@ -189,7 +197,7 @@ cudaError_t launch_loss(const float* X, const float* Y, int W, int H, double lam
   float* dx2 = dmu + npix;
   float* dxy = dx2 + npix;
   double* part = reinterpret_cast<double*>(dxy + npix + (npix & 1));
-  dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 3);
+  dim3 grid((W + TW - 1) / TW, (H + TH - 1) / TH, 1);
   const double inv_n = 1.0 / double(npix);
   count_launch();
   ssim_pass1<<<grid, NT, 0, st>>>(X, Y, W, H, dmu, dx2, dxy, part, inv_n);

@@ -9,7 +9,9 @@
 //   scatter  each block re-reads its chunk in input order, ranks every
 //            element stably within its warp (match_any per item slot,
 //            warp-private running counters) and across warps (per-digit
-//            prefix over the 8 warps), and writes it to its global slot
+//            prefix over the 8 warps), reorders each 2048-element round by
+//            digit in shared memory and writes it out as contiguous
+//            per-digit runs (coalesced stores)
 // Only the bit range where keys differ is sorted (min/max reduction first),
 // so positive fp64 depths cost ~6-7 passes, tile ids 2.
 #include <stdint.h>
@@ -25,6 +27,7 @@ constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kItems = 8;                                   // per thread per round
 constexpr int kRound = kSortThreads * kItems;               // 2048 elements
 constexpr int kBins = 256;
+static_assert(kSortThreads == kBins, "scatter_kernel: one thread per digit");
 
 template <typename K> GLOD_DEV unsigned digit_of(K k, int shift) { return unsigned(k >> shift) & 0xffu; }
 
@@ -47,7 +50,11 @@ scatter_kernel(const K* __restrict__ kin, K* __restrict__ kout, const int* __res
                int* __restrict__ vout, long long n, long long chunk, int shift,
                const unsigned* __restrict__ bh, int nblocks) {
   __shared__ unsigned base[kBins];                 // global slot of this block's next element per digit
-  __shared__ unsigned wcnt[kSortWarps][kBins];     // per-warp running counts within the round
+  __shared__ unsigned wcnt[kSortWarps][kBins];     // per-warp counts → per-warp offsets within the round
+  __shared__ unsigned dstart[kBins];               // round-local start of each digit's run
+  __shared__ long long scan_sm[kSortThreads / 32 + 1];
+  __shared__ K skey[kRound];                       // the round in (digit, input) order
+  __shared__ int sval[kRound];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int d = threadIdx.x; d < kBins; d += kSortThreads) base[d] = bh[(long long)d * nblocks + blockIdx.x];
   const long long lo = (long long)blockIdx.x * chunk, hi = min(n, lo + chunk);
@@ -76,27 +83,42 @@ scatter_kernel(const K* __restrict__ kin, K* __restrict__ kout, const int* __res
       pos[k] = p;
     }
     __syncthreads();
-    // per digit: exclusive prefix over warps, then advance the block base
-    for (int d = threadIdx.x; d < kBins; d += kSortThreads) {
-      unsigned run = base[d];
+    // per digit (thread d): exclusive prefix over warps, round total → scan
+    // over digits gives each digit's run start inside the round
+    unsigned tot = 0;
+    {
+      const int d = threadIdx.x;                   // kSortThreads == kBins
 #pragma unroll
       for (int w = 0; w < kSortWarps; ++w) {
         const unsigned c = wcnt[w][d];
-        wcnt[w][d] = run;
-        run += c;
+        wcnt[w][d] = tot;
+        tot += c;
       }
-      base[d] = run;
     }
+    const unsigned ds = unsigned(block_excl_scan((long long)tot, scan_sm));
+    dstart[threadIdx.x] = ds;
     __syncthreads();
+    // scatter into shared memory in (digit, input) order — stable
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
       if (dg[k] != 0xffffffffu) {
-        const unsigned o = wcnt[warp][dg[k]] + pos[k];
-        kout[o] = kv[k];
-        vout[o] = vv[k];
+        const unsigned lp = dstart[dg[k]] + wcnt[warp][dg[k]] + pos[k];
+        skey[lp] = kv[k];
+        sval[lp] = vv[k];
       }
     }
     __syncthreads();
+    // write out: consecutive threads → consecutive slots of one digit's run
+    const int cnt = int(min((long long)kRound, hi - r0));
+    for (int i = threadIdx.x; i < cnt; i += kSortThreads) {
+      const K key = skey[i];
+      const unsigned d = digit_of(key, shift);
+      const unsigned g = base[d] + (unsigned(i) - dstart[d]);
+      kout[g] = key;
+      vout[g] = sval[i];
+    }
+    __syncthreads();
+    base[threadIdx.x] += tot;
   }
 }
 
