@@ -112,6 +112,40 @@ int glod_spt_compact(const glod_lod_scene* scene, const glod_spt_compact_in* in,
                      const glod_spt_compact_out* out, void* scratch,
                      int64_t scratch_bytes, void* stream);
 
+/* ---- HSPT / SPT build -------------------------------- */
+typedef struct glod_hspt_build_in {
+  int64_t capacity;             /* hierarchy node slots                       */
+  int32_t root;                 /* Hierarchy.root                             */
+  int32_t min_subtree;          /* build_hspt min_subtree (>= 1)              */
+  const int32_t* parent;        /* [dev] [capacity], -1 = NONE                */
+  const int32_t* children;      /* [dev] [capacity*2], -1 = NONE              */
+  const double* means;          /* [dev] [capacity*3]                         */
+  const double* scales;         /* [dev] [capacity*3]                         */
+  double size_threshold;        /* volume threshold (> 0)                     */
+  double lod_threshold;         /* LodConfig.threshold used for the keys      */
+  int32_t metric;               /* 0 max_scale, 1 surface_area                */
+  int32_t corrected;            /* build_spt(corrected=...)                   */
+} glod_hspt_build_in;
+
+typedef struct glod_hspt_build_out {
+  int32_t* upper_ids;           /* [dev] [capacity] ascending                 */
+  int32_t* pass_ids;            /* [dev] [capacity] ascending passthrough roots */
+  int32_t* spt_roots;           /* [dev] [capacity] ascending = spt_id order  */
+  int32_t* spt_count;           /* [dev] [capacity] records per SPT           */
+  int64_t* spt_offset;          /* [dev] [capacity] first record of each SPT  */
+  int32_t* rec_node;            /* [dev] [capacity] record node ids           */
+  double* key_self;             /* [dev] [capacity]                           */
+  double* key_parent;           /* [dev] [capacity] (+inf at each SPT root)   */
+} glod_hspt_build_out;
+
+/* Replaces hspt.build_hspt (hspt.py:64-93) with spt.build_spt (spt.py:45-64)
+ * for every SPT root, bit-exact (same lists, record order and f64 keys).
+ * Synchronises the stream once; sizes[4] (host) = {n_upper, n_pass, n_spt,
+ * n_records}.  Free / unreachable node slots belong to no list. */
+int64_t glod_hspt_build_scratch_bytes(int64_t capacity);
+int glod_hspt_build(const glod_hspt_build_in* in, const glod_hspt_build_out* out, void* scratch,
+                    int64_t scratch_bytes, int64_t* sizes, void* stream);
+
 /* ======================================================================= *
  * Rasteriser (renderer.py)
  * ======================================================================= */
@@ -222,6 +256,18 @@ int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* 
                             void* stream);
 /* entry.block.attrs.put(pos, h.attrs.take(node_ids)) for every SPT row. */
 int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream);
+/* Serve path: wire payloads of the cut-delta protocol
+ * (protocol._wire_attrs, protocol.py:40-49; encode_spt_load /
+ * encode_upper_set :80-92).  Message k covers ids[seg_start[k] ..
+ * seg_start[k+1]) and is written at out + 23*seg_start[k] as the
+ * section-major little-endian f32 SoA [means 3n | scales 3n | rotations 4n
+ * | opacities n | base_colors 3n | sh_rest 9n] of master rows (f64 ->
+ * f32 round-to-nearest, as astype("<f4")).  master: [dev] packed f64,
+ * capacity rows; ids: [dev] int32 [n_rows]; seg_start: [dev] int64
+ * [n_msgs+1]; out: [dev] or mapped pinned host (glod_host_device_ptr),
+ * 23*n_rows floats. */
+int glod_wire_pack(const double* master, int64_t capacity, const int32_t* ids, const int64_t* seg_start,
+                   int32_t n_msgs, int64_t n_rows, float* out, void* stream);
 /* View-sharded training (no single-view counterpart): after the replicated
  * ADAM on the union `ids` of every rank's touched nodes, copy each updated
  * master row into this rank's resident cache block holding it — the rule of

@@ -28,6 +28,18 @@ class LodScene(C.Structure):
                 ("key_self", P), ("key_parent", P), ("rec_node", P)]
 
 
+class HsptBuildIn(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("root", C.c_int32), ("min_subtree", C.c_int32),
+                ("parent", P), ("children", P), ("means", P), ("scales", P),
+                ("size_threshold", C.c_double), ("lod_threshold", C.c_double),
+                ("metric", C.c_int32), ("corrected", C.c_int32)]
+
+
+class HsptBuildOut(C.Structure):
+    _fields_ = [("upper_ids", P), ("pass_ids", P), ("spt_roots", P), ("spt_count", P),
+                ("spt_offset", P), ("rec_node", P), ("key_self", P), ("key_parent", P)]
+
+
 class LodView(C.Structure):
     _fields_ = [("position", C.c_double * 3), ("planes", C.c_double * 24),
                 ("cull", C.c_int32), ("metric", C.c_int32), ("threshold", C.c_double)]
@@ -90,6 +102,9 @@ SIGNATURES = {
     "glod_spt_compact_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int64]),
     "glod_spt_compact": (C.c_int, [C.POINTER(LodScene), C.POINTER(CompactIn),
                                    C.POINTER(CompactOut), P, C.c_int64, P]),
+    "glod_hspt_build_scratch_bytes": (C.c_int64, [C.c_int64]),
+    "glod_hspt_build": (C.c_int, [C.POINTER(HsptBuildIn), C.POINTER(HsptBuildOut), P, C.c_int64,
+                                  C.POINTER(C.c_int64), P]),
     "glod_raster_create": (C.c_int, [C.POINTER(P)]),
     "glod_raster_destroy": (C.c_int, [P]),
     "glod_render_forward": (C.c_int, [P, P, C.c_int64, C.POINTER(Camera), P, P]),
@@ -102,6 +117,7 @@ SIGNATURES = {
                                  C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
+    "glod_wire_pack": (C.c_int, [P, C.c_int64, P, P, C.c_int32, C.c_int64, P, P]),
     "glod_refresh_resident_blocks": (C.c_int, [P, C.c_int64, P, C.c_int64, P, P, P, P, P, P]),
     "glod_cache_resident": (C.c_int, [P, P, P, C.c_int32]),
     "glod_cache_mark_dirty": (C.c_int, [P, P, C.c_int32]),

@@ -22,6 +22,8 @@ cudaError_t launch_adam(double* params, double* mv, long long* step, long long c
 cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
+cudaError_t launch_wire_pack(const double* master, long long cap, const int* ids, const long long* seg,
+                             int n_msgs, long long N, float* out, cudaStream_t st);
 cudaError_t launch_refresh_resident(const double* master, long long cap, const int* ids, long long n,
                                     const int* spt_of_node, const int* rec_of_node,
                                     const unsigned long long* res_block, const long long* res_rows, int* touched,
@@ -200,6 +202,15 @@ int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* 
   if (R > 0 && !out) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_gather(*plan, R, out, row_node, static_cast<cudaStream_t>(stream)),
                "glod_gather_render_rows");
+}
+
+int glod_wire_pack(const double* master, int64_t capacity, const int32_t* ids, const int64_t* seg_start,
+                   int32_t n_msgs, int64_t n_rows, float* out, void* stream) {
+  if (n_rows > 0 && (!master || !ids || !seg_start || !out || n_msgs <= 0))
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_wire_pack(master, capacity, ids, reinterpret_cast<const long long*>(seg_start),
+                                      n_msgs, n_rows, out, static_cast<cudaStream_t>(stream)),
+               "glod_wire_pack");
 }
 
 int glod_refresh_resident_blocks(const double* master, int64_t capacity, const int32_t* ids, int64_t n,

@@ -306,6 +306,44 @@ __global__ void readback_kernel(const unsigned char* __restrict__ src, unsigned 
   if (blockIdx.x == 0 && threadIdx.x < (bytes & 3)) dst[(words << 2) + threadIdx.x] = src[(words << 2) + threadIdx.x];
 }
 
+// Wire payloads of ServeSession.handle_pose (protocol.py:40-49,80-92): for
+// message k (rows [seg[k], seg[k+1]) of ids), the section-major f32 SoA of
+// master rows ids[...] at out + 23·seg[k].  blockIdx.y = section; one thread
+// per (row, column): consecutive threads write consecutive floats of one
+// message section (the out buffer may be mapped pinned host memory).
+template <int SEC>
+GLOD_DEV void wire_sec(const double* __restrict__ master, long long cap, const int* __restrict__ ids,
+                       const long long* __restrict__ seg, int n_msgs, long long N, float* __restrict__ out) {
+  constexpr int OFFS[7] = {0, 3, 6, 10, 11, 14, 23};
+  constexpr int COLS = OFFS[SEC + 1] - OFFS[SEC];
+  const long long local = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (local >= N * COLS) return;
+  const long long r = local / COLS;
+  const int col = int(local - r * COLS);
+  int lo = 0, hi = n_msgs - 1;                      // last k with seg[k] <= r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg[mid] <= r) lo = mid; else hi = mid - 1;
+  }
+  const long long a = seg[lo], n = seg[lo + 1] - a;
+  const long long node = ids[r];
+  out[23 * a + OFFS[SEC] * n + (r - a) * COLS + col] =
+      __double2float_rn(master[OFFS[SEC] * cap + node * COLS + col]);
+}
+
+__global__ void __launch_bounds__(256)
+wire_pack_kernel(const double* __restrict__ master, long long cap, const int* __restrict__ ids,
+                 const long long* __restrict__ seg, int n_msgs, long long N, float* __restrict__ out) {
+  switch (blockIdx.y) {
+    case 0: wire_sec<0>(master, cap, ids, seg, n_msgs, N, out); break;
+    case 1: wire_sec<1>(master, cap, ids, seg, n_msgs, N, out); break;
+    case 2: wire_sec<2>(master, cap, ids, seg, n_msgs, N, out); break;
+    case 3: wire_sec<3>(master, cap, ids, seg, n_msgs, N, out); break;
+    case 4: wire_sec<4>(master, cap, ids, seg, n_msgs, N, out); break;
+    case 5: wire_sec<5>(master, cap, ids, seg, n_msgs, N, out); break;
+  }
+}
+
 int grid_for(long long n, int tb) {
   long long g = (n + tb - 1) / tb;
   return int(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -321,6 +359,15 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
   const long long per_block = (long long)kGatherTB * kGatherIlp;
   const dim3 grid(unsigned((9 * R + per_block - 1) / per_block), 6);
   gather_rows_kernel<<<grid, kGatherTB, 0, st>>>(p, R, out, row_node);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wire_pack(const double* master, long long cap, const int* ids, const long long* seg,
+                             int n_msgs, long long N, float* out, cudaStream_t st) {
+  if (N <= 0 || n_msgs <= 0) return cudaSuccess;
+  count_launch();
+  const dim3 grid(unsigned((9 * N + 255) / 256), 6);
+  wire_pack_kernel<<<grid, 256, 0, st>>>(master, cap, ids, seg, n_msgs, N, out);
   return cudaGetLastError();
 }
 

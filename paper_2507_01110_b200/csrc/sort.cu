@@ -248,8 +248,12 @@ long long chunk_for(long long n) {
 
 // Scratch: histograms (256 × nblocks u32), their exclusive scan (u32),
 // 2 × u64 min/max, scan block sums.
+// Sized for the block count bound min(rounds, 148·4) rather than the exact
+// count, so the size is monotone in n (a buffer sized for n fits every
+// shorter sort).
 size_t radix_scratch_bytes(long long n) {
-  const long long nb = (n + chunk_for(n) - 1) / chunk_for(n);
+  const long long rounds = (n + kRound - 1) / kRound;
+  const long long nb = rounds < 148 * 4 ? rounds : 148 * 4;
   const size_t m = size_t(kBins) * size_t(nb > 0 ? nb : 1);
   return 2 * m * 4 + 64 + scan_scratch_bytes((long long)m) + 256;
 }

@@ -8,6 +8,7 @@ packs arguments and unpacks the device result into the reference's types.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -93,9 +94,67 @@ class RenderSet:
         return int(self.upper.size + self.passthrough.size + self.spt_nodes.size)
 
 
-def build_hspt(h: Hierarchy, size_threshold: float, min_subtree: int,
+def build_hspt(h, size_threshold: float, min_subtree: int, cfg: LodConfig,
+               corrected: bool = True) -> Hspt:
+    """Drop-in for hspt.build_hspt (hspt.py:64-93) on the GPU (K12,
+    csrc/build.cu): the volume-threshold partition and build_spt
+    (spt.py:45-64) of every SPT in one pass — same upper / passthrough /
+    SPT-root lists, record order and f64 keys, bit for bit.  Raises
+    ValueError like the reference for size_threshold <= 0 or
+    min_subtree < 1; needs a CUDA device (no CPU fallback)."""
+    if size_threshold <= 0:
+        raise ValueError("size_threshold must be > 0")
+    if min_subtree < 1:
+        raise ValueError("min_subtree must be >= 1")
+    import torch
+
+    from . import _lib
+    hh = Hierarchy.from_any(h)
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cap = hh.capacity
+    t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dt)
+    parent = t(hh.parent, torch.int32)
+    children = t(hh.children.reshape(-1), torch.int32)
+    means = t(hh.attrs.means.reshape(-1), torch.float64)
+    scales = t(hh.attrs.scales.reshape(-1), torch.float64)
+    i32 = lambda: torch.empty(cap, dtype=torch.int32, device=dev)
+    out_t = {"upper": i32(), "pass": i32(), "roots": i32(), "count": i32(),
+             "offset": torch.empty(cap, dtype=torch.int64, device=dev), "nodes": i32(),
+             "key_self": torch.empty(cap, dtype=torch.float64, device=dev),
+             "key_parent": torch.empty(cap, dtype=torch.float64, device=dev)}
+    scratch = torch.empty(int(L.glod_hspt_build_scratch_bytes(cap)), dtype=torch.uint8, device=dev)
+    bi = _lib.HsptBuildIn(capacity=cap, root=int(hh.root), min_subtree=int(min_subtree),
+                          parent=parent.data_ptr(), children=children.data_ptr(),
+                          means=means.data_ptr(), scales=scales.data_ptr(),
+                          size_threshold=float(size_threshold), lod_threshold=float(cfg.threshold),
+                          metric=0 if cfg.metric == "max_scale" else 1, corrected=int(bool(corrected)))
+    bo = _lib.HsptBuildOut(*[out_t[k].data_ptr() for k in ("upper", "pass", "roots", "count", "offset",
+                                                           "nodes", "key_self", "key_parent")])
+    sizes = (C.c_int64 * 4)()
+    _lib.check(L.glod_hspt_build(C.byref(bi), C.byref(bo), scratch.data_ptr(), scratch.numel(),
+                                 sizes, _lib.stream_ptr()))
+    nu, npass, S, R = (int(x) for x in sizes)
+    host = lambda k, n, dt: out_t[k][:n].cpu().numpy().astype(dt)
+    roots = host("roots", S, np.int64)
+    counts = host("count", S, np.int64)
+    flat = {"nodes": host("nodes", R, np.int64), "key_self": host("key_self", R, np.float64),
+            "key_parent": host("key_parent", R, np.float64), "offset": host("offset", S, np.int64),
+            "count": counts, "centers": hh.attrs.means[roots].copy(), "roots": roots}
+    spts = [Spt(root=int(r), root_center=flat["centers"][i], nodes=flat["nodes"][o:o + c],
+                key_self=flat["key_self"][o:o + c], key_parent=flat["key_parent"][o:o + c])
+            for i, (r, o, c) in enumerate(zip(roots, flat["offset"], counts))]
+    return Hspt(upper_nodes=host("upper", nu, np.int64), spts=spts,
+                passthrough_roots=host("pass", npass, np.int64),
+                size_threshold=float(size_threshold), min_subtree=int(min_subtree), lod=cfg,
+                spt_id_of={int(r): i for i, r in enumerate(roots)}, flat=flat)
+
+
+def build_hspt_host(h: Hierarchy, size_threshold: float, min_subtree: int,
                cfg: LodConfig) -> Hspt:
-    """Volume-threshold partition (hspt.py:64-93), vectorised SPT flattening."""
+    """Host (numpy) restatement of build_hspt (hspt.py:64-93) with vectorised
+    SPT flattening — scene tooling for CPU-only contexts (scene generators
+    in the CPU test-suite); the product build is `build_hspt` (device)."""
     if size_threshold <= 0:
         raise ValueError("size_threshold must be > 0")
     if min_subtree < 1:

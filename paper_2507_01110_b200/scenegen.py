@@ -26,7 +26,7 @@ import numpy as np
 
 from .core import AttributeArrays, Camera, LodConfig, rotmat_to_quat
 from .hierarchy import Hierarchy, build_hierarchy, node_depths
-from .hspt import Hspt, build_hspt
+from .hspt import Hspt, build_hspt, build_hspt_host
 
 
 def city_leaves(rng, n, extent=100.0, height=20.0, sh_sigma=0.05) -> AttributeArrays:
@@ -125,10 +125,14 @@ def designed_scene(spec: SceneSpec, device=None):
     scales[is_upper] = s_up
     scales[is_cut] = s_cut
     h.attrs.scales = scales
-    hspt = build_hspt(h, thr, spec.min_subtree, cfg)
+    # scene tooling: the device build (K12) when a GPU is present, the numpy
+    # restatement in CPU-only test contexts
+    import torch
+    build = build_hspt if torch.cuda.is_available() else build_hspt_host
+    hspt = build(h, thr, spec.min_subtree, cfg)
     if spec.relabel:
         h = relabel_slot_order(h, hspt)
-        hspt = build_hspt(h, thr, spec.min_subtree, cfg)
+        hspt = build(h, thr, spec.min_subtree, cfg)
     return h, hspt, cfg
 
 

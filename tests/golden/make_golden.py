@@ -327,7 +327,7 @@ def make_adam_cases():
     np.savez_compressed(OUT / "adam_cases.npz", **d)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     print("lod files", make_lod_cases())
     make_spt_cases()
     make_render_cases()
@@ -408,6 +408,55 @@ def make_cache_cases():
     np.savez_compressed(OUT / "cache_cases.npz", **d)
 
 
+def make_serve_cases():
+    """ServeSession.handle_pose message streams (protocol.py:152-193) over
+    camera paths: first pose, repeated pose (stats only), moves that load
+    and evict SPTs, a pose facing away (everything culled) and back."""
+    from glod.protocol import ServeSession
+    rng = np.random.default_rng(777)
+    d = {}
+    for case in range(4):
+        n = int(rng.choice([300, 900, 2000]))
+        h = build_hierarchy(random_leaves(rng, n))
+        if case % 2:
+            thr = _designed_scales(rng, h, int(rng.integers(2, 5)))
+            min_sub = 8
+        else:
+            h.attrs.scales = rng.uniform(0.05, 2.0, h.attrs.scales.shape)
+            thr = float(np.quantile(np.prod(h.attrs.scales, axis=1), 0.5))
+            min_sub = int(rng.choice([4, 8, 16]))
+        lod = LodConfig(threshold=float(rng.uniform(1.0, 20.0) if case % 2 == 0 else rng.uniform(0.5, 6.0)),
+                        metric=("max_scale", "surface_area")[case % 2])
+        hspt = build_hspt(h, thr, min_sub, lod)
+        sess = ServeSession(hierarchy=h, hspt=hspt, lod=lod)
+        p = f"c{case}_"
+        d.update({p + k: v for k, v in hier_arrays(h).items()})
+        d.update({p + k: v for k, v in hspt_arrays(hspt).items()})
+        cams = []
+        for v in range(8):
+            if v == 2:
+                cam = cams[1]                                     # repeated pose
+            elif v == 5:
+                c = cams[4]                                       # facing away
+                cam = look_at_camera(c.position, 2 * c.position, focal=(40.0, 40.0))
+            else:
+                pos = rng.uniform(-25, 25, 3) * (0.3 + 0.2 * v)
+                cam = look_at_camera(pos, rng.uniform(-3, 3, 3), focal=(40.0, 40.0))
+            cams.append(cam)
+            msgs = sess.handle_pose(cam)
+            d.update(cam_arrays(cam, p + f"v{v}_"))
+            d[p + f"v{v}_lens"] = np.array([len(m) for m in msgs], dtype=np.int64)
+            d[p + f"v{v}_bytes"] = np.frombuffer(b"".join(msgs), dtype=np.uint8)
+        d[p + "n_views"] = np.int64(len(cams))
+    d["n_cases"] = np.int64(4)
+    np.savez_compressed(OUT / "serve_cases.npz", **d)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}_cases"]()
+        sys.exit(0)
     make_scheduler_cases()
     make_cache_cases()
+    make_serve_cases()
