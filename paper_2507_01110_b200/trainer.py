@@ -358,21 +358,45 @@ class Trainer:
         self.last_render = counters
         return img
 
+    def _upload_target(self, target: torch.Tensor):
+        """Host (pinned) target → device on a side stream, double-buffered:
+        the copy overlaps this step's cut, gather and forward render; the
+        loss waits for it (event).  A buffer is refilled only after the
+        loss that read it two steps ago."""
+        dev = self.scene.device
+        if getattr(self, "_tgt_bufs", None) is None or self._tgt_bufs[0].shape != target.shape:
+            self._tgt_bufs = [torch.empty(target.shape, dtype=target.dtype, device=dev) for _ in range(2)]
+            self._tgt_stream = torch.cuda.Stream(device=dev)
+            self._tgt_used = [torch.cuda.Event(), torch.cuda.Event()]
+            self._tgt_done = [torch.cuda.Event(), torch.cuda.Event()]
+            self._tgt_slot = 1
+        k = self._tgt_slot = 1 - self._tgt_slot
+        with torch.cuda.stream(self._tgt_stream):
+            self._tgt_stream.wait_event(self._tgt_used[k])
+            self._tgt_bufs[k].copy_(target, non_blocking=True)
+            self._tgt_done[k].record()
+        self._target_dev = self._tgt_bufs[k]
+        return self._tgt_bufs[k], self._tgt_done[k]
+
     def train_step(self, iteration: int) -> dict:
         cfg, sc = self.cfg, self.scene
         self.current_view = next_view(self.graph, self.current_view, iteration, self.rng)
         self._next_view = self._predict_next(iteration) if cfg.prefetch else None
         cam, _ = self.views[self.current_view]
         target = self.targets[self.current_view]
+        tgt_ready = None
         if not self.device_targets:
-            self._target_dev = target.to(sc.device, non_blocking=True)
-            target = self._target_dev
+            target, tgt_ready = self._upload_target(target)
         R, rows, row_node, plan, _, counters = self._gather_view(cam, self.current_view)
         L = _lib.lib()
         st = _lib.stream_ptr()
         image = self.rast.forward(rows, R, cam)
         self._mark("forward")
+        if tgt_ready is not None:
+            torch.cuda.current_stream().wait_event(tgt_ready)
         value, dimg = self.rast.loss(image, target, cfg.loss_lambda)
+        if tgt_ready is not None:
+            self._tgt_used[self._tgt_slot].record()
         self._mark("loss")
         _lib.readback(self._h_loss[:value.numel()], value)
         torch.cuda.current_stream().synchronize()

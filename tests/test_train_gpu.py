@@ -189,3 +189,17 @@ def test_empty_view_trains():
         assert r["gaussians_rendered"] == 0 and np.isfinite(r["loss"])
     torch.cuda.synchronize()
     assert torch.equal(before, tr.scene.params)
+
+
+def test_host_targets_match_device_targets():
+    """e2e mode: targets in pinned host memory are uploaded on a side stream
+    (double-buffered, overlapping the cut/gather/forward); losses and
+    parameters are identical to device-resident targets."""
+    a, _, _ = make_case()
+    b, _, _ = make_case()
+    b.targets = [t.cpu().pin_memory() for t in b.targets]
+    b.device_targets = False
+    for it in range(1, 13):
+        assert a.train_step(it) == b.train_step(it), it
+    torch.cuda.synchronize()
+    assert torch.equal(a.scene.params, b.scene.params)
