@@ -171,34 +171,16 @@ GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
 // (l&7, l>>3) and (l&7, (l>>3)+4) of it.  Two pixels per lane halve the
 // per-pixel share of every per-splat cost (the splat read from shared
 // memory, the loop, and in the backward the warp reduction and the fp64
-// atomics).  Bit w of a splat's mask: it can reach a pixel of warp w's
-// block (bbox overlap and the conservative ellipse test), so each warp
-// iterates only over its own splats — skipping one changes none of its
-// pixels.
+// atomics).  Each warp iterates only over the splats that can reach its
+// block (bbox overlap and the conservative ellipse test, block_hit) —
+// skipping one changes none of its pixels.
 constexpr int kBlendWarps = 4;
 constexpr int kBlendTB = 32 * kBlendWarps;
-constexpr int kBatch = 256;                 // splats staged per round
 // The forward keeps one pixel per lane (8 warps, 8x4 blocks): its per-pixel
 // state is a sequential fp64 chain, so it wants more warps in flight more
 // than it wants the shared per-splat cost halved.
 constexpr int kFwdWarps = 8;
 constexpr int kFwdTB = 32 * kFwdWarps;
-
-// Mask of the warps (NW warps, 8 x BH pixel blocks, two per block row) a
-// splat can reach.
-template <int NW, int BH>
-GLOD_DEV unsigned warp_block_mask(const Splat& g, int ox, int oy) {
-  unsigned m = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const int xa = ox + (w & 1) * 8, ya = oy + (w >> 1) * BH;
-    if (g.x1 <= xa || g.x0 >= xa + 8 || g.y1 <= ya || g.y0 >= ya + BH) continue;
-    if (rect_hit(g, max(xa, int(g.x0)), min(xa + 7, int(g.x1) - 1), max(ya, int(g.y0)),
-                 min(ya + BH - 1, int(g.y1) - 1)))
-      m |= 1u << w;
-  }
-  return m;
-}
 
 // One Gaussian; returns its tile count (0 = contributes nothing) and sets
 // its depth key.
@@ -377,46 +359,77 @@ GLOD_DEV void fwd_pixel(const Splat& g, int px, int py, int inst, double& T, flo
   if (T <= kTEps) done = true;           // later alphas are gated to 0
 }
 
+// Can splat g reach a pixel of the W x H block at (xa, ya)?  Bbox overlap
+// and the conservative ellipse test (rect_hit): skipping a splat that fails
+// it changes none of the block's pixels.
+template <int W, int H>
+GLOD_DEV bool block_hit(const Splat& g, int xa, int ya) {
+  if (g.x1 <= xa || g.x0 >= xa + W || g.y1 <= ya || g.y0 >= ya + H) return false;
+  return rect_hit(g, max(xa, int(g.x0)), min(xa + W - 1, int(g.x1) - 1), max(ya, int(g.y0)),
+                  min(ya + H - 1, int(g.y1) - 1));
+}
+
+// Warp-streamed blending: every warp walks its tile's instance list on its
+// own, 32 splats per step (one coalesced 48-B record per lane, staged in a
+// warp-private shared slice), keeps the ones that can reach its pixel block
+// (ballot) and composites them in order.  No block barriers: a warp never
+// waits for a slower warp of the same tile, and a warp whose pixels are all
+// saturated leaves at once.  The other warps of the tile read the same
+// records, so the repeats are L1 hits.
+GLOD_DEV void load_splat(const Splat* __restrict__ sorted, int si, float4 (&dst)[3], Splat& g) {
+  const float4* src = reinterpret_cast<const float4*>(sorted) + 3LL * si;
+  float4* gv = reinterpret_cast<float4*>(&g);
+  gv[0] = __ldg(src);
+  gv[1] = __ldg(src + 1);
+  gv[2] = __ldg(src + 2);
+  dst[0] = gv[0];
+  dst[1] = gv[1];
+  dst[2] = gv[2];
+}
+
+GLOD_DEV void read_splat(const float4 (&src)[3], Splat& g) {
+  float4* gv = reinterpret_cast<float4*>(&g);
+  gv[0] = src[0];
+  gv[1] = src[1];
+  gv[2] = src[2];
+}
+
 __global__ void __launch_bounds__(kFwdTB)
 blend_fwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, float* __restrict__ image,
                  double* __restrict__ t_final, int* __restrict__ last_out) {
-  __shared__ Splat sm[kBatch];
-  __shared__ unsigned smask[kBatch];
+  __shared__ float4 sm[kFwdWarps][32][3];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  const int ox = tx * kTileW, oy = ty * kTileH;
   // warp w owns the 8x4 pixel block at (8(w&1), 4(w>>1))
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
-  const int px = ox + (wid & 1) * 8 + (ln & 7), py = oy + (wid >> 1) * 4 + (ln >> 3);
-  const unsigned mybit = 1u << wid;
+  const int bx = tx * kTileW + (wid & 1) * 8, by = ty * kTileH + (wid >> 1) * 4;
+  const int px = bx + (ln & 7), py = by + (ln >> 3);
   const bool inside = px < cam.w && py < cam.h;
   const int2 rg = range[tile];
   double T = 1.0;
   float cr = 0.f, cg = 0.f, cb = 0.f;
   int last = -1;
   bool done = !inside;
-  for (int base = rg.x; base < rg.y; base += kBatch) {
-    if (__syncthreads_count(!done) == 0) break;
-    for (int t = threadIdx.x; t < kBatch; t += kFwdTB) {
-      const int k = base + t;
-      if (k < rg.y) {
-        const Splat g = sorted[ival[k]];
-        sm[t] = g;
-        smask[t] = warp_block_mask<kFwdWarps, 4>(g, ox, oy);
-      }
+  for (int base = rg.x; base < rg.y; base += 32) {
+    if (__all_sync(0xffffffffu, done)) break;
+    const int k = base + ln;
+    bool mine = false;
+    if (k < rg.y) {
+      Splat g;
+      load_splat(sorted, ival[k], sm[wid][ln], g);
+      mine = block_hit<8, 4>(g, bx, by);
     }
-    __syncthreads();
-    const int cnt = min(kBatch, rg.y - base);
-    for (int c = 0; c < cnt; c += 32) {
-      if (__all_sync(0xffffffffu, done)) break;
-      unsigned bits = __ballot_sync(0xffffffffu, c + ln < cnt && (smask[c + ln] & mybit));
-      while (bits) {
-        const int j = c + __ffs(bits) - 1;
-        bits &= bits - 1;
-        fwd_pixel(sm[j], px, py, base + j, T, cr, cg, cb, last, done);
-      }
+    __syncwarp();
+    unsigned bits = __ballot_sync(0xffffffffu, mine);
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      Splat g;
+      read_splat(sm[wid][j], g);
+      fwd_pixel(g, px, py, base + j, T, cr, cg, cb, last, done);
     }
+    __syncwarp();
   }
   if (inside) {
     const long long pix = (long long)py * cam.w + px;
@@ -505,97 +518,76 @@ GLOD_DEV BwdPix bwd_init(const CamD& cam, int px, int py, const float* __restric
   return s;
 }
 
-// For each (splat, warp) with at least one hit the nine per-Gaussian
-// partials are warp-reduced (transposed reduction) and nine lanes issue one
-// fp64 reduction each (or, with one or two hitting lanes, those lanes issue
-// theirs directly).  Warps skip splats outside their block (mask) or beyond
-// their last contributor.
+// Warp-streamed like the forward: each warp walks its tile's list back to
+// front from its own last contributor, 32 splats per step.  For each
+// (splat, warp) with at least one hit the nine per-Gaussian partials are
+// warp-reduced (transposed reduction) and nine lanes issue one fp64
+// reduction each (or, with one or two hitting lanes, those lanes issue
+// theirs directly).
 __global__ void __launch_bounds__(kBlendTB, 8)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
                  double* __restrict__ g2) {
-  __shared__ float4 sm[kBatch][3];
-  __shared__ unsigned smask[kBatch];
-  __shared__ int max_last;
+  __shared__ float4 sm[kBlendWarps][32][3];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tw, ty = tile / cam.tw;
-  const int ox = tx * kTileW, oy = ty * kTileH;
   const int wid = int(threadIdx.x >> 5), ln = int(threadIdx.x & 31);
-  const int px = ox + (wid & 1) * 8 + (ln & 7);
-  const int py0 = oy + (wid >> 1) * 8 + (ln >> 3), py1 = py0 + 4;
-  const unsigned mybit = 1u << wid;
+  const int bx = tx * kTileW + (wid & 1) * 8, by = ty * kTileH + (wid >> 1) * 8;
+  const int px = bx + (ln & 7);
+  const int py0 = by + (ln >> 3), py1 = py0 + 4;
   const int2 rg = range[tile];
   BwdPix s0 = bwd_init(cam, px, py0, dimg, t_final, last_in);
   BwdPix s1 = bwd_init(cam, px, py1, dimg, t_final, last_in);
   int wlast = max(s0.last, s1.last);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wlast = max(wlast, __shfl_xor_sync(0xffffffffu, wlast, o));
-  if (threadIdx.x == 0) max_last = -1;
-  __syncthreads();
-  if (ln == 0) atomicMax(&max_last, wlast);
-  __syncthreads();
-  const int end = max_last + 1;   // nothing beyond the last contributor matters
-  const float4* src = reinterpret_cast<const float4*>(sorted);
-  for (int top = end; top > rg.x; top -= kBatch) {
-    const int lo = max(rg.x, top - kBatch);
-    __syncthreads();
-    for (int t = threadIdx.x; t < kBatch; t += kBlendTB) {
-      const int k = top - 1 - t;                   // slot t holds instance top-1-t
-      if (k >= lo) {
-        const long long si = ival[k];
-        Splat g;
-        float4* gv = reinterpret_cast<float4*>(&g);
-        gv[0] = src[3 * si];
-        gv[1] = src[3 * si + 1];
-        gv[2] = src[3 * si + 2];
-        sm[t][0] = gv[0];
-        sm[t][1] = gv[1];
-        sm[t][2] = gv[2];
-        smask[t] = warp_block_mask<kBlendWarps, 8>(g, ox, oy);
+  // nothing beyond this warp's last contributor matters
+  for (int top = min(wlast + 1, rg.y); top > rg.x; top -= 32) {
+    const int lo = max(rg.x, top - 32);
+    const int k = top - 1 - ln;                  // slot ln holds instance top-1-ln
+    bool mine = false;
+    if (k >= lo) {
+      Splat g;
+      load_splat(sorted, ival[k], sm[wid][ln], g);
+      mine = block_hit<8, 8>(g, bx, by);
+    }
+    __syncwarp();
+    unsigned bits = __ballot_sync(0xffffffffu, mine);
+    while (bits) {
+      const int j = __ffs(bits) - 1;             // ascending slot = back to front
+      bits &= bits - 1;
+      const int inst = top - 1 - j;
+      Splat g;
+      read_splat(sm[wid][j], g);
+      float cv[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) cv[u] = 0.f;
+      const bool h0 = bwd_pixel(g, px, py0, inst, s0, cv);
+      const bool h1 = bwd_pixel(g, px, py1, inst, s1, cv);
+      const bool hit = h0 || h1;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (bal == 0) continue;
+      double* dst = g2 + (long long)kG2 * g.idx;
+      if (__popc(bal) <= 2) {
+        // one or two hitting lanes: their partials go straight to the
+        // fp64 accumulators (cheaper than a 32-lane reduction)
+        if (hit) {
+#pragma unroll
+          for (int u = 0; u < 9; ++u)
+            if (cv[u] != 0.f) atomicAdd(dst + u, double(cv[u]));
+        }
+        continue;
+      }
+      const float t8 = warp_reduce8(*reinterpret_cast<const float(*)[8]>(cv), ln);
+      const float s8 = warp_sum(cv[8]);
+      if ((ln & 3) == 0) {
+        if (t8 != 0.f) atomicAdd(dst + (ln >> 2), double(t8));
+      } else if (ln == 1) {
+        if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
       }
     }
-    __syncthreads();
-    const int cnt = top - lo;
-    for (int c = 0; c < cnt; c += 32) {
-      const int jl = c + ln;
-      unsigned bits = __ballot_sync(0xffffffffu, jl < cnt && top - 1 - jl <= wlast && (smask[jl] & mybit));
-      while (bits) {
-        const int j = c + __ffs(bits) - 1;           // ascending slot = back to front
-        bits &= bits - 1;
-        const int inst = top - 1 - j;
-        Splat g;
-        *reinterpret_cast<float4*>(&g) = sm[j][0];
-        *(reinterpret_cast<float4*>(&g) + 1) = sm[j][1];
-        *(reinterpret_cast<float4*>(&g) + 2) = sm[j][2];
-        float cv[9];
-#pragma unroll
-        for (int u = 0; u < 9; ++u) cv[u] = 0.f;
-        const bool h0 = bwd_pixel(g, px, py0, inst, s0, cv);
-        const bool h1 = bwd_pixel(g, px, py1, inst, s1, cv);
-        const bool hit = h0 || h1;
-        const unsigned bal = __ballot_sync(0xffffffffu, hit);
-        if (bal == 0) continue;
-        double* dst = g2 + (long long)kG2 * g.idx;
-        if (__popc(bal) <= 2) {
-          // one or two hitting lanes: their partials go straight to the
-          // fp64 accumulators (cheaper than a 32-lane reduction)
-          if (hit) {
-#pragma unroll
-            for (int u = 0; u < 9; ++u)
-              if (cv[u] != 0.f) atomicAdd(dst + u, double(cv[u]));
-          }
-          continue;
-        }
-        const float t8 = warp_reduce8(*reinterpret_cast<const float(*)[8]>(cv), ln);
-        const float s8 = warp_sum(cv[8]);
-        if ((ln & 3) == 0) {
-          if (t8 != 0.f) atomicAdd(dst + (ln >> 2), double(t8));
-        } else if (ln == 1) {
-          if (s8 != 0.f) atomicAdd(dst + 8, double(s8));
-        }
-      }
-    }
+    __syncwarp();
   }
 }
 
