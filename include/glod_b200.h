@@ -43,11 +43,13 @@ uint64_t glod_launch_count(void);
 typedef struct glod_lod_scene {
   int64_t capacity;             /* hierarchy node slots                       */
   int32_t root;                 /* Hierarchy.root                             */
-  int32_t _pad0;
+  int32_t attr_stride;          /* doubles between consecutive nodes' means /
+                                   scales: 0 or 3 = dense [capacity*3];
+                                   GLOD_NODE_RECORD = node records          */
   const int32_t* children;      /* [dev] [capacity*2], -1 = NONE              */
   const int32_t* kind;          /* [dev] [capacity]: spt_id>=0 | -2 pass | -1 */
-  const double* means;          /* [dev] [capacity*3] live f64 means          */
-  const double* scales;         /* [dev] [capacity*3] live f64 scales         */
+  const double* means;          /* [dev] live f64 means (see attr_stride)     */
+  const double* scales;         /* [dev] live f64 scales                      */
   int32_t num_spts;
   int32_t key_f64;              /* 1: f64 keys, 0: f32 keys (file scenes)     */
   int64_t num_records;          /* total SPT records                          */
@@ -207,6 +209,19 @@ int glod_loss_l1_ssim(const float* rendered, const float* target, int32_t width,
  * Optimiser (trainer._adam_update, trainer.py:253-299)
  * ======================================================================= */
 
+/* Node records: the training engine's master layout, one 576-B (18-sector)
+ * record per node, f64 [capacity][GLOD_NODE_RECORD]:
+ *   [0, 23)   attribute values (means 3 | scales 3 | rotations 4 | opacity |
+ *             base_colors 3 | sh_rest 9)
+ *   [24, 70)  ADAM moments, (m, v) per attribute value (16-B aligned pairs)
+ *   70        per-node step count (int64 bits)
+ *   23, 71    padding
+ * so one ADAM update reads and writes whole records, and the LoD kernels read
+ * means/scales at stride GLOD_NODE_RECORD (glod_lod_scene.attr_stride). */
+#define GLOD_NODE_RECORD 72
+#define GLOD_REC_MV 24
+#define GLOD_REC_STEP 70
+
 /* One ADAM step, in place, on params[ids] from grads[rows]
  * (trainer._adam_update, trainer.py:253-299).  params: [dev] packed f64
  * block of `capacity` rows (section-major, as h.attrs).  mv: [dev] the ADAM
@@ -226,6 +241,13 @@ int glod_adam_step(double* params, double* mv, int64_t* step, int64_t capacity,
                    const int32_t* ids, const double* grads, const int32_t* rows,
                    int64_t grad_rows, int64_t n, const double* lrs, const double* bias_table,
                    int64_t bias_len, const struct glod_gather_plan* refresh, void* stream);
+/* The same step on node records (GLOD_NODE_RECORD layout above): params,
+ * moments and step count of a node are one contiguous record; the step
+ * counts are incremented in the same launch. */
+int glod_adam_step_records(double* records, int64_t capacity, const int32_t* ids, const double* grads,
+                           const int32_t* rows, int64_t grad_rows, int64_t n, const double* lrs,
+                           const double* bias_table, int64_t bias_len,
+                           const struct glod_gather_plan* refresh, void* stream);
 
 /* ======================================================================= *
  * Store / cache data movement (trainer.py:325-364, store.py:304-333)
@@ -248,6 +270,8 @@ typedef struct glod_gather_plan {
   int64_t n_sel;
   const uint64_t* seg_block;    /* [dev] [n_spt] device address of each block */
   const int64_t* seg_rows;      /* [dev] [n_spt] rows (prefix_len) per block  */
+  int64_t master_stride;        /* 0: master is a packed section-major block;
+                                   GLOD_NODE_RECORD: node records            */
 } glod_gather_plan;
 
 /* AttributeArrays.concat of the render set into `out` (packed f64, R =
@@ -276,7 +300,8 @@ int glod_wire_pack(const double* master, int64_t capacity, const int32_t* ids, c
  * res_block/res_rows: [dev] per SPT id, the resident block and its rows
  * (0 if not resident; glod_cache_resident); touched: [dev] int32 per SPT id,
  * set to 1 for every block written (feed to glod_cache_mark_dirty). */
-int glod_refresh_resident_blocks(const double* master, int64_t capacity, const int32_t* ids, int64_t n,
+int glod_refresh_resident_blocks(const double* master, int64_t capacity, int64_t master_stride,
+                                 const int32_t* ids, int64_t n,
                                  const int32_t* spt_of_node, const int32_t* rec_of_node,
                                  const uint64_t* res_block, const int64_t* res_rows, int32_t* touched,
                                  void* stream);

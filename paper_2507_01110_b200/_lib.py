@@ -9,7 +9,11 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libglod_b200.so"
+import os
+
+# GLOD_LIB: an alternative build of the same library (kernel variants for
+# A/B timing runs); default: the in-tree build.
+LIB_PATH = Path(os.environ.get("GLOD_LIB") or Path(__file__).resolve().parent / "libglod_b200.so")
 
 GLOD_OK = 0
 GLOD_ERR_INVALID_ARGUMENT = 1
@@ -21,7 +25,7 @@ P = C.c_void_p
 
 
 class LodScene(C.Structure):
-    _fields_ = [("capacity", C.c_int64), ("root", C.c_int32), ("_pad0", C.c_int32),
+    _fields_ = [("capacity", C.c_int64), ("root", C.c_int32), ("attr_stride", C.c_int32),
                 ("children", P), ("kind", P), ("means", P), ("scales", P),
                 ("num_spts", C.c_int32), ("key_f64", C.c_int32), ("num_records", C.c_int64),
                 ("spt_offset", P), ("spt_count", P), ("spt_root_rec", P), ("spt_center", P),
@@ -73,7 +77,8 @@ class RenderStats(C.Structure):
 class GatherPlan(C.Structure):
     _fields_ = [("master", P), ("capacity", C.c_int64), ("upper_ids", P), ("pass_ids", P),
                 ("n_upper", C.c_int32), ("n_pass", C.c_int32), ("sel_seg", P), ("sel_pos", P),
-                ("sel_node", P), ("n_sel", C.c_int64), ("seg_block", P), ("seg_rows", P)]
+                ("sel_node", P), ("n_sel", C.c_int64), ("seg_block", P), ("seg_rows", P),
+                ("master_stride", C.c_int64)]
 
 
 class StoreView(C.Structure):
@@ -115,10 +120,12 @@ SIGNATURES = {
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
     "glod_adam_step": (C.c_int, [P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
                                  C.POINTER(C.c_double), P, C.c_int64, P, P]),
+    "glod_adam_step_records": (C.c_int, [P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
+                                         C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
     "glod_wire_pack": (C.c_int, [P, C.c_int64, P, P, C.c_int32, C.c_int64, P, P]),
-    "glod_refresh_resident_blocks": (C.c_int, [P, C.c_int64, P, C.c_int64, P, P, P, P, P, P]),
+    "glod_refresh_resident_blocks": (C.c_int, [P, C.c_int64, C.c_int64, P, C.c_int64, P, P, P, P, P, P]),
     "glod_cache_resident": (C.c_int, [P, P, P, C.c_int32]),
     "glod_cache_mark_dirty": (C.c_int, [P, P, C.c_int32]),
     "glod_convert": (C.c_int, [P, P, C.c_int64, C.c_int32, P]),

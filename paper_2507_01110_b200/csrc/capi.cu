@@ -19,12 +19,16 @@ cudaError_t launch_adam(double* params, double* mv, long long* step, long long c
                         const int* ids, const double* grads, const int* rows, long long grad_rows,
                         long long n, const double* lrs, const double* bias, long long bias_len,
                         const glod_gather_plan* plan, cudaStream_t st);
+cudaError_t launch_adam_records(double* rec, const int* ids, const double* grads, const int* rows,
+                                long long grad_rows, long long n, const double* lrs, const double* bias,
+                                long long bias_len, const glod_gather_plan* plan, cudaStream_t st);
 cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, int* row_node,
                           cudaStream_t st);
 cudaError_t launch_scatter_back(const glod_gather_plan& p, cudaStream_t st);
 cudaError_t launch_wire_pack(const double* master, long long cap, const int* ids, const long long* seg,
                              int n_msgs, long long N, float* out, cudaStream_t st);
-cudaError_t launch_refresh_resident(const double* master, long long cap, const int* ids, long long n,
+cudaError_t launch_refresh_resident(const double* master, long long cap, long long mstride, const int* ids,
+                                    long long n,
                                     const int* spt_of_node, const int* rec_of_node,
                                     const unsigned long long* res_block, const long long* res_rows, int* touched,
                                     cudaStream_t st);
@@ -195,6 +199,17 @@ int glod_adam_step(double* params, double* mv, int64_t* step, int64_t capacity,
                "glod_adam_step");
 }
 
+int glod_adam_step_records(double* records, int64_t capacity, const int32_t* ids, const double* grads,
+                           const int32_t* rows, int64_t grad_rows, int64_t n, const double* lrs,
+                           const double* bias_table, int64_t bias_len, const glod_gather_plan* refresh,
+                           void* stream) {
+  (void)capacity;
+  if (n > 0 && (!records || !ids || !grads || !lrs)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_adam_records(records, ids, grads, rows, grad_rows, n, lrs, bias_table, bias_len,
+                                         refresh, static_cast<cudaStream_t>(stream)),
+               "glod_adam_step_records");
+}
+
 int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* row_node,
                             void* stream) {
   if (!plan) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
@@ -213,13 +228,14 @@ int glod_wire_pack(const double* master, int64_t capacity, const int32_t* ids, c
                "glod_wire_pack");
 }
 
-int glod_refresh_resident_blocks(const double* master, int64_t capacity, const int32_t* ids, int64_t n,
+int glod_refresh_resident_blocks(const double* master, int64_t capacity, int64_t master_stride,
+                                 const int32_t* ids, int64_t n,
                                  const int32_t* spt_of_node, const int32_t* rec_of_node,
                                  const uint64_t* res_block, const int64_t* res_rows, int32_t* touched,
                                  void* stream) {
   if (n > 0 && (!master || !ids || !spt_of_node || !rec_of_node || !res_block || !res_rows || !touched))
     return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
-  return check(glod::launch_refresh_resident(master, capacity, ids, n, spt_of_node, rec_of_node,
+  return check(glod::launch_refresh_resident(master, capacity, master_stride, ids, n, spt_of_node, rec_of_node,
                                              reinterpret_cast<const unsigned long long*>(res_block),
                                              reinterpret_cast<const long long*>(res_rows), touched,
                                              static_cast<cudaStream_t>(stream)),

@@ -17,19 +17,29 @@ __constant__ int kSecCols[6] = {3, 3, 4, 1, 3, 9};
 
 struct Src {
   const double* base;
-  long long rows;
+  long long rows;       // section stride (section-major blocks), or -record stride
   long long idx;
 };
+
+// Element (section offset OFF, column col) of a source row: section-major
+// blocks/master (rows > 0) or node records (rows = -GLOD_NODE_RECORD).
+GLOD_DEV double src_at(const Src& s, int OFF, int COLS, int col) {
+  return s.rows > 0 ? s.base[OFF * s.rows + s.idx * COLS + col] : s.base[s.idx * (-s.rows) + OFF + col];
+}
+
+GLOD_DEV long long master_rows(const glod_gather_plan& p) {
+  return p.master_stride ? -p.master_stride : p.capacity;
+}
 
 GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
   const long long n_mem = (long long)p.n_upper + p.n_pass;
   Src s;
   if (r < p.n_upper) {
     node = p.upper_ids[r];
-    s = {p.master, p.capacity, node};
+    s = {p.master, master_rows(p), node};
   } else if (r < n_mem) {
     node = p.pass_ids[r - p.n_upper];
-    s = {p.master, p.capacity, node};
+    s = {p.master, master_rows(p), node};
   } else {
     const long long k = r - n_mem;
     const int j = p.sel_seg[k];
@@ -63,7 +73,7 @@ GLOD_DEV void gather_sec(const glod_gather_plan& p, unsigned R, double* __restri
       const unsigned r = local / COLS;
       const int col = int(local - r * COLS);
       const Src s = row_source(p, r, node[k]);
-      v[k] = s.base[OFF * s.rows + s.idx * COLS + col];
+      v[k] = src_at(s, int(OFF), COLS, col);
     }
   }
 #pragma unroll
@@ -101,7 +111,8 @@ __global__ void scatter_back_kernel(glod_gather_plan p, long long n_sel) {
 #pragma unroll
   for (int k = 1; k < 6; ++k) sec += lane >= kSecOff[k];
   const int col = lane - kSecOff[sec], cols = kSecCols[sec];
-  blk[kSecOff[sec] * P + pos * cols + col] = p.master[kSecOff[sec] * p.capacity + node * cols + col];
+  const Src m = {p.master, master_rows(p), node};
+  blk[kSecOff[sec] * P + pos * cols + col] = src_at(m, kSecOff[sec], cols, col);
 }
 
 __global__ void f32_to_f64_kernel(const float4* __restrict__ in, double4* __restrict__ out, long long n4) {
@@ -216,7 +227,7 @@ pack_f32_kernel(const glod_prefix_item* __restrict__ items, int n_items, long lo
 // entry.block.attrs.put(pos, h.attrs.take(node_ids)), trainer.py:363,
 // applied to the union).  One thread per (node, column); a touched SPT is
 // flagged so the host marks its entry dirty.
-__global__ void refresh_resident_kernel(const double* __restrict__ master, long long cap,
+__global__ void refresh_resident_kernel(const double* __restrict__ master, long long cap, long long mstride,
                                         const int* __restrict__ ids, long long n,
                                         const int* __restrict__ spt_of_node, const int* __restrict__ rec_of_node,
                                         const unsigned long long* __restrict__ res_block,
@@ -236,7 +247,8 @@ __global__ void refresh_resident_kernel(const double* __restrict__ master, long 
   for (int k = 1; k < 6; ++k) sec += col >= kSecOff[k];
   const int c = col - kSecOff[sec], cols = kSecCols[sec];
   double* blk = reinterpret_cast<double*>(res_block[s]);
-  blk[kSecOff[sec] * rows + pos * cols + c] = master[kSecOff[sec] * cap + id * cols + c];
+  const Src m = {master, mstride ? -mstride : cap, id};
+  blk[kSecOff[sec] * rows + pos * cols + c] = src_at(m, kSecOff[sec], cols, c);
   if (col == 0) touched[s] = 1;
 }
 
@@ -418,13 +430,14 @@ cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long lon
   return cudaGetLastError();
 }
 
-cudaError_t launch_refresh_resident(const double* master, long long cap, const int* ids, long long n,
+cudaError_t launch_refresh_resident(const double* master, long long cap, long long mstride, const int* ids,
+                                    long long n,
                                     const int* spt_of_node, const int* rec_of_node,
                                     const unsigned long long* res_block, const long long* res_rows, int* touched,
                                     cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   count_launch();
-  refresh_resident_kernel<<<unsigned((23 * n + 255) / 256), 256, 0, st>>>(master, cap, ids, n, spt_of_node,
+  refresh_resident_kernel<<<unsigned((23 * n + 255) / 256), 256, 0, st>>>(master, cap, mstride, ids, n, spt_of_node,
                                                                            rec_of_node, res_block, res_rows, touched);
   return cudaGetLastError();
 }

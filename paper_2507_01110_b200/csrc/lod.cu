@@ -184,8 +184,11 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
         const uint32_t e = ld_cg(cur + i);
         const int node = int(e & kIdMask);
         const bool pass = e & kPass, start = e & kStart;
-        const double mx = sc.means[3 * node], my = sc.means[3 * node + 1], mz = sc.means[3 * node + 2];
-        const double s0 = sc.scales[3 * node], s1 = sc.scales[3 * node + 1], s2 = sc.scales[3 * node + 2];
+        const long long as = sc.attr_stride ? sc.attr_stride : 3;
+        const double* mp = sc.means + as * node;
+        const double* sp = sc.scales + as * node;
+        const double mx = mp[0], my = mp[1], mz = mp[2];
+        const double s0 = sp[0], s1 = sp[1], s2 = sp[2];
         bool keep = true;
         if (v.cull) keep = sphere_in_frustum(planes, mx, my, mz, mul(3.0, max3(s0, s1, s2)), start);
         if (keep) {

@@ -16,6 +16,10 @@
 #include "common.cuh"
 #include "raster.cuh"
 
+#ifndef GLOD_DIRECT_LANES
+#define GLOD_DIRECT_LANES 2
+#endif
+
 namespace glod {
 
 size_t radix_scratch_bytes(long long n);
@@ -176,6 +180,9 @@ GLOD_DEV bool tile_hit(const Splat& g, int tx, int ty) {
 // skipping one changes none of its pixels.
 constexpr int kBlendWarps = 4;
 constexpr int kBlendTB = 32 * kBlendWarps;
+// backward: up to this many hitting lanes issue their own fp64 atomics
+// instead of a warp reduction
+constexpr int kDirectLanes = GLOD_DIRECT_LANES;
 // The forward keeps one pixel per lane (8 warps, 8x4 blocks): its per-pixel
 // state is a sequential fp64 chain, so it wants more warps in flight more
 // than it wants the shared per-splat cost halved.
@@ -483,7 +490,8 @@ struct BwdPix {
 
 GLOD_DEV bool bwd_pixel(const Splat& g, int px, int py, int inst, BwdPix& s, float (&cv)[9]) {
   float dx, dy, q, gs, al;
-  if (!(s.inside && inst <= s.last && pixel_alpha(g, px, py, dx, dy, q, gs, al))) return false;
+  // outside pixels keep last = -1, so `inst <= s.last` also gates them
+  if (!(inst <= s.last && pixel_alpha(g, px, py, dx, dy, q, gs, al))) return false;
   float inv;                                           // 1/(1-α), 1-α ≥ 0.01: approx rcp
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.f - al));
   const float Tf = s.T * inv;                          // T before this splat
@@ -569,8 +577,8 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (bal == 0) continue;
       double* dst = g2 + (long long)kG2 * g.idx;
-      if (__popc(bal) <= 2) {
-        // one or two hitting lanes: their partials go straight to the
+      if (__popc(bal) <= kDirectLanes) {
+        // a few hitting lanes: their partials go straight to the
         // fp64 accumulators (cheaper than a 32-lane reduction)
         if (hit) {
 #pragma unroll

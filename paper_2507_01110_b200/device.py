@@ -98,10 +98,11 @@ class DeviceLodScene:
 
     def __init__(self, h: Hierarchy, hspt=None, means: torch.Tensor | None = None,
                  scales: torch.Tensor | None = None, root: int | None = None,
-                 force_f64_keys: bool = False):
+                 force_f64_keys: bool = False, attr_stride: int = 0):
         dev = _dev()
         self.device = dev
         self.cap = h.capacity
+        self.attr_stride = int(attr_stride)   # 0: dense [cap, 3]; else node records
         self.root = int(h.root if root is None else root)
         self.children = _t(h.children.reshape(-1), torch.int32, dev)
         kind = np.full(self.cap, -1, dtype=np.int32)
@@ -170,7 +171,7 @@ class DeviceLodScene:
     def _make_struct(self) -> _lib.LodScene:
         p = _lib.ptr
         return _lib.LodScene(
-            capacity=self.cap, root=self.root, _pad0=0, children=p(self.children), kind=p(self.kind),
+            capacity=self.cap, root=self.root, attr_stride=self.attr_stride, children=p(self.children), kind=p(self.kind),
             means=p(self.means), scales=p(self.scales), num_spts=self.S, key_f64=int(self.key_f64),
             num_records=self.R, spt_offset=p(self.spt_offset), spt_count=p(self.spt_count),
             spt_root_rec=p(self.spt_root_rec), spt_center=p(self.spt_center),

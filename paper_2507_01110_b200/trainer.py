@@ -81,25 +81,56 @@ def _packed(t: torch.Tensor, rows: int, name: str) -> torch.Tensor:
     raise KeyError(name)
 
 
+NODE_RECORD, REC_MV, REC_STEP = 72, 24, 70     # glod_b200.h GLOD_NODE_RECORD layout
+
+
 class DeviceScene:
-    """Master params + ADAM state + LoD tables + host store for one HSPT."""
+    """Master params + ADAM state + LoD tables + host store for one HSPT.
+
+    The master state is one 576-B node record per node (GLOD_NODE_RECORD,
+    glod_b200.h): 23 attribute values, 23 (m, v) moment pairs and the step
+    count, so ADAM moves whole records.  `params`, `mv` and `step` give the
+    reference-shaped views (packed section-major params, [cap][23][m, v]
+    moments, int64 steps)."""
 
     def __init__(self, h, hspt, device=None, store_location: str = "host"):
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.cap = h.capacity
-        self.params = torch.from_numpy(h.attrs.packed(np.float64)).to(dev)
-        # ADAM moments, row-major interleaved [cap][23][m, v] (glod_adam_step)
-        self.mv = torch.zeros(self.cap * FLOATS_PER_GAUSSIAN * 2, dtype=torch.float64, device=dev)
-        self.step = torch.zeros(self.cap, dtype=torch.int64, device=dev)
-        self.lod = DeviceLodScene(h, hspt, means=_packed(self.params, self.cap, "means"),
-                                  scales=_packed(self.params, self.cap, "scales"))
+        # records assembled on the device one section at a time (no host copy
+        # of the 576-B/node table: 69 GB at C5)
+        self.records = torch.zeros((self.cap, NODE_RECORD), dtype=torch.float64, device=dev)
+        off = 0
+        for name, cols in SECTIONS:
+            a = np.ascontiguousarray(getattr(h.attrs, name), dtype=np.float64).reshape(self.cap, cols)
+            self.records[:, off:off + cols] = torch.from_numpy(a).to(dev)
+            off += cols
+        self.lod = DeviceLodScene(h, hspt, means=self.records.view(-1), scales=self.records.view(-1)[3:],
+                                  attr_stride=NODE_RECORD)
         self.store = HostStore(h, hspt, location=store_location)
         self.hspt = hspt
 
+    @property
+    def params(self) -> torch.Tensor:
+        """Packed section-major copy of the attribute values (h.attrs layout)."""
+        parts, off = [], 0
+        for _, cols in SECTIONS:
+            parts.append(self.records[:, off:off + cols].reshape(-1))
+            off += cols
+        return torch.cat(parts)
+
+    @property
+    def mv(self) -> torch.Tensor:
+        """ADAM moments [cap][23][m, v] (a copy)."""
+        return self.records[:, REC_MV:REC_MV + 2 * FLOATS_PER_GAUSSIAN].reshape(-1)
+
+    @property
+    def step(self) -> torch.Tensor:
+        return self.records.view(torch.int64)[:, REC_STEP].contiguous()
+
     def moments_packed(self):
         """(m, v) as packed section-major f64 blocks (the h.attrs layout)."""
-        mv = self.mv.view(self.cap, FLOATS_PER_GAUSSIAN, 2)
+        mv = self.records[:, REC_MV:REC_MV + 2 * FLOATS_PER_GAUSSIAN].reshape(self.cap, FLOATS_PER_GAUSSIAN, 2)
         out = []
         for k in range(2):
             x = mv[:, :, k]
@@ -249,7 +280,8 @@ class Trainer:
         self._d_res.copy_(self._h_res, non_blocking=True)
         self._d_touched.zero_()
         _lib.check(_lib.lib().glod_refresh_resident_blocks(
-            _lib.ptr(sc.params), sc.cap, _lib.ptr(ids), int(ids.numel()), _lib.ptr(self._spt_of_node),
+            _lib.ptr(sc.records), sc.cap, NODE_RECORD, _lib.ptr(ids), int(ids.numel()),
+            _lib.ptr(self._spt_of_node),
             _lib.ptr(self._rec_of_node), _lib.ptr(self._d_res), _lib.ptr(self._d_res[S1:]),
             _lib.ptr(self._d_touched), _lib.stream_ptr()))
         _lib.readback(self._h_touched, self._d_touched)
@@ -331,10 +363,11 @@ class Trainer:
         rows = self._ensure("_rows", FLOATS_PER_GAUSSIAN * R, torch.float64)[:FLOATS_PER_GAUSSIAN * R]
         row_node = self._ensure("_row_node", R, torch.int32)[:max(R, 1)]
         plan = _lib.GatherPlan(
-            master=_lib.ptr(sc.params), capacity=sc.cap, upper_ids=_lib.ptr(sel.upper),
+            master=_lib.ptr(sc.records), capacity=sc.cap, upper_ids=_lib.ptr(sel.upper),
             pass_ids=_lib.ptr(sel.passthrough), n_upper=n_up, n_pass=n_pa,
             sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
-            n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]))
+            n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]),
+            master_stride=NODE_RECORD)
         _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
                                                       _lib.stream_ptr()))
         self._mark("gather")
@@ -413,15 +446,14 @@ class Trainer:
             U, GU = sparse_grad_allreduce(row_node[:R], grads, R, self.group)
             ids = U.to(torch.int32)
             nU = int(ids.numel())
-            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),
-                                        _lib.ptr(sc.step), sc.cap, _lib.ptr(ids), _lib.ptr(GU), None,
-                                        nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
+            _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(ids), _lib.ptr(GU),
+                                                None, nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
             self._refresh_union(ids)
             self._last_union = (ids, GU)
         else:
-            _lib.check(L.glod_adam_step(_lib.ptr(sc.params), _lib.ptr(sc.mv),
-                                        _lib.ptr(sc.step), sc.cap, _lib.ptr(row_node), _lib.ptr(grads),
-                                        None, R, R, self.lrs, _lib.ptr(bias), blen, C.byref(plan), st))
+            _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(row_node),
+                                                _lib.ptr(grads), None, R, R, self.lrs, _lib.ptr(bias), blen,
+                                                C.byref(plan), st))
         self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
         if self._pred is not None:
