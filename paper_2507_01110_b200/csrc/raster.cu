@@ -16,6 +16,12 @@
 #include "common.cuh"
 #include "raster.cuh"
 
+#ifndef GLOD_PRE_MINB
+#define GLOD_PRE_MINB 3     // ≤ 80 registers: more warps to hide the fp64 latency
+#endif
+#ifndef GLOD_PBWD_MINB
+#define GLOD_PBWD_MINB 4
+#endif
 #ifndef GLOD_DIRECT_LANES
 #define GLOD_DIRECT_LANES 2
 #endif
@@ -254,7 +260,7 @@ GLOD_DEV int preprocess_one(const double* __restrict__ attrs, long long n, long 
 // K5 over all Gaussians.  Also reduces, for the one host read-back of the
 // forward pass, stats = {Σ tile instances, min key, max key} over the
 // contributing splats (the depth sort only needs the bits where they differ).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, GLOD_PRE_MINB)
 preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat* __restrict__ splats,
                   unsigned long long* __restrict__ keys, int* __restrict__ vals, int* __restrict__ tiles,
                   int* __restrict__ bad, unsigned long long* __restrict__ stats) {
@@ -600,7 +606,7 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
 }
 
 // K9: 2D partials → gradients of the raw attributes (renderer.py:262-303).
-__global__ void __launch_bounds__(128, 4) preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
+__global__ void __launch_bounds__(128, GLOD_PBWD_MINB) preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
                                       const int* __restrict__ tiles_of, const double* __restrict__ g2,
                                       double* __restrict__ grads) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -93,7 +93,7 @@ class DeviceScene:
     reference-shaped views (packed section-major params, [cap][23][m, v]
     moments, int64 steps)."""
 
-    def __init__(self, h, hspt, device=None, store_location: str = "host"):
+    def __init__(self, h, hspt, device=None, store_location: str = "host", store: HostStore | None = None):
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.cap = h.capacity
@@ -107,7 +107,9 @@ class DeviceScene:
             off += cols
         self.lod = DeviceLodScene(h, hspt, means=self.records.view(-1), scales=self.records.view(-1)[3:],
                                   attr_stride=NODE_RECORD)
-        self.store = HostStore(h, hspt, location=store_location)
+        # a prebuilt store (e.g. scenefile.Scene.host_store: sections read from
+        # a .glod file straight into pinned memory) or one built from h.attrs
+        self.store = store if store is not None else HostStore(h, hspt, location=store_location)
         self.hspt = hspt
 
     @property
@@ -150,7 +152,7 @@ class Trainer:
     with targets (h, w, 3) float images (numpy or pinned torch)."""
 
     def __init__(self, h, hspt, views, cfg: TrainConfig, extent: float, device_targets: bool = True,
-                 group=None):
+                 group=None, store=None):
         import torch.distributed as dist
         self.cfg = cfg
         # view sharding: with an initialised process group of >1 ranks each
@@ -159,7 +161,7 @@ class Trainer:
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized() and \
             dist.get_world_size(group) > 1
-        self.scene = DeviceScene(h, hspt, store_location=cfg.store_location)
+        self.scene = DeviceScene(h, hspt, store_location=cfg.store_location, store=store)
         dev = self.scene.device
         self.cache = NativeCache(cfg.cache, self.scene.store)
         self.rast = Rasterizer()

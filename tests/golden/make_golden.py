@@ -452,6 +452,42 @@ def make_serve_cases():
     np.savez_compressed(OUT / "serve_cases.npz", **d)
 
 
+def make_scenefile_cases():
+    """write_scene bytes (store.py:157-234) and what open_scene reads back
+    (read_hierarchy / read_hspt / load_spt_prefix, store.py:304-393)."""
+    from glod.store import MemoryBacking, open_scene, write_scene
+    rng = np.random.default_rng(4242)
+    d = {}
+    for case in range(3):
+        n = int([150, 600, 1200][case])
+        h = build_hierarchy(random_leaves(rng, n))
+        h.attrs.sh_rest = rng.normal(0, 0.1, h.attrs.sh_rest.shape)
+        h.attrs.scales = rng.uniform(0.05, 2.0, h.attrs.scales.shape)
+        thr = float(np.quantile(np.prod(h.attrs.scales, axis=1), 0.5))
+        lod = LodConfig(threshold=float(rng.uniform(1.0, 20.0)), metric=("max_scale", "surface_area")[case % 2])
+        hspt = build_hspt(h, thr, [4, 8, 16][case], lod)
+        mb = MemoryBacking()
+        write_scene(h, hspt, mb)
+        p = f"c{case}_"
+        d.update({p + k: v for k, v in hier_arrays(h).items()})
+        d.update({p + k: v for k, v in hspt_arrays(hspt).items()})
+        d[p + "file"] = np.frombuffer(mb.tobytes(), dtype=np.uint8)
+        sc = open_scene(MemoryBacking(mb.tobytes()))
+        h2, hs2 = sc.read_hierarchy(), sc.read_hspt()
+        d.update({p + "rd_" + k: v for k, v in hier_arrays(h2).items()})
+        d.update({p + "rd_" + k: v for k, v in hspt_arrays(hs2).items()})
+        sid = len(hs2.spts) // 2
+        blk = sc.load_spt_prefix(sid, hs2.spts[sid].subtree_size // 2)
+        d[p + "pf_spt"] = np.int64(sid)
+        d[p + "pf_len"] = np.int64(blk.prefix_len)
+        d[p + "pf_means"] = blk.attrs.means
+        d[p + "pf_sh"] = blk.attrs.sh_rest
+        d[p + "pf_slot"] = np.int64(sc.spt_slot_start(sid))
+        d[p + "bytes_read"] = np.int64(sc.attribute_bytes_read)
+    d["n_cases"] = np.int64(3)
+    np.savez_compressed(OUT / "scenefile_cases.npz", **d)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -460,3 +496,4 @@ if __name__ == "__main__":
     make_scheduler_cases()
     make_cache_cases()
     make_serve_cases()
+    make_scenefile_cases()
