@@ -30,6 +30,7 @@ from .core import BYTES_PER_GAUSSIAN_F32, FLOATS_PER_GAUSSIAN, SECTIONS, Attribu
 from .device import DeviceLodScene
 from .renderer import Rasterizer
 from .scheduler import DEFAULT_K, DEFAULT_RANDOM_EVERY, build_view_graph, next_view
+from .hierarchy import Hierarchy
 from .store import HostStore
 
 DEFAULT_LEARNING_RATES = {
@@ -65,6 +66,10 @@ class TrainConfig:
     # where the f32 scene store lives: "host" (pinned DRAM, out-of-core) or
     # "device" (HBM, config C2 — fully device-resident)
     store_location: str = "host"
+    # densification schedule (trainer.py:68-70)
+    densify_interval: int = 500
+    dead_opacity_threshold: float = 0.005
+    spawns_per_densify: int | None = None   # None -> 0.5% of leaf count
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -161,6 +166,7 @@ class Trainer:
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized() and \
             dist.get_world_size(group) > 1
+        self.hierarchy = Hierarchy.from_any(h)        # host topology (attrs live on the device)
         self.scene = DeviceScene(h, hspt, store_location=cfg.store_location, store=store)
         dev = self.scene.device
         self.cache = NativeCache(cfg.cache, self.scene.store)
@@ -183,15 +189,7 @@ class Trainer:
             tt = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
             tt = tt.to(torch.float32)
             self.targets.append(tt.to(dev) if device_targets else tt.pin_memory())
-        S1 = max(self.scene.lod.S, 1)
-        self._h_sel = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()   # counts | ids | prefix
-        self._h_droot = torch.empty(S1, dtype=torch.float64).pin_memory()
-        self._h_dist = torch.empty(S1, dtype=torch.float64).pin_memory()
-        self._h_blk = torch.empty(2 * S1, dtype=torch.int64).pin_memory()       # ptr | rows
-        self._d_dist = torch.empty(S1, dtype=torch.float64, device=dev)
-        self._d_blk = torch.empty(2 * S1, dtype=torch.int64, device=dev)
-        self._h_pref = torch.empty(S1, dtype=torch.int32).pin_memory()
-        self._d_pref = torch.empty(S1, dtype=torch.int32, device=dev)
+        self._scene_buffers()
         self._h_total = torch.empty(2, dtype=torch.int64).pin_memory()
         self._h_loss = torch.empty(3, dtype=torch.float64).pin_memory()
         self._rows = None
@@ -201,15 +199,92 @@ class Trainer:
         self._bias_len = 0
         self._target_dev = None
         self.last_stats = {}
+        self._pf_rows_cap = cfg.cache.budget_bytes // BYTES_PER_GAUSSIAN_F32
+        self.timing = None          # {stage: [ms, ...]} when profiling is on
+        self._ev = []
+
+    def _scene_buffers(self):
+        """Per-HSPT host/device tables (rebuilt after densification)."""
+        dev = self.scene.device
+        S1 = max(self.scene.lod.S, 1)
+        self._h_sel = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()   # counts | ids | prefix
+        self._h_droot = torch.empty(S1, dtype=torch.float64).pin_memory()
+        self._h_dist = torch.empty(S1, dtype=torch.float64).pin_memory()
+        self._h_blk = torch.empty(2 * S1, dtype=torch.int64).pin_memory()       # ptr | rows
+        self._d_dist = torch.empty(S1, dtype=torch.float64, device=dev)
+        self._d_blk = torch.empty(2 * S1, dtype=torch.int64, device=dev)
+        self._h_pref = torch.empty(S1, dtype=torch.int32).pin_memory()
+        self._d_pref = torch.empty(S1, dtype=torch.int32, device=dev)
         # prefetch: last selection per view (host) and the predicted next view
         self._hist = {}
         self._next_view = None
         self._pred = None
-        self._pf_rows_cap = cfg.cache.budget_bytes // BYTES_PER_GAUSSIAN_F32
+        self._spec = None
         self._h_sel2 = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()
         self._h_droot2 = torch.empty(S1, dtype=torch.float64).pin_memory()
-        self.timing = None          # {stage: [ms, ...]} when profiling is on
-        self._ev = []
+        self._spt_of_node = None
+
+    def train(self, metrics_out=None) -> list:
+        """trainer.train (trainer.py:446-458): train_step for every iteration
+        up to cfg.total_iterations, densify every densify_interval."""
+        import json
+        records = []
+        for it in range(self.iteration + 1, self.cfg.total_iterations + 1):
+            rec = self.train_step(it)
+            if it % self.cfg.densify_interval == 0 and it < self.cfg.total_iterations:
+                rec.update(self.densify(self.cfg.dead_opacity_threshold, self.cfg.spawns_per_densify))
+            records.append(rec)
+            if metrics_out is not None:
+                metrics_out.write(json.dumps(rec) + "\n")
+        return records
+
+    # -- densification (trainer.densify, trainer.py:411-443) -------------------
+    def densify(self, dead_opacity_threshold: float = 0.005, spawns_per_densify: int | None = None) -> dict:
+        """Respawn dead leaves, spawn opacity-sampled leaves (host tree
+        surgery, densify.py, on the scheduler RNG like the reference), zero
+        the new nodes' moments, rebuild the HSPT on the device with the
+        surface-area metric (hspt.py:161-165) and re-lay the store and the
+        node records out for it (_sync_scene, trainer.py:395-408: the store
+        is rewritten from the authoritative master values, the cache starts
+        empty, byte counters survive)."""
+        from .densify import Moments, densify_tree
+        from .hspt import build_hspt
+        torch.cuda.synchronize()
+        sc, h = self.scene, self.hierarchy
+        rec = sc.records.cpu().numpy()
+        F = FLOATS_PER_GAUSSIAN
+
+        def unpack(cols_of_rec):
+            parts, off = [], 0
+            for _, c in SECTIONS:
+                parts.append(cols_of_rec[:, off:off + c] if c > 1 else cols_of_rec[:, off].copy())
+                off += c
+            return AttributeArrays(*[np.ascontiguousarray(p) for p in parts])
+
+        h.attrs = unpack(rec[:, :F])
+        mv = rec[:, REC_MV:REC_MV + 2 * F].reshape(-1, F, 2)
+        opt = Moments(unpack(mv[:, :, 0]), unpack(mv[:, :, 1]), rec.view(np.int64)[:, REC_STEP].copy())
+        del rec, mv
+        out = densify_tree(h, opt, self.rng, dead_opacity_threshold, spawns_per_densify)
+        old = sc.hspt
+        hs = build_hspt(h, old.size_threshold, old.min_subtree, LodConfig(old.lod.threshold, "surface_area"))
+        consumed = sc.store.attribute_bytes_read
+        location = sc.store.location
+        self.cache = None
+        self.scene = None
+        sc = None
+        torch.cuda.empty_cache()
+        self.scene = DeviceScene(h, hs, store_location=location)
+        self.scene.store.attribute_bytes_read = consumed
+        recs = self.scene.records
+        for k, blk in enumerate((opt.m, opt.v)):
+            cols = np.concatenate([np.asarray(a, dtype=np.float64).reshape(h.capacity, -1) for _, a in blk.arrays()],
+                                  axis=1)
+            recs[:, REC_MV + k:REC_MV + 2 * F:2] = torch.from_numpy(cols).to(recs.device)
+        recs.view(torch.int64)[:, REC_STEP] = torch.from_numpy(opt.step).to(recs.device)
+        self.cache = NativeCache(self.cfg.cache, self.scene.store)
+        self._scene_buffers()
+        return out
 
     # -- optional per-stage CUDA-event timing (bench.py) ---------------------
     def enable_timing(self, on: bool = True):

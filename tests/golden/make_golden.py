@@ -488,6 +488,64 @@ def make_scenefile_cases():
     np.savez_compressed(OUT / "scenefile_cases.npz", **d)
 
 
+def make_densify_cases():
+    """trainer.densify (trainer.py:411-443) on reference TrainStates: dead
+    leaves respawned, opacity-sampled spawns, moments reset/grown, the HSPT
+    rebuilt with the surface-area metric; plus the RNG's next draw."""
+    from glod.cache import DeviceCache
+    from glod.store import MemoryBacking, open_scene, write_scene
+    from glod.trainer import OptimizerState, TrainConfig, TrainState, densify
+    rng = np.random.default_rng(99)
+    d = {}
+    for case in range(3):
+        n = int([200, 700, 1500][case])
+        h = build_hierarchy(random_leaves(rng, n))
+        h.attrs.sh_rest = rng.normal(0, 0.1, h.attrs.sh_rest.shape)
+        h.attrs.scales = rng.uniform(0.05, 2.0, h.attrs.scales.shape)
+        leaves = h.leaf_ids
+        dead = rng.choice(leaves, size=max(2, n // 25), replace=False)
+        h.attrs.opacities[dead] = rng.uniform(0.0, 0.004, dead.size)
+        thr = float(np.quantile(np.prod(h.attrs.scales, axis=1), 0.5))
+        lod = LodConfig(threshold=float(rng.uniform(1.0, 20.0)), metric="max_scale")
+        hspt = build_hspt(h, thr, [4, 8, 16][case], lod)
+        mb = MemoryBacking()
+        write_scene(h, hspt, mb)
+        opt = OptimizerState.zeros(h.attrs)
+        for k in opt.m:
+            opt.m[k] = rng.normal(0, 1e-3, opt.m[k].shape)
+            opt.v[k] = rng.uniform(0, 1e-5, opt.v[k].shape)
+        opt.step = rng.integers(0, 50, h.capacity).astype(np.int64)
+        spawns = [None, 7, 0][case]
+        cfg = TrainConfig(total_iterations=1000, spawns_per_densify=spawns)
+        p = f"c{case}_"
+        # copies: densify mutates the hierarchy's arrays in place
+        d.update({p + k: np.array(v, copy=True) for k, v in hier_arrays(h).items()})
+        d.update({p + k: np.array(v, copy=True) for k, v in hspt_arrays(hspt).items()})
+        for k in opt.m:
+            d[p + "m_" + k] = opt.m[k].copy()
+            d[p + "v_" + k] = opt.v[k].copy()
+        d[p + "step"] = opt.step.copy()
+        d[p + "seed"] = np.int64(1000 + case)
+        d[p + "spawns"] = np.int64(-1 if spawns is None else spawns)
+        state = TrainState(config=cfg, hierarchy=h, hspt=hspt, scene=open_scene(mb),
+                           cache=DeviceCache(config=cfg.cache), graph=None, views=[], opt=opt,
+                           rng=np.random.default_rng(1000 + case), extent=1.0,
+                           skybox_ids=np.zeros(0, dtype=np.int64))
+        out = densify(state)
+        d[p + "out_spawned"] = np.int64(out["spawned"])
+        d[p + "out_respawned"] = np.int64(out["respawned"])
+        d.update({p + "out_" + k: v for k, v in hier_arrays(state.hierarchy).items()})
+        d[p + "out_free"] = np.array(state.hierarchy.free, dtype=np.int64)
+        d.update({p + "out_" + k: v for k, v in hspt_arrays(state.hspt).items()})
+        for k in state.opt.m:
+            d[p + "out_m_" + k] = state.opt.m[k]
+            d[p + "out_v_" + k] = state.opt.v[k]
+        d[p + "out_step"] = state.opt.step
+        d[p + "out_next_draw"] = np.float64(state.rng.random())
+    d["n_cases"] = np.int64(3)
+    np.savez_compressed(OUT / "densify_cases.npz", **d)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -497,3 +555,4 @@ if __name__ == "__main__":
     make_cache_cases()
     make_serve_cases()
     make_scenefile_cases()
+    make_densify_cases()
