@@ -300,6 +300,36 @@ preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat
   }
 }
 
+// Top-bits depth sort fix-up: within each run of keys whose bits
+// [begin_bit, end_bit) tie, the radix passes kept index order; the run's head
+// thread insertion-sorts it by the full 64-bit key (stable, so equal depths
+// stay in index order).  Runs are short (mostly 2); equal keys cost O(run).
+constexpr int kDepthBits = 32;
+
+__global__ void fixup_runs_kernel(unsigned long long* __restrict__ keys, int* __restrict__ vals, long long n,
+                                  int begin_bit, int end_bit) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long m = ((end_bit - begin_bit) >= 64 ? ~0ull : ((1ull << (end_bit - begin_bit)) - 1)) << begin_bit;
+  if (keys[i] == ~0ull) return;            // non-contributing splats (no instances): order irrelevant
+  const unsigned long long top = keys[i] & m;
+  if (i > 0 && (keys[i - 1] & m) == top) return;          // not a run head
+  long long j = i + 1;
+  while (j < n && (keys[j] & m) == top) ++j;
+  for (long long a = i + 1; a < j; ++a) {
+    const unsigned long long k = keys[a];
+    const int v = vals[a];
+    long long b = a - 1;
+    while (b >= i && keys[b] > k) {
+      keys[b + 1] = keys[b];
+      vals[b + 1] = vals[b];
+      --b;
+    }
+    keys[b + 1] = k;
+    vals[b + 1] = v;
+  }
+}
+
 __global__ void gather_kernel(const int* __restrict__ order, const Splat* __restrict__ splats,
                               const int* __restrict__ tiles, Splat* __restrict__ sorted,
                               int* __restrict__ tiles_sorted, long long n) {
@@ -914,12 +944,23 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   int end_bit = 0;
   if (n_inst > 0 && hs[1] != hs[2]) end_bit = 64 - __builtin_clzll(hs[1] ^ hs[2]);
   CK(R->temp.ensure(std::max(radix_scratch_bytes(n), scan_scratch_bytes(n + 1)), st));
+  // Radix passes only over the top kDepthBits of that range (4 passes instead
+  // of ~7); keys whose top bits tie (depths within ~2^-kDepthBits of the
+  // range — a few thousand pairs per view) are put in full (depth, index)
+  // order by the run fix-up, so the result is the exact lexsort order.
+  const int begin_bit = end_bit > kDepthBits ? end_bit - kDepthBits : 0;
   int alt = 0;
   if (end_bit > 0)
     CK(radix_sort_pairs<unsigned long long>(R->keys.as<unsigned long long>(), R->keys2.as<unsigned long long>(),
-                                            R->vals.as<int>(), R->vals2.as<int>(), n, 0, end_bit, R->temp.p,
+                                            R->vals.as<int>(), R->vals2.as<int>(), n, begin_bit, end_bit, R->temp.p,
                                             R->temp.cap, false, &alt, st));
   const int* order = alt ? R->vals2.as<int>() : R->vals.as<int>();
+  if (begin_bit > 0) {
+    count_launch();
+    fixup_runs_kernel<<<nb, TB, 0, st>>>(alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>(),
+                                         const_cast<int*>(order), n, begin_bit, end_bit);
+    CK(cudaGetLastError());
+  }
   count_launch();
   gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
                                    R->tiles_sorted.as<int>(), n);

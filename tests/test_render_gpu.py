@@ -136,3 +136,30 @@ def test_adam_golden():
                 want = d[f"it{it}_{tag}_{k}"].reshape(n, cols)
                 np.testing.assert_allclose(mv[:, off:off + cols, j], want, rtol=1e-12, atol=1e-300)
             off += cols
+
+
+def test_depth_order_exact_with_near_ties():
+    """The depth sort radix-sorts only the top 32 bits of the key range and
+    fixes up runs that tie there: opaque splats at depths 1e-12 apart (a
+    tie in the top bits), exactly equal depths (index order decides) and a
+    far splat widening the range must composite exactly as the reference's
+    lexsort((idx, depth)) order — image equal to the oracle's."""
+    from oracle.glod_oracle import Cam
+    from paper_2507_01110_b200.core import Camera
+    cam = Camera(position=np.zeros(3), orientation=np.array([1.0, 0.0, 0.0, 0.0]), focal=(40.0, 40.0),
+                 principal_point=(16.0, 16.0), resolution=(32, 32))
+    rng = np.random.default_rng(3)
+    depths = [10.0, 10.0 + 1e-12, 10.0 + 2e-12, 10.0, 10.0 - 1e-13, 25.0, 25.0, 1000.0]
+    n = len(depths) * 4
+    a = AttributeArrays.zeros(n)
+    for k in range(n):
+        z = depths[k % len(depths)] + (k // len(depths)) * 3e-13
+        a.means[k] = [rng.uniform(-0.2, 0.2) * z / 10, rng.uniform(-0.2, 0.2) * z / 10, z]
+    a.scales[:] = 0.3
+    a.scales[:, 2] = 0.05
+    a.rotations[:, 0] = 1.0
+    a.opacities[:] = 0.97
+    a.base_colors[:] = rng.uniform(0, 1, (n, 3))
+    img = Rn.render(a, cam)
+    want, _ = O.render_forward({k: getattr(a, k) for k in NAMES}, Cam.of(cam))
+    assert np.abs(img - want).max() <= IMG_TOL

@@ -31,6 +31,15 @@ from .test_render_gpu import assert_grads_close  # noqa: E402
 NAMES = [n for n, _ in SECTIONS]
 
 
+
+def same_state(a, b):
+    """Equal state across two runs of the same steps.  The backward blend
+    accumulates per-Gaussian partials with fp64 atomics whose order is not
+    fixed, so a sum that is not exact in fp64 may round differently between
+    runs (last-bit differences); everything else is deterministic."""
+    a, b = a.double(), b.double()
+    return torch.equal(a, b) or torch.allclose(a, b, rtol=1e-10, atol=1e-14)
+
 def _dict(a: AttributeArrays):
     return {k: np.array(getattr(a, k), copy=True) for k in NAMES}
 
@@ -149,15 +158,16 @@ def test_prefetch_is_invisible():
     torch.cuda.synchronize()
     st = a.cache.stats()
     assert st["prefetch_used_rows"] > 0 and b.cache.stats()["prefetched_rows"] == 0
-    assert torch.equal(a.scene.params, b.scene.params)
-    assert torch.equal(a.scene.mv, b.scene.mv)
+    assert same_state(a.scene.params, b.scene.params)
+    assert same_state(a.scene.mv, b.scene.mv)
     assert torch.equal(a.scene.step, b.scene.step)
     for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
-        assert torch.equal(sa, sb)
+        assert same_state(sa, sb)
     ea, eb = a.cache.entries(), b.cache.entries()
     assert [e[:3] + e[4:] for e in ea] == [e[:3] + e[4:] for e in eb]
     for x, y in zip(ea, eb):
-        assert np.array_equal(a.cache.read_block(x[3], x[2]), b.cache.read_block(y[3], y[2]))
+        ba, bb = a.cache.read_block(x[3], x[2]), b.cache.read_block(y[3], y[2])
+        assert np.array_equal(ba, bb) or np.allclose(ba, bb, rtol=1e-10, atol=1e-14)
 
 
 def test_device_store_matches_host_store():
@@ -168,9 +178,9 @@ def test_device_store_matches_host_store():
     for it in range(1, 11):
         assert a.train_step(it) == b.train_step(it), it
     torch.cuda.synchronize()
-    assert torch.equal(a.scene.params, b.scene.params)
+    assert same_state(a.scene.params, b.scene.params)
     for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
-        assert torch.equal(sa, sb.cpu())
+        assert same_state(sa, sb.cpu())
 
 
 def test_empty_view_trains():
@@ -202,4 +212,4 @@ def test_host_targets_match_device_targets():
     for it in range(1, 13):
         assert a.train_step(it) == b.train_step(it), it
     torch.cuda.synchronize()
-    assert torch.equal(a.scene.params, b.scene.params)
+    assert same_state(a.scene.params, b.scene.params)
