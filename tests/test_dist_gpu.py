@@ -87,3 +87,46 @@ def test_union_refresh_updates_resident_blocks():
     assert tr._h_touched.numpy()[sid] == 1
     tr.cache.mark_dirty(tr._h_touched.numpy())
     assert [e for e in tr.cache.entries() if e[0] == sid][0][4]
+
+
+def _two_rank_worker(rank, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2507_01110_b200.parallel import union_of_rows
+        tr, _, _ = make_case()
+        tr.rng = np.random.default_rng(100 + rank)      # each rank walks its own views
+        assert tr.distributed
+        unions = []
+        for it in range(1, 6):
+            rec = tr.train_step(it)
+            assert np.isfinite(rec["loss"])
+            ids, GU = tr._last_union
+            unions.append(int(ids.numel()))
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, f"params{rank}.npy"), tr.scene.records.cpu().numpy())
+        np.save(os.path.join(out_dir, f"unions{rank}.npy"), np.array(unions))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_view_sharded_training(tmp_path):
+    """Two ranks (two processes sharing this GPU, gloo transport) train
+    different views with the union gradient exchange: after every step the
+    replicated ADAM leaves both ranks with bit-identical node records
+    (params, moments, steps)."""
+    import torch.multiprocessing as mp
+    port = _port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_two_rank_worker, args=(r, port, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    a, b = np.load(tmp_path / "params0.npy"), np.load(tmp_path / "params1.npy")
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    ua, ub = np.load(tmp_path / "unions0.npy"), np.load(tmp_path / "unions1.npy")
+    assert np.array_equal(ua, ub) and ua.min() > 0
