@@ -264,13 +264,13 @@ class Scene:
                 "training_bytes_per_gaussian": attr + 2 * attr + RECORD_DTYPE.itemsize + 12}
 
     # -- device path -------------------------------------------------------------
-    def host_store(self, hspt: Hspt | None = None, location: str = "host") -> HostStore:
-        """HostStore over this file's slots: every attribute section read
+    def host_store(self, location: str = "host") -> HostStore:
+        """HostStore over this file's slots (the SPT directory gives the
+        per-SPT record offsets/counts): every attribute section read
         straight into page-locked memory (or HBM for location="device")."""
         import torch
         if self.sh_cols != 9:
             raise ValueError("the device path keeps degree-1 SH (9 columns)")
-        hs = hspt if hspt is not None else self.read_hspt()
         st = HostStore.__new__(HostStore)
         st.location = location
         st.slot_to_node = self.slot_to_node.copy()
@@ -287,7 +287,6 @@ class Scene:
             if self.f.readinto(memoryview(t.numpy()).cast("B")) != length:
                 raise CorruptFileError(f"truncated section {name!r}")
             st.sections.append(t.to("cuda") if location == "device" else t)
-        del hs
         return st
 
     def save_store(self, store: HostStore) -> None:

@@ -112,7 +112,7 @@ def test_trainer_on_file_store_matches_in_memory_store(tmp_path):
     budget = int(0.35 * hs.flat_records()["nodes"].size * 92)
     mk = lambda: TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=budget, flush_interval=5), scheduler_k=3)
     a = Trainer(h, hs, list(zip(cams, targets)), mk(), extent=2 * E)
-    b = Trainer(h, hs, list(zip(cams, targets)), mk(), extent=2 * E, store=sc.host_store(hs))
+    b = Trainer(h, hs, list(zip(cams, targets)), mk(), extent=2 * E, store=sc.host_store())
     for sa, sb in zip(a.scene.store.sections, b.scene.store.sections):
         assert torch.equal(sa, sb)
     assert b.scene.lod.key_f64 is False          # file keys are f32: the f32-key cut path
@@ -123,6 +123,6 @@ def test_trainer_on_file_store_matches_in_memory_store(tmp_path):
     assert same_state(a.scene.records, b.scene.records)
     sc.save_store(b.scene.store)
     sc2 = SF.open_scene(path)
-    st2 = sc2.host_store(hs)
+    st2 = sc2.host_store()
     for sa, sb in zip(st2.sections, b.scene.store.sections):
         assert torch.equal(sa, sb)
