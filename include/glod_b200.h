@@ -60,6 +60,18 @@ typedef struct glod_lod_scene {
   const void* key_self;         /* [dev] [R] f32|f64                          */
   const void* key_parent;       /* [dev] [R] f32|f64, descending per SPT      */
   const int32_t* rec_node;      /* [dev] [R] node id of each record           */
+  /* optional (NULL / 0: level-synchronous BFS): the candidate nodes a cut
+   * can visit — every node reachable from root without entering an SPT
+   * subtree (upper nodes, SPT roots, passthrough subtrees) — and the parent
+   * array.  With them the select evaluates every candidate at once (its own
+   * cull / take test, then a walk up its ancestor chain) instead of one
+   * grid barrier per BFS level. */
+  const int32_t* parent;        /* [dev] [capacity], -1 = NONE                */
+  const int32_t* cand;          /* [dev] [num_cand]: first the upper-BFS nodes
+                                   (upper nodes, SPT roots, passthrough roots),
+                                   then the passthrough-subtree members     */
+  int64_t num_cand;
+  int64_t num_cand_upper;
 } glod_lod_scene;
 
 /* Per-view parameters: camera position, frustum planes computed on the host

@@ -29,7 +29,8 @@ class LodScene(C.Structure):
                 ("children", P), ("kind", P), ("means", P), ("scales", P),
                 ("num_spts", C.c_int32), ("key_f64", C.c_int32), ("num_records", C.c_int64),
                 ("spt_offset", P), ("spt_count", P), ("spt_root_rec", P), ("spt_center", P),
-                ("key_self", P), ("key_parent", P), ("rec_node", P)]
+                ("key_self", P), ("key_parent", P), ("rec_node", P),
+                ("parent", P), ("cand", P), ("num_cand", C.c_int64), ("num_cand_upper", C.c_int64)]
 
 
 class HsptBuildIn(C.Structure):

@@ -168,8 +168,89 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
   }
   grid_sync(ws.bar);
 
-  // ---- level-synchronous BFS over the upper tree + passthrough subtrees ----
   int level = 0;
+  if (sc.cand) {
+    // ---- every candidate at once (no BFS levels) ----
+    // A node is visited by the level-synchronous BFS iff every proper
+    // ancestor up to the BFS start was kept by the cull and expanded (not
+    // taken): phase 1 evaluates each candidate's own tests into a flag byte
+    // (bit0 kept with the dgemm order, bit1 kept with the dgemv order used
+    // for the first frontier of a BFS — the root and passthrough starts —,
+    // bit2 taken: dist >= m_d, bit3 leaf); phase 2 walks each candidate's
+    // ancestor chain over those bytes and applies the BFS's rules (bit4:
+    // passthrough root, bit5: passthrough root expanded by its own bfs_cut).
+    uint8_t* flags = reinterpret_cast<uint8_t*>(ws.frontier[0]);
+    const long long as = sc.attr_stride ? sc.attr_stride : 3;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (long long i = gtid; i < sc.num_cand; i += gthreads) {
+      const int node = sc.cand[i];
+      const double* mp = sc.means + as * node;
+      const double* sp = sc.scales + as * node;
+      const double mx = mp[0], my = mp[1], mz = mp[2];
+      const double s0 = sp[0], s1 = sp[1], s2 = sp[2];
+      unsigned f = 3;
+      if (v.cull) {
+        const double r = mul(3.0, max3(s0, s1, s2));
+        f = (sphere_in_frustum(planes, mx, my, mz, r, false) ? 1u : 0u) |
+            (sphere_in_frustum(planes, mx, my, mz, r, true) ? 2u : 0u);
+      }
+      const double dist = norm3_plain(sub(mx, v.position[0]), sub(my, v.position[1]), sub(mz, v.position[2]));
+      const double md = min_distance(v.threshold, v.metric, s0, s1, s2);
+      if (dist >= md) f |= 4u;
+      if (sc.children[2 * node] == -1) f |= 8u;
+      if (sc.kind[node] == -2) f |= 16u;
+      flags[node] = uint8_t(f);
+    }
+    grid_sync(ws.bar);
+    // phase 2a: the upper-BFS candidates (upper nodes, SPT roots,
+    // passthrough roots — cand[0, num_cand_upper)): walk to the root; a
+    // visited passthrough root that its own bfs_cut expands gets bit 5
+    for (long long i = gtid; i < sc.num_cand_upper; i += gthreads) {
+      const int node = sc.cand[i];
+      bool ok = true;
+      for (int c = node; c != sc.root;) {
+        const int a = sc.parent[c];
+        const unsigned fa = ld_cg(flags + a);
+        if (!((fa & (a == sc.root ? 2u : 1u)) && !(fa & 4u))) { ok = false; break; }
+        c = a;
+      }
+      if (!ok) continue;
+      const int kd = sc.kind[node];
+      const unsigned f = ld_cg(flags + node);
+      const bool kept_up = f & (node == sc.root ? 2u : 1u);
+      const bool sel = f & 12u;                // taken or leaf
+      if (kd == -2) {                          // its own bfs_cut starts here (dgemv order)
+        if (kept_up && (f & 2u)) {
+          if (sel) atomicOr(ws.bm_pass + (node >> 5), 1u << (node & 31));
+          else flags[node] = uint8_t(f | 32u);  // expanded: its subtree is visited
+        }
+      } else if (kd >= 0) {
+        if (kept_up) atomicOr(ws.bm_spt + (kd >> 5), 1u << (kd & 31));
+      } else if (kept_up && sel) {
+        atomicOr(ws.bm_upper + (node >> 5), 1u << (node & 31));
+      }
+    }
+    grid_sync(ws.bar);
+    // phase 2b: passthrough-subtree members (cand[num_cand_upper, num_cand)):
+    // walk up to their passthrough root, which must have been expanded
+    for (long long i = sc.num_cand_upper + gtid; i < sc.num_cand; i += gthreads) {
+      const int node = sc.cand[i];
+      bool ok = true;
+      for (int c = node;;) {
+        const int a = sc.parent[c];
+        const unsigned fa = ld_cg(flags + a);
+        if (fa & 16u) { ok = fa & 32u; break; }   // the passthrough root
+        if (!((fa & 1u) && !(fa & 4u))) { ok = false; break; }
+        c = a;
+      }
+      if (!ok) continue;
+      const unsigned f = ld_cg(flags + node);
+      if ((f & 1u) && (f & 12u)) atomicOr(ws.bm_pass + (node >> 5), 1u << (node & 31));
+    }
+    grid_sync(ws.bar);
+    level = -1;
+  } else
+  // ---- level-synchronous BFS over the upper tree + passthrough subtrees ----
   for (; level < kMaxLevels; ++level) {
     const long long n = ld_cg(ws.lvl_count + level);
     if (n == 0) break;

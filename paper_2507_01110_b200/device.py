@@ -124,6 +124,9 @@ class DeviceLodScene:
                     "centers": np.zeros((0, 3)), "roots": np.zeros(0, np.int64)}
             self.spt_perm = np.zeros(0, np.int64)
         self.kind = _t(kind, torch.int32, dev)
+        self.parent = _t(h.parent.reshape(-1), torch.int32, dev)
+        self._kind_host = kind
+        self.set_candidates(h.children, kind)
         self.S = int(flat["roots"].size)
         self.R = int(flat["nodes"].size)
         self.key_f64 = force_f64_keys or not keys_are_f32_exact(flat["key_self"], flat["key_parent"])
@@ -168,6 +171,36 @@ class DeviceLodScene:
                                        dtype=torch.uint8, device=dev)
         self._struct = self._make_struct()
 
+    def set_candidates(self, children: np.ndarray, kind: np.ndarray):
+        """Every node a cut can visit: reachable from root without entering
+        an SPT subtree (upper nodes, SPT roots, passthrough subtrees)."""
+        ch = np.asarray(children).reshape(-1, 2)
+        up, pas = [], []
+        frontier = np.array([self.root], dtype=np.int64)
+        while frontier.size:                      # upper BFS region
+            up.append(frontier)
+            k = kind[frontier]
+            pas_roots = frontier[(k == -2) & (ch[frontier, 0] != -1)]
+            if pas_roots.size:
+                pas.append(pas_roots)
+            go = frontier[(k == -1) & (ch[frontier, 0] != -1)]
+            frontier = ch[go].ravel().astype(np.int64)
+        members = []
+        frontier = ch[np.concatenate(pas)].ravel().astype(np.int64) if pas else np.zeros(0, np.int64)
+        while frontier.size:                      # passthrough subtrees below their roots
+            members.append(frontier)
+            go = frontier[ch[frontier, 0] != -1]
+            frontier = ch[go].ravel().astype(np.int64)
+        cu = np.sort(np.concatenate(up))
+        cm = np.sort(np.concatenate(members)) if members else np.zeros(0, np.int64)
+        cand = np.concatenate([cu, cm]).astype(np.int32)
+        self.cand = _t(cand, torch.int32, self.device) if cand.size else torch.zeros(1, dtype=torch.int32,
+                                                                                      device=self.device)
+        self.num_cand = int(cand.size)
+        self.num_cand_upper = int(cu.size)
+        if hasattr(self, "_struct"):
+            self._struct = self._make_struct()
+
     def _make_struct(self) -> _lib.LodScene:
         p = _lib.ptr
         return _lib.LodScene(
@@ -175,7 +208,9 @@ class DeviceLodScene:
             means=p(self.means), scales=p(self.scales), num_spts=self.S, key_f64=int(self.key_f64),
             num_records=self.R, spt_offset=p(self.spt_offset), spt_count=p(self.spt_count),
             spt_root_rec=p(self.spt_root_rec), spt_center=p(self.spt_center),
-            key_self=p(self.key_self), key_parent=p(self.key_parent), rec_node=p(self.rec_node))
+            key_self=p(self.key_self), key_parent=p(self.key_parent), rec_node=p(self.rec_node),
+            parent=p(self.parent), cand=p(self.cand), num_cand=self.num_cand,
+            num_cand_upper=self.num_cand_upper)
 
     def upload_attrs(self, h: Hierarchy):
         """Refresh the live traversal attributes from a host hierarchy."""
@@ -277,6 +312,8 @@ def bfs_scene_for(h: Hierarchy, start) -> DeviceLodScene:
         dev = DeviceLodScene(h, None, root=h.root if start is None else int(start))
         _CACHE[key] = dev
     dev.children.copy_(torch.from_numpy(h.children.reshape(-1).astype(np.int32)))
+    dev.parent.copy_(torch.from_numpy(h.parent.reshape(-1).astype(np.int32)))
+    dev.set_candidates(h.children, dev._kind_host)
     dev.upload_attrs(h)
     return dev
 
