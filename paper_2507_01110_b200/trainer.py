@@ -509,14 +509,19 @@ class Trainer:
             self._tgt_used[self._tgt_slot].record()
         self._mark("loss")
         _lib.readback(self._h_loss[:value.numel()], value)
-        torch.cuda.current_stream().synchronize()
+        if getattr(self, "_loss_ev", None) is None:
+            self._loss_ev = torch.cuda.Event()
+        self._loss_ev.record()
+        # the backward is enqueued before the host waits for the loss: the
+        # non-finite check (trainer.py:360-367) only has to precede ADAM, the
+        # first write to the parameters
+        grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
+        self._mark("backward")
+        self._loss_ev.synchronize()
         loss_value = float(self._h_loss[0])
         if not np.isfinite(loss_value):
             raise NonFiniteLossError(f"iteration {iteration}: non-finite loss rendering view "
                                      f"{self.current_view} with {R} gaussians")
-        self._mark("loss_read")
-        grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
-        self._mark("backward")
         bias, blen = self._bias_table(iteration)
         if self.distributed:
             from .parallel import sparse_grad_allreduce

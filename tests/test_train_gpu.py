@@ -213,3 +213,20 @@ def test_host_targets_match_device_targets():
         assert a.train_step(it) == b.train_step(it), it
     torch.cuda.synchronize()
     assert same_state(a.scene.params, b.scene.params)
+
+
+def test_non_finite_loss_raises_before_adam():
+    """trainer.py:360-367: a non-finite loss raises NonFiniteLossError and
+    leaves the parameters untouched (the backward may already have run; the
+    check precedes ADAM, the first write to the parameters)."""
+    from paper_2507_01110_b200.trainer import NonFiniteLossError
+    tr, _, _ = make_case()
+    tr.train_step(1)
+    torch.cuda.synchronize()
+    before = tr.scene.records.clone()
+    for t in tr.targets:
+        t.fill_(float("nan"))
+    with pytest.raises(NonFiniteLossError):
+        tr.train_step(2)
+    torch.cuda.synchronize()
+    assert torch.equal(before, tr.scene.records)
