@@ -1,11 +1,11 @@
 """Device-resident training step (mirrors trainer.train_step, trainer.py:312-378).
 
 Layout in HBM (per scene):
-  params, m, v   packed f64 attribute blocks of `capacity` rows — the
-                 authoritative `h.attrs` and the ADAM moments
-                 (OptimizerState, trainer.py:93-124); 552 B per node
-  step           int64 [capacity] per-node ADAM step counts
-  LoD tables     DeviceLodScene (means/scales are views into `params`)
+  node records   f64 [capacity][72] (GLOD_NODE_RECORD): the authoritative
+                 `h.attrs` values, the ADAM moments (OptimizerState,
+                 trainer.py:93-124) and the per-node step count of a node in
+                 one 576-B record
+  LoD tables     DeviceLodScene (means/scales read at the record stride)
   cache blocks   one packed f64 block per resident SPT prefix (DeviceCache)
 Host: the pinned f32 store (HostStore), cache metadata, scheduler RNG.
 
