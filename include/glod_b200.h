@@ -407,6 +407,21 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n,
                         const int32_t* spt_ids, const double* d_root, const int32_t* prefix_len,
                         int64_t max_rows, int64_t* rows_out, void* stream);
 int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
+/* Implicit block refresh.  A cache block holds its prefix's 23*rows f64
+ * values (section-major) followed by one "touched" bit per row
+ * (ceil(rows/64) u64).  ADAM (glod_adam_step_records with a refresh plan)
+ * and glod_refresh_resident_blocks set a row's bit instead of writing the
+ * updated master row into the block (entry.block.attrs.put, trainer.py:363):
+ * a touched row's value is the master row, and the gather reads it from
+ * there.  Before a block is written back to the store (or overlaid by a
+ * reload) its touched rows are materialised from the master, which this
+ * call registers: master rows (packed section-major when master_stride = 0,
+ * else node records of that stride), the record node ids (rec_node, [dev],
+ * the LoD scene's) and each SPT id's first record (host int64[num_spts]). */
+int glod_cache_set_master(glod_cache* c, const double* master, int64_t capacity, int64_t master_stride,
+                          const int32_t* rec_node, const int64_t* rec_offset, int32_t num_spts);
+/* Materialise every resident block now (snapshots / tests). */
+int glod_cache_materialize(glod_cache* c, void* stream);
 /* Host tables of the resident blocks per SPT id (block address, rows; 0 if
  * not resident), for glod_refresh_resident_blocks. */
 int glod_cache_resident(const glod_cache* c, uint64_t* block, int64_t* rows, int32_t num_spts);

@@ -140,6 +140,8 @@ SIGNATURES = {
     "glod_cache_end_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int64, C.c_int32, P]),
     "glod_cache_prefetch": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, C.c_int64, P, P]),
     "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
+    "glod_cache_set_master": (C.c_int, [P, P, C.c_int64, C.c_int64, P, P, C.c_int32]),
+    "glod_cache_materialize": (C.c_int, [P, P]),
     "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
     "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),
     "glod_readback": (C.c_int, [P, P, C.c_int64, P]),

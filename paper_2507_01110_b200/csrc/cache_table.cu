@@ -29,6 +29,8 @@ cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item*
 cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
                             cudaStream_t st);
 long long transfer_chunks(long long rows);
+cudaError_t launch_materialize(const glod_mat_item* items, int n_items, long long total, const double* master,
+                               long long cap, long long mstride, const int* rec_node, cudaStream_t st);
 cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
                                long long nblocks, cudaStream_t st);
 cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
@@ -128,6 +130,13 @@ class Arena {
 }  // namespace
 
 struct CacheTable {
+  // implicit refresh (glod_cache_set_master): the master rows and each
+  // SPT's record node ids, to materialise touched rows before write-back
+  const double* m_master = nullptr;
+  int64_t m_cap = 0, m_stride = 0;
+  const int32_t* m_rec_node = nullptr;
+  std::vector<int64_t> m_rec_off;         // per spt_id
+  std::vector<glod_mat_item> m_items;
   int64_t budget;
   double d_min, d_max;
   int64_t flush_interval;
@@ -331,6 +340,12 @@ struct CacheTable {
 
 namespace {
 
+// A cache block: 23·P f64 values (section-major) + one touched bit per row.
+size_t block_bytes(int64_t P) {
+  const int64_t rows = P > 0 ? P : 1;
+  return size_t(kFloats * rows + (rows + 63) / 64) * sizeof(double);
+}
+
 struct Xfer {
   int32_t spt_id;
   int64_t slot, rows;
@@ -339,6 +354,41 @@ struct Xfer {
   int64_t overlay_rows;
   const float* src = nullptr;  // loads: prefetched f32 copy of the prefix (HBM)
 };
+
+// Touched rows of the blocks about to be written back (or overlaid) take
+// their master values first (the refresh trainer.py:363 made implicit).
+// The item table goes through `host` (pinned, stream-ordered reuse) when
+// given, else through a pageable copy (tests / explicit calls).
+cudaError_t materialize(CacheTable* c, const std::vector<Xfer>& v, cudaStream_t st, void* host = nullptr) {
+  if (!c->m_master || v.empty()) return cudaSuccess;
+  c->m_items.clear();
+  long long acc = 0;
+  for (const Xfer& x : v) {
+    glod_mat_item it;
+    it.block = x.block;
+    it.rows = x.rows;
+    it.elem_start = acc;
+    it.rec_offset = c->m_rec_off[x.spt_id];
+    c->m_items.push_back(it);
+    acc += kFloats * x.rows;
+  }
+  const size_t bytes = c->m_items.size() * sizeof(glod_mat_item);
+  const void* src = c->m_items.data();
+  if (host) {
+    memcpy(host, src, bytes);
+    src = host;
+  }
+  void* d = nullptr;
+  cudaError_t e = c->dalloc(&d, bytes, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = launch_materialize(static_cast<glod_mat_item*>(d), int(c->m_items.size()), acc, c->m_master, c->m_cap,
+                           c->m_stride, c->m_rec_node, st);
+  if (e == cudaSuccess) e = c->dfree(d, st);
+  return e;
+}
+
+size_t mat_bytes(const std::vector<Xfer>& v) { return (v.size() * sizeof(glod_mat_item) + 15) / 16 * 16; }
 
 // Host bytes of one batch's table: items + int2 block map.
 size_t table_bytes(const std::vector<Xfer>& v) {
@@ -387,8 +437,8 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
 // store is queued (CacheTable::pending) and issued at end_step.
 cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::vector<Xfer>& wbs,
                       bool join, bool wait_pf, const glod_store_view& sv, cudaStream_t st) {
-  const size_t load_bytes = table_bytes(loads);
-  cudaError_t e = c->ensure_items(load_bytes + table_bytes(wbs) + 64);
+  const size_t load_bytes = table_bytes(loads), wb_bytes = table_bytes(wbs);
+  cudaError_t e = c->ensure_items(load_bytes + wb_bytes + mat_bytes(wbs) + 96);
   if (e != cudaSuccess) return e;
   if (join) {
     e = cudaStreamWaitEvent(st, c->ev_wb, 0);
@@ -399,6 +449,10 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     e = cudaStreamWaitEvent(st, c->ev_pf, 0);
     if (e != cudaSuccess) return e;
   }
+  // before the loads: overlays read these blocks
+  e = materialize(c, wbs, st, reinterpret_cast<char*>(c->h_items) + (load_bytes + 15) / 16 * 16 +
+                                  (wb_bytes + 15) / 16 * 16);
+  if (e != cudaSuccess) return e;
   if (!loads.empty()) {
     glod_prefix_item* d = nullptr;
     const int2* bm = nullptr;
@@ -508,7 +562,7 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
       const int64_t nbytes = P * c->bytes_per_row;
       if (nbytes > c->budget) return cudaErrorNotPermitted;   // OverBudgetError
       void* blk = nullptr;
-      e = c->dalloc(&blk, size_t(kFloats) * size_t(P > 0 ? P : 1) * sizeof(double), st);
+      e = c->dalloc(&blk, block_bytes(P), st);
       if (e != cudaSuccess) return e;
       Xfer ld{sid, c->slot_start[sid], P, static_cast<double*>(blk), nullptr, 0};
       auto ev = evicted.find(sid);
@@ -762,6 +816,26 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n, 
                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
   return GLOD_OK;
+}
+
+int glod_cache_set_master(glod_cache* c, const double* master, int64_t capacity, int64_t master_stride,
+                          const int32_t* rec_node, const int64_t* rec_offset, int32_t num_spts) {
+  if (!c || !master || !rec_node || (num_spts > 0 && !rec_offset))
+    return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  c->t.m_master = master;
+  c->t.m_cap = capacity;
+  c->t.m_stride = master_stride;
+  c->t.m_rec_node = rec_node;
+  c->t.m_rec_off.assign(rec_offset, rec_offset + num_spts);
+  return GLOD_OK;
+}
+
+int glod_cache_materialize(glod_cache* c, void* stream) {
+  if (!c) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  std::vector<glod::Xfer> all;
+  for (const auto& e : c->t.lru) all.push_back({e.spt_id, 0, e.prefix_len, e.block, nullptr, 0});
+  cudaError_t e = glod::materialize(&c->t, all, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? GLOD_OK : glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
 }
 
 int glod_cache_resident(const glod_cache* c, uint64_t* block, int64_t* rows, int32_t num_spts) {

@@ -7,6 +7,14 @@
 
 namespace glod {
 
+// One block to materialise (cache_table.cu → gather.cu materialize_kernel).
+struct glod_mat_item {
+  double* block;
+  long long rows;
+  long long elem_start;    // 23 · rows of all earlier items
+  long long rec_offset;    // first record of the block's SPT in rec_node
+};
+
 // Host-side count of kernel launches issued by this library (reported by
 // bench.py as gpu_launches; defined in capi.cu).
 void count_launch(unsigned long long n = 1);

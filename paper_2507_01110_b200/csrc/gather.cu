@@ -1,10 +1,13 @@
 // K4: render-set gather and cache-block maintenance (trainer.py:325-364,
 // store.py:304-333 data movement).
 //
-//  gather_rows   render rows = master[upper ∪ passthrough] then, per selected
+//  gather_rows_t render rows = master[upper ∪ passthrough] then, per selected
 //                SPT, cache-block rows at the cut positions (AttributeArrays
-//                .take + concat, core.py:120-159) — one kernel, 23 f64/row.
-//  scatter_back  after ADAM: block[pos] = master[node] (trainer.py:363)
+//                .take + concat, core.py:120-159) — one transposing kernel;
+//                a block row whose touched bit is set is read from the master
+//                (the implicit refresh of trainer.py:363, see block_bits)
+//  materialize   touched rows → block before a write-back / overlay
+//  scatter_back  explicit block[pos] = master[node] (public C-ABI)
 //  convert       f32 store prefix ↔ f64 cache block (store.py:334,330)
 #include "common.cuh"
 #include "../../include/glod_b200.h"
@@ -27,6 +30,18 @@ GLOD_DEV double src_at(const Src& s, int OFF, int COLS, int col) {
   return s.rows > 0 ? s.base[OFF * s.rows + s.idx * COLS + col] : s.base[s.idx * (-s.rows) + OFF + col];
 }
 
+// Cache blocks carry one "touched" bit per row after their 23·rows values:
+// ADAM sets it instead of writing the updated master row into the block
+// (trainer.py:363's refresh made implicit) — a touched row's value IS the
+// master row; readers take it from there, and blocks are materialised
+// before they are written back.
+GLOD_DEV unsigned long long* block_bits(const double* blk, long long rows) {
+  return reinterpret_cast<unsigned long long*>(const_cast<double*>(blk) + 23 * rows);
+}
+GLOD_DEV bool row_touched(const double* blk, long long rows, long long pos) {
+  return (block_bits(blk, rows)[pos >> 6] >> (pos & 63)) & 1ull;
+}
+
 GLOD_DEV long long master_rows(const glod_gather_plan& p) {
   return p.master_stride ? -p.master_stride : p.capacity;
 }
@@ -44,59 +59,66 @@ GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
     const long long k = r - n_mem;
     const int j = p.sel_seg[k];
     node = p.sel_node[k];
-    s = {reinterpret_cast<const double*>(p.seg_block[j]), p.seg_rows[j], p.sel_pos[k]};
+    const double* blk = reinterpret_cast<const double*>(p.seg_block[j]);
+    const long long P = p.seg_rows[j], pos = p.sel_pos[k];
+    if (row_touched(blk, P, pos)) s = {p.master, master_rows(p), node};
+    else s = {blk, P, pos};
   }
   return s;
 }
 
-// One thread per (row, column) of one section (blockIdx.y = section):
-// section-major, so the writes are fully coalesced and a warp reads runs of
-// consecutive source rows; compile-time column counts.  Latency-bound
-// (plan lookups → source row), so each thread handles kGatherIlp values
-// (strided by the block size) and issues all its loads before its stores.
-constexpr int kGatherTB = 256, kGatherIlp = 4;
+// Transposing gather: one CTA per kTRows render rows.  Row sources are
+// resolved once per row into shared memory; rows are read as contiguous
+// 23-value runs (node records / untouched block rows read per section) into
+// a shared tile, which is written out section-major (the rasteriser's
+// layout) as contiguous per-section runs.
+constexpr int kTRows = 64, kTThreads = 256;
 
-template <int SEC>
-GLOD_DEV void gather_sec(const glod_gather_plan& p, unsigned R, double* __restrict__ out,
-                         int* __restrict__ row_node) {
-  constexpr int OFFS[7] = {0, 3, 6, 10, 11, 14, 23};
-  constexpr int COLS = OFFS[SEC + 1] - OFFS[SEC];
-  constexpr long long OFF = OFFS[SEC];
-  const unsigned base = blockIdx.x * (kGatherTB * kGatherIlp) + threadIdx.x;
-  if (base >= R * COLS) return;
-  double v[kGatherIlp];
-  int node[kGatherIlp];
+__global__ void __launch_bounds__(kTThreads)
+gather_rows_t_kernel(glod_gather_plan p, long long R, double* __restrict__ out, int* __restrict__ row_node) {
+  __shared__ double tile[kTRows][24];
+  __shared__ const double* s_base[kTRows];
+  __shared__ long long s_rows[kTRows], s_idx[kTRows];
+  const long long r0 = (long long)blockIdx.x * kTRows;
+  const int nr = int(min((long long)kTRows, R - r0));
+  if (threadIdx.x < nr) {
+    int node;
+    const Src s = row_source(p, r0 + threadIdx.x, node);
+    s_base[threadIdx.x] = s.base;
+    s_rows[threadIdx.x] = s.rows;
+    s_idx[threadIdx.x] = s.idx;
+    if (row_node) row_node[r0 + threadIdx.x] = node;
+  }
+  __syncthreads();
+  const int ne = nr * 23;
+  constexpr int kPer = (kTRows * 23 + kTThreads - 1) / kTThreads;
+  double v[kPer];
 #pragma unroll
-  for (int k = 0; k < kGatherIlp; ++k) {
-    const unsigned local = base + k * kGatherTB;
-    if (local < R * COLS) {
-      const unsigned r = local / COLS;
-      const int col = int(local - r * COLS);
-      const Src s = row_source(p, r, node[k]);
-      v[k] = src_at(s, int(OFF), COLS, col);
+  for (int k = 0; k < kPer; ++k) {                 // every load in flight before the tile writes
+    const int e = threadIdx.x + k * kTThreads;
+    if (e < ne) {
+      const int lw = e / 23, col = e - lw * 23;
+      int sec = 0;
+#pragma unroll
+      for (int q = 1; q < 6; ++q) sec += col >= kSecOff[q];
+      const Src s = {s_base[lw], s_rows[lw], s_idx[lw]};
+      v[k] = src_at(s, kSecOff[sec], kSecCols[sec], col - kSecOff[sec]);
     }
   }
 #pragma unroll
-  for (int k = 0; k < kGatherIlp; ++k) {
-    const unsigned local = base + k * kGatherTB;
-    if (local < R * COLS) {
-      out[OFF * R + local] = v[k];
-      const unsigned r = local / COLS;
-      if (SEC == 0 && local == r * COLS && row_node) row_node[r] = node[k];
-    }
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kTThreads;
+    if (e < ne) tile[e / 23][e % 23] = v[k];
   }
-}
-
-__global__ void __launch_bounds__(kGatherTB)
-gather_rows_kernel(glod_gather_plan p, long long R, double* __restrict__ out, int* __restrict__ row_node) {
-  const unsigned n = unsigned(R);
-  switch (blockIdx.y) {
-    case 0: gather_sec<0>(p, n, out, row_node); break;
-    case 1: gather_sec<1>(p, n, out, row_node); break;
-    case 2: gather_sec<2>(p, n, out, row_node); break;
-    case 3: gather_sec<3>(p, n, out, row_node); break;
-    case 4: gather_sec<4>(p, n, out, row_node); break;
-    case 5: gather_sec<5>(p, n, out, row_node); break;
+  __syncthreads();
+  for (int e = threadIdx.x; e < ne; e += kTThreads) {
+    int sec = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) sec += e >= nr * kSecOff[k];
+    const int off = kSecOff[sec], cols = kSecCols[sec];
+    const int local = e - nr * off;
+    const int lw = local / cols;
+    out[off * R + (r0 + lw) * cols + (local - lw * cols)] = tile[lw][off + local - lw * cols];
   }
 }
 
@@ -181,6 +203,7 @@ store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items
     const glod_prefix_item I = items[it];
     const long long local = e - I.elem_start;
     const long long rows = I.rows;
+    if (kLoad && local < (rows + 63) / 64) block_bits(I.block, rows)[local] = 0;
     int sec = 0;
 #pragma unroll
     for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
@@ -246,10 +269,12 @@ __global__ void refresh_resident_kernel(const double* __restrict__ master, long 
 #pragma unroll
   for (int k = 1; k < 6; ++k) sec += col >= kSecOff[k];
   const int c = col - kSecOff[sec], cols = kSecCols[sec];
-  double* blk = reinterpret_cast<double*>(res_block[s]);
-  const Src m = {master, mstride ? -mstride : cap, id};
-  blk[kSecOff[sec] * rows + pos * cols + c] = src_at(m, kSecOff[sec], cols, c);
-  if (col == 0) touched[s] = 1;
+  (void)master; (void)cap; (void)mstride; (void)c; (void)cols;
+  if (col == 0) {
+    const double* blk = reinterpret_cast<const double*>(res_block[s]);
+    atomicOr(block_bits(blk, rows) + (pos >> 6), 1ull << (pos & 63));   // implicit refresh
+    touched[s] = 1;
+  }
 }
 
 // Cache-path transfers driven by a block map: block b moves elements
@@ -274,6 +299,8 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
   const long long n = 23LL * I.rows;
   const long long c0 = (long long)bm.y * kChunk;
   const long long c1 = min(n, c0 + kChunk);
+  if (bm.y == 0)                                 // a freshly loaded block: no row touched
+    for (long long w = threadIdx.x; w < (I.rows + 63) / 64; w += blockDim.x) block_bits(I.block, I.rows)[w] = 0;
   if (I.src) {                                   // prefetched f32 copy in HBM
     for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
     return;
@@ -302,6 +329,35 @@ pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __res
   const long long c1 = min(n, c0 + kChunk);
   float* o = out + I.elem_start;
   for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[l]);
+}
+
+// Materialise touched rows before a block is written back / overlaid: one
+// thread per (block row, column); rows with the touched bit take the master
+// row (node = the SPT's record at that position).  Bits stay set (the row
+// now equals the master, so either source gives the same value).
+__global__ void __launch_bounds__(256)
+materialize_kernel(const glod_mat_item* __restrict__ items, int n_items, long long total,
+                   const double* __restrict__ master, long long cap, long long mstride,
+                   const int* __restrict__ rec_node) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int lo = 0, hi = n_items - 1;                     // last item with elem_start <= e
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (items[mid].elem_start <= e) lo = mid; else hi = mid - 1;
+  }
+  const glod_mat_item I = items[lo];
+  const long long local = e - I.elem_start;
+  const long long row = local / 23;
+  const int col = int(local - row * 23);
+  if (!row_touched(I.block, I.rows, row)) return;
+  int sec = 0;
+#pragma unroll
+  for (int k = 1; k < 6; ++k) sec += col >= kSecOff[k];
+  const int cols = kSecCols[sec], c = col - kSecOff[sec];
+  const long long node = rec_node[I.rec_offset + row];
+  const Src m = {master, mstride ? -mstride : cap, node};
+  I.block[kSecOff[sec] * I.rows + row * cols + c] = src_at(m, kSecOff[sec], cols, c);
 }
 
 // Small device→host read-backs written by a kernel straight into mapped
@@ -368,9 +424,7 @@ cudaError_t launch_gather(const glod_gather_plan& p, long long R, double* out, i
   if (R <= 0) return cudaSuccess;
   const int TB = 256;
   count_launch();
-  const long long per_block = (long long)kGatherTB * kGatherIlp;
-  const dim3 grid(unsigned((9 * R + per_block - 1) / per_block), 6);
-  gather_rows_kernel<<<grid, kGatherTB, 0, st>>>(p, R, out, row_node);
+  gather_rows_t_kernel<<<unsigned((R + kTRows - 1) / kTRows), kTThreads, 0, st>>>(p, R, out, row_node);
   return cudaGetLastError();
 }
 
@@ -380,6 +434,15 @@ cudaError_t launch_wire_pack(const double* master, long long cap, const int* ids
   count_launch();
   const dim3 grid(unsigned((9 * N + 255) / 256), 6);
   wire_pack_kernel<<<grid, 256, 0, st>>>(master, cap, ids, seg, n_msgs, N, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_materialize(const glod_mat_item* items, int n_items, long long total, const double* master,
+                               long long cap, long long mstride, const int* rec_node, cudaStream_t st) {
+  if (total <= 0 || n_items <= 0) return cudaSuccess;
+  count_launch();
+  materialize_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(items, n_items, total, master, cap, mstride,
+                                                                    rec_node);
   return cudaGetLastError();
 }
 

@@ -115,6 +115,9 @@ class DeviceLodScene:
             for key in ("offset", "count", "centers", "roots"):
                 flat[key] = flat[key][perm]
             self.spt_perm = perm.astype(np.int64)
+            # first (padded) record of each caller spt_id
+            self.rec_offset_by_sid = np.empty(perm.size, dtype=np.int64)
+            self.rec_offset_by_sid[perm] = flat["offset"]
             kind[flat["roots"]] = np.arange(flat["roots"].size, dtype=np.int32)
             if hspt.passthrough_roots.size:
                 kind[hspt.passthrough_roots] = -2

@@ -170,6 +170,7 @@ class Trainer:
         self.scene = DeviceScene(h, hspt, store_location=cfg.store_location, store=store)
         dev = self.scene.device
         self.cache = NativeCache(cfg.cache, self.scene.store)
+        self._register_master()
         self.rast = Rasterizer()
         self.views = [(Camera.from_any(c), t) for c, t in views]
         pos = np.stack([c.position for c, _ in self.views])
@@ -202,6 +203,13 @@ class Trainer:
         self._pf_rows_cap = cfg.cache.budget_bytes // BYTES_PER_GAUSSIAN_F32
         self.timing = None          # {stage: [ms, ...]} when profiling is on
         self._ev = []
+
+    def _register_master(self):
+        """Implicit block refresh: the cache materialises touched rows from
+        the node records before writing blocks back (glod_cache_set_master)."""
+        sc = self.scene
+        if sc.lod.S:
+            self.cache.set_master(sc.records, sc.cap, NODE_RECORD, sc.lod.rec_node, sc.lod.rec_offset_by_sid)
 
     def _scene_buffers(self):
         """Per-HSPT host/device tables (rebuilt after densification)."""
@@ -283,6 +291,7 @@ class Trainer:
             recs[:, REC_MV + k:REC_MV + 2 * F:2] = torch.from_numpy(cols).to(recs.device)
         recs.view(torch.int64)[:, REC_STEP] = torch.from_numpy(opt.step).to(recs.device)
         self.cache = NativeCache(self.cfg.cache, self.scene.store)
+        self._register_master()
         self._scene_buffers()
         return out
 
