@@ -198,7 +198,7 @@ def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
         line("blend_fwd_kernel", kt["fwd_alg"], kt["fwd_ms"], "issue-bound (per-pixel compositing)"),
         line("adam_records_kernel", kt["adam_alg"], stage_ms.get("adam"),
              "HBM (random 576-B node records); ms = adam stage"),
-        line("gather_rows_kernel", kt["gather_alg"], stage_ms.get("gather"),
+        line("gather_rows_t_kernel", kt["gather_alg"], stage_ms.get("gather"),
              "HBM (sparse rows); ms = gather stage"),
     ]
     return main

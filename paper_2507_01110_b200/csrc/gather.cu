@@ -332,32 +332,49 @@ pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __res
 }
 
 // Materialise touched rows before a block is written back / overlaid: one
-// thread per (block row, column); rows with the touched bit take the master
-// row (node = the SPT's record at that position).  Bits stay set (the row
-// now equals the master, so either source gives the same value).
+// thread per block row (items tile a flat row space; elem_start = 23 ·
+// earlier rows); a touched row copies its 23 master values (one contiguous
+// record run) into the block.  Bits stay set (the row now equals the
+// master, so either source gives the same value).
 __global__ void __launch_bounds__(256)
-materialize_kernel(const glod_mat_item* __restrict__ items, int n_items, long long total,
+materialize_kernel(const glod_mat_item* __restrict__ items, int n_items, long long total_rows,
                    const double* __restrict__ master, long long cap, long long mstride,
                    const int* __restrict__ rec_node) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  int lo = 0, hi = n_items - 1;                     // last item with elem_start <= e
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (items[mid].elem_start <= e) lo = mid; else hi = mid - 1;
+  __shared__ int s_lo, s_hi;
+  const long long base = (long long)blockIdx.x * blockDim.x;
+  if (threadIdx.x == 0) {                           // items covering this CTA's rows
+    const long long last = min(total_rows, base + (long long)blockDim.x) - 1;
+    int lo = 0, hi = n_items - 1;
+    while (lo < hi) { const int m = (lo + hi + 1) >> 1; if (items[m].elem_start / 23 <= base) lo = m; else hi = m - 1; }
+    s_lo = lo;
+    hi = n_items - 1;
+    while (lo < hi) { const int m = (lo + hi + 1) >> 1; if (items[m].elem_start / 23 <= last) lo = m; else hi = m - 1; }
+    s_hi = lo;
   }
+  __syncthreads();
+  const long long e = base + threadIdx.x;
+  if (e >= total_rows) return;
+  int lo = s_lo, hi = s_hi;
+  while (lo < hi) { const int m = (lo + hi + 1) >> 1; if (items[m].elem_start / 23 <= e) lo = m; else hi = m - 1; }
   const glod_mat_item I = items[lo];
-  const long long local = e - I.elem_start;
-  const long long row = local / 23;
-  const int col = int(local - row * 23);
+  const long long row = e - I.elem_start / 23;
   if (!row_touched(I.block, I.rows, row)) return;
-  int sec = 0;
-#pragma unroll
-  for (int k = 1; k < 6; ++k) sec += col >= kSecOff[k];
-  const int cols = kSecCols[sec], c = col - kSecOff[sec];
   const long long node = rec_node[I.rec_offset + row];
   const Src m = {master, mstride ? -mstride : cap, node};
-  I.block[kSecOff[sec] * I.rows + row * cols + c] = src_at(m, kSecOff[sec], cols, c);
+  double v[23];
+#pragma unroll
+  for (int col = 0; col < 23; ++col) {
+    const int sec = col < 3 ? 0 : col < 6 ? 1 : col < 10 ? 2 : col < 11 ? 3 : col < 14 ? 4 : 5;
+    constexpr int offs[6] = {0, 3, 6, 10, 11, 14};
+    v[col] = src_at(m, offs[sec], (sec == 2 ? 4 : sec == 3 ? 1 : sec == 5 ? 9 : 3), col - offs[sec]);
+  }
+#pragma unroll
+  for (int col = 0; col < 23; ++col) {
+    const int sec = col < 3 ? 0 : col < 6 ? 1 : col < 10 ? 2 : col < 11 ? 3 : col < 14 ? 4 : 5;
+    constexpr int offs[6] = {0, 3, 6, 10, 11, 14};
+    const int cols = sec == 2 ? 4 : sec == 3 ? 1 : sec == 5 ? 9 : 3;
+    I.block[offs[sec] * I.rows + row * cols + (col - offs[sec])] = v[col];
+  }
 }
 
 // Small device→host read-backs written by a kernel straight into mapped
@@ -441,8 +458,9 @@ cudaError_t launch_materialize(const glod_mat_item* items, int n_items, long lon
                                long long cap, long long mstride, const int* rec_node, cudaStream_t st) {
   if (total <= 0 || n_items <= 0) return cudaSuccess;
   count_launch();
-  materialize_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(items, n_items, total, master, cap, mstride,
-                                                                    rec_node);
+  const long long rows = total / 23;
+  materialize_kernel<<<unsigned((rows + 255) / 256), 256, 0, st>>>(items, n_items, rows, master, cap, mstride,
+                                                                   rec_node);
   return cudaGetLastError();
 }
 
