@@ -111,14 +111,17 @@ gather_rows_t_kernel(glod_gather_plan p, long long R, double* __restrict__ out, 
     if (e < ne) tile[e / 23][e % 23] = v[k];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < ne; e += kTThreads) {
-    int sec = 0;
+  // section-major output: per section a contiguous run of nr·cols values
+  // starting at off·R + r0·cols; walk the six runs with compile-time widths
 #pragma unroll
-    for (int k = 1; k < 6; ++k) sec += e >= nr * kSecOff[k];
-    const int off = kSecOff[sec], cols = kSecCols[sec];
-    const int local = e - nr * off;
-    const int lw = local / cols;
-    out[off * R + (r0 + lw) * cols + (local - lw * cols)] = tile[lw][off + local - lw * cols];
+  for (int sec = 0; sec < 6; ++sec) {
+    constexpr int offs[7] = {0, 3, 6, 10, 11, 14, 23};
+    const int off = offs[sec], cols = offs[sec + 1] - offs[sec];
+    double* dst = out + off * R + r0 * cols;
+    for (int l = threadIdx.x; l < nr * cols; l += kTThreads) {
+      const int lw = l / cols;
+      dst[l] = tile[lw][off + l - lw * cols];
+    }
   }
 }
 
