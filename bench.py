@@ -167,8 +167,8 @@ def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
                  accumulators, read-modify-write)
       blend_fwd: 52 B per instance + 24 B per pixel (image 12, T 8, last 4)
       adam:      1340 B per row (576-B node record — params, (m, v), step —
-                 read and written, grads 184, id 4) + 184 B per SPT row
-                 (cache-block refresh)
+                 read and written, grads 184, id 4) + 8 B per SPT row (the
+                 touched-bit atomic of the implicit cache-block refresh)
       gather:    372 B per row (184 read, 184 write, 4 node id)
 
     `traffic` is the ncu-measured DRAM bytes per launch of the same kernel
@@ -338,7 +338,7 @@ def run_ours(args):
         n_spt_rows = R - tr.last_stats["n_upper"] - tr.last_stats["n_pass"]
         alg["fwd"] += inst * 52 + npix * 24
         alg["bwd"] += inst * 52 + npix * 24 + R * 144
-        alg["adam"] += R * 1340 + n_spt_rows * 184
+        alg["adam"] += R * 1340 + n_spt_rows * 8      # + the touched-bit atomic per SPT row
         alg["gather"] += R * 372
     bt = tr.rast.blend_timing(False)
     stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
