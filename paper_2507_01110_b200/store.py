@@ -84,6 +84,44 @@ class HostStore:
                 self.sections.append(t.pin_memory() if pin else t)
         self.attribute_bytes_read = 0
 
+    @staticmethod
+    def from_scene(scene, location: str = "host") -> "HostStore":
+        """The store of an open scene: our scenefile.Scene (sections read from
+        the file straight into pinned memory) or the reference's
+        store.Scene (store.py:237-280; sections read through its backing)."""
+        if hasattr(scene, "host_store"):
+            return scene.host_store(location)
+        st = HostStore.__new__(HostStore)
+        st.location = location
+        st.slot_to_node = np.asarray(scene.slot_to_node, dtype=np.int64).copy()
+        st.nslots = int(scene.nslots)
+        st.record_offset = np.asarray(scene.spt_dir["record_offset"], dtype=np.int64)
+        st.record_count = np.asarray(scene.spt_dir["record_count"], dtype=np.int64)
+        st.total_records = int(st.record_count.sum())
+        st.attribute_bytes_read = 0
+        st.sections = []
+        buf = getattr(scene.backing, "buf", None)
+        for name, cols in SECTIONS:
+            off, length = scene.sections[name]
+            raw = bytes(buf[off:off + length]) if buf is not None else scene.backing.read(off, length)
+            t = torch.from_numpy(np.frombuffer(raw, dtype="<f4").reshape(st.nslots, cols).copy())
+            st.sections.append(t.to("cuda") if location == "device" else
+                               (t.pin_memory() if torch.cuda.is_available() else t))
+        return st
+
+    def to_scene(self, scene) -> None:
+        """Write the sections back into an open scene (every slot, the
+        reference's write_back, store.py:323-333)."""
+        if hasattr(scene, "save_store"):
+            scene.save_store(self)
+            return
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            off, length = scene.sections[name]
+            data = sec.cpu().numpy().astype("<f4", copy=False).tobytes()
+            if len(data) != length:
+                raise InvalidBlockError(f"store section {name!r} does not match the scene")
+            scene.backing.write(off, data)
+
     # -- directory ----------------------------------------------------------
     def _check(self, spt_id: int):
         if spt_id < 0 or spt_id >= self.record_count.size:

@@ -52,6 +52,7 @@ class TrainConfig:
     """Subset of trainer.TrainConfig (trainer.py:64-90) the step uses."""
 
     total_iterations: int = 1
+    init_iterations: int = 2000
     loss_lambda: float = 0.2
     learning_rates: dict = field(default_factory=lambda: dict(DEFAULT_LEARNING_RATES))
     lod: LodConfig = field(default_factory=lambda: LodConfig(threshold=1.0))
@@ -70,6 +71,9 @@ class TrainConfig:
     densify_interval: int = 500
     dead_opacity_threshold: float = 0.005
     spawns_per_densify: int | None = None   # None -> 0.5% of leaf count
+    skybox_points: int = 0                  # initialize() only (host)
+    size_threshold: float | None = None     # initialize() only (host)
+    min_subtree: int = 32                   # hspt.DEFAULT_MIN_SUBTREE
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -157,7 +161,7 @@ class Trainer:
     with targets (h, w, 3) float images (numpy or pinned torch)."""
 
     def __init__(self, h, hspt, views, cfg: TrainConfig, extent: float, device_targets: bool = True,
-                 group=None, store=None):
+                 group=None, store=None, graph=None, rng=None):
         import torch.distributed as dist
         self.cfg = cfg
         # view sharding: with an initialised process group of >1 ranks each
@@ -174,9 +178,12 @@ class Trainer:
         self.rast = Rasterizer()
         self.views = [(Camera.from_any(c), t) for c, t in views]
         pos = np.stack([c.position for c, _ in self.views])
-        self.graph = build_view_graph(pos, k=cfg.scheduler_k, exploration=cfg.scheduler_exploration,
-                                      random_every=cfg.scheduler_random_every)
-        self.rng = np.random.default_rng(cfg.seed)
+        # the drop-in (train_step(state, it)) passes the reference state's own
+        # view graph and RNG, so the draw sequence advances the caller's RNG
+        self.graph = graph if graph is not None else build_view_graph(
+            pos, k=cfg.scheduler_k, exploration=cfg.scheduler_exploration,
+            random_every=cfg.scheduler_random_every)
+        self.rng = rng if rng is not None else np.random.default_rng(cfg.seed)
         self.current_view = 0
         self.iteration = 0
         self.extent = float(extent)
@@ -294,6 +301,22 @@ class Trainer:
         self._register_master()
         self._scene_buffers()
         return out
+
+    # -- optimizer state in / cache flush (drop-in train_step) ----------------
+    def load_optimizer(self, opt) -> None:
+        """ADAM moments and per-node steps from an OptimizerState
+        (trainer.py:93-124; dict- or attribute-keyed) into the node records."""
+        recs = self.scene.records
+        for k, blk in enumerate((opt.m, opt.v)):
+            c = np.concatenate([_moment(blk, n).reshape(self.scene.cap, -1) for n, _ in SECTIONS], axis=1)
+            recs[:, REC_MV + k:REC_MV + 2 * FLOATS_PER_GAUSSIAN:2] = torch.from_numpy(c).to(recs.device)
+        recs.view(torch.int64)[:, REC_STEP] = torch.from_numpy(
+            np.ascontiguousarray(opt.step, dtype=np.int64)).to(recs.device)
+
+    def flush_cache(self) -> None:
+        """Write every dirty resident block back to the store and empty the
+        cache (the reference's flush, cache.py:98-106)."""
+        self.cache.end_step(0, mark_dirty=False)
 
     # -- optional per-stage CUDA-event timing (bench.py) ---------------------
     def enable_timing(self, on: bool = True):
@@ -556,6 +579,147 @@ class Trainer:
         self.iteration = iteration
         self.last_stats["n_instances"] = self.rast.stats()["n_instances"]
         self._last_grads = grads
+        self._last_image = image
+        self._last_rows = row_node[:R]
         out = {"iteration": iteration, "view": self.current_view, "loss": loss_value}
         out.update(counters)
         return out
+
+
+# ---------------------------------------------------------------------------
+# Drop-in at the reference's signature: train_step(state, iteration)
+# ---------------------------------------------------------------------------
+@dataclass
+class OptimizerState:
+    """trainer.OptimizerState (trainer.py:93-124): per-node ADAM moments
+    mirroring every attribute array, plus per-node step counts."""
+
+    m: dict
+    v: dict
+    step: np.ndarray
+
+    @staticmethod
+    def zeros(attrs) -> "OptimizerState":
+        m = {n: np.zeros_like(np.asarray(getattr(attrs, n), dtype=np.float64)) for n, _ in SECTIONS}
+        v = {n: np.zeros_like(np.asarray(getattr(attrs, n), dtype=np.float64)) for n, _ in SECTIONS}
+        return OptimizerState(m=m, v=v, step=np.zeros(len(attrs), dtype=np.int64))
+
+
+@dataclass
+class TrainState:
+    """trainer.TrainState (trainer.py:127-146), field for field.  The
+    reference's own TrainState objects are accepted as well (duck-typed)."""
+
+    config: TrainConfig
+    hierarchy: object
+    hspt: object
+    scene: object
+    cache: object
+    graph: object
+    views: list
+    opt: OptimizerState
+    rng: np.random.Generator
+    extent: float
+    skybox_ids: np.ndarray
+    current_view: int = 0
+    iteration: int = 0
+
+    @property
+    def mean_lr(self) -> float:
+        return self.config.learning_rates["means"] * self.extent
+
+
+def _config_of(c) -> TrainConfig:
+    """Our TrainConfig from a reference (or our own) TrainConfig."""
+    if isinstance(c, TrainConfig):
+        return c
+    cc = c.cache
+    return TrainConfig(
+        total_iterations=c.total_iterations, init_iterations=c.init_iterations, loss_lambda=c.loss_lambda,
+        learning_rates=dict(c.learning_rates), lod=LodConfig(float(c.lod.threshold), c.lod.metric),
+        cache=CacheConfig(budget_bytes=cc.budget_bytes, d_min=cc.d_min, d_max=cc.d_max,
+                          flush_interval=cc.flush_interval),
+        scheduler_k=c.scheduler_k, scheduler_exploration=c.scheduler_exploration,
+        scheduler_random_every=c.scheduler_random_every, seed=c.seed, densify_interval=c.densify_interval,
+        dead_opacity_threshold=c.dead_opacity_threshold, spawns_per_densify=c.spawns_per_densify,
+        skybox_points=c.skybox_points, size_threshold=c.size_threshold, min_subtree=c.min_subtree)
+
+
+def _moment(blk, name):
+    return np.asarray(blk[name] if isinstance(blk, dict) else getattr(blk, name), dtype=np.float64)
+
+
+def _flush_host_cache(state):
+    """A warm reference cache is flushed into its store first (the device
+    cache starts empty): dirty blocks written back in LRU order, exactly
+    what the reference's tick_and_maybe_flush does at a flush."""
+    cache = state.cache
+    entries = getattr(cache, "entries", None)
+    if entries:
+        for e in list(entries.values()):
+            if e.dirty:
+                state.scene.write_back(e.block)
+        entries.clear()
+        cache.resident_bytes = 0
+
+
+def _trainer_of(state) -> "Trainer":
+    tr = getattr(state, "_device_trainer", None)
+    if tr is not None and tr._state_key == (id(state.hspt), id(state.scene)):
+        return tr
+    from .hspt import Hspt
+    _flush_host_cache(state)
+    h, hs = Hierarchy.from_any(state.hierarchy), Hspt.from_any(state.hspt)
+    store = HostStore.from_scene(state.scene)
+    tr = Trainer(h, hs, state.views, _config_of(state.config), extent=float(state.extent), store=store,
+                 graph=state.graph, rng=state.rng)
+    tr.current_view, tr.iteration = int(state.current_view), int(state.iteration)
+    tr.load_optimizer(state.opt)
+    tr._state_key = (id(state.hspt), id(state.scene))
+    state._device_trainer = tr
+    return tr
+
+
+def train_step(state, iteration: int) -> dict:
+    """trainer.train_step(state, iteration) (trainer.py:312-378) on the
+    device.  The first call uploads the state (hierarchy values, ADAM
+    moments and steps, the scene store; a warm host cache is flushed into
+    the store first) into a per-state device Trainer; later calls only run
+    steps.  The scheduler draws advance `state.rng` itself, and
+    `state.current_view` / `state.iteration` follow the reference.  The
+    device is authoritative for parameters, moments, store and cache:
+    `sync_state(state)` copies them back (a cache flush point, like
+    save_checkpoint's, trainer.py:464-465) before host code reads
+    `state.hierarchy.attrs`, `state.opt` or the scene."""
+    tr = _trainer_of(state)
+    out = tr.train_step(iteration)
+    state.current_view, state.iteration = tr.current_view, iteration
+    return out
+
+
+def sync_state(state) -> None:
+    """Device → reference state: flush the device cache (dirty blocks written
+    back to the store), then copy the master attribute values into
+    `state.hierarchy.attrs`, the moments/steps into `state.opt` and the
+    store sections into `state.scene`'s backing."""
+    tr = getattr(state, "_device_trainer", None)
+    if tr is None:
+        return
+    tr.flush_cache()
+    torch.cuda.synchronize()
+    sc = tr.scene
+    rec = sc.records.cpu().numpy()
+    off = 0
+    h = state.hierarchy
+    for name, cols in SECTIONS:
+        vals = rec[:, off:off + cols]
+        getattr(h.attrs, name)[...] = vals.reshape(getattr(h.attrs, name).shape)
+        for k, blk in enumerate((state.opt.m, state.opt.v)):
+            mv = rec[:, REC_MV + 2 * off + k:REC_MV + 2 * (off + cols):2]
+            if isinstance(blk, dict):
+                blk[name][...] = mv.reshape(blk[name].shape)
+            else:
+                getattr(blk, name)[...] = mv.reshape(getattr(blk, name).shape)
+        off += cols
+    state.opt.step[...] = rec.view(np.int64)[:, REC_STEP]
+    sc.store.to_scene(state.scene)

@@ -546,6 +546,176 @@ def make_densify_cases():
     np.savez_compressed(OUT / "densify_cases.npz", **d)
 
 
+
+def make_train_cases():
+    """trainer.train_step (trainer.py:312-378) on reference TrainStates built
+    from a .glod file (write_scene → open_scene → read_hierarchy/read_hspt,
+    so every value is f32-representable and the SPT keys are f32): per step
+    the scheduled view, every returned counter, the loss and the rendered
+    node-id order; the rendered image and the raw gradients for the first
+    steps; the full state (params, moments, step counts, store sections,
+    cache entries with their blocks) at checkpoints.  The traces cover
+    misses, hits, LRU evictions, same-step re-misses of a replaced dirty
+    entry (the stale-store quirk, trainer.py:333-341) and periodic flushes
+    (cache.py:98-106)."""
+    sys.path.insert(0, str(OUT.parent.parent))
+    from glod.cache import CacheConfig, DeviceCache
+    from glod.hierarchy import Hierarchy as RefHierarchy
+    from glod.scheduler import build_view_graph
+    from glod.store import MemoryBacking, open_scene, write_scene
+    import glod.trainer as TR
+    from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene, orbit_views, scene_extent
+
+    events = {}
+    orig_insert = DeviceCache.insert
+    orig_tick = DeviceCache.tick_and_maybe_flush
+
+    def insert(self, entry):
+        out = orig_insert(self, entry)
+        for sid, _ in out:
+            k = "replace_dirty" if sid == entry.spt_id else "evict_dirty"
+            events[k] = events.get(k, 0) + 1
+        return out
+
+    def tick(self, it):
+        out = orig_tick(self, it)
+        if out:
+            events["flush"] = events.get("flush", 0) + len(out)
+        return out
+
+    DeviceCache.insert, DeviceCache.tick_and_maybe_flush = insert, tick
+    cap_rows = {}
+    orig_cut, orig_pos, orig_fwd, orig_bwd = TR.cut_hspt, TR._spt_positions, TR.render_forward, TR.backward
+
+    def cut(*a, **k):
+        rs = orig_cut(*a, **k)
+        cap_rows["rows"] = [np.asarray(rs.upper, np.int64), np.asarray(rs.passthrough, np.int64)]
+        return rs
+
+    def pos(spt, d):
+        out = orig_pos(spt, d)
+        cap_rows["rows"].append(np.asarray(out[2], np.int64))
+        return out
+
+    def fwd(attrs, cam):
+        ctx = orig_fwd(attrs, cam)
+        cap_rows["image"] = ctx.image.copy()
+        return ctx
+
+    def bwd(ctx, dimg):
+        g = orig_bwd(ctx, dimg)
+        cap_rows["grads"] = np.concatenate([np.asarray(getattr(g, n), np.float64).reshape(-1, c)
+                                            for n, c in (("means", 3), ("scales", 3), ("rotations", 4),
+                                                         ("opacities", 1), ("base_colors", 3), ("sh_rest", 9))],
+                                           axis=1)
+        return g
+
+    TR.cut_hspt, TR._spt_positions, TR.render_forward, TR.backward = cut, pos, fwd, bwd
+    d = {}
+    specs = [  # leaves, seed, spt_leaves, budget (share of all records), flush, steps, res, views, k
+        (1500, 3, 256, 0.6, 7, 16, (64, 48), 8, 4),
+        (1500, 5, 128, 0.3, 5, 16, (64, 48), 8, 3),
+    ]
+    try:
+        for case, (n, seed, sptl, bfrac, flush, steps, res, nviews, k) in enumerate(specs):
+            events.clear()
+            h, hs, cfg = designed_scene(SceneSpec(n_leaves=n, spt_leaves=sptl, seed=seed, pass_fraction=0.1))
+            a = h.attrs
+            rh = RefHierarchy(attrs=AttributeArrays(a.means.copy(), a.scales.copy(), a.rotations.copy(),
+                                                    a.opacities.copy(), a.base_colors.copy(), a.sh_rest.copy()),
+                              parent=h.parent.astype(np.int32).copy(), children=h.children.astype(np.int32).copy(),
+                              root=int(h.root))
+            lod = LodConfig(cfg.threshold, cfg.metric)
+            rhs = build_hspt(rh, hs.size_threshold, hs.min_subtree, lod)
+            mb = MemoryBacking()
+            write_scene(rh, rhs, mb)
+            file_bytes = mb.tobytes()
+            scene = open_scene(mb)
+            h2, hs2 = scene.read_hierarchy(), scene.read_hspt()
+            E = scene_extent(n)
+            cams = orbit_views(nviews, 1.5 * E, 0.6 * E, resolution=res, focal=(70.0, 70.0), seed=seed,
+                               jitter=0.2)
+            cams = [Camera(position=c.position, orientation=c.orientation, focal=c.focal,
+                           principal_point=c.principal_point, resolution=c.resolution, near=c.near)
+                    for c in cams]
+            rng = np.random.default_rng(seed)
+            # f32-representable targets: the device keeps targets in f32
+            targets = [np.clip(rng.normal(0.5, 0.2, (res[1], res[0], 3)), 0, 1).astype(np.float32)
+                       .astype(np.float64) for _ in cams]
+            nrec = sum(s.subtree_size for s in hs2.spts)
+            budget = int(bfrac * nrec * 92)
+            tcfg = TR.TrainConfig(total_iterations=steps, lod=lod,
+                                  cache=CacheConfig(budget_bytes=budget, flush_interval=flush),
+                                  scheduler_k=k, seed=seed)
+            graph = build_view_graph(np.stack([c.position for c in cams]), k=k)
+            extent = 2.0 * E
+            st = TR.TrainState(config=tcfg, hierarchy=h2, hspt=hs2, scene=scene,
+                               cache=DeviceCache(config=tcfg.cache), graph=graph,
+                               views=list(zip(cams, targets)), opt=TR.OptimizerState.zeros(h2.attrs),
+                               rng=np.random.default_rng(seed), extent=extent,
+                               skybox_ids=np.zeros(0, dtype=np.int64))
+            p = f"c{case}_"
+            d[p + "file"] = np.frombuffer(file_bytes, dtype=np.uint8)
+            d.update({p + k2: v for k2, v in hier_arrays(h2).items()})
+            d.update({p + k2: v for k2, v in hspt_arrays(hs2).items()})
+            for v, c in enumerate(cams):
+                d.update(cam_arrays(c, p + f"cam{v}_"))
+            d[p + "targets"] = np.stack(targets).astype(np.float32)
+            d[p + "n_views"] = np.int64(nviews)
+            d[p + "budget"] = np.int64(budget)
+            d[p + "flush"] = np.int64(flush)
+            d[p + "k"] = np.int64(k)
+            d[p + "seed"] = np.int64(seed)
+            d[p + "extent"] = np.float64(extent)
+            d[p + "steps"] = np.int64(steps)
+            d[p + "lod_T"] = np.float64(lod.threshold)
+            d[p + "lod_metric"] = np.int64(0 if lod.metric == "max_scale" else 1)
+            checkpoints = (1, steps)
+            counters = []
+            for it in range(1, steps + 1):
+                r = TR.train_step(st, it)
+                counters.append([r["view"], r["gaussians_rendered"], r["gaussians_loaded_from_store"],
+                                 r["cache_hits"], r["bytes_streamed"]])
+                q = p + f"it{it}_"
+                d[q + "loss"] = np.float64(r["loss"])
+                d[q + "rows"] = np.concatenate(cap_rows["rows"]).astype(np.int32)
+                if it <= 2:
+                    d[q + "image"] = cap_rows["image"]
+                    d[q + "grads"] = cap_rows["grads"]
+                if it in checkpoints:
+                    d.update({q + "p_" + k2: np.array(v, copy=True) for k2, v in hier_arrays(h2).items()
+                              if k2 in ("means", "scales", "rotations", "opacities", "base_colors", "sh_rest")})
+                    for k2 in st.opt.m:
+                        d[q + "m_" + k2] = st.opt.m[k2].copy()
+                        d[q + "v_" + k2] = st.opt.v[k2].copy()
+                    d[q + "step"] = st.opt.step.copy()
+                    sc = st.scene
+                    for name, cols in (("means", 3), ("scales", 3), ("rotations", 4), ("opacities", 1),
+                                       ("base_colors", 3), ("sh_rest", 9)):
+                        off, length = sc.sections[name]
+                        d[q + "store_" + name] = np.frombuffer(bytes(sc.backing.buf[off:off + length]),
+                                                               dtype="<f4").copy()
+                    ents = list(st.cache.entries.values())
+                    d[q + "cache_sid"] = np.array([e.spt_id for e in ents], dtype=np.int64)
+                    d[q + "cache_dist"] = np.array([e.cached_distance for e in ents], dtype=np.float64)
+                    d[q + "cache_prefix"] = np.array([e.prefix_len for e in ents], dtype=np.int64)
+                    d[q + "cache_dirty"] = np.array([e.dirty for e in ents], dtype=np.int64)
+                    d[q + "cache_blocks"] = (np.concatenate([np.concatenate(
+                        [np.asarray(getattr(e.block.attrs, nm), np.float64).reshape(e.prefix_len, -1)
+                         for nm in ("means", "scales", "rotations", "opacities", "base_colors", "sh_rest")],
+                        axis=1) for e in ents]) if ents else np.zeros((0, 23)))
+            d[p + "counters"] = np.array(counters, dtype=np.int64)
+            d[p + "checkpoints"] = np.array(checkpoints, dtype=np.int64)
+            d[p + "events"] = np.array([events.get("evict_dirty", 0), events.get("replace_dirty", 0),
+                                        events.get("flush", 0)], dtype=np.int64)
+            print("train case", case, "counters", counters, "events", dict(events))
+    finally:
+        DeviceCache.insert, DeviceCache.tick_and_maybe_flush = orig_insert, orig_tick
+        TR.cut_hspt, TR._spt_positions, TR.render_forward, TR.backward = orig_cut, orig_pos, orig_fwd, orig_bwd
+    d["n_cases"] = np.int64(len(specs))
+    np.savez_compressed(OUT / "train_cases.npz", **d)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -556,3 +726,4 @@ if __name__ == "__main__":
     make_serve_cases()
     make_scenefile_cases()
     make_densify_cases()
+    make_train_cases()
