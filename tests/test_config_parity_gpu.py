@@ -1,0 +1,203 @@
+"""Parity at the BASELINE.json configs, not just at unit size.
+
+  C1  100k leaves (G-spt), 256×256, f=220: 8 scheduled train steps, each
+      checked from an identical state (the oracle re-synced from a snapshot
+      of the device state before every step): counters exact, loss, image
+      ≤ 1e-4 max-abs, gradients ≤ 1e-3 relative, post-step params.
+  C2  1M leaves, one 1080p view (≈260k rendered), device-resident store:
+      render-row ids exact against the C oracle cut, row values exact, image
+      ≤ 1e-4 over the full frame, gradients of the L1+SSIM loss ≤ 1e-3.
+  C4  10M leaves, one 1080p view (≈2.6M rendered, out-of-core store): the
+      GPU renders the whole frame; the oracle composites a 1920×24 strip
+      (every splat clipped to the strip rows — the same per-pixel sequence
+      as the full frame) and the gradients of an upstream that is zero
+      outside the strip.
+
+Gradient criterion: the floor-relaxed check of test_render_gpu
+(|g−g_ref| ≤ 1e-3·(|g_ref| + 1e-2·max|g_ref|)); next to it the pure relative
+error on entries above 1e-6·max is measured and written, with the image
+errors, to gpurun_out/parity_report.jsonl (summarised under profiles/)."""
+from __future__ import annotations
+
+import json
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import glod_oracle as O  # noqa: E402
+from oracle.train_oracle import OracleTrainer  # noqa: E402
+from paper_2507_01110_b200.cache import CacheConfig  # noqa: E402
+from paper_2507_01110_b200.core import SECTIONS, AttributeArrays, Frustum  # noqa: E402
+from paper_2507_01110_b200.scenegen import SceneSpec, designed_scene, orbit_views, scene_extent  # noqa: E402
+from paper_2507_01110_b200.trainer import TrainConfig, Trainer  # noqa: E402
+
+from .test_render_gpu import assert_grads_close  # noqa: E402
+from .test_train_gpu import _dict, restore, snapshot  # noqa: E402
+
+NAMES = [n for n, _ in SECTIONS]
+REPORT = Path(os.environ.get("GLOD_PARITY_REPORT", Path(__file__).resolve().parent.parent / "gpurun_out"
+                             / "parity_report.jsonl"))
+
+
+def grad_stats(got, want):
+    """Pure relative error on entries above 1e-6·max (per attribute)."""
+    out = {}
+    for k in NAMES:
+        g = np.asarray(getattr(got, k) if not isinstance(got, dict) else got[k], np.float64).ravel()
+        w = np.asarray(want[k], np.float64).ravel()
+        m = np.abs(w).max() if w.size else 0.0
+        sel = np.abs(w) > 1e-6 * m
+        rel = np.abs(g[sel] - w[sel]) / np.abs(w[sel]) if sel.any() else np.zeros(1)
+        out[k] = {"n": int(sel.sum()), "max_rel": float(rel.max()), "p999_rel": float(np.quantile(rel, 0.999)),
+                  "p99_rel": float(np.quantile(rel, 0.99))}
+    return out
+
+
+def report(rec):
+    try:
+        REPORT.parent.mkdir(parents=True, exist_ok=True)
+        with open(REPORT, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+    except OSError:
+        pass
+
+
+def oracle_cut(h, hs, cfg, cam):
+    flat = hs.flat_records()
+    kind = np.full(h.capacity, -1, np.int32)
+    kind[flat["roots"]] = np.arange(flat["roots"].size)
+    kind[hs.passthrough_roots] = -2
+    return O.cut_hspt(h.root, h.children, kind, h.attrs.means, h.attrs.scales, flat["offset"], flat["count"],
+                      flat["roots"], flat["centers"], flat["key_self"], flat["key_parent"], flat["nodes"],
+                      cam.position, cfg.threshold, cfg.metric_code, Frustum.from_camera(cam).planes)
+
+
+def test_c1_train_steps_match_oracle():
+    n = 100_000
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=n, spt_leaves=4096, seed=11))
+    E = scene_extent(n)
+    cams = orbit_views(32, 1.3 * E, 0.7 * E, resolution=(256, 256), focal=(220.0, 220.0), seed=11,
+                       jitter=0.15, target_jitter=0.1 * E)
+    rng = np.random.default_rng(11)
+    targets = [np.clip(rng.normal(0.5, 0.2, (256, 256, 3)), 0, 1).astype(np.float32).astype(np.float64)
+               for _ in cams]
+    records = hs.flat_records()["nodes"].size
+    budget = int(0.5 * records * 92)
+    tcfg = TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=budget, flush_interval=5), scheduler_k=16, seed=11)
+    tr = Trainer(h, hs, list(zip(cams, targets)), tcfg, extent=2 * E)
+    flat = hs.flat_records()
+    kind = np.full(h.capacity, -1, np.int32)
+    kind[flat["roots"]] = np.arange(flat["roots"].size)
+    kind[hs.passthrough_roots] = -2
+    st = tr.scene.store
+    lrs = dict(tcfg.learning_rates)
+    lrs["means"] *= 2 * E
+    orc = OracleTrainer(_dict(h.attrs), h.children, h.root, kind, flat, [s.cpu().numpy() for s in st.sections],
+                        [st.spt_slot_start(i) for i in range(len(hs.spts))],
+                        [(O.Cam.of(c), t) for c, t in zip(cams, targets)], cfg.threshold, cfg.metric_code, budget,
+                        flush_interval=5, lrs=lrs)
+    rec = {"config": "C1", "leaves": n, "resolution": [256, 256], "steps": []}
+    for it in range(1, 9):
+        snap = snapshot(tr)
+        got = tr.train_step(it)
+        restore(orc, snap)
+        want, extra = orc.train_step(it, view=got["view"])
+        where = f"C1 step {it}"
+        for k in ("view", "gaussians_rendered", "gaussians_loaded_from_store", "cache_hits", "bytes_streamed"):
+            assert got[k] == want[k], (where, k, got[k], want[k])
+        assert abs(got["loss"] - want["loss"]) <= 1e-5 * abs(want["loss"]), where
+        img_err = float(np.abs(tr._last_image.cpu().numpy() - extra["image"]).max())
+        assert img_err <= 1e-4, (where, img_err)
+        np.testing.assert_array_equal(tr._last_rows.cpu().numpy(), extra["row_nodes"], err_msg=where)
+        R = got["gaussians_rendered"]
+        g = AttributeArrays.from_packed(tr._last_grads[:23 * R].cpu().numpy(), R)
+        assert_grads_close(g, extra["grads"], where=where)
+        rec["steps"].append({"view": got["view"], "rendered": R, "loaded": got["gaussians_loaded_from_store"],
+                             "hits": got["cache_hits"], "image_max_abs": img_err,
+                             "loss_rel": abs(got["loss"] - want["loss"]) / abs(want["loss"]),
+                             "grad_rel_above_1e-6max": grad_stats(g, extra["grads"])})
+    assert sum(s["loaded"] for s in rec["steps"]) > 0 and sum(s["hits"] for s in rec["steps"]) > 0
+    report(rec)
+
+
+def _render_and_check(tr, h, hs, cfg, cam, view, rows=None, tag=""):
+    """GPU: cut + gather + full-frame forward, loss gradient, backward.
+    Oracle: the same rows (ids checked against the C oracle cut), forward
+    (optionally on a row strip) and backward of the same upstream."""
+    w, hh = cam.resolution
+    img = tr.render_view(view)
+    R = tr.last_render["gaussians_rendered"]
+    ids = tr._row_node[:R].cpu().numpy().astype(np.int64)
+    rs = oracle_cut(h, hs, cfg, cam)
+    want_ids = np.concatenate([rs["upper"], rs["passthrough"]] + list(rs["selected"])).astype(np.int64)
+    np.testing.assert_array_equal(ids, want_ids, err_msg=f"{tag} render-row ids")
+    A = AttributeArrays.from_packed(tr._rows[:23 * R].cpu().numpy(), R)
+    n_mem = rs["upper"].size + rs["passthrough"].size
+    for k in NAMES:   # upper/passthrough rows from the f64 master, SPT rows f32 from the store
+        src = np.asarray(getattr(h.attrs, k))[want_ids]
+        src = np.concatenate([src[:n_mem], src[n_mem:].astype(np.float32).astype(np.float64)])
+        np.testing.assert_array_equal(getattr(A, k), src, err_msg=f"{tag} row values {k}")
+    rng = np.random.default_rng(5)
+    target = torch.from_numpy(np.clip(rng.normal(0.5, 0.2, (hh, w, 3)), 0, 1).astype(np.float32)).cuda()
+    _, dimg = tr.rast.loss(img, target, 0.2)
+    up = dimg.clone()
+    if rows is not None:
+        up[:rows[0]] = 0
+        up[rows[1]:] = 0
+    grads = tr.rast.backward(up)
+    torch.cuda.synchronize()
+    Ad = {k: getattr(A, k) for k in NAMES}
+    ref_img, octx = O.render_forward(Ad, O.Cam.of(cam), rows=rows)
+    gpu_img = img.cpu().numpy().astype(np.float64)
+    if rows is not None:
+        gpu_img, ref_cmp = gpu_img[rows[0]:rows[1]], ref_img[rows[0]:rows[1]]
+    else:
+        ref_cmp = ref_img
+    err = float(np.abs(gpu_img - ref_cmp).max())
+    assert err <= 1e-4, (tag, err)
+    gref = O.backward(octx, up.cpu().numpy().astype(np.float64))
+    g = AttributeArrays.from_packed(grads[:23 * R].cpu().numpy(), R)
+    if rows is not None:
+        # only the splats that reach the strip carry gradient
+        touched = np.zeros(R, bool)
+        for s in octx["splats"]:
+            touched[s[0]] = True
+        assert not np.any(np.abs(np.stack([np.abs(getattr(g, k)).reshape(R, -1).max(1) for k in NAMES], 1)
+                                 .max(1)[~touched]) > 0), f"{tag}: gradient outside the strip"
+    assert_grads_close(g, gref, where=tag)
+    return {"rendered": int(R), "image_max_abs": err, "strip_rows": list(rows) if rows else None,
+            "splats_composited": len(octx["splats"]), "grad_rel_above_1e-6max": grad_stats(g, gref)}
+
+
+def test_c2_1080p_view_matches_oracle():
+    n = 1_000_000
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=n, spt_leaves=4096, seed=1), device="cuda")
+    E = scene_extent(n)
+    cams = orbit_views(4, 1.3 * E, 0.7 * E, resolution=(1920, 1080), seed=1, jitter=0.15, target_jitter=0.1 * E)
+    records = hs.flat_records()["nodes"].size
+    tr = Trainer(h, hs, [(c, np.zeros((1080, 1920, 3), np.float32)) for c in cams],
+                 TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=2 * records * 92), store_location="device"),
+                 extent=2 * E)
+    rec = _render_and_check(tr, h, hs, cfg, cams[0], 0, tag="C2 view 0")
+    assert rec["rendered"] > 100_000
+    rec.update({"config": "C2", "leaves": n, "resolution": [1920, 1080]})
+    report(rec)
+
+
+def test_c4_1080p_strip_matches_oracle():
+    n = 10_000_000
+    h, hs, cfg = designed_scene(SceneSpec(n_leaves=n, spt_leaves=8192, seed=0), device="cuda")
+    E = scene_extent(n)
+    cams = orbit_views(4, 1.3 * E, 0.7 * E, resolution=(1920, 1080), seed=0, jitter=0.15, target_jitter=0.1 * E)
+    tr = Trainer(h, hs, [(c, np.zeros((1080, 1920, 3), np.float32)) for c in cams],
+                 TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=1 << 30)), extent=2 * E)
+    rows = (528, 552)                      # a 24-row strip through the image centre
+    rec = _render_and_check(tr, h, hs, cfg, cams[1], 1, rows=rows, tag="C4 view 1 strip")
+    assert rec["rendered"] > 1_000_000
+    rec.update({"config": "C4", "leaves": n, "resolution": [1920, 1080]})
+    report(rec)
