@@ -284,6 +284,9 @@ typedef struct glod_gather_plan {
   const int64_t* seg_rows;      /* [dev] [n_spt] rows (prefix_len) per block  */
   int64_t master_stride;        /* 0: master is a packed section-major block;
                                    GLOD_NODE_RECORD: node records            */
+  int32_t spt_from_master;      /* 1: SPT rows read from the master too (view-
+                                   sharded training: the replicated node
+                                   records are authoritative, csrc/exchange.cu) */
 } glod_gather_plan;
 
 /* AttributeArrays.concat of the render set into `out` (packed f64, R =
@@ -317,6 +320,54 @@ int glod_refresh_resident_blocks(const double* master, int64_t capacity, int64_t
                                  const int32_t* spt_of_node, const int32_t* rec_of_node,
                                  const uint64_t* res_block, const int64_t* res_rows, int32_t* touched,
                                  void* stream);
+/* ======================================================================= *
+ * K11-exchange: sparse gradient exchange of view-sharded training (SURVEY
+ * §8e, csrc/exchange.cu).  No reference counterpart (the reference has no
+ * multi-device path); it replaces the python all-reduce of
+ * round 1 (parallel.sparse_grad_allreduce).  Contract: the gradient ADAM
+ * applies to node i = Σ over ranks of that step's per-view gradients.
+ * Ownership: owner(id) = (id >> 5) mod nranks.  U = the union of every
+ * rank's render-row ids, laid out owner-major (owner chunks, each sorted).
+ * ======================================================================= */
+typedef struct glod_xchg glod_xchg;
+/* ncclGetUniqueId into 128 bytes (rank 0 creates, the caller broadcasts). */
+int glod_nccl_unique_id(void* out128);
+/* Exchange context for `nranks` ranks over node ids [0, capacity).  With a
+ * unique id, the context owns an NCCL communicator (ncclCommInitRank) and
+ * the composed calls below are available; with NULL only the phase calls
+ * (transport supplied by the caller). */
+int glod_xchg_create(int32_t nranks, int32_t rank, int64_t capacity, const void* nccl_id128,
+                     glod_xchg** out);
+int glod_xchg_destroy(glod_xchg* x);
+/* Phases 1-4 over NCCL: all-gather of the row ids, on-device union,
+ * gradients (packed section-major, R rows) bucketed by owner and sent
+ * point to point (grouped ncclSend/ncclRecv), summed by the owner source by
+ * source.  *n_owned = rows of this rank's chunk (glod_xchg_owned). */
+int glod_grad_exchange(glod_xchg* x, const int32_t* row_node, const double* grads, int64_t R,
+                       int64_t* n_owned, void* stream);
+/* Phase 5 over NCCL: each owner's updated attribute rows (first 23 values
+ * of its node records, after ADAM) broadcast; every rank writes all of U
+ * into its node records (stride in doubles). */
+int glod_param_allgather(glod_xchg* x, double* records, int64_t stride, void* stream);
+/* The phases, for a caller-supplied transport.  union: ids_all [dev] n
+ * gathered ids (-1 = padding) -> owner_off [host] nranks+1 offsets (syncs). */
+int glod_xchg_union(glod_xchg* x, const int32_t* ids_all, int64_t n, int64_t* owner_off, void* stream);
+int glod_xchg_union_ids(glod_xchg* x, const int32_t** ids, int64_t* n);
+/* pack: this rank's rows bucketed by owner into wire rows of 24 f64
+ * (owner-local position, 23 gradients); counts [host] nranks (syncs). */
+int glod_xchg_pack(glod_xchg* x, const int32_t* row_node, const double* grads, int64_t R, int64_t* counts,
+                   const double** send, void* stream);
+int glod_xchg_begin_accumulate(glod_xchg* x, double** acc, int64_t* n_owned, void* stream);
+/* add one source's received wire rows (call once per source, rank order) */
+int glod_xchg_accumulate(glod_xchg* x, const double* rows, int64_t m, void* stream);
+int glod_xchg_owned(glod_xchg* x, const int32_t** ids, const double** grads, int64_t* n);
+/* pack_params: this rank's chunk of the |U| x 23 row-major buffer from the
+ * node records; scatter_params: all of it back into the node records. */
+int glod_xchg_pack_params(glod_xchg* x, const double* records, int64_t stride, double** params, void* stream);
+int glod_xchg_scatter_params(glod_xchg* x, double* records, int64_t stride, void* stream);
+/* {|U|, owned rows, bytes sent, bytes received} of the last step. */
+int glod_xchg_stats(glod_xchg* x, int64_t* out4);
+
 /* Elementwise f32 -> f64 (to_f64=1) or f64 -> f32 (store write-back). */
 int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* stream);
 

@@ -9,6 +9,8 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
+import numpy as np
+
 import os
 
 # GLOD_LIB: an alternative build of the same library (kernel variants for
@@ -79,7 +81,7 @@ class GatherPlan(C.Structure):
     _fields_ = [("master", P), ("capacity", C.c_int64), ("upper_ids", P), ("pass_ids", P),
                 ("n_upper", C.c_int32), ("n_pass", C.c_int32), ("sel_seg", P), ("sel_pos", P),
                 ("sel_node", P), ("n_sel", C.c_int64), ("seg_block", P), ("seg_rows", P),
-                ("master_stride", C.c_int64)]
+                ("master_stride", C.c_int64), ("spt_from_master", C.c_int32)]
 
 
 class StoreView(C.Structure):
@@ -144,6 +146,20 @@ SIGNATURES = {
     "glod_cache_materialize": (C.c_int, [P, P]),
     "glod_cache_entries": (C.c_int, [P, P, P, P, P, P, C.c_int64]),
     "glod_memcpy_d2h": (C.c_int, [P, P, C.c_int64]),
+    "glod_nccl_unique_id": (C.c_int, [P]),
+    "glod_xchg_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, P, C.POINTER(P)]),
+    "glod_xchg_destroy": (C.c_int, [P]),
+    "glod_grad_exchange": (C.c_int, [P, P, P, C.c_int64, C.POINTER(C.c_int64), P]),
+    "glod_param_allgather": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_xchg_union": (C.c_int, [P, P, C.c_int64, C.POINTER(C.c_int64), P]),
+    "glod_xchg_union_ids": (C.c_int, [P, C.POINTER(P), C.POINTER(C.c_int64)]),
+    "glod_xchg_pack": (C.c_int, [P, P, P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(P), P]),
+    "glod_xchg_begin_accumulate": (C.c_int, [P, C.POINTER(P), C.POINTER(C.c_int64), P]),
+    "glod_xchg_accumulate": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_xchg_owned": (C.c_int, [P, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int64)]),
+    "glod_xchg_pack_params": (C.c_int, [P, P, C.c_int64, C.POINTER(P), P]),
+    "glod_xchg_scatter_params": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_xchg_stats": (C.c_int, [P, P]),
     "glod_readback": (C.c_int, [P, P, C.c_int64, P]),
     "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
     "glod_sort_pairs_u64": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
@@ -206,6 +222,24 @@ def stream_ptr(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+class _DevArray:
+    """__cuda_array_interface__ over a library-owned device buffer, so
+    torch.as_tensor can view it without a copy."""
+
+    def __init__(self, addr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"data": (int(addr), False), "shape": tuple(int(x) for x in shape),
+                                         "typestr": typestr, "version": 3, "strides": None}
+
+
+def device_view(addr: int, shape, dtype):
+    """A torch tensor viewing `addr` (device memory owned by the library)."""
+    import torch
+    typestr = {torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8", torch.float32: "<f4"}[dtype]
+    if int(np.prod(shape)) == 0 or not addr:
+        return torch.empty(shape, dtype=dtype, device="cuda")
+    return torch.as_tensor(_DevArray(addr, shape, typestr), device="cuda")
 
 
 def readback(host_pinned, src, nbytes: int | None = None, stream=None):

@@ -19,11 +19,20 @@ OBJ = ROOT / "build" / "obj"
 LIB = PKG / "libglod_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+_NCCL = Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / "site-packages" / "nvidia" / "nccl"
+if not (_NCCL / "include" / "nccl.h").exists():
+    import site
+    for sp in site.getsitepackages():
+        if (Path(sp) / "nvidia" / "nccl" / "include" / "nccl.h").exists():
+            _NCCL = Path(sp) / "nvidia" / "nccl"
+# NCCL: the torch-bundled build (the same libnccl.so.2 torch.distributed loads)
+NCCL_INC, NCCL_LIB = _NCCL / "include", _NCCL / "lib"
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-    f"-I{ROOT / 'include'}", f"-I{CSRC}",
+    f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{NCCL_INC}",
 ]
 
 
@@ -59,7 +68,8 @@ def build(verbose: bool = False) -> Path:
         objs = list(ex.map(lambda s: _compile(s, True), srcs))
     if _stale(LIB, objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
-               *[str(o) for o in objs], "-o", str(LIB), "-lcudart"]
+               *[str(o) for o in objs], "-o", str(LIB), "-lcudart",
+               f"-L{NCCL_LIB}", "-l:libnccl.so.2", f"-Xlinker=-rpath={NCCL_LIB}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

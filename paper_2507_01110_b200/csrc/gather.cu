@@ -61,7 +61,7 @@ GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
     node = p.sel_node[k];
     const double* blk = reinterpret_cast<const double*>(p.seg_block[j]);
     const long long P = p.seg_rows[j], pos = p.sel_pos[k];
-    if (row_touched(blk, P, pos)) s = {p.master, master_rows(p), node};
+    if (p.spt_from_master || row_touched(blk, P, pos)) s = {p.master, master_rows(p), node};
     else s = {blk, P, pos};
   }
   return s;

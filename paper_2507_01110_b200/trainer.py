@@ -166,7 +166,7 @@ class Trainer:
         self.cfg = cfg
         # view sharding: with an initialised process group of >1 ranks each
         # step's gradients are summed over ranks on the union of touched
-        # nodes (parallel.sparse_grad_allreduce) before a replicated ADAM
+        # nodes and ADAM runs owner-sharded (parallel.py, csrc/exchange.cu)
         self.group = group
         self.distributed = dist.is_available() and dist.is_initialized() and \
             dist.get_world_size(group) > 1
@@ -176,6 +176,9 @@ class Trainer:
         self.cache = NativeCache(cfg.cache, self.scene.store)
         self._register_master()
         self.rast = Rasterizer()
+        if self.distributed:
+            from .parallel import make_exchange
+            self.xchg = make_exchange(self.scene.cap, group)
         self.views = [(Camera.from_any(c), t) for c, t in views]
         pos = np.stack([c.position for c, _ in self.views])
         # the drop-in (train_step(state, it)) passes the reference state's own
@@ -264,6 +267,12 @@ class Trainer:
         empty, byte counters survive)."""
         from .densify import Moments, densify_tree
         from .hspt import build_hspt
+        if self.distributed:
+            # the ranks' moments live with their owners and the tree surgery
+            # draws on the scheduler RNG, which differs per rank: a sharded
+            # densify would give every rank a different hierarchy
+            raise NotImplementedError("densify in view-sharded training: gather the state on one rank "
+                                      "(sync_state) and densify there")
         torch.cuda.synchronize()
         sc, h = self.scene, self.hierarchy
         rec = sc.records.cpu().numpy()
@@ -360,42 +369,6 @@ class Trainer:
         return t
 
     # ------------------------------------------------------------------
-    def _refresh_union(self, ids: torch.Tensor):
-        """View-sharded step: every resident cache block of this rank takes
-        the new master values of the rows any rank updated (the union `ids`);
-        touched SPTs are marked dirty before the next step's decisions."""
-        sc, dev = self.scene, self.scene.device
-        hs = sc.hspt
-        S = len(hs.spts)
-        if getattr(self, "_spt_of_node", None) is None:
-            flat = hs.flat_records()
-            spt_of = np.full(sc.cap, -1, dtype=np.int32)
-            rec_of = np.full(sc.cap, -1, dtype=np.int32)
-            for k in range(S):
-                o, c = int(flat["offset"][k]), int(flat["count"][k])
-                nodes = flat["nodes"][o:o + c]
-                spt_of[nodes] = k
-                rec_of[nodes] = np.arange(c, dtype=np.int32)
-            self._spt_of_node = torch.from_numpy(spt_of).to(dev)
-            self._rec_of_node = torch.from_numpy(rec_of).to(dev)
-            S1 = max(S, 1)
-            self._h_res = torch.empty(2 * S1, dtype=torch.int64).pin_memory()
-            self._d_res = torch.empty(2 * S1, dtype=torch.int64, device=dev)
-            self._d_touched = torch.zeros(S1, dtype=torch.int32, device=dev)
-            self._h_touched = torch.zeros(S1, dtype=torch.int32).pin_memory()
-        S1 = max(S, 1)
-        hr = self._h_res.numpy()
-        self.cache.resident(hr[:S1].view(np.uint64), hr[S1:])
-        self._d_res.copy_(self._h_res, non_blocking=True)
-        self._d_touched.zero_()
-        _lib.check(_lib.lib().glod_refresh_resident_blocks(
-            _lib.ptr(sc.records), sc.cap, NODE_RECORD, _lib.ptr(ids), int(ids.numel()),
-            _lib.ptr(self._spt_of_node),
-            _lib.ptr(self._rec_of_node), _lib.ptr(self._d_res), _lib.ptr(self._d_res[S1:]),
-            _lib.ptr(self._d_touched), _lib.stream_ptr()))
-        _lib.readback(self._h_touched, self._d_touched)
-        self._touched_pending = True
-
     def select(self, cam: Camera, spec_cam: Camera | None = None):
         """LoD select + one D2H of the per-SPT table (the step's host sync).
         With `spec_cam`, a speculative select of that (predicted next) view
@@ -445,10 +418,6 @@ class Trainer:
         self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
         S1 = max(sc.lod.S, 1)
-        if getattr(self, "_touched_pending", False):
-            # last step's union refresh (read back under this step's sync)
-            self.cache.mark_dirty(self._h_touched.numpy())
-            self._touched_pending = False
         hd, hb = self._h_dist.numpy(), self._h_blk.numpy()
         loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
         if view is not None:
@@ -476,7 +445,7 @@ class Trainer:
             pass_ids=_lib.ptr(sel.passthrough), n_upper=n_up, n_pass=n_pa,
             sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
             n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]),
-            master_stride=NODE_RECORD)
+            master_stride=NODE_RECORD, spt_from_master=int(self.distributed))
         _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
                                                       _lib.stream_ptr()))
         self._mark("gather")
@@ -556,14 +525,13 @@ class Trainer:
                                      f"{self.current_view} with {R} gaussians")
         bias, blen = self._bias_table(iteration)
         if self.distributed:
-            from .parallel import sparse_grad_allreduce
-            U, GU = sparse_grad_allreduce(row_node[:R], grads, R, self.group)
-            ids = U.to(torch.int32)
-            nU = int(ids.numel())
-            _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(ids), _lib.ptr(GU),
-                                                None, nU, nU, self.lrs, _lib.ptr(bias), blen, None, st))
-            self._refresh_union(ids)
-            self._last_union = (ids, GU)
+            # sparse exchange: owner sums + owner-sharded ADAM + replication
+            # of the updated rows (parallel.py)
+            self.xchg.reduce(row_node[:max(R, 1)], grads, R)
+            ids, G, n_own = self.xchg.owned()
+            _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(ids), _lib.ptr(G),
+                                                None, n_own, n_own, self.lrs, _lib.ptr(bias), blen, None, st))
+            self.xchg.allgather_params(sc.records, NODE_RECORD)
         else:
             _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(row_node),
                                                 _lib.ptr(grads), None, R, R, self.lrs, _lib.ptr(bias), blen,
