@@ -267,9 +267,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    shared_gpu = world > ndev
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU over NCCL (the exchange's NCCL communicator lives
+        # in the C library); more ranks than GPUs (a 1-GPU box): the group
+        # runs gloo around the same device phases (NCCL refuses a duplicate
+        # device) — a functional run, reported as such
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     h, hs, cfg, cams, E, build_s = make_workload(args, device="cuda")
     targets = synthetic_targets(len(cams), args.width, args.height, args.seed)
     tcfg = TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=args.budget_mb << 20),
@@ -411,6 +420,10 @@ def run_ours(args):
                    "leaves": args.leaves, "nodes": int(tr.scene.cap), "resolution": [args.width, args.height],
                    "views": args.views, "cache_budget_mb": args.budget_mb, "spts": int(tr.scene.lod.S),
                    "spt_records": int(tr.scene.lod.R), "parallelism": f"views x{world}",
+                   "transport": ("single GPU" if world == 1 else
+                                 f"gloo, {world} ranks sharing {ndev} GPU(s)" if shared_gpu else
+                                 "NCCL (glod_grad_exchange / glod_param_allgather)"),
+                   "exchange": (tr.xchg.stats() if world > 1 else None),
                    "render_set": stats.get("rendered"), "n_spt_selected": stats.get("n_spt"),
                    "prefix_total": stats.get("prefix_total"), "n_instances": stats.get("n_instances"),
                    "loaded_last_step": recs[-1]["gaussians_loaded_from_store"],
@@ -535,8 +548,23 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _relaunch_distributed(args) -> int:
+    """`--gpus N` without a torchrun environment: re-exec this script as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     else:

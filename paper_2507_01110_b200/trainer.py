@@ -176,6 +176,10 @@ class Trainer:
         self.cache = NativeCache(cfg.cache, self.scene.store)
         self._register_master()
         self.rast = Rasterizer()
+        # SPT render rows from the master records instead of the cache
+        # blocks: required when ranks share updates (the replicated records
+        # are authoritative); selectable on one GPU for comparisons
+        self.spt_from_master = self.distributed
         if self.distributed:
             from .parallel import make_exchange
             self.xchg = make_exchange(self.scene.cap, group)
@@ -445,7 +449,7 @@ class Trainer:
             pass_ids=_lib.ptr(sel.passthrough), n_upper=n_up, n_pass=n_pa,
             sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
             n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]),
-            master_stride=NODE_RECORD, spt_from_master=int(self.distributed))
+            master_stride=NODE_RECORD, spt_from_master=int(self.spt_from_master))
         _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
                                                       _lib.stream_ptr()))
         self._mark("gather")
@@ -528,15 +532,18 @@ class Trainer:
             # sparse exchange: owner sums + owner-sharded ADAM + replication
             # of the updated rows (parallel.py)
             self.xchg.reduce(row_node[:max(R, 1)], grads, R)
+            self._mark("exchange")
             ids, G, n_own = self.xchg.owned()
             _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(ids), _lib.ptr(G),
                                                 None, n_own, n_own, self.lrs, _lib.ptr(bias), blen, None, st))
+            self._mark("adam")
             self.xchg.allgather_params(sc.records, NODE_RECORD)
+            self._mark("replicate")
         else:
             _lib.check(L.glod_adam_step_records(_lib.ptr(sc.records), sc.cap, _lib.ptr(row_node),
                                                 _lib.ptr(grads), None, R, R, self.lrs, _lib.ptr(bias), blen,
                                                 C.byref(plan), st))
-        self._mark("adam")
+            self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
         if self._pred is not None:
             # the copy engines fetch the next view's misses while this
