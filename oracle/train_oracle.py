@@ -118,13 +118,24 @@ class OracleTrainer:
                           self.spt["key_self"], self.spt["key_parent"], self.spt["nodes"],
                           cam.position, self.T, self.metric, planes)
 
-    def train_step(self, iteration, view):
+    def train_step(self, iteration, view, timing=None):
         """trainer.train_step (trainer.py:312-378) for the scheduled `view`
         (scheduler.next_view is host code shared by both sides); returns
-        (counters, extras)."""
+        (counters, extras).  `timing` (a dict) receives per-stage seconds
+        (the CPU baseline's breakdown)."""
+        import time
+        clock = [time.perf_counter()]
+
+        def mark(name):
+            if timing is not None:
+                t = time.perf_counter()
+                timing[name] = timing.get(name, 0.0) + t - clock[0]
+                clock[0] = t
+
         self.current_view = view
         cam, target = self.views[self.current_view]
         rs = self.cut(cam)
+        mark("cut")
         bytes_before, hits_before = self.bytes_read, self.hits
         loaded = 0
         mem = np.concatenate([rs["upper"], rs["passthrough"]]).astype(np.int64)
@@ -146,9 +157,15 @@ class OracleTrainer:
             rows.append((e, pos, nodes, off))
             off += pos.size
         A = {k: np.concatenate([p[k] for p in parts]) for k in NAMES}
+        mark("gather")
         img, ctx = O.render_forward(A, cam)
+        mark("forward")
         value, dimg = O.ssim_l1_loss(img, target, self.lam)
+        mark("loss")
         G = O.backward(ctx, dimg)
+        mark("backward")
+        if timing is not None:
+            timing["splats_backward"] = len(ctx["splats"])
         O.adam_update(self.P, self.M, self.V, self.step, mem, G, np.arange(mem.size), self.lrs)
         for e, pos, nodes, o in rows:
             O.adam_update(self.P, self.M, self.V, self.step, nodes, G, np.arange(o, o + pos.size),
@@ -156,12 +173,14 @@ class OracleTrainer:
             for k in NAMES:
                 e[2][k][pos] = self.P[k][nodes]
             e[3] = True
+        mark("adam")
         if iteration % self.flush_interval == 0:
             for sid, e in list(self.cache.items()):
                 if e[3]:
                     self._write_back(sid, e[2])
             self.cache.clear()
             self.resident = 0
+        mark("flush")
         counters = {"iteration": iteration, "view": self.current_view, "loss": float(value),
                     "gaussians_rendered": int(A["means"].shape[0]),
                     "gaussians_loaded_from_store": int(loaded),

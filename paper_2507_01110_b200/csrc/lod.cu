@@ -23,11 +23,7 @@ namespace glod {
 namespace {
 
 constexpr int kSelectThreads = 512;
-constexpr int kCompactThreads = 512;
-constexpr int kRows = 8;                          // items per thread per tile
-constexpr int kTile = kCompactThreads * kRows;    // 4096 virtual records
-constexpr int kAlign = 4;                         // records per lane group (16-B vector loads)
-constexpr int kGroups = 4;                        // groups per lane in flight (K1 phase C)
+constexpr int kAlign = 4;                         // records per group (16-B vector loads)
 constexpr int kMaxLevels = 250;
 
 constexpr uint32_t kPass = 1u << 31;   // entry belongs to a passthrough BFS
@@ -348,297 +344,313 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: order-preserving compaction of every selected prefix.
+// K1: order-preserving compaction of every selected prefix (spt.py:67-75,
+// trainer._spt_positions :302-309), three launches, no grid barriers:
+//   k1a  prefix_kernel  one warp per selected SPT: prefix length (the
+//        caller's, or a 32-ary ballot search of #{key_parent > d}), root
+//        rule, virtual segment length (padded to kAlign records)
+//   k1b  segscan_kernel one CTA: exclusive scan of the segment lengths
+//        (the selected prefixes laid end to end in one virtual space)
+//   k1c  compact_kernel persistent CTAs take 4096-record tiles in order
+//        (atomic ticket), stream each key_self once with 16-B vector loads,
+//        rank the selections with a block scan, get the tile's output
+//        offset by decoupled look-back over the predecessors' published
+//        counts, stage the selections in shared memory and write them as
+//        coalesced runs.
 // ---------------------------------------------------------------------------
+constexpr int kCThreads = 256;
+constexpr int kCGroups = 4;                                  // kAlign-record groups per thread
+constexpr int kCTile = kCThreads * kCGroups * kAlign;        // 4096 virtual records
+constexpr int kSegCache = 128;                               // segments cached per tile
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
 struct CompactScratch {
-  unsigned int* bar;            // [2]
-  unsigned long long* status;   // [max_tiles] decoupled look-back words
-  long long* block_cnt;         // [grid]
+  unsigned int* ticket;         // [1] tile ticket
+  unsigned long long* status;   // [max_tiles] look-back words (flag | value)
   size_t zero_bytes;
 };
 
 size_t max_tiles(int64_t num_records, int32_t S) {
-  return size_t((num_records + S + kTile - 1) / kTile) + 1;
+  return size_t((num_records + int64_t(kAlign) * S + kCTile - 1) / kCTile) + 2;
 }
 
-CompactScratch carve_compact(void* base, int32_t S, int64_t R, int grid) {
+CompactScratch carve_compact(void* base, int32_t S, int64_t R) {
   CompactScratch s;
   char* p = static_cast<char*>(base);
-  s.bar = reinterpret_cast<unsigned int*>(p);
-  size_t off = 256;
-  s.status = reinterpret_cast<unsigned long long*>(p + off);
-  off += 8 * max_tiles(R, S);
-  s.zero_bytes = off;
-  off = align_up(off);
-  s.block_cnt = reinterpret_cast<long long*>(p + off);
+  s.ticket = reinterpret_cast<unsigned int*>(p);
+  s.status = reinterpret_cast<unsigned long long*>(p + 256);
+  s.zero_bytes = 256 + 8 * max_tiles(R, S);
   return s;
 }
 
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
-
-// 4 consecutive keys, aligned by the record layout (device.pad_records)
+// kAlign consecutive keys, aligned by the record layout (device.pad_records)
 GLOD_DEV void load4(const float* p, long long a, float (&v)[4]) {
-  const float4 x = *reinterpret_cast<const float4*>(p + a);
+  const float4 x = __ldcs(reinterpret_cast<const float4*>(p + a));
   v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
 }
 GLOD_DEV void load4(const double* p, long long a, double (&v)[4]) {
-  const double2 x = *reinterpret_cast<const double2*>(p + a);
-  const double2 y = *reinterpret_cast<const double2*>(p + a + 2);
+  const double2 x = __ldcs(reinterpret_cast<const double2*>(p + a));
+  const double2 y = __ldcs(reinterpret_cast<const double2*>(p + a + 2));
   v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
-}
-GLOD_DEV int rootrec_of(const LodScene& sc, const CompactIn& in, int j) {
-  return sc.spt_root_rec[in.spt_ids[j]];
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kCompactThreads, 2)
-compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
-  __shared__ long long sm[kCompactThreads / 32 + 1];
-  __shared__ int cnt[kRows][kCompactThreads / 32];
-  __shared__ long long tile_base_sh;
-  __shared__ int seg_lo_sh, seg_hi_sh;
-  __shared__ long long seg_start_sh, seg_off_sh;
-  __shared__ double seg_d_sh;
-  __shared__ int seg_rr_sh, seg_rootrec_sh;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps = kCompactThreads / 32;
-  const long long gthreads = (long long)gridDim.x * blockDim.x;
+__global__ void __launch_bounds__(256)
+prefix_kernel(LodScene sc, CompactIn in, CompactOut out) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const int n_spt = *in.n_spt;
   const K* key_self = static_cast<const K*>(sc.key_self);
-
-  // phase A: prefix length and root rule per selected SPT (spt.py:70-73);
-  // the prefix comes from the caller when known, else a warp-cooperative
-  // 32-ary search over key_parent (one warp per SPT)
-  {
-    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nw = gthreads >> 5;
-    for (long long j = gw; j < n_spt; j += nw) {
-      const int s = in.spt_ids[j];
-      const double d = in.dist[j];
-      int pl;
-      if (in.known_prefix) {
-        pl = in.known_prefix[j];
-      } else {
-        const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
-        long long a = 0, b = sc.spt_count[s];        // answer in [a, b]
-        while (b - a > 32) {
-          const long long step = (b - a + 31) / 32;
-          const long long probe = a + step * lane;    // lane 0 probes a (known > d or start)
-          const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
-          const unsigned m = __ballot_sync(0xffffffffu, gt);
-          const int last = 31 - __clz(m);             // last probe with key_parent > d
-          const long long na = a + step * last;
-          b = min(b, na + step);
-          a = na;
-        }
-        // finish linearly over ≤ 32 candidates
-        const long long probe = a + lane;
-        const bool gt = probe < b && double(kp[probe]) > d;
+  for (long long j = gw; j < n_spt; j += nw) {
+    const int s = in.spt_ids[j];
+    const double d = in.dist[j];
+    int pl;
+    if (in.known_prefix) {
+      pl = in.known_prefix[j];
+    } else {
+      // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
+      const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
+      long long a = 0, b = sc.spt_count[s];
+      while (b - a > 32) {
+        const long long step = (b - a + 31) / 32;
+        const long long probe = a + step * lane;
+        const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
         const unsigned m = __ballot_sync(0xffffffffu, gt);
-        pl = int(a + __popc(m));
+        const int last = 31 - __clz(m);
+        const long long na = a + step * last;
+        b = min(b, na + step);
+        a = na;
       }
-      const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
-      if (lane == 0) {
-        out.prefix_len[j] = pl;
-        out.root_rule[j] = rr;
-        // virtual segment length, padded to the record alignment so every
-        // segment (and every lane's 4-item group) starts 16-B aligned
-        out.seg_start[j] = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;
-      }
+      const long long probe = a + lane;
+      const bool gt = probe < b && double(kp[probe]) > d;
+      pl = int(a + __popc(__ballot_sync(0xffffffffu, gt)));
     }
-  }
-  grid_sync(ws.bar);
-
-  // phase B: exclusive scan of segment lengths (block partition + offsets)
-  long long lo, hi;
-  block_range(n_spt, blockIdx.x, gridDim.x, lo, hi);
-  {
-    long long c = 0;
-    for (long long j = lo + threadIdx.x; j < hi; j += blockDim.x) c += ld_cg(out.seg_start + j);
-    c = block_sum(c, sm);
-    if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = c;
-  }
-  grid_sync(ws.bar);
-  {
-    long long base = sum_before(ws.block_cnt, blockIdx.x, sm);
-    long long span = hi - lo, chunk = (span + blockDim.x - 1) / blockDim.x;
-    long long j0 = lo + chunk * threadIdx.x, j1 = min(hi, j0 + chunk);
-    long long c = 0;
-    for (long long j = j0; j < j1; ++j) c += ld_cg(out.seg_start + j);
-    long long o = base + block_excl_scan(c, sm);
-    for (long long j = j0; j < j1; ++j) {
-      long long len = ld_cg(out.seg_start + j);
-      out.seg_start[j] = o;
-      o += len;
+    // root rule (spt.py:72-73): d >= key_self[root] selects exactly [root]
+    const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
+    if (lane == 0) {
+      out.prefix_len[j] = pl;
+      out.root_rule[j] = rr;
+      out.seg_start[j] = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;   // length for now
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) out.total[1] = o;
-  }
-  grid_sync(ws.bar);
-
-  // phase C: every warp owns a contiguous range of the virtual record space
-  // (the selected prefixes laid end to end).  C1 counts each warp range's
-  // selections; after a grid barrier each warp's output offset is the sum
-  // of all earlier ranges; C2 re-streams its range and writes the
-  // selections in order.  Inside a range everything is warp-synchronous:
-  // striped coalesced key loads (kUnroll×32 keys in flight per warp),
-  // ballot + popc for the in-order ranks, no block barriers.
-  const long long total = ld_cg(out.total + 1);
-  const long long nwarps_g = (long long)gridDim.x * nwarps;
-  const long long gwarp = (long long)blockIdx.x * nwarps + warp;
-  __shared__ long long wcount[kCompactThreads / 32];
-  // per-warp staging of one lane-group step's selections (≤ 32·kAlign)
-  __shared__ int st_seg[kCompactThreads / 32][32 * kAlign];
-  __shared__ int st_pos[kCompactThreads / 32][32 * kAlign];
-  __shared__ int st_node[kCompactThreads / 32][32 * kAlign];
-  // waves small enough that the second pass re-reads the keys from L2
-  const long long wave = sc.key_f64 ? (8ll << 20) : (16ll << 20);
-  long long wave_base = 0;                      // selections before this wave
-  for (long long w_lo = 0; w_lo < total || (total == 0 && w_lo == 0); w_lo += wave) {
-  const long long w_len = min(wave, total - w_lo);
-  // warp ranges in whole kAlign groups (virtual segments are padded to kAlign)
-  const long long g_len = w_len / kAlign;
-  const long long r_lo = w_lo + kAlign * (g_len * gwarp / nwarps_g);
-  const long long r_hi = w_lo + kAlign * (g_len * (gwarp + 1) / nwarps_g);
-  long long run = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) {
-      // offset of this warp range = earlier waves + earlier blocks + earlier warps of this block
-      const long long blk = sum_before(ws.block_cnt, blockIdx.x, sm);
-      const long long all = sum_before(ws.block_cnt, gridDim.x, sm);
-      long long w_before = 0;
-      for (int w = 0; w < warp; ++w) w_before += wcount[w];
-      run = wave_base + blk + w_before;
-      if (threadIdx.x == 0 && blockIdx.x == 0 && w_lo + w_len >= total) out.total[0] = wave_base + all;
-      wave_base += all;
-    }
-    // per-lane segment cursor
-    int j = -1;
-    long long s_start = 0, s_end = -1, off = 0;
-    double d = 0.0;
-    int rr = 0, rootrec = 0, seglen = 0;
-    long long count = 0;
-    for (long long base = r_lo; base < r_hi; base += 32LL * kAlign * kGroups) {
-      // lane-owned groups of kAlign consecutive virtual records; a group
-      // never straddles a segment (segments are padded to kAlign)
-      int segk[kGroups], loc[kGroups], len[kGroups];
-      long long addr[kGroups];
-      bool isrr[kGroups];
-#pragma unroll
-      for (int k = 0; k < kGroups; ++k) {
-        const long long vg = base + ((long long)k * 32 + lane) * kAlign;
-        segk[k] = -1;
-        loc[k] = 0;
-        len[k] = 0;
-        addr[k] = 0;
-        isrr[k] = false;
-        if (vg < r_hi) {
-          if (vg >= s_end) {                         // move the cursor (usually 0-1 steps)
-            if (j < 0 || vg >= s_end + 64 * kAlign) {
-              int a = (j < 0 ? 0 : j), bb = n_spt;
-              while (a < bb) { int m = (a + bb) >> 1; if (ld_cg(out.seg_start + m) <= vg) a = m + 1; else bb = m; }
-              j = a - 1;
-            } else {
-              while (j + 1 < n_spt && ld_cg(out.seg_start + j + 1) <= vg) ++j;
-            }
-            s_start = ld_cg(out.seg_start + j);
-            s_end = j + 1 < n_spt ? ld_cg(out.seg_start + j + 1) : total;
-            const int sp = in.spt_ids[j];
-            off = sc.spt_offset[sp];
-            d = in.dist[j];
-            rr = ld_cg(out.root_rule + j);
-            rootrec = sc.spt_root_rec[sp];
-            seglen = rr ? 1 : ld_cg(out.prefix_len + j);
-          }
-          segk[k] = j;
-          loc[k] = int(vg - s_start);
-          len[k] = seglen;
-          isrr[k] = rr;
-          addr[k] = off + (rr ? rootrec : loc[k]);
-        }
-      }
-      // every group's key vector is requested before any is used
-      K kv[kGroups][kAlign];
-#pragma unroll
-      for (int k = 0; k < kGroups; ++k) load4(key_self, (segk[k] >= 0 && !isrr[k]) ? addr[k] : 0, kv[k]);
-      unsigned mask[kGroups];
-#pragma unroll
-      for (int k = 0; k < kGroups; ++k) {
-        mask[k] = 0;
-        if (segk[k] >= 0) {
-          if (isrr[k]) {
-            mask[k] = 1u;                            // [root] (spt.py:72-73)
-          } else {
-            const double d_k = segk[k] == j ? d : in.dist[segk[k]];
-#pragma unroll
-            for (int e = 0; e < kAlign; ++e)
-              if (loc[k] + e < len[k] && double(kv[k][e]) <= d_k) mask[k] |= 1u << e;
-          }
-        }
-      }
-      if (pass == 0) {
-#pragma unroll
-        for (int k = 0; k < kGroups; ++k) count += __popc(mask[k]);
-        continue;
-      }
-      int4 node[kGroups];
-#pragma unroll
-      for (int k = 0; k < kGroups; ++k) {
-        node[k] = make_int4(0, 0, 0, 0);
-        if (mask[k]) {
-          if (isrr[k]) node[k].x = sc.rec_node[addr[k]];
-          else node[k] = *reinterpret_cast<const int4*>(sc.rec_node + addr[k]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kGroups; ++k) {
-        const int c = __popc(mask[k]);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        // stage the group's selections in order in shared memory, then the
-        // warp writes them out as coalesced runs of the three arrays
-        int o = incl - c;
-        const int nd[4] = {node[k].x, node[k].y, node[k].z, node[k].w};
-#pragma unroll
-        for (int e = 0; e < kAlign; ++e) {
-          if (mask[k] & (1u << e)) {
-            st_seg[warp][o] = segk[k];
-            st_pos[warp][o] = isrr[k] ? rootrec_of(sc, in, segk[k]) : loc[k] + e;
-            st_node[warp][o] = nd[e];
-            ++o;
-          }
-        }
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-        for (int i = lane; i < tot; i += 32) {
-          out.sel_seg[run + i] = st_seg[warp][i];
-          out.sel_pos[run + i] = st_pos[warp][i];
-          out.sel_node[run + i] = st_node[warp][i];
-        }
-        __syncwarp();
-        run += tot;
-      }
-    }
-    if (pass == 0) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
-      if (lane == 0) wcount[warp] = count;
-      __syncthreads();
-      long long c = 0;
-      if (threadIdx.x < nwarps) c = wcount[threadIdx.x];
-      c = block_sum(c, sm);
-      if (threadIdx.x == 0) ws.block_cnt[blockIdx.x] = c;
-      grid_sync(ws.bar);
-    }
-  }
-  grid_sync(ws.bar);            // block_cnt is rewritten by the next wave
-  if (total == 0) break;
   }
 }
+
+__global__ void __launch_bounds__(1024) segscan_kernel(CompactIn in, CompactOut out) {
+  __shared__ long long sm[1024 / 32 + 1];
+  const int n_spt = *in.n_spt;
+  long long carry = 0;
+  for (int base = 0; base < n_spt; base += blockDim.x) {
+    const int j = base + threadIdx.x;
+    const long long len = j < n_spt ? out.seg_start[j] : 0;
+    const long long ex = block_excl_scan(len, sm);
+    const long long tot = sm[(blockDim.x + 31) >> 5];
+    __syncthreads();
+    if (j < n_spt) out.seg_start[j] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    out.total[1] = carry;     // virtual records
+    out.total[0] = 0;         // selections (the last tile overwrites)
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kCThreads, sizeof(K) == 4 ? 4 : 3)
+compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
+  extern __shared__ int stage[];                 // [3][kCTile]: seg, pos, node
+  __shared__ long long sm[kCThreads / 32 + 1];
+  __shared__ long long c_vstart[kSegCache + 1];
+  __shared__ long long c_off[kSegCache];
+  __shared__ double c_d[kSegCache];
+  __shared__ int c_len[kSegCache], c_rr[kSegCache], c_rootrec[kSegCache];
+  __shared__ unsigned int tile_sh;
+  __shared__ int j0_sh, nseg_sh;
+  __shared__ long long excl_sh;
+  const int lane = threadIdx.x & 31;
+  const int n_spt = *in.n_spt;
+  const long long total = out.total[1];
+  const long long ntiles = (total + kCTile - 1) / kCTile;
+  const K* key_self = static_cast<const K*>(sc.key_self);
+  int* st_seg = stage;
+  int* st_pos = stage + kCTile;
+  int* st_node = stage + 2 * kCTile;
+
+  for (;;) {
+    if (threadIdx.x == 0) tile_sh = atomicAdd(ws.ticket, 1u);
+    __syncthreads();
+    const long long tile = tile_sh;
+    if (tile >= ntiles) break;
+    const long long t_lo = tile * kCTile, t_hi = min(total, t_lo + kCTile);
+
+    // segments overlapping the tile -> shared cache (seg_start is sorted)
+    if (threadIdx.x == 0) {
+      int a = 0, b = n_spt;                        // last j with seg_start[j] <= t_lo
+      while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= t_lo) a = m + 1; else b = m; }
+      j0_sh = a - 1;
+    }
+    __syncthreads();
+    const int j0 = j0_sh;
+    int valid = 0;
+    if (threadIdx.x < kSegCache) {
+      const int j = j0 + threadIdx.x;
+      if (j < n_spt && (threadIdx.x == 0 || out.seg_start[j] < t_hi)) {
+        valid = 1;
+        const int sp = in.spt_ids[j];
+        const int rr = out.root_rule[j];
+        c_vstart[threadIdx.x] = out.seg_start[j];
+        c_off[threadIdx.x] = sc.spt_offset[sp];
+        c_d[threadIdx.x] = in.dist[j];
+        c_rr[threadIdx.x] = rr;
+        c_len[threadIdx.x] = rr ? 1 : out.prefix_len[j];
+        c_rootrec[threadIdx.x] = sc.spt_root_rec[sp];
+      }
+    }
+    const int nseg = __syncthreads_count(valid);
+    // more than kSegCache segments start inside this tile: the cached ones
+    // end before the uncached ones start; those groups use a global search
+    const long long cache_end = (j0 + nseg < n_spt) ? out.seg_start[j0 + nseg] : total;
+
+    // keys: kCGroups aligned groups of kAlign records per thread, all loads
+    // issued before any is used
+    int seg[kCGroups], loc[kCGroups], len[kCGroups], rrk[kCGroups], rootrec[kCGroups];
+    long long addr[kCGroups];
+    double dk[kCGroups];
+    int cur = 0;
+#pragma unroll
+    for (int g = 0; g < kCGroups; ++g) {
+      const long long v = t_lo + (long long)(g * kCThreads + threadIdx.x) * kAlign;
+      seg[g] = -1;
+      len[g] = 0;
+      loc[g] = 0;
+      rrk[g] = 0;
+      rootrec[g] = 0;
+      addr[g] = 0;
+      dk[g] = 0.0;
+      if (v < t_hi) {
+        if (v < cache_end) {
+          int a = 0, b = nseg;                     // last cached segment starting <= v
+          while (a < b) { const int m = (a + b) >> 1; if (c_vstart[m] <= v) a = m + 1; else b = m; }
+          cur = a - 1;
+          seg[g] = j0 + cur;
+          loc[g] = int(v - c_vstart[cur]);
+          len[g] = c_len[cur];
+          rrk[g] = c_rr[cur];
+          rootrec[g] = c_rootrec[cur];
+          dk[g] = c_d[cur];
+          addr[g] = c_off[cur] + (rrk[g] ? rootrec[g] : loc[g]);
+        } else {
+          int a = j0 + nseg, b = n_spt;
+          while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= v) a = m + 1; else b = m; }
+          const int j = a - 1;
+          const int sp = in.spt_ids[j];
+          seg[g] = j;
+          loc[g] = int(v - out.seg_start[j]);
+          rrk[g] = out.root_rule[j];
+          len[g] = rrk[g] ? 1 : out.prefix_len[j];
+          rootrec[g] = sc.spt_root_rec[sp];
+          dk[g] = in.dist[j];
+          addr[g] = sc.spt_offset[sp] + (rrk[g] ? rootrec[g] : loc[g]);
+        }
+      }
+    }
+    K kv[kCGroups][kAlign];
+#pragma unroll
+    for (int g = 0; g < kCGroups; ++g)
+      load4(key_self, (seg[g] >= 0 && !rrk[g] && loc[g] < len[g]) ? addr[g] : 0, kv[g]);
+    unsigned mask[kCGroups];
+    int count = 0;
+#pragma unroll
+    for (int g = 0; g < kCGroups; ++g) {
+      mask[g] = 0;
+      if (seg[g] >= 0) {
+        if (rrk[g]) {
+          mask[g] = loc[g] == 0 ? 1u : 0u;         // [root]
+        } else {
+#pragma unroll
+          for (int e = 0; e < kAlign; ++e)
+            if (loc[g] + e < len[g] && double(kv[g][e]) <= dk[g]) mask[g] |= 1u << e;
+        }
+      }
+      count += __popc(mask[g]);
+    }
+    // rank inside the tile: thread order = virtual order (group-major), so
+    // the block scan runs over (group, thread) — one scan per group
+    long long run = 0;
+    long long g_off[kCGroups];
+#pragma unroll
+    for (int g = 0; g < kCGroups; ++g) {
+      const long long c = __popc(mask[g]);
+      g_off[g] = run + block_excl_scan(c, sm);
+      run += sm[kCThreads / 32];
+      __syncthreads();
+    }
+    const long long agg = run;
+
+    // decoupled look-back (warp 0)
+    if (threadIdx.x < 32) {
+      if (lane == 0)
+        atomicExch(ws.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (unsigned long long)agg);
+      long long excl = 0;
+      if (tile > 0) {
+        long long pred = tile - 1;
+        for (;;) {
+          const long long idx = pred - lane;
+          unsigned long long sv = idx >= 0 ? atomicAdd(ws.status + idx, 0ull) : kFlagIncl;
+          while (__any_sync(0xffffffffu, (sv >> 62) == 0)) {
+            if ((sv >> 62) == 0) sv = atomicAdd(ws.status + idx, 0ull);
+          }
+          const unsigned incl = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+          const int first = incl ? __ffs(incl) - 1 : 32;
+          long long v = lane <= first ? (long long)(sv & kValMask) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          excl += v;
+          if (incl) break;
+          pred -= 32;
+        }
+        if (lane == 0) atomicExch(ws.status + tile, kFlagIncl | (unsigned long long)(excl + agg));
+      }
+      if (lane == 0) {
+        excl_sh = excl;
+        if (tile == ntiles - 1) out.total[0] = excl + agg;
+      }
+    }
+    // stage the selections (seg, position in the prefix, node) in order
+#pragma unroll
+    for (int g = 0; g < kCGroups; ++g) {
+      if (!mask[g]) continue;
+      long long o = g_off[g];
+      if (rrk[g]) {
+        st_seg[o] = seg[g];
+        st_pos[o] = rootrec[g];
+        st_node[o] = sc.rec_node[addr[g]];
+      } else {
+        const int4 nd = *reinterpret_cast<const int4*>(sc.rec_node + addr[g]);
+        const int n4[4] = {nd.x, nd.y, nd.z, nd.w};
+#pragma unroll
+        for (int e = 0; e < kAlign; ++e)
+          if (mask[g] & (1u << e)) {
+            st_seg[o] = seg[g];
+            st_pos[o] = loc[g] + e;
+            st_node[o] = n4[e];
+            ++o;
+          }
+      }
+    }
+    __syncthreads();
+    const long long base = excl_sh;
+    for (long long i = threadIdx.x; i < agg; i += kCThreads) {
+      out.sel_seg[base + i] = st_seg[i];
+      out.sel_pos[base + i] = st_pos[i];
+      out.sel_node[base + i] = st_node[i];
+    }
+    __syncthreads();
+  }
+}
+
+constexpr size_t kCompactSmem = 3 * size_t(kCTile) * sizeof(int);
 
 int coop_grid(const void* kernel, int threads) {
   int dev = 0, sms = 0, per_sm = 0;
@@ -663,11 +675,17 @@ size_t select_scratch_bytes(int64_t cap, int32_t S, int grid) {
 }
 
 size_t compact_scratch_bytes(int32_t S, int64_t R, int grid) {
-  return align_up(256 + 8 * max_tiles(R, S)) + 8 * size_t(grid) + 256;
+  (void)grid;
+  return align_up(256 + 8 * max_tiles(R, S)) + 256;
 }
 
 int select_grid() { return coop_grid((const void*)select_kernel, kSelectThreads); }
-int compact_grid() { return coop_grid((const void*)compact_kernel<float>, kCompactThreads); }
+int compact_grid() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms * 4;
+}
 
 cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut& out,
                           void* scratch, size_t scratch_bytes, cudaStream_t st) {
@@ -685,16 +703,26 @@ cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut&
 
 cudaError_t launch_compact(const LodScene& sc, const CompactIn& in, const CompactOut& out,
                            void* scratch, size_t scratch_bytes, cudaStream_t st) {
-  const int grid = compact_grid();
-  if (scratch_bytes < compact_scratch_bytes(sc.num_spts, sc.num_records, grid)) return cudaErrorInvalidValue;
-  CompactScratch ws = carve_compact(scratch, sc.num_spts, sc.num_records, grid);
+  if (scratch_bytes < compact_scratch_bytes(sc.num_spts, sc.num_records, 0)) return cudaErrorInvalidValue;
+  CompactScratch ws = carve_compact(scratch, sc.num_spts, sc.num_records);
   cudaError_t e = cudaMemsetAsync(scratch, 0, ws.zero_bytes, st);
   if (e != cudaSuccess) return e;
-  LodScene a = sc; CompactIn b = in; CompactOut c = out; CompactScratch d = ws;
-  void* args[] = {&a, &b, &c, &d};
-  count_launch();
-  const void* fn = sc.key_f64 ? (const void*)compact_kernel<double> : (const void*)compact_kernel<float>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kCompactThreads), args, 0, st);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(compact_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactSmem));
+    cudaFuncSetAttribute(compact_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactSmem));
+    attr_set = true;
+  }
+  const int S = sc.num_spts > 0 ? sc.num_spts : 1;
+  const unsigned pgrid = unsigned((S + 7) / 8);
+  if (sc.key_f64) prefix_kernel<double><<<pgrid, 256, 0, st>>>(sc, in, out);
+  else prefix_kernel<float><<<pgrid, 256, 0, st>>>(sc, in, out);
+  segscan_kernel<<<1, 1024, 0, st>>>(in, out);
+  const unsigned grid = unsigned(compact_grid());
+  if (sc.key_f64) compact_kernel<double><<<grid, kCThreads, kCompactSmem, st>>>(sc, in, out, ws);
+  else compact_kernel<float><<<grid, kCThreads, kCompactSmem, st>>>(sc, in, out, ws);
+  count_launch(3);
+  return cudaGetLastError();
 }
 
 }  // namespace glod
