@@ -182,6 +182,10 @@ typedef struct glod_render_stats {
   int64_t n_gaussians;          /* rows in the render set                    */
   int64_t n_instances;          /* (gaussian, 16x16 tile) pairs              */
   int32_t tiles_x, tiles_y;
+  int32_t depth_full_sort;      /* 1: near-tied depths formed long runs and the
+                                   depth order was finished with full-width
+                                   radix passes (K6)                          */
+  int32_t reserved;
 } glod_render_stats;
 
 int glod_raster_create(glod_raster** out);

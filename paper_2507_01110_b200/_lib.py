@@ -74,7 +74,8 @@ class Camera(C.Structure):
 
 class RenderStats(C.Structure):
     _fields_ = [("n_gaussians", C.c_int64), ("n_instances", C.c_int64),
-                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32)]
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("depth_full_sort", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class GatherPlan(C.Structure):

@@ -523,6 +523,19 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
   cudaError_t e = c->init(sv);
   if (e == cudaSuccess) e = c->issue_pending();       // end_step was skipped
   if (e != cudaSuccess) return e;
+  // OverBudgetError before any state changes (the reference raises from
+  // insert; an entry larger than the budget can never be resident, so a
+  // prefix over budget that is not a hit now would be inserted)
+  for (int32_t j = 0; j < n; ++j) {
+    if (int64_t(prefix_len[j]) * c->bytes_per_row <= c->budget) continue;
+    auto it = c->map.find(spt_ids[j]);
+    bool hit = false;
+    if (it != c->map.end()) {
+      const double cd = it->second->cached_distance, d = d_root[j];
+      hit = cd == 0.0 ? d == 0.0 : (c->d_min <= d / cd && d / cd <= c->d_max);
+    }
+    if (!hit) return cudaErrorNotPermitted;
+  }
   // write-backs of earlier steps already finished: nothing to wait for
   if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
   std::vector<Xfer> loads, wbs;
@@ -579,6 +592,9 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
         // f32 rounding of the evicted block, the rest the untouched store
         ld.overlay = ev->second.first;
         ld.overlay_rows = ev->second.second;      // its row count = its section stride
+        // rows past the overlay come from the store: wait for a write-back
+        // of an earlier step still writing them
+        if (ld.overlay_rows < P && c->wb_prev.count(sid)) join = true;
       } else if (c->wb_prev.count(sid)) {
         join = true;                 // store rows still being written back
       }

@@ -345,34 +345,47 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
 
 // ---------------------------------------------------------------------------
 // K1: order-preserving compaction of every selected prefix (spt.py:67-75,
-// trainer._spt_positions :302-309), three launches, no grid barriers:
-//   k1a  prefix_kernel  one warp per selected SPT: prefix length (the
-//        caller's, or a 32-ary ballot search of #{key_parent > d}), root
-//        rule, virtual segment length (padded to kAlign records)
-//   k1b  segscan_kernel one CTA: exclusive scan of the segment lengths
-//        (the selected prefixes laid end to end in one virtual space)
-//   k1c  compact_kernel persistent CTAs take 4096-record tiles in order
-//        (atomic ticket), stream each key_self once with 16-B vector loads,
-//        rank the selections with a block scan, get the tile's output
-//        offset by decoupled look-back over the predecessors' published
-//        counts, stage the selections in shared memory and write them as
-//        coalesced runs.
+// trainer._spt_positions :302-309); two launches (three when many prefixes
+// must be searched), no grid barriers, no memset:
+//   prefix_kernel   one warp per selected SPT: prefix length (the caller's,
+//                   or a 32-ary ballot search of #{key_parent > d}), root
+//                   rule, virtual segment length (padded to kAlign records)
+//                   — run inside segscan_kernel when it is cheap
+//   segscan_kernel  one CTA: exclusive scan of the segment lengths (the
+//                   selected prefixes laid end to end in one virtual
+//                   space); resets the tile ticket and the look-back words
+//   compact_kernel  persistent CTAs take tiles in order (atomic ticket).
+//                   Warp w of a tile owns a contiguous 128·G-record span;
+//                   lane l's group g = records [g·128 + 4l, +4), so every
+//                   key load is a coalesced 16-B vector load and all G are
+//                   issued before any is used.  Ranks: warp scans per group
+//                   (four counts packed per word), warp totals, the tile's
+//                   offset by decoupled look-back; selections are written
+//                   straight out (each group's run is contiguous).  Every
+//                   key_self is read once.
 // ---------------------------------------------------------------------------
-constexpr int kCThreads = 256;
-constexpr int kCGroups = 4;                                  // kAlign-record groups per thread
-constexpr int kCTile = kCThreads * kCGroups * kAlign;        // 4096 virtual records
+constexpr int kCThreads = 128;
+constexpr int kCWarps = kCThreads / 32;
+constexpr int kCBlocksPerSM = 8;
+template <typename K> struct CTile {
+  static constexpr int G = sizeof(K) == 4 ? 4 : 2;            // groups per lane
+  static constexpr int kWarpRecs = 32 * kAlign * G;           // 512 / 256
+  static constexpr int kTile = kCWarps * kWarpRecs;           // 2048 / 1024
+};
+constexpr int kSubTiles = 8;                                // sub-tiles per look-back tile
+constexpr int kMinTile = 1024;
 constexpr int kSegCache = 128;                               // segments cached per tile
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 struct CompactScratch {
-  unsigned int* ticket;         // [1] tile ticket
-  unsigned long long* status;   // [max_tiles] look-back words (flag | value)
-  size_t zero_bytes;
+  unsigned int* ticket;         // [1] tile ticket (reset by segscan_kernel)
+  unsigned long long* status;   // [max_tiles] look-back words (reset by segscan_kernel)
+  long long max_tiles;
 };
 
 size_t max_tiles(int64_t num_records, int32_t S) {
-  return size_t((num_records + int64_t(kAlign) * S + kCTile - 1) / kCTile) + 2;
+  return size_t((num_records + int64_t(kAlign) * S + kMinTile - 1) / kMinTile) + 2;
 }
 
 CompactScratch carve_compact(void* base, int32_t S, int64_t R) {
@@ -380,8 +393,18 @@ CompactScratch carve_compact(void* base, int32_t S, int64_t R) {
   char* p = static_cast<char*>(base);
   s.ticket = reinterpret_cast<unsigned int*>(p);
   s.status = reinterpret_cast<unsigned long long*>(p + 256);
-  s.zero_bytes = 256 + 8 * max_tiles(R, S);
+  s.max_tiles = (long long)max_tiles(R, S);
   return s;
+}
+
+// look-back words: one aligned 64-bit access (flag and value together)
+GLOD_DEV unsigned long long ld_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+GLOD_DEV void st_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
 
 // kAlign consecutive keys, aligned by the record layout (device.pad_records)
@@ -395,51 +418,59 @@ GLOD_DEV void load4(const double* p, long long a, double (&v)[4]) {
   v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
 }
 
+// prefix length / root rule / padded segment length of selected SPT j
 template <typename K>
-__global__ void __launch_bounds__(256)
-prefix_kernel(LodScene sc, CompactIn in, CompactOut out) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const int n_spt = *in.n_spt;
+GLOD_DEV void spt_prefix(const LodScene& sc, const CompactIn& in, const CompactOut& out, long long j, int lane) {
   const K* key_self = static_cast<const K*>(sc.key_self);
-  for (long long j = gw; j < n_spt; j += nw) {
-    const int s = in.spt_ids[j];
-    const double d = in.dist[j];
-    int pl;
-    if (in.known_prefix) {
-      pl = in.known_prefix[j];
-    } else {
-      // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
-      const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
-      long long a = 0, b = sc.spt_count[s];
-      while (b - a > 32) {
-        const long long step = (b - a + 31) / 32;
-        const long long probe = a + step * lane;
-        const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
-        const unsigned m = __ballot_sync(0xffffffffu, gt);
-        const int last = 31 - __clz(m);
-        const long long na = a + step * last;
-        b = min(b, na + step);
-        a = na;
-      }
-      const long long probe = a + lane;
-      const bool gt = probe < b && double(kp[probe]) > d;
-      pl = int(a + __popc(__ballot_sync(0xffffffffu, gt)));
+  const int s = in.spt_ids[j];
+  const double d = in.dist[j];
+  int pl;
+  if (in.known_prefix) {
+    pl = in.known_prefix[j];
+  } else {
+    // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
+    const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
+    long long a = 0, b = sc.spt_count[s];
+    while (b - a > 32) {
+      const long long step = (b - a + 31) / 32;
+      const long long probe = a + step * lane;
+      const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
+      const unsigned m = __ballot_sync(0xffffffffu, gt);
+      const int last = 31 - __clz(m);
+      const long long na = a + step * last;
+      b = min(b, na + step);
+      a = na;
     }
-    // root rule (spt.py:72-73): d >= key_self[root] selects exactly [root]
-    const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
-    if (lane == 0) {
-      out.prefix_len[j] = pl;
-      out.root_rule[j] = rr;
-      out.seg_start[j] = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;   // length for now
-    }
+    const long long probe = a + lane;
+    const bool gt = probe < b && double(kp[probe]) > d;
+    pl = int(a + __popc(__ballot_sync(0xffffffffu, gt)));
+  }
+  // root rule (spt.py:72-73): d >= key_self[root] selects exactly [root]
+  const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
+  if (lane == 0) {
+    out.prefix_len[j] = pl;
+    out.root_rule[j] = rr;
+    out.seg_start[j] = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;   // length for now
   }
 }
 
-__global__ void __launch_bounds__(1024) segscan_kernel(CompactIn in, CompactOut out) {
+template <typename K>
+__global__ void __launch_bounds__(256) prefix_kernel(LodScene sc, CompactIn in, CompactOut out) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int n_spt = *in.n_spt;
+  for (long long j = gw; j < n_spt; j += nw) spt_prefix<K>(sc, in, out, j, threadIdx.x & 31);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(1024)
+segscan_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws, int with_prefix) {
   __shared__ long long sm[1024 / 32 + 1];
   const int n_spt = *in.n_spt;
+  if (with_prefix) {
+    for (long long j = threadIdx.x >> 5; j < n_spt; j += blockDim.x >> 5) spt_prefix<K>(sc, in, out, j, threadIdx.x & 31);
+    __syncthreads();
+  }
   long long carry = 0;
   for (int base = 0; base < n_spt; base += blockDim.x) {
     const int j = base + threadIdx.x;
@@ -450,48 +481,146 @@ __global__ void __launch_bounds__(1024) segscan_kernel(CompactIn in, CompactOut 
     if (j < n_spt) out.seg_start[j] = carry + ex;
     carry += tot;
   }
+  const long long ntiles = (carry + CTile<K>::kTile - 1) / CTile<K>::kTile;   // upper bound (1 sub-tile)
+  for (long long t = threadIdx.x; t < ntiles && t < ws.max_tiles; t += blockDim.x) ws.status[t] = 0;
   if (threadIdx.x == 0) {
     out.total[1] = carry;     // virtual records
     out.total[0] = 0;         // selections (the last tile overwrites)
+    *ws.ticket = 0;
   }
 }
 
+// key <= d, exactly: for f32 keys against the largest float <= d (no
+// per-key f32 -> f64 conversion), for f64 keys directly
+GLOD_DEV bool key_le(float k, double, float df) { return k <= df; }
+GLOD_DEV bool key_le(double k, double d, float) { return k <= d; }
+
+// The segments overlapping a tile, cached in shared memory.
+struct SegCache {
+  long long vstart[kSegCache + 1];
+  long long off[kSegCache];
+  double d[kSegCache];
+  float df[kSegCache];
+  int len[kSegCache], rr[kSegCache], rootrec[kSegCache];
+};
+
+// One sub-tile's kAlign-record groups of this lane: segment, position,
+// key-vector address and selection mask (bit e: record e selected).
+template <typename K, int G>
+struct Groups {
+  int seg[G], loc[G], len[G];
+  long long addr[G];
+  unsigned rrmask;
+  unsigned mask[G];
+
+  // segment, position and key address of each group (no key loads)
+  GLOD_DEV void locate(const LodScene& sc, const CompactIn& in, const CompactOut& out, const SegCache& c,
+                       int j0, int nseg, long long cache_end, int n_spt, long long w_lo, long long t_hi,
+                       int lane) {
+    rrmask = 0;
+    int cur = -1;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const long long v = w_lo + g * (32 * kAlign) + lane * kAlign;
+      seg[g] = -1;
+      len[g] = 0;
+      loc[g] = 0;
+      addr[g] = 0;
+      if (v < t_hi) {
+        if (v < cache_end) {
+          if (cur < 0) {
+            int a = 0, b = nseg;                   // last cached segment starting <= v
+            while (a < b) { const int m = (a + b) >> 1; if (c.vstart[m] <= v) a = m + 1; else b = m; }
+            cur = a - 1;
+          } else {
+            while (cur + 1 < nseg && c.vstart[cur + 1] <= v) ++cur;
+          }
+          seg[g] = cur;                            // local index
+          loc[g] = int(v - c.vstart[cur]);
+          len[g] = c.len[cur];
+          if (c.rr[cur]) rrmask |= 1u << g;
+          addr[g] = c.off[cur] + (c.rr[cur] ? c.rootrec[cur] : loc[g]);
+        } else {
+          int a = j0 + nseg, b = n_spt;
+          while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= v) a = m + 1; else b = m; }
+          const int j = a - 1;
+          const int sp = in.spt_ids[j];
+          seg[g] = kSegCache + j;                  // global index, tagged
+          loc[g] = int(v - out.seg_start[j]);
+          const int rr = out.root_rule[j];
+          len[g] = rr ? 1 : out.prefix_len[j];
+          if (rr) rrmask |= 1u << g;
+          addr[g] = sc.spt_offset[sp] + (rr ? sc.spt_root_rec[sp] : loc[g]);
+        }
+      }
+    }
+  }
+
+  // the keys of every group (all loads issued first), then the masks
+  GLOD_DEV void evaluate(const LodScene& sc, const CompactIn& in, const SegCache& c) {
+    const K* key_self = static_cast<const K*>(sc.key_self);
+    K kv[G][kAlign];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      load4(key_self, (seg[g] >= 0 && !((rrmask >> g) & 1u) && loc[g] < len[g]) ? addr[g] : 0, kv[g]);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      mask[g] = 0;
+      if (seg[g] >= 0) {
+        if ((rrmask >> g) & 1u) {
+          mask[g] = loc[g] == 0 ? 1u : 0u;         // [root]
+        } else {
+          const double d = seg[g] < kSegCache ? c.d[seg[g]] : in.dist[seg[g] - kSegCache];
+          const float df = seg[g] < kSegCache ? c.df[seg[g]] : __double2float_rd(d);
+#pragma unroll
+          for (int e = 0; e < kAlign; ++e)
+            if (loc[g] + e < len[g] && key_le(kv[g][e], d, df)) mask[g] |= 1u << e;
+        }
+      }
+    }
+  }
+};
+
 template <typename K>
-__global__ void __launch_bounds__(kCThreads, sizeof(K) == 4 ? 4 : 3)
+__global__ void __launch_bounds__(kCThreads, kCBlocksPerSM)
 compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
-  extern __shared__ int stage[];                 // [3][kCTile]: seg, pos, node
-  __shared__ long long sm[kCThreads / 32 + 1];
-  __shared__ long long c_vstart[kSegCache + 1];
-  __shared__ long long c_off[kSegCache];
-  __shared__ double c_d[kSegCache];
-  __shared__ int c_len[kSegCache], c_rr[kSegCache], c_rootrec[kSegCache];
+  constexpr int G = CTile<K>::G;
+  constexpr int kWarpRecs = CTile<K>::kWarpRecs;
+  constexpr int kSubTile = CTile<K>::kTile;
+  __shared__ SegCache c;
+  __shared__ long long sub_cnt[kSubTiles][kCWarps];
+  __shared__ unsigned masks[kSubTiles][kCThreads];
   __shared__ unsigned int tile_sh;
-  __shared__ int j0_sh, nseg_sh;
+  __shared__ int j0_sh;
   __shared__ long long excl_sh;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n_spt = *in.n_spt;
   const long long total = out.total[1];
-  const long long ntiles = (total + kCTile - 1) / kCTile;
-  const K* key_self = static_cast<const K*>(sc.key_self);
-  int* st_seg = stage;
-  int* st_pos = stage + kCTile;
-  int* st_node = stage + 2 * kCTile;
+  // sub-tiles per look-back tile: as many as keep every CTA busy (large
+  // inputs amortise the look-back over more records, small ones keep
+  // their parallelism)
+  const long long nsub_ll = total / (2ll * gridDim.x * kSubTile);
+  const int nsub = int(nsub_ll < 1 ? 1 : (nsub_ll > kSubTiles ? kSubTiles : nsub_ll));
+  const long long kTile = (long long)nsub * kSubTile;
+  const long long ntiles = (total + kTile - 1) / kTile;
 
   for (;;) {
-    if (threadIdx.x == 0) tile_sh = atomicAdd(ws.ticket, 1u);
+    if (threadIdx.x == 0) {
+      const unsigned t = atomicAdd(ws.ticket, 1u);
+      tile_sh = t;
+      if ((long long)t < ntiles) {   // last j with seg_start[j] <= tile start
+        const long long lo = (long long)t * kTile;
+        int a = 0, b = n_spt;
+        while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= lo) a = m + 1; else b = m; }
+        j0_sh = a - 1;
+      }
+    }
     __syncthreads();
     const long long tile = tile_sh;
     if (tile >= ntiles) break;
-    const long long t_lo = tile * kCTile, t_hi = min(total, t_lo + kCTile);
-
-    // segments overlapping the tile -> shared cache (seg_start is sorted)
-    if (threadIdx.x == 0) {
-      int a = 0, b = n_spt;                        // last j with seg_start[j] <= t_lo
-      while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= t_lo) a = m + 1; else b = m; }
-      j0_sh = a - 1;
-    }
-    __syncthreads();
+    const long long t_lo = tile * kTile, t_hi = min(total, t_lo + kTile);
     const int j0 = j0_sh;
+    // segments overlapping the tile -> shared cache (seg_start is sorted)
     int valid = 0;
     if (threadIdx.x < kSegCache) {
       const int j = j0 + threadIdx.x;
@@ -499,158 +628,150 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
         valid = 1;
         const int sp = in.spt_ids[j];
         const int rr = out.root_rule[j];
-        c_vstart[threadIdx.x] = out.seg_start[j];
-        c_off[threadIdx.x] = sc.spt_offset[sp];
-        c_d[threadIdx.x] = in.dist[j];
-        c_rr[threadIdx.x] = rr;
-        c_len[threadIdx.x] = rr ? 1 : out.prefix_len[j];
-        c_rootrec[threadIdx.x] = sc.spt_root_rec[sp];
+        c.vstart[threadIdx.x] = out.seg_start[j];
+        c.off[threadIdx.x] = sc.spt_offset[sp];
+        c.d[threadIdx.x] = in.dist[j];
+        c.df[threadIdx.x] = __double2float_rd(in.dist[j]);
+        c.rr[threadIdx.x] = rr;
+        c.len[threadIdx.x] = rr ? 1 : out.prefix_len[j];
+        c.rootrec[threadIdx.x] = sc.spt_root_rec[sp];
       }
     }
     const int nseg = __syncthreads_count(valid);
-    // more than kSegCache segments start inside this tile: the cached ones
-    // end before the uncached ones start; those groups use a global search
+    // more than kSegCache segments in this tile: groups past the cached ones
+    // find their segment with a global search
     const long long cache_end = (j0 + nseg < n_spt) ? out.seg_start[j0 + nseg] : total;
 
-    // keys: kCGroups aligned groups of kAlign records per thread, all loads
-    // issued before any is used
-    int seg[kCGroups], loc[kCGroups], len[kCGroups], rrk[kCGroups], rootrec[kCGroups];
-    long long addr[kCGroups];
-    double dk[kCGroups];
-    int cur = 0;
+    // pass A: stream the keys once, keep each lane's selection masks
+    // (kAlign bits per group) in shared memory, count per sub-tile
+#pragma unroll 1
+    for (int st = 0; st < nsub; ++st) {
+      Groups<K, G> gr;
+      gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt,
+                t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs, t_hi, lane);
+      gr.evaluate(sc, in, c);
+      int cnt = 0;
+      unsigned packed_mask = 0;
 #pragma unroll
-    for (int g = 0; g < kCGroups; ++g) {
-      const long long v = t_lo + (long long)(g * kCThreads + threadIdx.x) * kAlign;
-      seg[g] = -1;
-      len[g] = 0;
-      loc[g] = 0;
-      rrk[g] = 0;
-      rootrec[g] = 0;
-      addr[g] = 0;
-      dk[g] = 0.0;
-      if (v < t_hi) {
-        if (v < cache_end) {
-          int a = 0, b = nseg;                     // last cached segment starting <= v
-          while (a < b) { const int m = (a + b) >> 1; if (c_vstart[m] <= v) a = m + 1; else b = m; }
-          cur = a - 1;
-          seg[g] = j0 + cur;
-          loc[g] = int(v - c_vstart[cur]);
-          len[g] = c_len[cur];
-          rrk[g] = c_rr[cur];
-          rootrec[g] = c_rootrec[cur];
-          dk[g] = c_d[cur];
-          addr[g] = c_off[cur] + (rrk[g] ? rootrec[g] : loc[g]);
-        } else {
-          int a = j0 + nseg, b = n_spt;
-          while (a < b) { const int m = (a + b) >> 1; if (out.seg_start[m] <= v) a = m + 1; else b = m; }
-          const int j = a - 1;
-          const int sp = in.spt_ids[j];
-          seg[g] = j;
-          loc[g] = int(v - out.seg_start[j]);
-          rrk[g] = out.root_rule[j];
-          len[g] = rrk[g] ? 1 : out.prefix_len[j];
-          rootrec[g] = sc.spt_root_rec[sp];
-          dk[g] = in.dist[j];
-          addr[g] = sc.spt_offset[sp] + (rrk[g] ? rootrec[g] : loc[g]);
-        }
+      for (int g = 0; g < G; ++g) {
+        cnt += __popc(gr.mask[g]);
+        packed_mask |= gr.mask[g] << (kAlign * g);
       }
+      masks[st][threadIdx.x] = packed_mask;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (lane == 0) sub_cnt[st][warp] = cnt;
     }
-    K kv[kCGroups][kAlign];
+    __syncthreads();
+    long long agg = 0;
+    for (int st = 0; st < nsub; ++st)
 #pragma unroll
-    for (int g = 0; g < kCGroups; ++g)
-      load4(key_self, (seg[g] >= 0 && !rrk[g] && loc[g] < len[g]) ? addr[g] : 0, kv[g]);
-    unsigned mask[kCGroups];
-    int count = 0;
-#pragma unroll
-    for (int g = 0; g < kCGroups; ++g) {
-      mask[g] = 0;
-      if (seg[g] >= 0) {
-        if (rrk[g]) {
-          mask[g] = loc[g] == 0 ? 1u : 0u;         // [root]
-        } else {
-#pragma unroll
-          for (int e = 0; e < kAlign; ++e)
-            if (loc[g] + e < len[g] && double(kv[g][e]) <= dk[g]) mask[g] |= 1u << e;
-        }
-      }
-      count += __popc(mask[g]);
-    }
-    // rank inside the tile: thread order = virtual order (group-major), so
-    // the block scan runs over (group, thread) — one scan per group
-    long long run = 0;
-    long long g_off[kCGroups];
-#pragma unroll
-    for (int g = 0; g < kCGroups; ++g) {
-      const long long c = __popc(mask[g]);
-      g_off[g] = run + block_excl_scan(c, sm);
-      run += sm[kCThreads / 32];
-      __syncthreads();
-    }
-    const long long agg = run;
-
-    // decoupled look-back (warp 0)
-    if (threadIdx.x < 32) {
-      if (lane == 0)
-        atomicExch(ws.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (unsigned long long)agg);
+      for (int w = 0; w < kCWarps; ++w) agg += sub_cnt[st][w];
+    // decoupled look-back over the big tiles (warp 0, 32 predecessors per step)
+    if (warp == 0) {
+      if (lane == 0) st_u64(ws.status + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | (unsigned long long)agg);
       long long excl = 0;
       if (tile > 0) {
-        long long pred = tile - 1;
-        for (;;) {
+        for (long long pred = tile - 1;; pred -= 32) {
           const long long idx = pred - lane;
-          unsigned long long sv = idx >= 0 ? atomicAdd(ws.status + idx, 0ull) : kFlagIncl;
-          while (__any_sync(0xffffffffu, (sv >> 62) == 0)) {
-            if ((sv >> 62) == 0) sv = atomicAdd(ws.status + idx, 0ull);
+          unsigned long long sv = kFlagIncl;
+          if (idx >= 0) {
+            sv = ld_u64(ws.status + idx);
+            while ((sv >> 62) == 0) sv = ld_u64(ws.status + idx);
           }
-          const unsigned incl = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
-          const int first = incl ? __ffs(incl) - 1 : 32;
+          const unsigned incl_m = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+          const int first = incl_m ? __ffs(incl_m) - 1 : 32;
           long long v = lane <= first ? (long long)(sv & kValMask) : 0;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           excl += v;
-          if (incl) break;
-          pred -= 32;
+          if (incl_m) break;
         }
-        if (lane == 0) atomicExch(ws.status + tile, kFlagIncl | (unsigned long long)(excl + agg));
+        if (lane == 0) st_u64(ws.status + tile, kFlagIncl | (unsigned long long)(excl + agg));
       }
       if (lane == 0) {
         excl_sh = excl;
         if (tile == ntiles - 1) out.total[0] = excl + agg;
       }
     }
-    // stage the selections (seg, position in the prefix, node) in order
+    __syncthreads();
+    // pass B: rank inside each group run from the kept masks and write the
+    // selections in order (no key is read twice)
+    long long run = excl_sh;
+#pragma unroll 1
+    for (int st = 0; st < nsub; ++st) {
+      long long w_off = 0, st_tot = 0;
 #pragma unroll
-    for (int g = 0; g < kCGroups; ++g) {
-      if (!mask[g]) continue;
-      long long o = g_off[g];
-      if (rrk[g]) {
-        st_seg[o] = seg[g];
-        st_pos[o] = rootrec[g];
-        st_node[o] = sc.rec_node[addr[g]];
-      } else {
-        const int4 nd = *reinterpret_cast<const int4*>(sc.rec_node + addr[g]);
-        const int n4[4] = {nd.x, nd.y, nd.z, nd.w};
-#pragma unroll
-        for (int e = 0; e < kAlign; ++e)
-          if (mask[g] & (1u << e)) {
-            st_seg[o] = seg[g];
-            st_pos[o] = loc[g] + e;
-            st_node[o] = n4[e];
-            ++o;
-          }
+      for (int w = 0; w < kCWarps; ++w) {
+        w_off += w < warp ? sub_cnt[st][w] : 0;
+        st_tot += sub_cnt[st][w];
       }
+      Groups<K, G> gr;
+      gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt,
+                t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs, t_hi, lane);
+      const unsigned packed_mask = masks[st][threadIdx.x];
+#pragma unroll
+      for (int g = 0; g < G; ++g) gr.mask[g] = (packed_mask >> (kAlign * g)) & ((1u << kAlign) - 1u);
+      // warp-inclusive scans of the per-group counts, four packed per word
+      unsigned packed[(G + 3) / 4], incl[(G + 3) / 4];
+#pragma unroll
+      for (int i = 0; i < (G + 3) / 4; ++i) packed[i] = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) packed[g >> 2] |= unsigned(__popc(gr.mask[g])) << (8 * (g & 3));
+#pragma unroll
+      for (int i = 0; i < (G + 3) / 4; ++i) {
+        unsigned x = packed[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        incl[i] = x;
+      }
+      // node ids of every group with a selection, all loads issued first
+      int4 nd[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        nd[g] = make_int4(0, 0, 0, 0);
+        if (gr.mask[g]) {
+          if ((gr.rrmask >> g) & 1u) nd[g].x = sc.rec_node[gr.addr[g]];
+          else nd[g] = *reinterpret_cast<const int4*>(sc.rec_node + gr.addr[g]);
+        }
+      }
+      long long gsum = 0;
+      const long long base = run + w_off;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const unsigned x = (incl[g >> 2] >> (8 * (g & 3))) & 0xffu;
+        const unsigned cg = (packed[g >> 2] >> (8 * (g & 3))) & 0xffu;
+        const unsigned gt = __shfl_sync(0xffffffffu, x, 31);
+        if (gr.mask[g]) {
+          const int sg = gr.seg[g];
+          const int j = sg < kSegCache ? j0 + sg : sg - kSegCache;
+          long long o = base + gsum + x - cg;
+          if ((gr.rrmask >> g) & 1u) {
+            out.sel_seg[o] = j;
+            out.sel_pos[o] = sg < kSegCache ? c.rootrec[sg] : sc.spt_root_rec[in.spt_ids[j]];
+            out.sel_node[o] = nd[g].x;
+          } else {
+            const int n4[4] = {nd[g].x, nd[g].y, nd[g].z, nd[g].w};
+#pragma unroll
+            for (int e = 0; e < kAlign; ++e)
+              if (gr.mask[g] & (1u << e)) {
+                out.sel_seg[o] = j;
+                out.sel_pos[o] = gr.loc[g] + e;
+                out.sel_node[o] = n4[e];
+                ++o;
+              }
+          }
+        }
+        gsum += gt;
+      }
+      run += st_tot;
     }
-    __syncthreads();
-    const long long base = excl_sh;
-    for (long long i = threadIdx.x; i < agg; i += kCThreads) {
-      out.sel_seg[base + i] = st_seg[i];
-      out.sel_pos[base + i] = st_pos[i];
-      out.sel_node[base + i] = st_node[i];
-    }
-    __syncthreads();
+    __syncthreads();            // the segment cache and counts are rewritten next tile
   }
 }
-
-constexpr size_t kCompactSmem = 3 * size_t(kCTile) * sizeof(int);
 
 int coop_grid(const void* kernel, int threads) {
   int dev = 0, sms = 0, per_sm = 0;
@@ -684,7 +805,7 @@ int compact_grid() {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms * 4;
+  return sms * kCBlocksPerSM;
 }
 
 cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut& out,
@@ -701,28 +822,27 @@ cudaError_t launch_select(const LodScene& sc, const LodView& v, const SelectOut&
                                      args, 0, st);
 }
 
+template <typename K>
+cudaError_t launch_compact_t(const LodScene& sc, const CompactIn& in, const CompactOut& out,
+                             const CompactScratch& ws, cudaStream_t st) {
+  // prefix searches run inside the scan CTA when they are cheap (known
+  // prefix lengths, or few SPTs), else one warp per SPT over the grid
+  const bool split = !in.known_prefix && sc.num_spts > 32;
+  if (split) {
+    prefix_kernel<K><<<unsigned((sc.num_spts + 7) / 8), 256, 0, st>>>(sc, in, out);
+    count_launch();
+  }
+  segscan_kernel<K><<<1, 1024, 0, st>>>(sc, in, out, ws, split ? 0 : 1);
+  compact_kernel<K><<<unsigned(compact_grid()), kCThreads, 0, st>>>(sc, in, out, ws);
+  count_launch(2);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_compact(const LodScene& sc, const CompactIn& in, const CompactOut& out,
                            void* scratch, size_t scratch_bytes, cudaStream_t st) {
   if (scratch_bytes < compact_scratch_bytes(sc.num_spts, sc.num_records, 0)) return cudaErrorInvalidValue;
   CompactScratch ws = carve_compact(scratch, sc.num_spts, sc.num_records);
-  cudaError_t e = cudaMemsetAsync(scratch, 0, ws.zero_bytes, st);
-  if (e != cudaSuccess) return e;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(compact_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactSmem));
-    cudaFuncSetAttribute(compact_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCompactSmem));
-    attr_set = true;
-  }
-  const int S = sc.num_spts > 0 ? sc.num_spts : 1;
-  const unsigned pgrid = unsigned((S + 7) / 8);
-  if (sc.key_f64) prefix_kernel<double><<<pgrid, 256, 0, st>>>(sc, in, out);
-  else prefix_kernel<float><<<pgrid, 256, 0, st>>>(sc, in, out);
-  segscan_kernel<<<1, 1024, 0, st>>>(in, out);
-  const unsigned grid = unsigned(compact_grid());
-  if (sc.key_f64) compact_kernel<double><<<grid, kCThreads, kCompactSmem, st>>>(sc, in, out, ws);
-  else compact_kernel<float><<<grid, kCThreads, kCompactSmem, st>>>(sc, in, out, ws);
-  count_launch(3);
-  return cudaGetLastError();
+  return sc.key_f64 ? launch_compact_t<double>(sc, in, out, ws, st) : launch_compact_t<float>(sc, in, out, ws, st);
 }
 
 }  // namespace glod

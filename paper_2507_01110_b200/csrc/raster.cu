@@ -303,11 +303,17 @@ preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat
 // Top-bits depth sort fix-up: within each run of keys whose bits
 // [begin_bit, end_bit) tie, the radix passes kept index order; the run's head
 // thread insertion-sorts it by the full 64-bit key (stable, so equal depths
-// stay in index order).  Runs are short (mostly 2); equal keys cost O(run).
+// stay in index order).  Runs are short (mostly 2).  A run longer than
+// kMaxFixRun (near-equal depths spanning many splats, e.g. a fronto-parallel
+// facade in a scene whose depth range is large) is left alone and flagged:
+// the host then finishes the order with full-width radix passes over the
+// top-sorted keys (stable, so the result is the same exact order) — never
+// the O(run²) worst case.
 constexpr int kDepthBits = 32;
+constexpr long long kMaxFixRun = 64;
 
 __global__ void fixup_runs_kernel(unsigned long long* __restrict__ keys, int* __restrict__ vals, long long n,
-                                  int begin_bit, int end_bit) {
+                                  int begin_bit, int end_bit, unsigned long long* __restrict__ long_run) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const unsigned long long m = ((end_bit - begin_bit) >= 64 ? ~0ull : ((1ull << (end_bit - begin_bit)) - 1)) << begin_bit;
@@ -315,7 +321,11 @@ __global__ void fixup_runs_kernel(unsigned long long* __restrict__ keys, int* __
   const unsigned long long top = keys[i] & m;
   if (i > 0 && (keys[i - 1] & m) == top) return;          // not a run head
   long long j = i + 1;
-  while (j < n && (keys[j] & m) == top) ++j;
+  while (j < n && j - i <= kMaxFixRun && (keys[j] & m) == top) ++j;
+  if (j - i > kMaxFixRun) {
+    atomicMax(long_run, 1ull);
+    return;
+  }
   for (long long a = i + 1; a < j; ++a) {
     const unsigned long long k = keys[a];
     const int v = vals[a];
@@ -807,6 +817,7 @@ struct Buf {
 struct RasterCtx {
   Buf splats, sorted, keys, keys2, vals, vals2, tiles, tiles_sorted, offs;
   Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin;
+  bool long_runs = false;       // last forward finished its depth order with full-width passes
   CamD cam{};
   const double* attrs = nullptr;
   long long n = 0, n_inst = 0, n_visible = 0;
@@ -955,11 +966,26 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
                                             R->vals.as<int>(), R->vals2.as<int>(), n, begin_bit, end_bit, R->temp.p,
                                             R->temp.cap, false, &alt, st));
   const int* order = alt ? R->vals2.as<int>() : R->vals.as<int>();
+  R->long_runs = false;
   if (begin_bit > 0) {
     count_launch();
     fixup_runs_kernel<<<nb, TB, 0, st>>>(alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>(),
-                                         const_cast<int*>(order), n, begin_bit, end_bit);
+                                         const_cast<int*>(order), n, begin_bit, end_bit, stats + 3);
     CK(cudaGetLastError());
+    CK(launch_readback(hp + 64, stats + 3, 8, st));
+    CK(cudaStreamSynchronize(st));
+    if (*reinterpret_cast<const unsigned long long*>(hp + 64)) {
+      // long tie runs: full-width stable passes over the top-sorted order
+      R->long_runs = true;
+      int alt2 = 0;
+      unsigned long long* k0 = alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>();
+      unsigned long long* k1 = alt ? R->keys.as<unsigned long long>() : R->keys2.as<unsigned long long>();
+      int* v0 = alt ? R->vals2.as<int>() : R->vals.as<int>();
+      int* v1 = alt ? R->vals.as<int>() : R->vals2.as<int>();
+      CK(radix_sort_pairs<unsigned long long>(k0, k1, v0, v1, n, 0, end_bit, R->temp.p, R->temp.cap, false,
+                                              &alt2, st));
+      order = alt2 ? v1 : v0;
+    }
   }
   count_launch();
   gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
@@ -1027,6 +1053,8 @@ void raster_stats(const RasterCtx* R, glod_render_stats* out) {
   out->n_instances = R->n_inst;
   out->tiles_x = R->cam.tw;
   out->tiles_y = R->cam.th;
+  out->depth_full_sort = R->long_runs ? 1 : 0;
+  out->reserved = 0;
 }
 
 bool raster_bad_input(const RasterCtx* R, int* section, int* index) {

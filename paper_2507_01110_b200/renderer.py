@@ -129,7 +129,7 @@ class Rasterizer:
         s = _lib.RenderStats()
         _lib.check(_lib.lib().glod_render_stats_get(self._h, C.byref(s)))
         return {"n_gaussians": s.n_gaussians, "n_instances": s.n_instances,
-                "tiles": (s.tiles_x, s.tiles_y)}
+                "tiles": (s.tiles_x, s.tiles_y), "depth_full_sort": bool(s.depth_full_sort)}
 
     def loss(self, rendered: torch.Tensor, target: torch.Tensor, lam: float = 0.2,
              value: torch.Tensor | None = None, grad: torch.Tensor | None = None, stream=None):

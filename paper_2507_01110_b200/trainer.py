@@ -460,14 +460,21 @@ class Trainer:
                     "bytes_streamed": int(loaded * sc.store.bytes_per_gaussian)}
         return R, rows, row_node, plan, None, counters
 
-    def render_view(self, view: int, image: torch.Tensor | None = None) -> torch.Tensor:
+    def render_view(self, view: int, image: torch.Tensor | None = None,
+                    next_view: int | None = None) -> torch.Tensor:
         """Serve/bench path (cli.cmd_render, cli.py:139-189): cut + cache +
-        gather + forward render of one view; no parameter updates."""
+        gather + forward render of one view; no parameter updates.  With
+        `next_view` (a camera path known one frame ahead) the copy engines
+        prefetch that view's cache misses while this frame renders, as the
+        training step does for the scheduler's next draw; decisions and
+        counters are unchanged."""
         cam, _ = self.views[view]
-        self._next_view = None
+        self._next_view = next_view if self.cfg.prefetch else None
         R, rows, _, _, _, counters = self._gather_view(cam, view)
         img = self.rast.forward(rows, R, cam, image=image)
         self.cache.end_step(-1, mark_dirty=False)
+        if self._pred is not None:
+            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
         self._mark("forward")
         self._collect()
         self.last_render = counters

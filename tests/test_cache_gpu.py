@@ -88,6 +88,18 @@ def test_native_cache_over_budget():
     with pytest.raises(OverBudgetError):
         nat.step(np.array([0], np.int32), np.array([1.0]), np.array([4], np.int32), z,
                  np.zeros(1, np.uint64), np.zeros(1, np.int64))
+    # the error leaves no partial state: an over-budget SPT after ones that
+    # fit raises before anything is inserted, evicted or counted
+    nat.step(np.array([1], np.int32), np.array([1.0]), np.array([2], np.int32), z,
+             np.zeros(1, np.uint64), np.zeros(1, np.int64))
+    before, stats = nat.entries(), nat.stats()
+    with pytest.raises(OverBudgetError):
+        nat.step(np.array([2, 3, 0], np.int32), np.array([1.0, 1.0, 1.0]), np.array([1, 1, 4], np.int32),
+                 np.zeros(3), np.zeros(3, np.uint64), np.zeros(3, np.int64))
+    assert nat.entries() == before
+    after = nat.stats()
+    assert (after["hits"], after["misses"], after["loaded_rows"]) == (stats["hits"], stats["misses"],
+                                                                     stats["loaded_rows"])
 
 
 def _write_block(address: int, values: np.ndarray):

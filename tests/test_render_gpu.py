@@ -163,3 +163,64 @@ def test_depth_order_exact_with_near_ties():
     img = Rn.render(a, cam)
     want, _ = O.render_forward({k: getattr(a, k) for k in NAMES}, Cam.of(cam))
     assert np.abs(img - want).max() <= IMG_TOL
+
+
+def _facade(n, rng, jitter_rel, far=16):
+    """n splats on a fronto-parallel plane at depth ≈ 10 (depths within
+    `jitter_rel` relative, some exactly equal) plus `far` splats at depth
+    1000 that widen the key range: with the top-32-bit radix passes the
+    whole facade is ONE tie run (renderer.py:127's lexsort order must
+    still come out exactly)."""
+    a = AttributeArrays.zeros(n + far)
+    z = 10.0 * (1.0 + jitter_rel * rng.uniform(-1, 1, n))
+    z[::5] = 10.0                              # exact ties: index order decides
+    a.means[:n] = np.stack([rng.uniform(-4, 4, n), rng.uniform(-4, 4, n), z], 1)
+    a.means[n:] = np.stack([rng.uniform(-300, 300, far), rng.uniform(-300, 300, far), np.full(far, 1000.0)], 1)
+    a.scales[:] = rng.uniform(0.02, 0.08, (n + far, 3))
+    a.rotations[:, 0] = 1.0
+    a.opacities[:] = rng.uniform(0.3, 0.9, n + far)
+    a.base_colors[:] = rng.uniform(0, 1, (n + far, 3))
+    return a
+
+
+def test_facade_depth_order_exact():
+    """fixup_runs_kernel's worst case: a 20k-splat facade whose depths tie in
+    the top 32 bits of the key range — the long run is detected and the
+    order finished by full-width radix passes; the image equals the oracle's."""
+    from paper_2507_01110_b200.core import Camera
+    rng = np.random.default_rng(8)
+    a = _facade(20_000, rng, 1e-9)
+    cam = Camera(position=np.zeros(3), orientation=np.array([1.0, 0.0, 0.0, 0.0]), focal=(100.0, 100.0),
+                 principal_point=(64.0, 64.0), resolution=(128, 128))
+    ctx = Rn.render_forward(a, cam)
+    assert Rn._rasterizer().stats()["depth_full_sort"]
+    want, _ = O.render_forward({k: getattr(a, k) for k in NAMES}, O.Cam.of(cam))
+    assert np.abs(ctx.image - want).max() <= IMG_TOL
+
+
+def test_facade_render_time_bounded():
+    """1M facade splats, depths within 1e-9 relative, must render within 2x
+    the time of the same splats at random depths (no O(run²) fix-up)."""
+    import time as _t
+    from paper_2507_01110_b200.core import Camera
+    rng = np.random.default_rng(9)
+    cam = Camera(position=np.zeros(3), orientation=np.array([1.0, 0.0, 0.0, 0.0]), focal=(1400.0, 1400.0),
+                 principal_point=(960.0, 540.0), resolution=(1920, 1080))
+    fac = _facade(1_000_000, rng, 1e-9)
+    rnd = AttributeArrays(*(np.array(getattr(fac, k), copy=True) for k in NAMES))
+    rnd.means[:1_000_000, 2] = rng.uniform(5.0, 15.0, 1_000_000)
+    rast = Rn.Rasterizer()
+    times = {}
+    for name, a in (("random", rnd), ("facade", fac)):
+        t = torch.from_numpy(a.packed()).cuda()
+        ts = []
+        for r in range(4):
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
+            rast.forward(t, len(a), cam)
+            torch.cuda.synchronize()
+            ts.append(_t.perf_counter() - t0)
+        times[name] = min(ts[1:])
+        if name == "facade":
+            assert rast.stats()["depth_full_sort"]
+    assert times["facade"] <= 2.0 * times["random"], times

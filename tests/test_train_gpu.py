@@ -230,3 +230,20 @@ def test_non_finite_loss_raises_before_adam():
         tr.train_step(2)
     torch.cuda.synchronize()
     assert torch.equal(before, tr.scene.records)
+
+
+def test_render_prefetch_is_invisible():
+    """render_view with the next frame known prefetches that frame's misses
+    on the copy engines: identical images and counters to the path without."""
+    a, _, _ = make_case(budget_frac=0.3)
+    b, _, _ = make_case(budget_frac=0.3)
+    n = len(a.views)
+    used = 0
+    for f in range(12):
+        v, nv = (3 * f) % n, (3 * f + 3) % n
+        ia = a.render_view(v)
+        ib = b.render_view(v, next_view=nv)
+        assert a.last_render == b.last_render, f
+        assert torch.equal(ia, ib), f
+    torch.cuda.synchronize()
+    assert b.cache.stats()["prefetch_used_rows"] > 0

@@ -14,7 +14,12 @@ import subprocess
 
 M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
      "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
-     "smsp__inst_executed.sum", "launch__registers_per_thread"]
+     "smsp__inst_executed.sum", "launch__registers_per_thread",
+     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
 UNIT = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
         "Tbyte": 1e12}
 
@@ -34,8 +39,13 @@ def main():
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("unnamed>::", "")
         name = name.split("<")[0] if name.startswith(("store_xfer", "scatter_kernel")) else name
         for m in M:
+            if m not in h:
+                continue
             u = units[h.index(m)]
-            v = float(d[m].replace(",", ""))
+            try:
+                v = float(d[m].replace(",", ""))
+            except ValueError:
+                continue
             agg[name][m].append(v * UNIT.get(u, 1.0))
     res = {}
     print("| kernel | launches | ms | DRAM MB/launch | DRAM GB/s | issue active % | warps active % | regs |")
@@ -47,8 +57,12 @@ def main():
         iss = sum(d[M[3]]) / n
         wa = sum(d[M[4]]) / n
         regs = d[M[6]][0]
+        mean = lambda m: (sum(d[m]) / len(d[m])) if d.get(m) else None
         res[name] = {"launches": n, "ms": ms, "dram_bytes_per_launch": by, "dram_gbs": by / (ms * 1e-3) / 1e9,
-                     "issue_active_pct": iss, "warps_active_pct": wa, "registers": regs, "source": a.rep}
+                     "issue_active_pct": iss, "warps_active_pct": wa, "registers": regs,
+                     "smem_wavefronts_pct": mean(M[7]),
+                     "pipe_pct": {"alu": mean(M[8]), "fma": mean(M[9]), "xu": mean(M[10]), "lsu": mean(M[11])},
+                     "warp_instructions": sum(d[M[5]]) / n, "source": a.rep}
         print(f"| {name} | {n} | {ms:.3f} | {by / 1e6:.1f} | {by / (ms * 1e-3) / 1e9:.0f} | {iss:.1f} | {wa:.1f} | {regs:.0f} |")
     if a.json:
         json.dump(res, open(a.json, "w"), indent=1)
