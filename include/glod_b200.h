@@ -482,6 +482,16 @@ int glod_cache_materialize(glod_cache* c, void* stream);
 int glod_cache_resident(const glod_cache* c, uint64_t* block, int64_t* rows, int32_t num_spts);
 /* Mark the resident entries whose flag is set dirty (host int32 per SPT id). */
 int glod_cache_mark_dirty(glod_cache* c, const int32_t* flags, int32_t num_spts);
+/* Disk mode (the reference's FileBacking, store.py:84-112):
+ * the store stays in a .glod file (`fd` opened read-write, section_offset[k]
+ * = byte offset of attribute section k).  Misses are pread() into pinned
+ * bounce buffers and copied to HBM (prefetches while the GPU computes),
+ * write-backs are copied back and pwrite()n before the next read.  Call
+ * before the first step; the store view's section pointers are unused. */
+int glod_cache_set_file(glod_cache* c, int32_t fd, const int64_t* section_offset);
+/* Issue pending write-backs and (disk mode) complete them into the file;
+ * reports the bytes read from / written to the file so far. */
+int glod_cache_flush_io(glod_cache* c, int64_t* bytes_read, int64_t* bytes_written);
 /* Resident entries in LRU order (front first), up to `capacity`. */
 int glod_cache_entries(const glod_cache* c, int32_t* spt_id, double* cached_distance,
                        int64_t* prefix_len, uint64_t* block, int32_t* dirty, int64_t capacity);

@@ -139,6 +139,8 @@ SIGNATURES = {
     "glod_cache_create": (C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_int64, C.c_int32, P,
                                     C.c_int32, C.POINTER(P)]),
     "glod_cache_destroy": (C.c_int, [P]),
+    "glod_cache_set_file": (C.c_int, [P, C.c_int32, P]),
+    "glod_cache_flush_io": (C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "glod_cache_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, P, P, P, P, P]),
     "glod_cache_end_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int64, C.c_int32, P]),
     "glod_cache_prefetch": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, C.c_int64, P, P]),

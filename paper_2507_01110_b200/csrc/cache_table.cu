@@ -11,6 +11,7 @@
 // side stream).
 #include <stdint.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <list>
@@ -194,6 +195,36 @@ struct CacheTable {
   std::vector<PendingWb> pending;
   float* hsec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
+  // Disk mode (the reference's FileBacking, store.py:
+  // 84-112): the store stays in the .glod file.  Reads of SPT prefixes are
+  // pread()s of the 6 section ranges into pinned bounce buffers followed by
+  // one H2D copy (cold misses: on the main stream before the load kernel;
+  // prefetches: on the prefetch stream, issued while the GPU computes the
+  // current step); write-backs are D2H copies into a pinned bounce buffer
+  // and pwrite()s, completed before the next read of the file, so every
+  // read sees every earlier write-back exactly as the reference's
+  // synchronous write_back.
+  struct DiskPiece {
+    int64_t file_off;
+    size_t buf_off, bytes;
+  };
+  struct DiskIO {
+    int fd = -1;
+    int64_t off[6] = {0, 0, 0, 0, 0, 0};      // byte offset of section k in the file
+    float* rd = nullptr;                       // pinned: cold-miss reads
+    size_t rd_cap = 0;
+    float* pfb = nullptr;                      // pinned: prefetch reads
+    size_t pfb_cap = 0;
+    char* wbb = nullptr;                       // pinned: write-back bytes awaiting pwrite
+    size_t wbb_cap = 0, wbb_used = 0;
+    float* dtmp = nullptr;                     // device f32 copies of cold misses
+    size_t dtmp_cap = 0;
+    cudaEvent_t rd_done = nullptr, pf_done = nullptr, wb_done = nullptr;
+    std::vector<DiskPiece> writes;
+    int64_t bytes_read = 0, bytes_written = 0;
+  } disk;
+  bool disk_mode() const { return disk.fd >= 0; }
+
   // Prefetch (glod_cache_prefetch): the predicted misses of the next view
   // are copied store → f32 HBM buffers by the copy engines on `pf_st`
   // while the current step computes; the next cache_step converts a
@@ -233,9 +264,14 @@ struct CacheTable {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_pf, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_pf_free, cudaEventDisableTiming);
     if (e != cudaSuccess) return e;
+    if (disk_mode()) {
+      for (cudaEvent_t* ev : {&disk.rd_done, &disk.pf_done, &disk.wb_done})
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
     // host addresses of the store sections (the view holds device-mapped
     // addresses; the copy engines take the host side under UVA)
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < 6 && !disk_mode(); ++k) {
       cudaPointerAttributes at;
       e = cudaPointerGetAttributes(&at, sv.section[k]);
       if (e != cudaSuccess) return e;
@@ -284,6 +320,7 @@ struct CacheTable {
 
   // Issue the queued write-back DMA (side stream).
   cudaError_t issue_pending() {
+    if (disk_mode()) return issue_pending_disk();
     for (PendingWb& w : pending) {
       cudaError_t e = cudaStreamWaitEvent(side, ev_packed[w.sb], 0);
       if (e != cudaSuccess) return e;
@@ -302,7 +339,83 @@ struct CacheTable {
     return cudaSuccess;
   }
 
+  // ---- disk mode helpers ----------------------------------------------
+  static cudaError_t ensure_pinned(void** p, size_t* cap, size_t bytes) {
+    if (bytes <= *cap) return cudaSuccess;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *cap = 0;
+    const size_t want = bytes + bytes / 2 + (size_t(1) << 20);
+    cudaError_t e = cudaMallocHost(p, want);
+    if (e == cudaSuccess) *cap = want;
+    return e;
+  }
+  // 6 preads of a prefix into dst (section-major, `rows` rows per section)
+  bool read_prefix(int64_t slot, int64_t rows, float* dst) {
+    for (int k = 0; k < 6; ++k) {
+      const int cols = kSecOffH[k + 1] - kSecOffH[k];
+      const size_t bytes = size_t(cols) * size_t(rows) * sizeof(float);
+      char* d = reinterpret_cast<char*>(dst + (int64_t)kSecOffH[k] * rows);
+      const int64_t at = disk.off[k] + slot * cols * int64_t(sizeof(float));
+      size_t done = 0;
+      while (done < bytes) {
+        const ssize_t r = pread(disk.fd, d + done, bytes - done, at + int64_t(done));
+        if (r <= 0) return false;
+        done += size_t(r);
+      }
+      disk.bytes_read += int64_t(bytes);
+    }
+    return true;
+  }
+  // complete every write-back: wait for its D2H copy, then pwrite
+  cudaError_t flush_disk_writes() {
+    if (disk.writes.empty()) return cudaSuccess;
+    cudaError_t e = cudaEventSynchronize(disk.wb_done);
+    if (e != cudaSuccess) return e;
+    for (const DiskPiece& p : disk.writes) {
+      size_t done = 0;
+      while (done < p.bytes) {
+        const ssize_t r = pwrite(disk.fd, disk.wbb + p.buf_off + done, p.bytes - done, p.file_off + int64_t(done));
+        if (r <= 0) return cudaErrorUnknown;
+        done += size_t(r);
+      }
+      disk.bytes_written += int64_t(p.bytes);
+    }
+    disk.writes.clear();
+    disk.wbb_used = 0;
+    wb_prev.clear();
+    return cudaSuccess;
+  }
+  cudaError_t issue_pending_disk() {
+    for (PendingWb& w : pending) {
+      size_t need = 0;
+      for (size_t i = 0; i < w.size.size(); ++i) need += w.size[i];
+      if (disk.wbb_used + need > disk.wbb_cap) {
+        cudaError_t e = flush_disk_writes();       // drains the bounce buffer
+        if (e == cudaSuccess) e = ensure_pinned(reinterpret_cast<void**>(&disk.wbb), &disk.wbb_cap, need);
+        if (e != cudaSuccess) return e;
+      }
+      cudaError_t e = cudaStreamWaitEvent(side, ev_packed[w.sb], 0);
+      if (e != cudaSuccess) return e;
+      for (size_t i = 0; i < w.size.size(); ++i) {
+        // w.dst holds the file offset of the piece in disk mode
+        e = cudaMemcpyAsync(disk.wbb + disk.wbb_used, w.src[i], w.size[i], cudaMemcpyDeviceToHost, side);
+        if (e != cudaSuccess) return e;
+        disk.writes.push_back({int64_t(reinterpret_cast<intptr_t>(w.dst[i])), disk.wbb_used, w.size[i]});
+        disk.wbb_used += w.size[i];
+      }
+      e = cudaEventRecord(ev_stage[w.sb], side);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_wb, side);
+      if (e == cudaSuccess) e = cudaEventRecord(disk.wb_done, side);
+      if (e != cudaSuccess) return e;
+      for (int32_t sid : w.sids) wb_prev[sid] = 1;
+    }
+    pending.clear();
+    return cudaSuccess;
+  }
+
   ~CacheTable() {
+    if (disk_mode()) flush_disk_writes();
     if (side) cudaStreamSynchronize(side);
     if (pf_st) cudaStreamSynchronize(pf_st);
     cudaDeviceSynchronize();
@@ -323,6 +436,12 @@ struct CacheTable {
       if (ev_packed[k]) cudaEventDestroy(ev_packed[k]);
     }
     if (pool) cudaMemPoolDestroy(pool);
+    if (disk.rd) cudaFreeHost(disk.rd);
+    if (disk.pfb) cudaFreeHost(disk.pfb);
+    if (disk.wbb) cudaFreeHost(disk.wbb);
+    if (disk.dtmp) cudaFree(disk.dtmp);
+    for (cudaEvent_t ev : {disk.rd_done, disk.pf_done, disk.wb_done})
+      if (ev) cudaEventDestroy(ev);
   }
 
   // pinned item table of at least `bytes`, safe to rewrite
@@ -502,7 +621,9 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     for (const Xfer& x : wbs) {
       for (int k = 0; k < 6; ++k) {
         const int cols = kSecOffH[k + 1] - kSecOffH[k];
-        w.dst.push_back(c->hsec[k] + x.slot * cols);
+        w.dst.push_back(c->disk_mode()
+                            ? reinterpret_cast<void*>(intptr_t(c->disk.off[k] + x.slot * cols * int64_t(sizeof(float))))
+                            : static_cast<void*>(c->hsec[k] + x.slot * cols));
         w.src.push_back(staging + acc + (long long)kSecOffH[k] * x.rows);
         w.size.push_back(size_t(cols) * size_t(x.rows) * sizeof(float));
       }
@@ -535,6 +656,11 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
       hit = cd == 0.0 ? d == 0.0 : (c->d_min <= d / cd && d / cd <= c->d_max);
     }
     if (!hit) return cudaErrorNotPermitted;
+  }
+  // disk mode: every earlier write-back reaches the file before it is read
+  if (c->disk_mode()) {
+    e = c->flush_disk_writes();
+    if (e != cudaSuccess) return e;
   }
   // write-backs of earlier steps already finished: nothing to wait for
   if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
@@ -624,6 +750,39 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
     block_out[j] = reinterpret_cast<uint64_t>(en.block);
     rows_out[j] = en.prefix_len;
   }
+  if (c->disk_mode()) {
+    // misses without a prefetch: pread into the pinned bounce, one H2D copy
+    // on this stream, then the load kernel converts from HBM (overlaid
+    // rows of a block evicted this step still come from that block)
+    size_t rows = 0;
+    for (const Xfer& x : loads)
+      if (!x.src) rows += size_t(x.rows);
+    if (rows > 0) {
+      const size_t bytes = rows * kFloats * sizeof(float);
+      e = cudaEventSynchronize(c->disk.rd_done);
+      if (e == cudaSuccess)
+        e = CacheTable::ensure_pinned(reinterpret_cast<void**>(&c->disk.rd), &c->disk.rd_cap, bytes);
+      if (e == cudaSuccess && bytes > c->disk.dtmp_cap) {
+        if (c->disk.dtmp) cudaFree(c->disk.dtmp);
+        c->disk.dtmp = nullptr;
+        c->disk.dtmp_cap = 0;
+        const size_t want = bytes + bytes / 2;
+        e = cudaMalloc(&c->disk.dtmp, want);
+        if (e == cudaSuccess) c->disk.dtmp_cap = want;
+      }
+      if (e != cudaSuccess) return e;
+      size_t at = 0;
+      for (Xfer& x : loads) {
+        if (x.src) continue;
+        if (!c->read_prefix(x.slot, x.rows, c->disk.rd + at)) return cudaErrorUnknown;
+        x.src = c->disk.dtmp + at;
+        at += size_t(x.rows) * kFloats;
+      }
+      e = cudaMemcpyAsync(c->disk.dtmp, c->disk.rd, bytes, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaEventRecord(c->disk.rd_done, st);
+      if (e != cudaSuccess) return e;
+    }
+  }
   e = run_batch(c, loads, wbs, join, wait_pf, sv, st);
   if (e != cudaSuccess) return e;
   // every prefetch of the last step is done with once the load kernel ran
@@ -696,6 +855,10 @@ cudaError_t cache_prefetch(CacheTable* c, const glod_store_view& sv, int32_t n, 
   if (e != cudaSuccess) return e;
   *rows_out = 0;
   if (!c->pfmem.ready()) return cudaSuccess;
+  if (c->disk_mode()) {                       // the file holds every write-back so far
+    e = c->flush_disk_writes();
+    if (e != cudaSuccess) return e;
+  }
   if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
   struct Want {
     int32_t sid;
@@ -733,6 +896,25 @@ cudaError_t cache_prefetch(CacheTable* c, const glod_store_view& sv, int32_t n, 
   if (e != cudaSuccess) return e;
   auto issue = [&](const std::vector<Want>& v) -> cudaError_t {
     if (v.empty()) return cudaSuccess;
+    if (c->disk_mode()) {
+      // pread on the host now (the GPU is busy with this step), then the
+      // copy engines move the bounce buffer's prefixes to their HBM buffers
+      size_t bytes = 0;
+      for (const Want& w : v) bytes += size_t(w.rows) * kFloats * sizeof(float);
+      cudaError_t er = cudaEventSynchronize(c->disk.pf_done);
+      if (er == cudaSuccess)
+        er = CacheTable::ensure_pinned(reinterpret_cast<void**>(&c->disk.pfb), &c->disk.pfb_cap, bytes);
+      if (er != cudaSuccess) return er;
+      size_t at = 0;
+      for (const Want& w : v) {
+        if (!c->read_prefix(c->slot_start[w.sid], w.rows, c->disk.pfb + at)) return cudaErrorUnknown;
+        er = cudaMemcpyAsync(w.buf, c->disk.pfb + at, size_t(w.rows) * kFloats * sizeof(float),
+                             cudaMemcpyHostToDevice, c->pf_st);
+        if (er != cudaSuccess) return er;
+        at += size_t(w.rows) * kFloats;
+      }
+      return cudaEventRecord(c->disk.pf_done, c->pf_st);
+    }
     std::vector<void*> dst, src;
     std::vector<size_t> size;
     dst.reserve(6 * v.size()); src.reserve(6 * v.size()); size.reserve(6 * v.size());
@@ -790,6 +972,24 @@ int glod_cache_create(int64_t budget_bytes, double d_min, double d_max, int64_t 
   cudaGetDevice(&c->t.device);
   glod::retain_pool_memory();
   *out = c;
+  return GLOD_OK;
+}
+
+int glod_cache_set_file(glod_cache* c, int32_t fd, const int64_t* section_offset) {
+  if (!c || fd < 0 || !section_offset) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (c->t.ready) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "set the file before the first step");
+  c->t.disk.fd = fd;
+  for (int k = 0; k < 6; ++k) c->t.disk.off[k] = section_offset[k];
+  return GLOD_OK;
+}
+
+int glod_cache_flush_io(glod_cache* c, int64_t* bytes_read, int64_t* bytes_written) {
+  if (!c) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  cudaError_t e = c->t.issue_pending();
+  if (e == cudaSuccess && c->t.disk_mode()) e = c->t.flush_disk_writes();
+  if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
+  if (bytes_read) *bytes_read = c->t.disk.bytes_read;
+  if (bytes_written) *bytes_written = c->t.disk.bytes_written;
   return GLOD_OK;
 }
 

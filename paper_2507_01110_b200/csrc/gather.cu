@@ -304,8 +304,20 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
   const long long c1 = min(n, c0 + kChunk);
   if (bm.y == 0)                                 // a freshly loaded block: no row touched
     for (long long w = threadIdx.x; w < (I.rows + 63) / 64; w += blockDim.x) block_bits(I.block, I.rows)[w] = 0;
-  if (I.src) {                                   // prefetched f32 copy in HBM
-    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
+  if (I.src) {                                   // f32 copy in HBM (prefetch / disk read)
+    if (I.overlay_rows == 0) {
+      for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
+      return;
+    }
+    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {
+      int sec = 0;
+#pragma unroll
+      for (int k = 1; k < 6; ++k) sec += l >= kSecOff[k] * I.rows;
+      const long long within = l - kSecOff[sec] * I.rows;
+      const long long row = within / kSecCols[sec];
+      I.block[l] = row < I.overlay_rows ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
+                                        : double(I.src[l]);
+    }
     return;
   }
   for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {

@@ -289,6 +289,14 @@ class Scene:
             st.sections.append(t.to("cuda") if location == "device" else t)
         return st
 
+    def disk_store(self):
+        """Disk mode: a store that stays in this file (store.DiskStore)."""
+        from .store import DiskStore
+        if self.sh_cols != 9:
+            raise ValueError("the device path keeps degree-1 SH (9 columns)")
+        self.f.flush()
+        return DiskStore(self)
+
     def save_store(self, store: HostStore) -> None:
         """Write the store's sections back into the file (store.py:323-333 for
         every slot), e.g. after training or at a flush."""

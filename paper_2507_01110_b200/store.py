@@ -203,3 +203,72 @@ class HostStore:
                 "gaussian_count": int(n), "attribute_total_bytes": int(n) * attr,
                 "optimizer_total_bytes": int(n) * 2 * attr, "spt_metadata_total_bytes": int(n) * 12,
                 "training_bytes_per_gaussian": attr + 2 * attr + 12 + 12}
+
+
+class DiskStore(HostStore):
+    """Disk mode (the reference's FileBacking,
+    store.py:84-112): the six attribute sections stay in the .glod file.
+    The device cache pread()s missed prefixes into pinned bounce buffers and
+    copies them to HBM (prefetches overlap the GPU's work on the current
+    step) and pwrite()s write-backs (glod_cache_set_file); nothing of the
+    store is held in host memory.  `sections` are read-only memory maps of
+    the file for host-side inspection (they show the file as written so
+    far; call the cache's flush_io() first)."""
+
+    def __init__(self, scene):
+        import os
+        self.location = "disk"
+        self.path = str(scene.path)
+        self.slot_to_node = np.asarray(scene.slot_to_node, dtype=np.int64).copy()
+        self.nslots = int(scene.nslots)
+        self.record_offset = np.asarray(scene.spt_dir["record_offset"], dtype=np.int64)
+        self.record_count = np.asarray(scene.spt_dir["record_count"], dtype=np.int64)
+        self.total_records = int(self.record_count.sum())
+        self.attribute_bytes_read = 0
+        self.section_offsets = np.array([scene.sections[name][0] for name, _ in SECTIONS], dtype=np.int64)
+        self.fd = os.open(self.path, os.O_RDWR)
+
+    def __del__(self):
+        import os
+        try:
+            os.close(self.fd)
+        except Exception:
+            pass
+
+    @property
+    def sections(self):
+        out = []
+        for (name, cols), off in zip(SECTIONS, self.section_offsets):
+            m = np.memmap(self.path, dtype="<f4", mode="r", offset=int(off), shape=(self.nslots, cols))
+            out.append(torch.from_numpy(np.array(m)))
+        return out
+
+    def load_spt_prefix(self, spt_id: int, prefix_len: int) -> AttributeBlock:
+        self._check(spt_id)
+        if prefix_len > int(self.record_count[spt_id]):
+            raise InvalidBlockError(f"prefix {prefix_len} exceeds record count "
+                                    f"{int(self.record_count[spt_id])}")
+        s = self.spt_slot_start(spt_id)
+        parts = []
+        for (name, cols), off in zip(SECTIONS, self.section_offsets):
+            a = np.fromfile(self.path, dtype="<f4", count=prefix_len * cols, offset=int(off) + 4 * cols * s)
+            parts.append(a.reshape(prefix_len, cols) if cols > 1 else a)
+        self.attribute_bytes_read += prefix_len * self.bytes_per_gaussian
+        return AttributeBlock(spt_id, int(prefix_len), AttributeArrays(*parts))
+
+    def write_back(self, block: AttributeBlock) -> None:
+        import os
+        self._check(block.spt_id)
+        s = self.spt_slot_start(block.spt_id)
+        for (name, cols), off in zip(SECTIONS, self.section_offsets):
+            v = np.asarray(getattr(block.attrs, name), dtype="<f4").reshape(block.prefix_len, cols)
+            os.pwrite(self.fd, v.tobytes(), int(off) + 4 * cols * s)
+
+    def device_view(self):
+        from . import _lib
+        v = _lib.StoreView()
+        v.nslots = self.nslots
+        return v
+
+    def to_scene(self, scene) -> None:
+        """The file is the store: nothing to copy (flush the cache first)."""

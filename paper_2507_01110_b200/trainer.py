@@ -330,6 +330,7 @@ class Trainer:
         """Write every dirty resident block back to the store and empty the
         cache (the reference's flush, cache.py:98-106)."""
         self.cache.end_step(0, mark_dirty=False)
+        self.cache.flush_io()               # disk store: write-backs reach the file
 
     # -- optional per-stage CUDA-event timing (bench.py) ---------------------
     def enable_timing(self, on: bool = True):

@@ -247,3 +247,42 @@ def test_render_prefetch_is_invisible():
         assert torch.equal(ia, ib), f
     torch.cuda.synchronize()
     assert b.cache.stats()["prefetch_used_rows"] > 0
+
+
+def test_disk_store_matches_host_store(tmp_path):
+    """Disk mode (FileBacking, store.py:84-112): the store
+    stays in the .glod file — misses pread + H2D (prefetches overlapping the
+    step), write-backs D2H + pwrite before the next read.  Against the
+    pinned-DRAM store of the same file: identical counters every step
+    (misses, hits, evictions, re-misses, flushes), the same parameters, and
+    after a flush the file holds exactly the pinned store's bytes."""
+    import shutil
+    from paper_2507_01110_b200 import scenefile as SF
+    h0, hs0, cfg = designed_scene(SceneSpec(n_leaves=6000, spt_leaves=256, seed=3, pass_fraction=0.1))
+    pa, pb = tmp_path / "a.glod", tmp_path / "b.glod"
+    SF.write_scene(h0, hs0, pa)
+    shutil.copy(pa, pb)
+    sa, sb = SF.open_scene(pa), SF.open_scene(pb)
+    h, hs = sa.read_hierarchy(), sa.read_hspt()
+    E = scene_extent(6000)
+    cams = orbit_views(10, 1.5 * E, 0.6 * E, resolution=(96, 64), focal=(70.0, 70.0), seed=3, jitter=0.2)
+    rng = np.random.default_rng(3)
+    targets = [np.clip(rng.normal(0.5, 0.2, (64, 96, 3)), 0, 1) for _ in cams]
+    budget = int(0.3 * hs.flat_records()["nodes"].size * 92)
+    mk = lambda store: Trainer(h, hs, list(zip(cams, targets)),
+                               TrainConfig(lod=cfg, cache=CacheConfig(budget_bytes=budget, flush_interval=7),
+                                           scheduler_k=4, seed=3), extent=2 * E, store=store)
+    a, b = mk(sa.host_store()), mk(sb.disk_store())
+    assert b.scene.store.location == "disk"
+    for it in range(1, 16):
+        ra, rb = a.train_step(it), b.train_step(it)
+        assert ra == rb, it
+    a.flush_cache()
+    b.flush_cache()
+    torch.cuda.synchronize()
+    io = b.cache.flush_io()
+    assert io["file_bytes_read"] > 0 and io["file_bytes_written"] > 0
+    assert same_state(a.scene.params, b.scene.params)
+    assert same_state(a.scene.mv, b.scene.mv)
+    for sa_, sb_ in zip(a.scene.store.sections, b.scene.store.sections):
+        assert same_state(sa_, sb_)
