@@ -443,6 +443,8 @@ def run_ours(args):
     # ---- per-stage timing (separate pass; CUDA events per stage) ---------
     tr.enable_timing(True)
     tr.rast.blend_timing(True)
+    if os.environ.get("GLOD_BENCH_STEP_TIMES") == "1":
+        tr.host_timing = {}
     npix = args.width * args.height
     alg = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0, "gather": 0.0}
     n_t = max(3, args.steps // 4)
@@ -457,6 +459,10 @@ def run_ours(args):
         alg["gather"] += R * 372
     bt = tr.rast.blend_timing(False)
     stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
+    if tr.host_timing is not None:
+        print("host ms per stage:", {k: round(float(np.mean(v)), 3) for k, v in tr.host_timing.items()},
+              file=sys.stderr)
+        tr.host_timing = None
     tr.enable_timing(False)
     kt = {"fwd_ms": bt["fwd_ms"] / max(bt["fwd_launches"], 1), "bwd_ms": bt["bwd_ms"] / max(bt["bwd_launches"], 1),
           "fwd_alg": alg["fwd"] / n_t, "bwd_alg": alg["bwd"] / n_t, "adam_alg": alg["adam"] / n_t,

@@ -378,8 +378,13 @@ int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* str
 /* The pinned host store (store.py's slot-ordered f32 sections), as device-
  * accessible addresses of page-locked host memory (glod_host_device_ptr). */
 typedef struct glod_store_view {
-  const float* section[6];      /* [host-mapped] section k: nslots x cols_k   */
+  const float* section[6];      /* [host-mapped] first value of section k     */
   int64_t nslots;
+  /* 0: section-major (section k is nslots x cols_k, the .glod file's
+   * layout); 23: interleaved rows — one 92-B row per slot, section[k] =
+   * row base + column offset of k — so an SPT prefix is ONE contiguous
+   * range (one copy-engine transfer).  Other values are rejected. */
+  int64_t row_stride;
 } glod_store_view;
 
 /* One SPT prefix transfer: `rows` slots starting at `slot_start` <-> the
@@ -398,8 +403,9 @@ typedef struct glod_prefix_item {
   const double* overlay;        /* [dev]                                       */
   int64_t overlay_rows;
   /* loads only: when non-NULL the prefix is read from this packed f32
-   * section-major copy in HBM (a prefetch, glod_cache_prefetch) instead of
-   * the store; overlay is then unused. */
+   * copy in HBM, laid out like the store (row order for an interleaved
+   * store, else section-major; a prefetch, glod_cache_prefetch) instead of
+   * the store. */
   const float* src;             /* [dev]                                       */
 } glod_prefix_item;
 
@@ -512,6 +518,11 @@ int glod_sort_pairs_u32(uint32_t* keys, uint32_t* keys_alt, int32_t* vals, int32
  * never queues behind bulk D2H DMA).  The caller synchronises the stream
  * before reading host_pinned. */
 int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream);
+/* The reverse: a stream-ordered small host→device upload read by a kernel
+ * from page-locked memory (no copy-engine queueing behind the cache's bulk
+ * prefetch DMA).  host_pinned must stay unchanged until the stream has run
+ * the upload; pageable memory falls back to cudaMemcpyAsync. */
+int glod_upload(void* dst, const void* host_pinned, int64_t bytes, void* stream);
 /* Synchronous device→host copy (snapshots / tests). */
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 

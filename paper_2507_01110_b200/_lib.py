@@ -86,7 +86,7 @@ class GatherPlan(C.Structure):
 
 
 class StoreView(C.Structure):
-    _fields_ = [("section", P * 6), ("nslots", C.c_int64)]
+    _fields_ = [("section", P * 6), ("nslots", C.c_int64), ("row_stride", C.c_int64)]
 
 
 class PrefixItem(C.Structure):
@@ -164,6 +164,7 @@ SIGNATURES = {
     "glod_xchg_scatter_params": (C.c_int, [P, P, C.c_int64, P]),
     "glod_xchg_stats": (C.c_int, [P, P]),
     "glod_readback": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_upload": (C.c_int, [P, P, C.c_int64, P]),
     "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
     "glod_sort_pairs_u64": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
                                       C.POINTER(C.c_int32), P]),
@@ -243,6 +244,13 @@ def device_view(addr: int, shape, dtype):
     if int(np.prod(shape)) == 0 or not addr:
         return torch.empty(shape, dtype=dtype, device="cuda")
     return torch.as_tensor(_DevArray(addr, shape, typestr), device="cuda")
+
+
+def upload(dst, host_pinned, nbytes: int | None = None, stream=None):
+    """Stream-ordered small upload of a pinned host tensor into a device
+    tensor (kernel-read through the mapped address; see glod_upload)."""
+    n = host_pinned.numel() * host_pinned.element_size() if nbytes is None else nbytes
+    check(lib().glod_upload(ptr(dst), ptr(host_pinned), int(n), stream_ptr(stream)))
 
 
 def readback(host_pinned, src, nbytes: int | None = None, stream=None):

@@ -27,15 +27,13 @@ namespace glod {
 
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
-cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
-                            cudaStream_t st);
 long long transfer_chunks(long long rows);
 cudaError_t launch_materialize(const glod_mat_item* items, int n_items, long long total, const double* master,
                                long long cap, long long mstride, const int* rec_node, cudaStream_t st);
 cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
                                long long nblocks, cudaStream_t st);
 cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
-                               cudaStream_t st);
+                               int interleaved, cudaStream_t st);
 
 namespace {
 
@@ -168,10 +166,10 @@ struct CacheTable {
   // step (so a replaced dirty entry is written back after its stale reload,
   // and every written-back block is read before this step's ADAM refresh
   // rewrites it — the reference writes back at eviction); the copy engines
-  // then move the f32 rows into the pinned store on the side stream
-  // (cudaMemcpyBatchAsync, 6 section ranges per block).  The DMA is issued
-  // at end_step, when the step's kernels are queued and the host is idle
-  // (the batch call costs ~0.3 µs per range of host time).  Two persistent
+  // then move the f32 rows into the pinned store on the side stream (one
+  // cudaMemcpyAsync per block for an interleaved store: the staging copy is
+  // in row order).  The copies are issued at end_step, when the step's
+  // kernels are queued and the host is idle.  Two persistent
   // f32 staging buffers used alternately; the main stream reuses one only
   // after the side stream's copies out of it (ev_stage).  The main stream
   // waits for write-backs only when a load reads store rows a not yet
@@ -193,7 +191,8 @@ struct CacheTable {
     std::vector<int32_t> sids;
   };
   std::vector<PendingWb> pending;
-  float* hsec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  float* dsec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool interleaved = false;
 
   // Disk mode (the reference's FileBacking, store.py:
   // 84-112): the store stays in the .glod file.  Reads of SPT prefixes are
@@ -269,14 +268,10 @@ struct CacheTable {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
       if (e != cudaSuccess) return e;
     }
-    // host addresses of the store sections (the view holds device-mapped
-    // addresses; the copy engines take the host side under UVA)
-    for (int k = 0; k < 6 && !disk_mode(); ++k) {
-      cudaPointerAttributes at;
-      e = cudaPointerGetAttributes(&at, sv.section[k]);
-      if (e != cudaSuccess) return e;
-      hsec[k] = static_cast<float*>(at.hostPointer ? at.hostPointer : const_cast<float*>(sv.section[k]));
-    }
+    // store addresses for the copy engines (UVA: the mapped pinned pages
+    // or, for a device-resident store, HBM); interleaved: one row per slot
+    interleaved = !disk_mode() && sv.row_stride != 0;
+    for (int k = 0; k < 6 && !disk_mode(); ++k) dsec[k] = const_cast<float*>(sv.section[k]);
     // Arenas sized from the budget (counted in f32 store bytes): resident
     // f64 blocks ≤ 2·budget, blocks dropped within a step ≤ 2·budget more;
     // prefetch copies ≤ budget.  Capped by free HBM; a failed reservation
@@ -324,12 +319,10 @@ struct CacheTable {
     for (PendingWb& w : pending) {
       cudaError_t e = cudaStreamWaitEvent(side, ev_packed[w.sb], 0);
       if (e != cudaSuccess) return e;
-      cudaMemcpyAttributes attr = {};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t attr_idx = 0, fail = 0;
-      e = cudaMemcpyBatchAsync(w.dst.data(), w.src.data(), w.size.data(), w.dst.size(), &attr, &attr_idx,
-                               1, &fail, side);
+      // one copy-engine transfer per range: a prefix of an interleaved
+      // store is one range (6 for a section-major one)
+      for (size_t i = 0; i < w.dst.size() && e == cudaSuccess; ++i)
+        e = cudaMemcpyAsync(w.dst[i], w.src[i], w.size[i], cudaMemcpyDefault, side);
       if (e == cudaSuccess) e = cudaEventRecord(ev_stage[w.sb], side);
       if (e == cudaSuccess) e = cudaEventRecord(ev_wb, side);
       if (e != cudaSuccess) return e;
@@ -499,7 +492,8 @@ cudaError_t materialize(CacheTable* c, const std::vector<Xfer>& v, cudaStream_t 
   }
   void* d = nullptr;
   cudaError_t e = c->dalloc(&d, bytes, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = host ? launch_upload(d, src, bytes, st) : cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
     e = launch_materialize(static_cast<glod_mat_item*>(d), int(c->m_items.size()), acc, c->m_master, c->m_cap,
                            c->m_stride, c->m_rec_node, st);
@@ -542,7 +536,7 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
   void* d = nullptr;
   cudaError_t e = c->dalloc(&d, bytes, st);
   if (e != cudaSuccess) return e;
-  e = cudaMemcpyAsync(d, base, bytes, cudaMemcpyHostToDevice, st);
+  e = launch_upload(d, base, bytes, st);        // pinned table, off the copy engines
   if (e != cudaSuccess) return e;
   *d_items = static_cast<glod_prefix_item*>(d);
   *d_bmap = reinterpret_cast<const int2*>(static_cast<char*>(d) + items_bytes);
@@ -610,7 +604,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     }
     float* staging = c->stage[sb];
     e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
-    if (e == cudaSuccess) e = launch_pack_blocks(d, bm, nb, staging, st);
+    if (e == cudaSuccess) e = launch_pack_blocks(d, bm, nb, staging, c->interleaved, st);
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e == cudaSuccess) e = cudaEventRecord(c->ev_packed[sb], st);
     if (e != cudaSuccess) return e;
@@ -619,11 +613,19 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     w.dst.reserve(6 * wbs.size()); w.src.reserve(6 * wbs.size()); w.size.reserve(6 * wbs.size());
     long long acc = 0;
     for (const Xfer& x : wbs) {
+      if (c->interleaved) {
+        w.dst.push_back(static_cast<void*>(c->dsec[0] + x.slot * kFloats));
+        w.src.push_back(staging + acc);
+        w.size.push_back(size_t(kFloats) * size_t(x.rows) * sizeof(float));
+        acc += kFloats * x.rows;
+        w.sids.push_back(x.spt_id);
+        continue;
+      }
       for (int k = 0; k < 6; ++k) {
         const int cols = kSecOffH[k + 1] - kSecOffH[k];
         w.dst.push_back(c->disk_mode()
                             ? reinterpret_cast<void*>(intptr_t(c->disk.off[k] + x.slot * cols * int64_t(sizeof(float))))
-                            : static_cast<void*>(c->hsec[k] + x.slot * cols));
+                            : static_cast<void*>(c->dsec[k] + x.slot * cols));
         w.src.push_back(staging + acc + (long long)kSecOffH[k] * x.rows);
         w.size.push_back(size_t(cols) * size_t(x.rows) * sizeof(float));
       }
@@ -841,8 +843,9 @@ cudaError_t cache_end_step(CacheTable* c, const glod_store_view& sv, int64_t ite
 
 // Prefetch of a predicted view (the scheduler's next draw): every selected
 // SPT the table would miss now is copied store → f32 HBM buffer on the
-// prefetch stream by the copy engines (6 section ranges per prefix, one
-// cudaMemcpyBatchAsync), ordered after every write-back issued so far.
+// prefetch stream by the copy engines (one cudaMemcpyAsync per prefix of an
+// interleaved store, 6 section ranges otherwise), ordered after every
+// write-back issued so far.
 // Read-only on the table; correctness never depends on the prediction
 // (cache_step checks the prefix length and same-step evictions before
 // using one, and a flush drops them).
@@ -915,24 +918,22 @@ cudaError_t cache_prefetch(CacheTable* c, const glod_store_view& sv, int32_t n, 
       }
       return cudaEventRecord(c->disk.pf_done, c->pf_st);
     }
-    std::vector<void*> dst, src;
-    std::vector<size_t> size;
-    dst.reserve(6 * v.size()); src.reserve(6 * v.size()); size.reserve(6 * v.size());
     for (const Want& w : v) {
       const int64_t slot = c->slot_start[w.sid];
+      if (c->interleaved) {
+        cudaError_t er = cudaMemcpyAsync(w.buf, c->dsec[0] + slot * kFloats, size_t(w.rows) * kFloats * sizeof(float),
+                                         cudaMemcpyDefault, c->pf_st);
+        if (er != cudaSuccess) return er;
+        continue;
+      }
       for (int k = 0; k < 6; ++k) {
         const int cols = kSecOffH[k + 1] - kSecOffH[k];
-        dst.push_back(w.buf + (int64_t)kSecOffH[k] * w.rows);
-        src.push_back(c->hsec[k] + slot * cols);
-        size.push_back(size_t(cols) * size_t(w.rows) * sizeof(float));
+        cudaError_t er = cudaMemcpyAsync(w.buf + (int64_t)kSecOffH[k] * w.rows, c->dsec[k] + slot * cols,
+                                         size_t(cols) * size_t(w.rows) * sizeof(float), cudaMemcpyDefault, c->pf_st);
+        if (er != cudaSuccess) return er;
       }
     }
-    cudaMemcpyAttributes attr = {};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail = 0;
-    return cudaMemcpyBatchAsync(dst.data(), src.data(), size.data(), dst.size(), &attr, &attr_idx, 1,
-                                &fail, c->pf_st);
+    return cudaSuccess;
   };
   e = issue(now);
   if (e == cudaSuccess && !after_wb.empty()) {
@@ -1005,6 +1006,8 @@ int glod_cache_step(glod_cache* c, const glod_store_view* store, int32_t n, cons
   if (!c || !store || (n > 0 && (!spt_ids || !d_root || !prefix_len || !dist_out || !block_out ||
                                  !rows_out)) || !counters_out)
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (store->row_stride != 0 && store->row_stride != 23)
+    return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
   cudaError_t e = glod::cache_step(&c->t, *store, n, spt_ids, d_root, prefix_len, dist_out, block_out,
                                    rows_out, counters_out, counters_out + 1,
                                    static_cast<cudaStream_t>(stream));
@@ -1017,6 +1020,8 @@ int glod_cache_step(glod_cache* c, const glod_store_view* store, int32_t n, cons
 int glod_cache_end_step(glod_cache* c, const glod_store_view* store, int64_t iteration,
                         int32_t mark_dirty, void* stream) {
   if (!c || !store) return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (store->row_stride != 0 && store->row_stride != 23)
+    return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
   cudaError_t e = glod::cache_end_step(&c->t, *store, iteration, mark_dirty,
                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
@@ -1028,6 +1033,8 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n, 
                         int64_t* rows_out, void* stream) {
   if (!c || !store || !rows_out || (n > 0 && (!spt_ids || !d_root || !prefix_len)))
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (store->row_stride != 0 && store->row_stride != 23)
+    return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
   cudaError_t e = glod::cache_prefetch(&c->t, *store, n, spt_ids, d_root, prefix_len, max_rows, rows_out,
                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));

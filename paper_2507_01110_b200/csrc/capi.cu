@@ -33,9 +33,10 @@ cudaError_t launch_refresh_resident(const double* master, long long cap, long lo
                                     const unsigned long long* res_block, const long long* res_rows, int* touched,
                                     cudaStream_t st);
 cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, cudaStream_t st);
-cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
+cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, cudaStream_t st);
+cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 }  // namespace glod
 
 struct glod_raster {
@@ -254,6 +255,11 @@ int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* str
                "glod_convert");
 }
 
+int glod_upload(void* dst, const void* host_pinned, int64_t bytes, void* stream) {
+  if ((!host_pinned || !dst) && bytes > 0) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  return check(glod::launch_upload(dst, host_pinned, bytes, static_cast<cudaStream_t>(stream)), "glod_upload");
+}
+
 int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream) {
   if ((!host_pinned || !src) && bytes > 0) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_readback(host_pinned, src, bytes, static_cast<cudaStream_t>(stream)),
@@ -268,6 +274,8 @@ int glod_host_device_ptr(void* host, void** dev) {
 int glod_store_load_prefixes(const glod_store_view* store, const glod_prefix_item* items,
                              int32_t n_items, int64_t total_elems, void* stream) {
   if (!store || (n_items > 0 && !items)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (store->row_stride != 0 && store->row_stride != 23)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
   return check(glod::launch_store_xfer(*store, items, n_items, total_elems, 1,
                                        static_cast<cudaStream_t>(stream)),
                "glod_store_load_prefixes");
@@ -276,6 +284,8 @@ int glod_store_load_prefixes(const glod_store_view* store, const glod_prefix_ite
 int glod_store_write_back(const glod_store_view* store, const glod_prefix_item* items,
                           int32_t n_items, int64_t total_elems, void* stream) {
   if (!store || (n_items > 0 && !items)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (store->row_stride != 0 && store->row_stride != 23)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
   return check(glod::launch_store_xfer(*store, items, n_items, total_elems, 0,
                                        static_cast<cudaStream_t>(stream)),
                "glod_store_write_back");

@@ -15,6 +15,12 @@ struct glod_mat_item {
   long long rec_offset;    // first record of the block's SPT in rec_node
 };
 
+// Small stream-ordered transfers that stay off the copy engines (gather.cu):
+// kernel reads of mapped pinned memory / kernel writes of ≤ 64 bytes.
+cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, cudaStream_t st);
+cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
+cudaError_t launch_set_bytes(void* dst, const void* src, int bytes, cudaStream_t st);
+
 // Host-side count of kernel launches issued by this library (reported by
 // bench.py as gpu_launches; defined in capi.cu).
 void count_launch(unsigned long long n = 1);

@@ -259,9 +259,9 @@ int nccl_fail(ncclResult_t r) { return glod::set_error(GLOD_ERR_CUDA, ncclGetErr
 
 int read_offsets(glod_xchg* x, cudaStream_t st) {
   // off[o] = base[o * Wmax], off[N] = base[N * Wmax] (= |U|)
+  // kernel read-backs: the D2H copy engine may be busy with write-backs
   for (int o = 0; o <= x->N; ++o)
-    XCUDA(cudaMemcpyAsync(x->h_off + o, x->base + (long long)o * x->Wmax, sizeof(uint32_t),
-                          cudaMemcpyDeviceToHost, st));
+    XCUDA(launch_readback(x->h_off + o, x->base + (long long)o * x->Wmax, sizeof(uint32_t), st));
   XCUDA(cudaStreamSynchronize(st));
   x->off.assign(x->N + 1, 0);
   for (int o = 0; o <= x->N; ++o) x->off[o] = x->h_off[o];
@@ -385,7 +385,7 @@ int glod_xchg_pack(glod_xchg* x, const int32_t* row_node, const double* grads, i
     count_launch();
   }
   XCUDA(cudaGetLastError());
-  XCUDA(cudaMemcpyAsync(x->h_counts, x->d_count, x->N * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  XCUDA(launch_readback(x->h_counts, x->d_count, x->N * sizeof(long long), st));
   XCUDA(cudaStreamSynchronize(st));
   x->send_cnt.assign(x->h_counts, x->h_counts + x->N);
   if (counts)
@@ -475,9 +475,9 @@ int glod_grad_exchange(glod_xchg* x, const int32_t* row_node, const double* grad
   const int N = x->N;
   // 1. row counts, then the padded id lists
   long long myR = R;
-  XCUDA(cudaMemcpyAsync(x->d_count, &myR, sizeof(long long), cudaMemcpyHostToDevice, st));
+  XCUDA(launch_set_bytes(x->d_count, &myR, sizeof(long long), st));
   XNCCL(ncclAllGather(x->d_count, x->d_counts_all, 1, ncclInt64, x->comm, st));
-  XCUDA(cudaMemcpyAsync(x->h_counts, x->d_counts_all, N * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  XCUDA(launch_readback(x->h_counts, x->d_counts_all, N * sizeof(long long), st));
   XCUDA(cudaStreamSynchronize(st));
   long long Rmax = 1;
   for (int s = 0; s < N; ++s) Rmax = x->h_counts[s] > Rmax ? x->h_counts[s] : Rmax;
@@ -491,7 +491,7 @@ int glod_grad_exchange(glod_xchg* x, const int32_t* row_node, const double* grad
   // 3. bucket by owner; the count matrix tells every rank what it receives
   if (int rc = glod_xchg_pack(x, row_node, grads, R, nullptr, nullptr, stream)) return rc;
   XNCCL(ncclAllGather(x->d_count, x->d_counts_all, N, ncclInt64, x->comm, st));
-  XCUDA(cudaMemcpyAsync(x->h_counts, x->d_counts_all, (size_t)N * N * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  XCUDA(launch_readback(x->h_counts, x->d_counts_all, (size_t)N * N * sizeof(long long), st));
   XCUDA(cudaStreamSynchronize(st));
   x->recv_cnt.assign(N, 0);
   long long total_recv = 0;

@@ -9,6 +9,8 @@
 //  materialize   touched rows → block before a write-back / overlay
 //  scatter_back  explicit block[pos] = master[node] (public C-ABI)
 //  convert       f32 store prefix ↔ f64 cache block (store.py:334,330)
+#include <string.h>
+
 #include "common.cuh"
 #include "../../include/glod_b200.h"
 
@@ -182,6 +184,54 @@ GLOD_DEV int find_item(const glod_prefix_item* items, int lo, int hi, long long 
   return lo;
 }
 
+// Element l of an item's flat 23·rows index space → (row, block index).
+// Section-major stores (row_stride 0) take l in block order (section, row,
+// column); interleaved stores (row_stride 23: one 92-B row per slot) take
+// l in row order, so the store side of every transfer is one contiguous
+// run and the block side (always section-major) is computed.
+__constant__ unsigned char kColSecG[23] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 4, 4, 5, 5, 5, 5, 5, 5, 5, 5, 5};
+
+struct ElemMap {
+  long long row;      // prefix row
+  long long blk;      // index into the section-major f64 block
+  long long within;   // row·cols + column (index within the section)
+  int sec;
+};
+
+GLOD_DEV ElemMap map_elem(long long l, long long rows, bool interleaved) {
+  ElemMap m;
+  if (interleaved) {
+    m.row = l < 0xffffffffLL ? (long long)(unsigned(l) / 23u) : l / 23;
+    const int col = int(l - m.row * 23);
+    m.sec = kColSecG[col];
+    m.within = m.row * kSecCols[m.sec] + (col - kSecOff[m.sec]);
+    m.blk = kSecOff[m.sec] * rows + m.within;
+  } else {
+    int sec = 0;
+#pragma unroll
+    for (int k = 1; k < 6; ++k) sec += l >= kSecOff[k] * rows;
+    m.sec = sec;
+    m.within = l - kSecOff[sec] * rows;
+    m.row = m.within / kSecCols[sec];
+    m.blk = l;
+  }
+  return m;
+}
+
+// sv.section[sec] without a local-memory copy of the parameter array
+GLOD_DEV const float* section_of(const glod_store_view& sv, int sec) {
+  const float* p = sv.section[0];
+#pragma unroll
+  for (int k = 1; k < 6; ++k) p = sec == k ? sv.section[k] : p;
+  return p;
+}
+
+// Store address of element l of a prefix starting at slot `slot`.
+GLOD_DEV float* store_at(const glod_store_view& sv, long long slot, long long l, const ElemMap& m) {
+  if (sv.row_stride) return const_cast<float*>(sv.section[0]) + slot * 23 + l;
+  return const_cast<float*>(section_of(sv, m.sec)) + slot * kSecCols[m.sec] + m.within;
+}
+
 // Grid-stride over 256-element chunks: the write-back runs on a side stream
 // beside the main step, so its grid is capped (a few CTAs keep the posted
 // PCIe writes saturated) instead of flooding every SM with long-latency
@@ -191,6 +241,7 @@ __global__ void __launch_bounds__(256)
 store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items, int n_items,
                   long long total) {
   __shared__ int s_lo, s_hi;
+  const bool il = sv.row_stride != 0;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < total;
        base += (long long)gridDim.x * blockDim.x) {
     __syncthreads();
@@ -207,44 +258,19 @@ store_xfer_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items
     const long long local = e - I.elem_start;
     const long long rows = I.rows;
     if (kLoad && local < (rows + 63) / 64) block_bits(I.block, rows)[local] = 0;
-    int sec = 0;
-#pragma unroll
-    for (int k = 1; k < 6; ++k) sec += local >= kSecOff[k] * rows;
-    const long long within = local - kSecOff[sec] * rows;
-    float* host = const_cast<float*>(sv.section[sec]) + I.slot_start * kSecCols[sec] + within;
+    const ElemMap m = map_elem(local, rows, il);
     if (kLoad && I.src) {
-      I.block[local] = double(I.src[local]);    // prefetched copy in HBM
+      I.block[m.blk] = double(I.src[local]);    // prefetched copy in HBM (the store's layout)
     } else if (kLoad) {
       // overlay: rows below overlay_rows are the f32 rounding of a block whose
       // write-back to these store rows is still in flight (cache_table.cu)
-      const long long row = within / kSecCols[sec];
-      I.block[local] = row < I.overlay_rows
-                           ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
-                           : double(*host);
+      I.block[m.blk] = m.row < I.overlay_rows
+                           ? double(float(I.overlay[kSecOff[m.sec] * I.overlay_rows + m.within]))
+                           : double(*store_at(sv, I.slot_start, local, m));
     } else {
-      *host = float(I.block[local]);
+      *store_at(sv, I.slot_start, local, m) = float(I.block[m.blk]);
     }
   }
-}
-
-// Write-back staging: every block of the batch → f32, packed in the items'
-// flat element order (section ranges then go to the store by DMA).
-__global__ void __launch_bounds__(256)
-pack_f32_kernel(const glod_prefix_item* __restrict__ items, int n_items, long long total,
-                float* __restrict__ out) {
-  __shared__ int s_lo, s_hi;
-  const long long base = (long long)blockIdx.x * blockDim.x;
-  if (base >= total) return;
-  if (threadIdx.x == 0) {
-    const long long last = min(total, base + (long long)blockDim.x) - 1;
-    s_lo = find_item(items, 0, n_items - 1, base);
-    s_hi = find_item(items, s_lo, n_items - 1, last);
-  }
-  __syncthreads();
-  const long long e = base + threadIdx.x;
-  if (e >= total) return;
-  const int it = s_lo == s_hi ? s_lo : find_item(items, s_lo, s_hi, e);
-  out[e] = float(items[it].block[e - items[it].elem_start]);
 }
 
 // View-sharded training: after the replicated ADAM on the union U of every
@@ -286,14 +312,6 @@ __global__ void refresh_resident_kernel(const double* __restrict__ master, long 
 // contiguous span of one prefix.
 constexpr int kChunk = 2048;
 
-// sv.section[sec] without a local-memory copy of the parameter array
-GLOD_DEV const float* section_of(const glod_store_view& sv, int sec) {
-  const float* p = sv.section[0];
-#pragma unroll
-  for (int k = 1; k < 6; ++k) p = sec == k ? sv.section[k] : p;
-  return p;
-}
-
 __global__ void __launch_bounds__(256)
 load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items,
                    const int2* __restrict__ bmap) {
@@ -302,48 +320,41 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
   const long long n = 23LL * I.rows;
   const long long c0 = (long long)bm.y * kChunk;
   const long long c1 = min(n, c0 + kChunk);
+  const bool il = sv.row_stride != 0;
   if (bm.y == 0)                                 // a freshly loaded block: no row touched
     for (long long w = threadIdx.x; w < (I.rows + 63) / 64; w += blockDim.x) block_bits(I.block, I.rows)[w] = 0;
-  if (I.src) {                                   // f32 copy in HBM (prefetch / disk read)
-    if (I.overlay_rows == 0) {
-      for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
-      return;
-    }
-    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {
-      int sec = 0;
-#pragma unroll
-      for (int k = 1; k < 6; ++k) sec += l >= kSecOff[k] * I.rows;
-      const long long within = l - kSecOff[sec] * I.rows;
-      const long long row = within / kSecCols[sec];
-      I.block[l] = row < I.overlay_rows ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
-                                        : double(I.src[l]);
-    }
+  if (I.src && !il && I.overlay_rows == 0) {     // section-major f32 copy in HBM (disk read)
+    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
     return;
   }
   for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {
-    int sec = 0;
-#pragma unroll
-    for (int k = 1; k < 6; ++k) sec += l >= kSecOff[k] * I.rows;
-    const long long within = l - kSecOff[sec] * I.rows;
-    const long long row = within / kSecCols[sec];
+    const ElemMap m = map_elem(l, I.rows, il);
     // overlay: rows below overlay_rows are the f32 rounding of a block whose
-    // write-back to these store rows is still in flight (cache_table.cu)
-    I.block[l] = row < I.overlay_rows
-                     ? double(float(I.overlay[kSecOff[sec] * I.overlay_rows + within]))
-                     : double(section_of(sv, sec)[I.slot_start * kSecCols[sec] + within]);
+    // write-back to these store rows is still in flight (cache_table.cu);
+    // src: the prefix's f32 copy in HBM (prefetch / disk read), laid out
+    // like the store
+    I.block[m.blk] = m.row < I.overlay_rows
+                         ? double(float(I.overlay[kSecOff[m.sec] * I.overlay_rows + m.within]))
+                         : double(I.src ? I.src[l] : *store_at(sv, I.slot_start, l, m));
   }
 }
 
+// Write-back staging: the block as f32 in the store's layout (row order for
+// an interleaved store, so one copy per prefix moves it).
 __global__ void __launch_bounds__(256)
 pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __restrict__ bmap,
-                   float* __restrict__ out) {
+                   float* __restrict__ out, int interleaved) {
   const int2 bm = bmap[blockIdx.x];
   const glod_prefix_item I = items[bm.x];
   const long long n = 23LL * I.rows;
   const long long c0 = (long long)bm.y * kChunk;
   const long long c1 = min(n, c0 + kChunk);
   float* o = out + I.elem_start;
-  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[l]);
+  if (!interleaved) {
+    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[l]);
+    return;
+  }
+  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[map_elem(l, I.rows, true).blk]);
 }
 
 // Materialise touched rows before a block is written back / overlaid: one
@@ -517,12 +528,45 @@ cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes,
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_f32(const glod_prefix_item* items, int n_items, long long total, float* out,
-                            cudaStream_t st) {
-  if (n_items <= 0 || total <= 0) return cudaSuccess;
-  const int TB = 256;
+// Stream-ordered small host→device upload from page-locked memory, read by
+// a kernel through the mapped address: the copy engines may be busy with
+// the cache's bulk prefetch DMA, and a main-stream cudaMemcpyAsync would
+// queue behind it.  Pageable sources fall back to cudaMemcpyAsync.
+cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, cudaStream_t st) {
+  if (bytes <= 0) return cudaSuccess;
+  void* src = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&src, const_cast<void*>(host_pinned), 0);
+  if (e != cudaSuccess || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3)) {
+    cudaGetLastError();
+    return cudaMemcpyAsync(dst, host_pinned, size_t(bytes), cudaMemcpyHostToDevice, st);
+  }
+  const long long words = (bytes + 3) >> 2;
+  const int grid = int(words > 256 * 64 ? 64 : (words + 255) / 256);
   count_launch();
-  pack_f32_kernel<<<unsigned((total + TB - 1) / TB), TB, 0, st>>>(items, n_items, total, out);
+  readback_kernel<<<grid, 256, 0, st>>>(static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst),
+                                        bytes);
+  return cudaGetLastError();
+}
+
+namespace {
+struct Bytes64 {
+  unsigned long long w[8];
+};
+__global__ void set_bytes_kernel(unsigned long long* dst, Bytes64 v, int words) {
+  if (int(threadIdx.x) < words) dst[threadIdx.x] = v.w[threadIdx.x];
+}
+}  // namespace
+
+// Stream-ordered write of ≤ 64 host bytes (a multiple of 8; dst 8-aligned)
+// carried in the kernel parameters — for initial values that would
+// otherwise be a pageable cudaMemcpyAsync through the copy engine.
+cudaError_t launch_set_bytes(void* dst, const void* src, int bytes, cudaStream_t st) {
+  if (bytes <= 0 || bytes > 64 || (bytes & 7) || (reinterpret_cast<uintptr_t>(dst) & 7))
+    return cudaErrorInvalidValue;
+  Bytes64 v = {};
+  memcpy(v.w, src, size_t(bytes));
+  count_launch();
+  set_bytes_kernel<<<1, 32, 0, st>>>(static_cast<unsigned long long*>(dst), v, bytes / 8);
   return cudaGetLastError();
 }
 
@@ -549,10 +593,10 @@ cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item
 }
 
 cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
-                               cudaStream_t st) {
+                               int interleaved, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
   count_launch();
-  pack_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(items, bmap, out);
+  pack_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(items, bmap, out, interleaved);
   return cudaGetLastError();
 }
 

@@ -927,7 +927,7 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   for (int k = 0; k < 8; ++k) ib[k] = 0x7fffffff;
   unsigned long long* is = reinterpret_cast<unsigned long long*>(init + 32);
   is[0] = 0; is[1] = ~0ull; is[2] = 0; is[3] = 0;
-  CK(cudaMemcpyAsync(R->bad.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  CK(launch_set_bytes(R->bad.p, init, sizeof(init), st));
   unsigned long long* stats = reinterpret_cast<unsigned long long*>(static_cast<char*>(R->bad.p) + 32);
   const int TB = 256;
   const int nb = int((n + TB - 1) / TB);

@@ -280,14 +280,18 @@ cudaError_t radix_sort_pairs(K* keys, K* keys_alt, int* vals, int* vals_alt, lon
   const size_t scan_bytes = scratch_bytes - (2 * m * 4 + 64);
   if (range_bits) {
     unsigned long long init[2] = {~0ull, 0ull};
-    cudaError_t e = cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    cudaError_t e = launch_set_bytes(mm, init, sizeof(init), st);
     if (e != cudaSuccess) return e;
     count_launch();
     minmax_kernel<K><<<148 * 4, kSortThreads, 0, st>>>(keys, n, reinterpret_cast<K*>(mm));
-    unsigned long long h[2];
-    e = cudaMemcpyAsync(h, mm, sizeof(h), cudaMemcpyDeviceToHost, st);
+    // read back through a kernel into pinned memory (the D2H copy engine may
+    // be busy with the cache's write-back DMA)
+    static thread_local unsigned long long* hp = nullptr;
+    if (!hp && (e = cudaMallocHost(&hp, 16)) != cudaSuccess) return e;
+    e = launch_readback(hp, mm, 16, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return e;
+    const unsigned long long h[2] = {hp[0], hp[1]};
     if (h[0] > h[1]) return cudaSuccess;               // no valid keys
     const unsigned long long diff = (h[0] ^ h[1]) >> begin_bit << begin_bit;
     if (diff == 0) return cudaSuccess;                 // all valid keys equal: order kept

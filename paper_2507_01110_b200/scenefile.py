@@ -266,8 +266,8 @@ class Scene:
     # -- device path -------------------------------------------------------------
     def host_store(self, location: str = "host") -> HostStore:
         """HostStore over this file's slots (the SPT directory gives the
-        per-SPT record offsets/counts): every attribute section read
-        straight into page-locked memory (or HBM for location="device")."""
+        per-SPT record offsets/counts): every attribute section read and
+        interleaved into page-locked rows (or HBM for location="device")."""
         import torch
         if self.sh_cols != 9:
             raise ValueError("the device path keeps degree-1 SH (9 columns)")
@@ -279,14 +279,16 @@ class Scene:
         st.record_count = self.spt_dir["record_count"].astype(np.int64)
         st.total_records = int(st.record_count.sum())
         st.attribute_bytes_read = 0
-        st.sections = []
-        for name, cols in _attr_specs(self.sh_cols):
+        from .store import alloc_rows, fill_section
+        st.rows, st.sections = alloc_rows(st.nslots, location)
+        tmp = np.empty(self.nslots * 9, dtype="<f4")
+        for (name, cols), sec in zip(_attr_specs(self.sh_cols), st.sections):
             off, length = self._section(name)
-            t = torch.empty((self.nslots, cols), dtype=torch.float32, pin_memory=torch.cuda.is_available())
+            buf = tmp[:self.nslots * cols]
             self.f.seek(off)
-            if self.f.readinto(memoryview(t.numpy()).cast("B")) != length:
+            if self.f.readinto(memoryview(buf).cast("B")) != length:
                 raise CorruptFileError(f"truncated section {name!r}")
-            st.sections.append(t.to("cuda") if location == "device" else t)
+            fill_section(sec, buf.reshape(self.nslots, cols))
         return st
 
     def disk_store(self):

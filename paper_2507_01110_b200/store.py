@@ -5,9 +5,12 @@ six little-endian f32 sections in *slot* order — every non-SPT node first
 (ascending id), then each SPT's records in record order — so an SPT cut
 prefix is one contiguous range per section.  Where the reference reads
 prefixes from a file/memory backing, this store keeps the sections in
-page-locked host memory and moves prefixes to HBM with cudaMemcpyAsync
-(6 contiguous ranges per prefix, store.py:304-312); write-back is the
-reverse copy.  Byte counters follow the reference exactly
+page-locked host memory *interleaved* — one 92-B row per slot, the six
+sections as column slices of a [nslots, 23] array — so an SPT prefix
+(store.py:304-312) is ONE contiguous range and moves to HBM as one
+copy-engine transfer (cudaMemcpyAsync); write-back is the reverse copy.
+The .glod file keeps the reference's section-major layout (disk mode reads
+it directly).  Byte counters follow the reference exactly
 (`attribute_bytes_read += prefix_len · 92`, store.py:311).
 """
 from __future__ import annotations
@@ -54,6 +57,32 @@ def slot_order(h, hspt) -> np.ndarray:
     return np.concatenate([head, flat["nodes"]]).astype(np.int64)
 
 
+def alloc_rows(nslots: int, location: str = "host", pin: bool = True, interleaved: bool = True):
+    """One [nslots, 23] f32 array (page-locked host memory, or HBM for
+    location="device") and the six attribute sections as column-slice views
+    of it (interleaved rows: glod_store_view.row_stride = 23).  With
+    interleaved=False: six separate section arrays (the file's layout;
+    row_stride = 0) and rows = None."""
+    def empty(shape):
+        if location == "device":
+            return torch.empty(shape, dtype=torch.float32, device="cuda")
+        return torch.empty(shape, dtype=torch.float32, pin_memory=pin and torch.cuda.is_available())
+    if not interleaved:
+        return None, [empty((nslots, cols)) for _, cols in SECTIONS]
+    rows = empty((nslots, 23))
+    secs, off = [], 0
+    for _, cols in SECTIONS:
+        secs.append(rows[:, off:off + cols])
+        off += cols
+    return rows, secs
+
+
+def fill_section(sec: torch.Tensor, values) -> None:
+    """Write one section (an (nslots, cols) array) into its column slice."""
+    v = torch.from_numpy(np.ascontiguousarray(np.asarray(values, dtype=np.float32)).reshape(sec.shape))
+    sec.copy_(v.to(sec.device) if sec.is_cuda else v)
+
+
 class HostStore:
     """Pinned host store + per-SPT directory, built from (hierarchy, hspt).
 
@@ -63,7 +92,7 @@ class HostStore:
 
     bytes_per_gaussian = BYTES_PER_GAUSSIAN_F32
 
-    def __init__(self, h, hspt, pin: bool = True, location: str = "host"):
+    def __init__(self, h, hspt, pin: bool = True, location: str = "host", interleaved: bool = True):
         if location not in ("host", "device"):
             raise ValueError("location must be 'host' or 'device'")
         self.location = location
@@ -73,15 +102,9 @@ class HostStore:
         self.record_offset = flat["offset"].astype(np.int64)
         self.record_count = flat["count"].astype(np.int64)
         self.total_records = int(self.record_count.sum())
-        pin = pin and torch.cuda.is_available()
-        self.sections = []
-        for name, cols in SECTIONS:
-            arr = np.asarray(getattr(h.attrs, name))[self.slot_to_node].astype(np.float32)
-            t = torch.from_numpy(np.ascontiguousarray(arr.reshape(self.nslots, cols)))
-            if location == "device":
-                self.sections.append(t.to("cuda"))
-            else:
-                self.sections.append(t.pin_memory() if pin else t)
+        self.rows, self.sections = alloc_rows(self.nslots, location, pin, interleaved)
+        for (name, cols), sec in zip(SECTIONS, self.sections):
+            fill_section(sec, np.asarray(getattr(h.attrs, name))[self.slot_to_node])
         self.attribute_bytes_read = 0
 
     @staticmethod
@@ -99,14 +122,12 @@ class HostStore:
         st.record_count = np.asarray(scene.spt_dir["record_count"], dtype=np.int64)
         st.total_records = int(st.record_count.sum())
         st.attribute_bytes_read = 0
-        st.sections = []
+        st.rows, st.sections = alloc_rows(st.nslots, location)
         buf = getattr(scene.backing, "buf", None)
-        for name, cols in SECTIONS:
+        for (name, cols), sec in zip(SECTIONS, st.sections):
             off, length = scene.sections[name]
             raw = bytes(buf[off:off + length]) if buf is not None else scene.backing.read(off, length)
-            t = torch.from_numpy(np.frombuffer(raw, dtype="<f4").reshape(st.nslots, cols).copy())
-            st.sections.append(t.to("cuda") if location == "device" else
-                               (t.pin_memory() if torch.cuda.is_available() else t))
+            fill_section(sec, np.frombuffer(raw, dtype="<f4").reshape(st.nslots, cols))
         return st
 
     def to_scene(self, scene) -> None:
@@ -178,18 +199,32 @@ class HostStore:
             off += cols * P
 
     def device_view(self):
-        """glod_store_view of the pinned sections (device-mapped addresses)."""
+        """glod_store_view of the store (device-mapped addresses of the pinned
+        rows; row_stride 23 for the interleaved layout)."""
         if getattr(self, "_view", None) is None:
             import ctypes as C
             from . import _lib
             v = _lib.StoreView()
-            for k, sec in enumerate(self.sections):
-                if sec.is_cuda:
-                    v.section[k] = sec.data_ptr()
-                    continue
-                dp = C.c_void_p()
-                _lib.check(_lib.lib().glod_host_device_ptr(C.c_void_p(sec.data_ptr()), C.byref(dp)))
-                v.section[k] = dp.value
+            rows = getattr(self, "rows", None)
+            if rows is not None:            # interleaved: sections at column offsets of one row
+                base = rows.data_ptr()
+                if not rows.is_cuda:
+                    dp = C.c_void_p()
+                    _lib.check(_lib.lib().glod_host_device_ptr(C.c_void_p(base), C.byref(dp)))
+                    base = dp.value
+                off = 0
+                for k, (_, cols) in enumerate(SECTIONS):
+                    v.section[k] = base + 4 * off
+                    off += cols
+                v.row_stride = 23
+            else:
+                for k, sec in enumerate(self.sections):
+                    if sec.is_cuda:
+                        v.section[k] = sec.data_ptr()
+                        continue
+                    dp = C.c_void_p()
+                    _lib.check(_lib.lib().glod_host_device_ptr(C.c_void_p(sec.data_ptr()), C.byref(dp)))
+                    v.section[k] = dp.value
             v.nslots = self.nslots
             self._view = v
         return self._view

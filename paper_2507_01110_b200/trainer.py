@@ -216,6 +216,8 @@ class Trainer:
         self.last_stats = {}
         self._pf_rows_cap = cfg.cache.budget_bytes // BYTES_PER_GAUSSIAN_F32
         self.timing = None          # {stage: [ms, ...]} when profiling is on
+        self.host_timing = None     # {stage: [host ms, ...]} (enable_host_timing)
+        self._host_last = None
         self._ev = []
 
     def _register_master(self):
@@ -342,6 +344,12 @@ class Trainer:
         e = torch.cuda.Event(enable_timing=True)
         e.record()
         self._ev.append((name, e))
+        if self.host_timing is not None:
+            import time
+            t = time.perf_counter()
+            if self._host_last is not None and name != "start":
+                self.host_timing.setdefault(name, []).append((t - self._host_last) * 1e3)
+            self._host_last = t
 
     def _collect(self):
         if self.timing is None or not self._ev:
@@ -427,15 +435,17 @@ class Trainer:
         loaded, hits = self.cache.step(spt_ids, d_root, prefix, hd, hb[:S1], hb[S1:])
         if view is not None:
             self._hist[view] = (spt_ids.copy(), d_root.copy(), prefix.copy())
-        # the next view's predicted selection; its misses are prefetched
-        # once this step's kernels are queued (train_step)
+        # the next view's predicted selection: its misses are prefetched by
+        # the copy engines once this step's backward is queued (train_step)
+        # or its frame is rendered (render_view)
         self._pred = self._hist.get(nv, self._spec) if nv is not None else None
         if n_sp:
             # the prefix at the cached distance is the entry's prefix_len
             self._h_pref.numpy()[:n_sp] = hb[S1:S1 + n_sp]
-            self._d_dist.copy_(self._h_dist, non_blocking=True)
-            self._d_blk.copy_(self._h_blk, non_blocking=True)
-            self._d_pref.copy_(self._h_pref, non_blocking=True)
+            # kernel uploads: the H2D copy engine is busy with the prefetch
+            _lib.upload(self._d_dist, self._h_dist)
+            _lib.upload(self._d_blk, self._h_blk)
+            _lib.upload(self._d_pref, self._h_pref)
         self._mark("cache")
         cmp = sc.lod.compact(sel.counts[2:3], sel.spt_ids, self._d_dist, known_prefix=self._d_pref)
         _lib.readback(self._h_total[:1], cmp.total[:1])
@@ -530,6 +540,10 @@ class Trainer:
         # first write to the parameters
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
         self._mark("backward")
+        if self._pred is not None:
+            # the copy engines fetch the next view's misses during the
+            # backward and ADAM; issued here, where the host would only wait
+            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
         self._loss_ev.synchronize()
         loss_value = float(self._h_loss[0])
         if not np.isfinite(loss_value):
@@ -553,10 +567,6 @@ class Trainer:
                                                 C.byref(plan), st))
             self._mark("adam")
         self.cache.end_step(iteration, mark_dirty=True)
-        if self._pred is not None:
-            # the copy engines fetch the next view's misses while this
-            # step's backward and ADAM run
-            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
         self._mark("scatter_flush")
         self._collect()
         self.iteration = iteration

@@ -118,16 +118,18 @@ def _write_block_async(address: int, values: np.ndarray):
     assert int(err) == 0
 
 
+@pytest.mark.parametrize("interleaved", [True, False])
 @pytest.mark.parametrize("seed,budget_frac", [(3, 0.15), (4, 0.4)])
-def test_native_cache_block_contents(seed, budget_frac):
+def test_native_cache_block_contents(seed, budget_frac, interleaved):
     """Block and store *contents* through evictions, write-backs, reloads of
     blocks evicted earlier in the same step (overlay path) and flushes,
     against a numpy mirror of the reference's load → insert → write_back
     order (trainer.py:329-345, store.py:314-333).  Blocks rendered in a step
     are modified between steps (the ADAM refresh) so every write-back
-    carries new values."""
+    carries new values.  Both store layouts: interleaved rows (one copy per
+    prefix) and section-major (six per prefix)."""
     h, hs, _ = designed_scene(SceneSpec(n_leaves=4000, spt_leaves=128, seed=seed, relabel=False))
-    st = HostStore(h, hs)
+    st = HostStore(h, hs, interleaved=interleaved)
     S = len(hs.spts)
     counts = hs.flat_records()["count"]
     cfg = CacheConfig(budget_bytes=max(int(budget_frac * counts.sum() * 92 / 3), int(counts.max()) * 92),
@@ -194,3 +196,51 @@ def test_native_cache_block_contents(seed, budget_frac):
         torch.cuda.synchronize()
         for k_, sec in enumerate(st.sections):
             np.testing.assert_array_equal(sec.numpy(), store[k_], err_msg=f"store after step {it}")
+
+
+@pytest.mark.parametrize("interleaved", [True, False])
+def test_store_transfer_capi(interleaved):
+    """glod_store_load_prefixes / glod_store_write_back (the zero-copy
+    public transfers, store.py:314-333) on both store layouts: loaded blocks
+    hold f64(store rows) section-major; written-back blocks land as f32 in
+    the right slots and nothing else changes."""
+    import ctypes as C
+    from paper_2507_01110_b200 import _lib
+    h, hs, _ = designed_scene(SceneSpec(n_leaves=3000, spt_leaves=128, seed=7, relabel=False))
+    st = HostStore(h, hs, interleaved=interleaved)
+    counts = hs.flat_records()["count"]
+    rng = np.random.default_rng(0)
+    sids = rng.choice(len(counts), 6, replace=False)
+    P = [int(max(1, counts[s] * f)) for s, f in zip(sids, rng.uniform(0.2, 1.0, 6))]
+    blocks = [torch.zeros(23 * p + (p + 63) // 64, dtype=torch.float64, device="cuda") for p in P]
+    items = (_lib.PrefixItem * 6)()
+    acc = 0
+    for j, (s, p) in enumerate(zip(sids, P)):
+        items[j].slot_start = st.spt_slot_start(int(s))
+        items[j].rows = p
+        items[j].elem_start = acc
+        items[j].block = blocks[j].data_ptr()
+        acc += 23 * p
+    ditems = torch.frombuffer(bytearray(bytes(items)), dtype=torch.uint8).cuda()
+    view = st.device_view()
+    L = _lib.lib()
+    _lib.check(L.glod_store_load_prefixes(C.byref(view), _lib.ptr(ditems), 6, acc, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    host = [s.numpy().copy() for s in st.sections]
+    for j, (s, p) in enumerate(zip(sids, P)):
+        sl = st.spt_slot_start(int(s))
+        want = np.concatenate([sec[sl:sl + p].reshape(-1).astype(np.float64) for sec in host])
+        np.testing.assert_array_equal(blocks[j][:23 * p].cpu().numpy(), want)
+    for j, p in enumerate(P):
+        blocks[j][:23 * p] = torch.from_numpy(rng.normal(size=23 * p)).cuda()
+    _lib.check(L.glod_store_write_back(C.byref(view), _lib.ptr(ditems), 6, acc, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    for j, (s, p) in enumerate(zip(sids, P)):
+        sl = st.spt_slot_start(int(s))
+        b = blocks[j][:23 * p].cpu().numpy().astype(np.float32)
+        off = 0
+        for k, (_, c) in enumerate(SECTIONS):
+            host[k][sl:sl + p] = b[off:off + c * p].reshape(host[k][sl:sl + p].shape)
+            off += c * p
+    for k, sec in enumerate(st.sections):
+        np.testing.assert_array_equal(sec.numpy(), host[k])

@@ -58,11 +58,30 @@ def main():
     print("streams busy us:", {str(s): round(v, 1) for s, v in busy.items()})
     t0, t1 = mk[0]["ts"], mk[-1]["ts"] + mk[-1]["dur"]
     print(f"main stream span {t1 - t0:.0f} us over {a.steps} steps, busy {busy[main_sid]:.0f} us")
+    def short(n):
+        n = n.replace("(anonymous namespace)::", "").replace("glod::", "").replace("void ", "")
+        return n.split("(")[0][-48:]
     gaps = []
+    others = [k for sid, v in streams.items() if sid != main_sid for k in v]
     for p, q in zip(mk[:-1], mk[1:]):
         g = q["ts"] - (p["ts"] + p["dur"])
         if g > 5:
-            gaps.append((g, p["name"][:50], q["name"][:50]))
+            gaps.append((g, short(p["name"]), short(q["name"])))
+        if g > 150:
+            # what ran on the other streams during the gap
+            t_a, t_b = p["ts"] + p["dur"], q["ts"]
+            ov = [k for k in others if k["ts"] < t_b and k["ts"] + k["dur"] > t_a]
+            by = {}
+            for k in ov:
+                key = (k["args"].get("stream"), k["name"][:24])
+                b = by.setdefault(key, [0, 0.0, 0])
+                b[0] += 1
+                b[1] += min(k["ts"] + k["dur"], t_b) - max(k["ts"], t_a)
+                b[2] += k["args"].get("bytes", 0) or 0
+            last_end = max([k["ts"] + k["dur"] for k in ov if k["ts"] + k["dur"] <= t_b + 2] or [0])
+            print(f"gap {g:.0f} us before {short(q['name'])}: other streams "
+                  + "; ".join(f"s{s_} {n} x{c} {t:.0f}us {b / 1e6:.1f}MB" for (s_, n), (c, t, b) in by.items())
+                  + f"; last other op ended {t_b - last_end:.0f} us before the gap end")
     agg = {}
     for g, p, q in gaps:
         key = (p.split("(")[0][-40:], q.split("(")[0][-40:])
@@ -72,6 +91,26 @@ def main():
     print(f"idle gaps >5us on main stream: total {sum(g for g, _, _ in gaps):.0f} us")
     for (p, q), (n, tot) in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
         print(f"  {tot / a.steps:8.1f} us/step  x{n:3d}  after {p}  ->  before {q}")
+    # per-stream activity relative to each step's first main-stream kernel
+    firsts = []
+    for st_ev in steps:
+        ks = [k for k in mk if st_ev["ts"] <= k["ts"] <= st_ev["ts"] + st_ev["dur"] + 20000]
+        if ks:
+            firsts.append(ks[0]["ts"])
+    for s_id, v in streams.items():
+        v = sorted(v, key=lambda k: k["ts"])
+        cats = {}
+        for k in v:
+            cats[k.get("cat")] = cats.get(k.get("cat"), 0) + 1
+        print(f"stream {s_id}: {len(v)} ops {cats}")
+        if s_id == main_sid:
+            continue
+        for f in firsts:
+            w = [k for k in v if f - 8000 <= k["ts"] < f + 8000]
+            if w:
+                print(f"   rel. step start {f:.0f}: first {w[0]['ts'] - f:+.0f} us, last end "
+                      f"{max(k['ts'] + k['dur'] for k in w) - f:+.0f} us, busy {sum(k['dur'] for k in w):.0f} us, "
+                      f"n={len(w)}")
     kagg = {}
     for k in mk:
         n = k["name"].split("(")[0][-45:]
