@@ -380,29 +380,49 @@ __global__ void ranges_kernel(const unsigned* __restrict__ ikey, long long n, in
 
 // Per-pixel alpha with an explicit rounding sequence so the forward and the
 // backward kernels produce bit-identical values (no contraction variance).
-GLOD_DEV bool pixel_alpha(const Splat& g, int px, int py, float& dx, float& dy, float& q,
-                          float& gauss, float& alpha) {
-  if (px < g.x0 || px >= g.x1 || py < g.y0 || py >= g.y1) return false;
-  dx = __fsub_rn(float(px - g.x0), g.mx);
-  dy = __fsub_rn(float(py - g.y0), g.my);
-  // q = a dx² + c dy² + 2 b dy dx   (renderer.py:151-152), explicit FMAs
-  // (the forward and backward kernels evaluate the identical sequence)
-  q = __fmaf_rn(__fmul_rn(g.ca, dx), dx,
-                __fmaf_rn(__fmul_rn(g.cc, dy), dy, __fmul_rn(__fmul_rn(__fmul_rn(2.0f, g.cb), dx), dy)));
+// The x-dependent factors of q are per (splat, column) — `SplatRow` holds
+// them so a lane's two pixels of one column share them.
+//   q = a dx² + c dy² + 2 b dy dx   (renderer.py:151-152)
+//     = fma(a·dx, dx, fma(c·dy, dy, ((2b)·dx)·dy))
+struct SplatCol {
+  float dx, adx, bdx;   // dx, a·dx, (2b)·dx
+};
+GLOD_DEV SplatCol splat_col(const Splat& g, int xi) {
+  SplatCol c;
+  c.dx = __fsub_rn(float(xi), g.mx);
+  c.adx = __fmul_rn(g.ca, c.dx);
+  c.bdx = __fmul_rn(__fmul_rn(2.0f, g.cb), c.dx);
+  return c;
+}
+// α of the pixel at bbox-relative row yi (the caller tested the bbox).
+// `a` is the unclamped opac·G (its < 0.99 test selects the live branch).
+GLOD_DEV bool col_alpha(const Splat& g, const SplatCol& c, int yi, float& dy, float& gauss, float& a,
+                        float& alpha) {
+  dy = __fsub_rn(float(yi), g.my);
+  const float q = __fmaf_rn(c.adx, c.dx, __fmaf_rn(__fmul_rn(g.cc, dy), dy, __fmul_rn(c.bdx, dy)));
   if (!(q <= kQMax)) return false;
   // exp(-q/2) = 2^(q · (-log2(e)/2)): one multiply + MUFU.EX2
   // (q ≤ 32: the argument is ≥ -23.1, far from the denormal range)
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gauss) : "f"(__fmul_rn(q, -0.72134752044448170368f)));
-  const float a = __fmul_rn(g.opac, gauss);
+  a = __fmul_rn(g.opac, gauss);
   alpha = fminf(a, kAlphaMax);
   return alpha > 0.0f;
 }
 
 // Front-to-back compositing of one pixel with one splat (renderer.py:149-164).
+// The α part is branch-free (every lane evaluates it; the warp runs the
+// union of its lanes' paths anyway), the fp64 blend only where α > 0.
 GLOD_DEV void fwd_pixel(const Splat& g, int px, int py, int inst, double& T, float& cr, float& cg, float& cb,
                         int& last, bool& done) {
-  float dx, dy, q, gs, al;
-  if (done || !pixel_alpha(g, px, py, dx, dy, q, gs, al)) return;
+  const int xi = px - g.x0, yi = py - g.y0;
+  const bool act = !done && unsigned(xi) < unsigned(g.x1 - g.x0) && unsigned(yi) < unsigned(g.y1 - g.y0);
+  const SplatCol c = splat_col(g, xi);
+  const float dy = __fsub_rn(float(yi), g.my);
+  const float q = __fmaf_rn(c.adx, c.dx, __fmaf_rn(__fmul_rn(g.cc, dy), dy, __fmul_rn(c.bdx, dy)));
+  float gs;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gs) : "f"(__fmul_rn(q, -0.72134752044448170368f)));
+  const float al = fminf(__fmul_rn(g.opac, gs), kAlphaMax);
+  if (!(act && q <= kQMax && al > 0.0f)) return;
   const double w = double(al) * T;
   cr += float(w) * g.r;
   cg += float(w) * g.g;
@@ -534,13 +554,25 @@ struct BwdPix {
   bool inside;
 };
 
-GLOD_DEV bool bwd_pixel(const Splat& g, int px, int py, int inst, BwdPix& s, float (&cv)[9]) {
-  float dx, dy, q, gs, al;
-  // outside pixels keep last = -1, so `inst <= s.last` also gates them
-  if (!(inst <= s.last && pixel_alpha(g, px, py, dx, dy, q, gs, al))) return false;
+// One pixel of a lane's column, branch-free: `active` carries the bbox and
+// last-contributor tests; a pixel that does not composite this splat (not
+// active, q > 32 or α = 0) runs the same instructions with α = 0, which
+// leaves its state unchanged and adds exact zeros (no divergent paths and
+// no re-zeroed accumulators per exit).  The dl/dq terms use the shared
+// column factors (2a·dx, 2b·dx).
+GLOD_DEV bool bwd_pixel(const Splat& g, const SplatCol& c, int yi, bool active, BwdPix& s, float (&cv)[9],
+                        float a2dx, float b2dx, float nhop) {
+  const float dy = __fsub_rn(float(yi), g.my);
+  const float q = __fmaf_rn(c.adx, c.dx, __fmaf_rn(__fmul_rn(g.cc, dy), dy, __fmul_rn(c.bdx, dy)));
+  float gs;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(gs) : "f"(__fmul_rn(q, -0.72134752044448170368f)));
+  const float a = __fmul_rn(g.opac, gs);
+  const float alr = fminf(a, kAlphaMax);
+  const bool ok = active && q <= kQMax && alr > 0.0f;
+  const float al = ok ? alr : 0.0f;
   float inv;                                           // 1/(1-α), 1-α ≥ 0.01: approx rcp
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(1.f - al));
-  const float Tf = s.T * inv;                          // T before this splat
+  const float Tf = ok ? s.T * inv : s.T;               // T before this splat
   const float w = al * Tf;
   cv[0] += w * s.gr; cv[1] += w * s.gg; cv[2] += w * s.gb;   // dl_dcolor
   const float gc = s.gr * g.r + s.gg * g.g + s.gb * g.b;
@@ -548,16 +580,16 @@ GLOD_DEV bool bwd_pixel(const Splat& g, int px, int py, int inst, BwdPix& s, flo
   const float dla = gc * Tf - grear * inv;
   s.rr += w * g.r; s.rg += w * g.g; s.rb += w * g.b;
   s.T = Tf;
-  if (__fmul_rn(g.opac, gs) < kAlphaMax) {             // live: unclamped
-    cv[3] += gs * dla;
-    const float dq = -0.5f * g.opac * gs * dla;
-    cv[4] += -dq * (2.f * g.ca * dx + 2.f * g.cb * dy);
-    cv[5] += -dq * (2.f * g.cb * dx + 2.f * g.cc * dy);
-    cv[6] += dq * dx * dx;
-    cv[7] += dq * dx * dy;
-    cv[8] += dq * dy * dy;
-  }
-  return true;
+  const float gd = (ok && a < kAlphaMax) ? gs * dla : 0.0f;   // live: unclamped
+  cv[3] += gd;
+  const float dq = nhop * gd;                          // -0.5·opac·G·dl/dα
+  cv[4] += -dq * (a2dx + 2.f * g.cb * dy);
+  cv[5] += -dq * (b2dx + 2.f * g.cc * dy);
+  const float dqdx = dq * c.dx;
+  cv[6] += dqdx * c.dx;
+  cv[7] += dqdx * dy;
+  cv[8] += dq * dy * dy;
+  return ok;
 }
 
 GLOD_DEV BwdPix bwd_init(const CamD& cam, int px, int py, const float* __restrict__ dimg,
@@ -617,8 +649,16 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
       float cv[9];
 #pragma unroll
       for (int u = 0; u < 9; ++u) cv[u] = 0.f;
-      const bool h0 = bwd_pixel(g, px, py0, inst, s0, cv);
-      const bool h1 = bwd_pixel(g, px, py1, inst, s1, cv);
+      // bbox tests once per lane (both pixels share the column)
+      const int xi = px - g.x0, yi0 = py0 - g.y0;
+      const unsigned bh = unsigned(g.y1 - g.y0);
+      const bool inx = unsigned(xi) < unsigned(g.x1 - g.x0);
+      const bool p0 = inx && unsigned(yi0) < bh && inst <= s0.last;
+      const bool p1 = inx && unsigned(yi0 + 4) < bh && inst <= s1.last;
+      const SplatCol c = splat_col(g, xi);
+      const float a2dx = 2.f * g.ca * c.dx, b2dx = 2.f * g.cb * c.dx, nhop = -0.5f * g.opac;
+      const bool h0 = bwd_pixel(g, c, yi0, p0, s0, cv, a2dx, b2dx, nhop);
+      const bool h1 = bwd_pixel(g, c, yi0 + 4, p1, s1, cv, a2dx, b2dx, nhop);
       const bool hit = h0 || h1;
       const unsigned bal = __ballot_sync(0xffffffffu, hit);
       if (bal == 0) continue;

@@ -244,6 +244,7 @@ class Trainer:
         self._next_view = None
         self._pred = None
         self._spec = None
+        self._sel_ev = self._spec_ev = None
         self._h_sel2 = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()
         self._h_droot2 = torch.empty(S1, dtype=torch.float64).pin_memory()
         self._spt_of_node = None
@@ -385,8 +386,9 @@ class Trainer:
     def select(self, cam: Camera, spec_cam: Camera | None = None):
         """LoD select + one D2H of the per-SPT table (the step's host sync).
         With `spec_cam`, a speculative select of that (predicted next) view
-        runs into the alternate outputs and is read back under the same
-        sync; its per-SPT table lands in self._spec."""
+        is enqueued after the read-back the host waits for, so it runs on
+        the GPU while the host makes this step's cache decisions; its
+        per-SPT table is read later (`_spec_table`, before the prefetch)."""
         sc = self.scene
         sel = sc.lod.select(cam, self.cfg.lod, cull=True)
         S1 = max(sc.lod.S, 1)
@@ -399,19 +401,41 @@ class Trainer:
             rb(hd, sel.d_root[:S1])
 
         read(sel, self._h_sel, self._h_droot)
+        if self._sel_ev is None:
+            self._sel_ev, self._spec_ev = torch.cuda.Event(), torch.cuda.Event()
+        self._sel_ev.record()
+        self._spec = None
         if spec_cam is not None:
             read(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True), self._h_sel2, self._h_droot2)
-        torch.cuda.current_stream().synchronize()
+            self._spec_ev.record()
+            self._spec = "pending"
+        self._sel_ev.synchronize()
         h = self._h_sel
         n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
-        self._spec = None
-        if spec_cam is not None:
+        return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
+
+    def _spec_table(self):
+        """The speculative select's per-SPT table (spt ids, d_root,
+        prefix), read back behind this step's select (select())."""
+        if isinstance(self._spec, str):
+            self._spec_ev.synchronize()
+            S1 = max(self.scene.lod.S, 1)
             h2 = self._h_sel2
             k = int(h2[2])
-            self._spec = (sc.lod.spt_perm[h2[4:4 + k].numpy().astype(np.int64)],
+            self._spec = (self.scene.lod.spt_perm[h2[4:4 + k].numpy().astype(np.int64)],
                           self._h_droot2[:k].numpy().copy(), h2[4 + S1:4 + S1 + k].numpy().copy())
-        return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
+        return self._spec
+
+    def _prefetch_next(self):
+        """Copy-engine prefetch of the predicted next view's misses."""
+        pred = self._pred
+        if pred is None:
+            return
+        if isinstance(pred, str):
+            pred = self._spec_table()
+        if pred is not None:
+            self.cache.prefetch(*pred, max_rows=self._pf_rows_cap)
 
     def _predict_next(self, iteration: int):
         """The scheduler's draw for iteration+1, from a copy of the RNG
@@ -438,7 +462,7 @@ class Trainer:
         # the next view's predicted selection: its misses are prefetched by
         # the copy engines once this step's backward is queued (train_step)
         # or its frame is rendered (render_view)
-        self._pred = self._hist.get(nv, self._spec) if nv is not None else None
+        self._pred = self._hist.get(nv, self._spec) if nv is not None else None   # "pending": spec
         if n_sp:
             # the prefix at the cached distance is the entry's prefix_len
             self._h_pref.numpy()[:n_sp] = hb[S1:S1 + n_sp]
@@ -484,8 +508,7 @@ class Trainer:
         R, rows, _, _, _, counters = self._gather_view(cam, view)
         img = self.rast.forward(rows, R, cam, image=image)
         self.cache.end_step(-1, mark_dirty=False)
-        if self._pred is not None:
-            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
+        self._prefetch_next()
         self._mark("forward")
         self._collect()
         self.last_render = counters
@@ -540,10 +563,9 @@ class Trainer:
         # first write to the parameters
         grads = self.rast.backward(dimg, self._ensure("_grads", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64))
         self._mark("backward")
-        if self._pred is not None:
-            # the copy engines fetch the next view's misses during the
-            # backward and ADAM; issued here, where the host would only wait
-            self.cache.prefetch(*self._pred, max_rows=self._pf_rows_cap)
+        # the copy engines fetch the next view's misses during the backward
+        # and ADAM; issued here, where the host would only wait
+        self._prefetch_next()
         self._loss_ev.synchronize()
         loss_value = float(self._h_loss[0])
         if not np.isfinite(loss_value):
