@@ -189,7 +189,6 @@ GLOD_DEV int find_item(const glod_prefix_item* items, int lo, int hi, long long 
 // column); interleaved stores (row_stride 23: one 92-B row per slot) take
 // l in row order, so the store side of every transfer is one contiguous
 // run and the block side (always section-major) is computed.
-__constant__ unsigned char kColSecG[23] = {0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 4, 4, 4, 5, 5, 5, 5, 5, 5, 5, 5, 5};
 
 struct ElemMap {
   long long row;      // prefix row
@@ -203,7 +202,7 @@ GLOD_DEV ElemMap map_elem(long long l, long long rows, bool interleaved) {
   if (interleaved) {
     m.row = l < 0xffffffffLL ? (long long)(unsigned(l) / 23u) : l / 23;
     const int col = int(l - m.row * 23);
-    m.sec = kColSecG[col];
+    m.sec = (col >= 3) + (col >= 6) + (col >= 10) + (col >= 11) + (col >= 14);
     m.within = m.row * kSecCols[m.sec] + (col - kSecOff[m.sec]);
     m.blk = kSecOff[m.sec] * rows + m.within;
   } else {
@@ -306,37 +305,73 @@ __global__ void refresh_resident_kernel(const double* __restrict__ master, long 
   }
 }
 
-// Cache-path transfers driven by a block map: block b moves elements
-// [chunk·kChunk, (chunk+1)·kChunk) of item bmap[b].x (chunk = bmap[b].y),
-// so no thread searches the item table and every block streams one
-// contiguous span of one prefix.
-constexpr int kChunk = 2048;
+// Cache-path transfers driven by a block map: block b moves rows
+// [chunk·kChunkRows, (chunk+1)·kChunkRows) of item bmap[b].x (chunk =
+// bmap[b].y), so no thread searches the item table.  Each CTA transposes its
+// rows through a shared f32 tile ([row][23], row order): the store side
+// (rows of an interleaved store / prefetch copy, or six section runs of a
+// section-major one) and the block side (six section runs) are both read
+// and written as contiguous runs.
+constexpr int kChunkRows = 88;
+constexpr int kTileLd = 23;
+
+// Section runs of rows [r0, r0 + nr) of a section-major array of `rows`
+// rows: calls f(tile index, array index) for every value, consecutive
+// threads on consecutive array indices.
+template <typename F>
+GLOD_DEV void for_section_runs(long long rows, long long r0, int nr, F f) {
+#pragma unroll
+  for (int sec = 0; sec < 6; ++sec) {
+    constexpr int offs[7] = {0, 3, 6, 10, 11, 14, 23};
+    const int off = offs[sec], cols = offs[sec + 1] - offs[sec];
+    const long long base = off * rows + r0 * cols;
+    for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
+      const int r = i / cols;
+      f(r * kTileLd + off + (i - r * cols), base + i);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(256)
 load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items,
                    const int2* __restrict__ bmap) {
+  __shared__ float tile[kChunkRows * kTileLd];
   const int2 bm = bmap[blockIdx.x];
   const glod_prefix_item I = items[bm.x];
-  const long long n = 23LL * I.rows;
-  const long long c0 = (long long)bm.y * kChunk;
-  const long long c1 = min(n, c0 + kChunk);
+  const long long r0 = (long long)bm.y * kChunkRows;
+  const int nr = int(min((long long)kChunkRows, I.rows - r0));
   const bool il = sv.row_stride != 0;
   if (bm.y == 0)                                 // a freshly loaded block: no row touched
     for (long long w = threadIdx.x; w < (I.rows + 63) / 64; w += blockDim.x) block_bits(I.block, I.rows)[w] = 0;
-  if (I.src && !il && I.overlay_rows == 0) {     // section-major f32 copy in HBM (disk read)
-    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) I.block[l] = double(I.src[l]);
-    return;
+  // 1. the prefix rows in f32, from the prefetch / disk copy in HBM or the
+  //    mapped store, laid out like the store
+  if (il) {
+    const float* src = I.src ? I.src + r0 * 23 : sv.section[0] + (I.slot_start + r0) * 23;
+    for (int i = threadIdx.x; i < nr * 23; i += blockDim.x) tile[i] = src[i];
+  } else if (I.src) {
+    for_section_runs(I.rows, r0, nr, [&](int t, long long k) { tile[t] = I.src[k]; });
+  } else {
+#pragma unroll
+    for (int sec = 0; sec < 6; ++sec) {
+      constexpr int offs[7] = {0, 3, 6, 10, 11, 14, 23};
+      const int off = offs[sec], cols = offs[sec + 1] - offs[sec];
+      const float* src = section_of(sv, sec) + (I.slot_start + r0) * cols;
+      for (int i = threadIdx.x; i < nr * cols; i += blockDim.x) {
+        const int r = i / cols;
+        tile[r * kTileLd + off + (i - r * cols)] = src[i];
+      }
+    }
   }
-  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) {
-    const ElemMap m = map_elem(l, I.rows, il);
-    // overlay: rows below overlay_rows are the f32 rounding of a block whose
-    // write-back to these store rows is still in flight (cache_table.cu);
-    // src: the prefix's f32 copy in HBM (prefetch / disk read), laid out
-    // like the store
-    I.block[m.blk] = m.row < I.overlay_rows
-                         ? double(float(I.overlay[kSecOff[m.sec] * I.overlay_rows + m.within]))
-                         : double(I.src ? I.src[l] : *store_at(sv, I.slot_start, l, m));
+  // 2. overlay: rows below overlay_rows are the f32 rounding of a block whose
+  //    write-back to these store rows is still in flight (cache_table.cu)
+  const int nov = int(max(0LL, min((long long)nr, I.overlay_rows - r0)));
+  if (nov > 0) {
+    __syncthreads();
+    for_section_runs(I.overlay_rows, r0, nov, [&](int t, long long k) { tile[t] = float(I.overlay[k]); });
   }
+  __syncthreads();
+  // 3. the f64 block, section-major
+  for_section_runs(I.rows, r0, nr, [&](int t, long long k) { I.block[k] = double(tile[t]); });
 }
 
 // Write-back staging: the block as f32 in the store's layout (row order for
@@ -344,17 +379,20 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
 __global__ void __launch_bounds__(256)
 pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __restrict__ bmap,
                    float* __restrict__ out, int interleaved) {
+  __shared__ float tile[kChunkRows * kTileLd];
   const int2 bm = bmap[blockIdx.x];
   const glod_prefix_item I = items[bm.x];
-  const long long n = 23LL * I.rows;
-  const long long c0 = (long long)bm.y * kChunk;
-  const long long c1 = min(n, c0 + kChunk);
+  const long long r0 = (long long)bm.y * kChunkRows;
+  const int nr = int(min((long long)kChunkRows, I.rows - r0));
   float* o = out + I.elem_start;
-  if (!interleaved) {
-    for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[l]);
+  if (!interleaved) {                  // same layout as the block: a straight convert
+    for_section_runs(I.rows, r0, nr, [&](int, long long k) { o[k] = float(I.block[k]); });
     return;
   }
-  for (long long l = c0 + threadIdx.x; l < c1; l += blockDim.x) o[l] = float(I.block[map_elem(l, I.rows, true).blk]);
+  for_section_runs(I.rows, r0, nr, [&](int t, long long k) { tile[t] = float(I.block[k]); });
+  __syncthreads();
+  float* dst = o + r0 * 23;
+  for (int i = threadIdx.x; i < nr * 23; i += blockDim.x) dst[i] = tile[i];
 }
 
 // Materialise touched rows before a block is written back / overlaid: one
@@ -582,7 +620,7 @@ cudaError_t launch_refresh_resident(const double* master, long long cap, long lo
   return cudaGetLastError();
 }
 
-long long transfer_chunks(long long rows) { return (23 * rows + kChunk - 1) / kChunk; }
+long long transfer_chunks(long long rows) { return (rows + kChunkRows - 1) / kChunkRows; }
 
 cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
                                long long nblocks, cudaStream_t st) {
