@@ -523,6 +523,10 @@ int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* strea
  * prefetch DMA).  host_pinned must stay unchanged until the stream has run
  * the upload; pageable memory falls back to cudaMemcpyAsync. */
 int glod_upload(void* dst, const void* host_pinned, int64_t bytes, void* stream);
+/* Diagnostics: %globaltimer stamps (ns) of the last select launch's block 0
+ * at its phase boundaries (start, flags, upper walks, passthrough walks,
+ * bitmap counts, id lists, d_root/prefix); synchronises the device. */
+int glod_debug_select_phases(int64_t* ns_out7);
 /* Synchronous device→host copy (snapshots / tests). */
 int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes);
 

@@ -165,6 +165,7 @@ SIGNATURES = {
     "glod_xchg_stats": (C.c_int, [P, P]),
     "glod_readback": (C.c_int, [P, P, C.c_int64, P]),
     "glod_upload": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_debug_select_phases": (C.c_int, [P]),
     "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
     "glod_sort_pairs_u64": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_int64,
                                       C.POINTER(C.c_int32), P]),

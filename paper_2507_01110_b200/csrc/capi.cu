@@ -36,6 +36,7 @@ cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, c
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
 cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, cudaStream_t st);
+cudaError_t select_phase_ns(long long* out7);
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 }  // namespace glod
 
@@ -253,6 +254,14 @@ int glod_convert(const void* in, void* out, int64_t n, int32_t to_f64, void* str
   if (n > 0 && (!in || !out)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_convert(in, out, n, to_f64, static_cast<cudaStream_t>(stream)),
                "glod_convert");
+}
+
+int glod_debug_select_phases(int64_t* ns_out7) {
+  if (!ns_out7) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  long long t[7];
+  const int rc = check(glod::select_phase_ns(t), "glod_debug_select_phases");
+  for (int k = 0; k < 7; ++k) ns_out7[k] = t[k];
+  return rc;
 }
 
 int glod_upload(void* dst, const void* host_pinned, int64_t bytes, void* stream) {

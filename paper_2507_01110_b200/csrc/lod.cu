@@ -76,22 +76,25 @@ GLOD_DEV bool sphere_in_frustum(const double* P, double x, double y, double z,
   return true;
 }
 
+// #{kp[i] > d} over a descending run (np.searchsorted(-key_parent, -d,
+// 'left')) by one warp: 32-ary ballot search, ⌈log32 n⌉ dependent loads
+// instead of log2 n.  Every lane returns the count.
 template <typename K>
-GLOD_DEV int prefix_search(const K* kp, int n, double d) {
-  // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (double(kp[mid]) > d) lo = mid + 1; else hi = mid;
+GLOD_DEV int warp_count_gt(const K* kp, long long n, double d, int lane) {
+  long long a = 0, b = n;
+  while (b - a > 32) {
+    const long long step = (b - a + 31) / 32;
+    const long long probe = a + step * lane;
+    const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
+    const unsigned m = __ballot_sync(0xffffffffu, gt);
+    const int last = 31 - __clz(m);
+    const long long na = a + step * last;
+    b = min(b, na + step);
+    a = na;
   }
-  return lo;
-}
-
-GLOD_DEV int prefix_len_of(const LodScene& sc, int s, double d) {
-  const int64_t off = sc.spt_offset[s];
-  const int n = sc.spt_count[s];
-  return sc.key_f64 ? prefix_search(static_cast<const double*>(sc.key_parent) + off, n, d)
-                    : prefix_search(static_cast<const float*>(sc.key_parent) + off, n, d);
+  const long long probe = a + lane;
+  const bool gt = probe < b && double(kp[probe]) > d;
+  return int(a + __popc(__ballot_sync(0xffffffffu, gt)));
 }
 
 GLOD_DEV double key_self_at(const LodScene& sc, int64_t rec) {
@@ -150,19 +153,33 @@ GLOD_DEV long long sum_before(const long long* cnt, int b, long long* sm) {
   return block_sum(v, sm);
 }
 
+// Phase timestamps of the last select launch (block 0; diagnostics only:
+// glod_debug_select_phases).
+__device__ unsigned long long g_sel_ts[8];
+GLOD_DEV void sel_stamp(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sel_ts[k] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kSelectThreads)
 select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
+  sel_stamp(0);
   __shared__ long long sm[kSelectThreads / 32 + 1];
   __shared__ double planes[24];
   if (threadIdx.x < 24) planes[threadIdx.x] = v.planes[threadIdx.x];
   const int lane = threadIdx.x & 31;
   const long long gthreads = (long long)gridDim.x * blockDim.x;
   const long long gwarp0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ws.frontier[0][0] = uint32_t(sc.root) | kStart;
-    ws.lvl_count[0] = 1;
+  if (!sc.cand) {                        // the level-synchronous BFS starts at the root
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ws.frontier[0][0] = uint32_t(sc.root) | kStart;
+      ws.lvl_count[0] = 1;
+    }
+    grid_sync(ws.bar);
   }
-  grid_sync(ws.bar);
 
   int level = 0;
   if (sc.cand) {
@@ -198,6 +215,7 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
       flags[node] = uint8_t(f);
     }
     grid_sync(ws.bar);
+    sel_stamp(1);
     // phase 2a: the upper-BFS candidates (upper nodes, SPT roots,
     // passthrough roots — cand[0, num_cand_upper)): walk to the root; a
     // visited passthrough root that its own bfs_cut expands gets bit 5
@@ -227,6 +245,7 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
       }
     }
     grid_sync(ws.bar);
+    sel_stamp(2);
     // phase 2b: passthrough-subtree members (cand[num_cand_upper, num_cand)):
     // walk up to their passthrough root, which must have been expanded
     for (long long i = sc.num_cand_upper + gtid; i < sc.num_cand; i += gthreads) {
@@ -244,6 +263,7 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
       if ((f & 1u) && (f & 12u)) atomicOr(ws.bm_pass + (node >> 5), 1u << (node & 31));
     }
     grid_sync(ws.bar);
+    sel_stamp(3);
     level = -1;
   } else
   // ---- level-synchronous BFS over the upper tree + passthrough subtrees ----
@@ -317,6 +337,7 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
     ws.block_cnt[2 * gridDim.x + blockIdx.x] = c_sp;
   }
   grid_sync(ws.bar);
+  sel_stamp(4);
   const long long b_up = sum_before(ws.block_cnt, blockIdx.x, sm);
   const long long b_pa = sum_before(ws.block_cnt + gridDim.x, blockIdx.x, sm);
   const long long b_sp = sum_before(ws.block_cnt + 2 * gridDim.x, blockIdx.x, sm);
@@ -330,17 +351,25 @@ select_kernel(LodScene sc, LodView v, SelectOut out, SelectScratch ws) {
     out.counts[3] = level;
   }
   grid_sync(ws.bar);
+  sel_stamp(5);
 
   // ---- stage 2 prologue: d_root (BLAS ddot norm, hspt.py:150) + prefix ----
+  // one warp per selected SPT (32-ary prefix search)
   const int n_spt = ld_cg(out.counts + 2);
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n_spt; j += gthreads) {
+  for (long long j = gwarp0 >> 5; j < n_spt; j += gthreads >> 5) {
     const int s = ld_cg(out.spt_ids + j);
     const double d = norm3_ddot(sub(sc.spt_center[3 * s], v.position[0]),
                                 sub(sc.spt_center[3 * s + 1], v.position[1]),
                                 sub(sc.spt_center[3 * s + 2], v.position[2]));
-    out.d_root[j] = d;
-    out.prefix_len[j] = prefix_len_of(sc, s, d);
+    const int64_t off = sc.spt_offset[s];
+    const int pl = sc.key_f64 ? warp_count_gt(static_cast<const double*>(sc.key_parent) + off, sc.spt_count[s], d, lane)
+                              : warp_count_gt(static_cast<const float*>(sc.key_parent) + off, sc.spt_count[s], d, lane);
+    if (lane == 0) {
+      out.d_root[j] = d;
+      out.prefix_len[j] = pl;
+    }
   }
+  sel_stamp(6);
 }
 
 // ---------------------------------------------------------------------------
@@ -429,21 +458,7 @@ GLOD_DEV void spt_prefix(const LodScene& sc, const CompactIn& in, const CompactO
     pl = in.known_prefix[j];
   } else {
     // np.searchsorted(-key_parent, -d, 'left') == #{key_parent > d}
-    const K* kp = static_cast<const K*>(sc.key_parent) + sc.spt_offset[s];
-    long long a = 0, b = sc.spt_count[s];
-    while (b - a > 32) {
-      const long long step = (b - a + 31) / 32;
-      const long long probe = a + step * lane;
-      const bool gt = probe < b && (probe == a || double(kp[probe]) > d);
-      const unsigned m = __ballot_sync(0xffffffffu, gt);
-      const int last = 31 - __clz(m);
-      const long long na = a + step * last;
-      b = min(b, na + step);
-      a = na;
-    }
-    const long long probe = a + lane;
-    const bool gt = probe < b && double(kp[probe]) > d;
-    pl = int(a + __popc(__ballot_sync(0xffffffffu, gt)));
+    pl = warp_count_gt(static_cast<const K*>(sc.key_parent) + sc.spt_offset[s], sc.spt_count[s], d, lane);
   }
   // root rule (spt.py:72-73): d >= key_self[root] selects exactly [root]
   const int rr = d >= double(key_self[sc.spt_offset[s] + sc.spt_root_rec[s]]);
@@ -798,6 +813,14 @@ size_t select_scratch_bytes(int64_t cap, int32_t S, int grid) {
 size_t compact_scratch_bytes(int32_t S, int64_t R, int grid) {
   (void)grid;
   return align_up(256 + 8 * max_tiles(R, S)) + 256;
+}
+
+cudaError_t select_phase_ns(long long* out7) {
+  unsigned long long t[8];
+  cudaError_t e = cudaMemcpyFromSymbol(t, g_sel_ts, sizeof(t));
+  if (e != cudaSuccess) return e;
+  for (int k = 0; k < 7; ++k) out7[k] = (long long)t[k];
+  return cudaSuccess;
 }
 
 int select_grid() { return coop_grid((const void*)select_kernel, kSelectThreads); }

@@ -858,6 +858,7 @@ struct RasterCtx {
   Buf splats, sorted, keys, keys2, vals, vals2, tiles, tiles_sorted, offs;
   Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin;
   bool long_runs = false;       // last forward finished its depth order with full-width passes
+  cudaEvent_t ev_runs = nullptr;  // the long-run flag's read-back landed
   CamD cam{};
   const double* attrs = nullptr;
   long long n = 0, n_inst = 0, n_visible = 0;
@@ -1007,59 +1008,69 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
                                             R->temp.cap, false, &alt, st));
   const int* order = alt ? R->vals2.as<int>() : R->vals.as<int>();
   R->long_runs = false;
-  if (begin_bit > 0) {
+  // the rest of the forward from a depth order: instances, tile sort, blend
+  auto tail = [&](const int* ord) -> cudaError_t {
     count_launch();
-    fixup_runs_kernel<<<nb, TB, 0, st>>>(alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>(),
-                                         const_cast<int*>(order), n, begin_bit, end_bit, stats + 3);
+    gather_kernel<<<nb, TB, 0, st>>>(ord, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
+                                     R->tiles_sorted.as<int>(), n);
     CK(cudaGetLastError());
-    CK(launch_readback(hp + 64, stats + 3, 8, st));
-    CK(cudaStreamSynchronize(st));
-    if (*reinterpret_cast<const unsigned long long*>(hp + 64)) {
-      // long tie runs: full-width stable passes over the top-sorted order
-      R->long_runs = true;
+    CK(cudaMemsetAsync(R->tiles_sorted.as<int>() + n, 0, 4, st));
+    CK(exclusive_scan_i32(R->tiles_sorted.as<int>(), R->offs.as<long long>(), n + 1, R->temp.p, R->temp.cap, st));
+    CK(R->ikey.ensure(4 * n_inst + 4, st));
+    CK(R->ikey2.ensure(4 * n_inst + 4, st));
+    CK(R->ival.ensure(4 * n_inst + 4, st));
+    CK(R->ival2.ensure(4 * n_inst + 4, st));
+    count_launch();
+    emit_kernel<<<nb, TB, 0, st>>>(R->sorted.as<Splat>(), R->tiles_sorted.as<int>(), R->offs.as<long long>(),
+                                   cam.tw, R->ikey.as<unsigned>(), R->ival.as<int>(), n);
+    CK(cudaGetLastError());
+    if (n_inst > 0) {
+      const int kb = bits_for(ntiles);
+      CK(R->temp.ensure(radix_scratch_bytes(n_inst), st));
       int alt2 = 0;
-      unsigned long long* k0 = alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>();
-      unsigned long long* k1 = alt ? R->keys.as<unsigned long long>() : R->keys2.as<unsigned long long>();
-      int* v0 = alt ? R->vals2.as<int>() : R->vals.as<int>();
-      int* v1 = alt ? R->vals.as<int>() : R->vals2.as<int>();
-      CK(radix_sort_pairs<unsigned long long>(k0, k1, v0, v1, n, 0, end_bit, R->temp.p, R->temp.cap, false,
-                                              &alt2, st));
-      order = alt2 ? v1 : v0;
+      CK(radix_sort_pairs<unsigned>(R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(), R->ival.as<int>(),
+                                    R->ival2.as<int>(), n_inst, 0, kb, R->temp.p, R->temp.cap, false, &alt2, st));
+      R->ikey_sorted = alt2 ? R->ikey2.as<unsigned>() : R->ikey.as<unsigned>();
+      R->ival_sorted = alt2 ? R->ival2.as<int>() : R->ival.as<int>();
+      count_launch();
+      ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey_sorted, n_inst, R->range.as<int2>());
+      CK(cudaGetLastError());
     }
-  }
-  count_launch();
-  gather_kernel<<<nb, TB, 0, st>>>(order, R->splats.as<Splat>(), R->tiles.as<int>(), R->sorted.as<Splat>(),
-                                   R->tiles_sorted.as<int>(), n);
-  CK(cudaGetLastError());
-  CK(cudaMemsetAsync(R->tiles_sorted.as<int>() + n, 0, 4, st));
-  CK(exclusive_scan_i32(R->tiles_sorted.as<int>(), R->offs.as<long long>(), n + 1, R->temp.p, R->temp.cap, st));
-  CK(R->ikey.ensure(4 * n_inst + 4, st));
-  CK(R->ikey2.ensure(4 * n_inst + 4, st));
-  CK(R->ival.ensure(4 * n_inst + 4, st));
-  CK(R->ival2.ensure(4 * n_inst + 4, st));
-  count_launch();
-  emit_kernel<<<nb, TB, 0, st>>>(R->sorted.as<Splat>(), R->tiles_sorted.as<int>(), R->offs.as<long long>(),
-                                 cam.tw, R->ikey.as<unsigned>(), R->ival.as<int>(), n);
-  CK(cudaGetLastError());
-  if (n_inst > 0) {
-    const int kb = bits_for(ntiles);
-    CK(R->temp.ensure(radix_scratch_bytes(n_inst), st));
-    int alt2 = 0;
-    CK(radix_sort_pairs<unsigned>(R->ikey.as<unsigned>(), R->ikey2.as<unsigned>(), R->ival.as<int>(),
-                                  R->ival2.as<int>(), n_inst, 0, kb, R->temp.p, R->temp.cap, false, &alt2, st));
-    R->ikey_sorted = alt2 ? R->ikey2.as<unsigned>() : R->ikey.as<unsigned>();
-    R->ival_sorted = alt2 ? R->ival2.as<int>() : R->ival.as<int>();
     count_launch();
-    ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey_sorted, n_inst, R->range.as<int2>());
-    CK(cudaGetLastError());
-  }
+    timing_begin(R, 0, st);
+    blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
+                                                         R->range.as<int2>(), cam, image,
+                                                         R->tfinal.as<double>(), R->last.as<int>());
+    timing_end(R, 0, st);
+    return cudaGetLastError();
+  };
+  if (begin_bit == 0) return tail(order);
   count_launch();
-  timing_begin(R, 0, st);
-  blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
-                                                       R->range.as<int2>(), cam, image,
-                                                       R->tfinal.as<double>(), R->last.as<int>());
-  timing_end(R, 0, st);
-  return cudaGetLastError();
+  fixup_runs_kernel<<<nb, TB, 0, st>>>(alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>(),
+                                       const_cast<int*>(order), n, begin_bit, end_bit, stats + 3);
+  CK(cudaGetLastError());
+  CK(launch_readback(hp + 64, stats + 3, 8, st));
+  if (!R->ev_runs) CK(cudaEventCreateWithFlags(&R->ev_runs, cudaEventDisableTiming));
+  CK(cudaEventRecord(R->ev_runs, st));
+  // the rest is enqueued before the host looks at the long-run flag, so the
+  // GPU never idles on this check; in the rare case of long tie runs the
+  // order is finished by full-width stable radix passes over the top-sorted
+  // keys and everything after the sort is enqueued again (stream order
+  // makes the second pass overwrite the first)
+  CK(tail(order));
+  CK(cudaEventSynchronize(R->ev_runs));
+  if (*reinterpret_cast<const unsigned long long*>(hp + 64)) {
+    R->long_runs = true;
+    int alt2 = 0;
+    unsigned long long* k0 = alt ? R->keys2.as<unsigned long long>() : R->keys.as<unsigned long long>();
+    unsigned long long* k1 = alt ? R->keys.as<unsigned long long>() : R->keys2.as<unsigned long long>();
+    int* v0 = alt ? R->vals2.as<int>() : R->vals.as<int>();
+    int* v1 = alt ? R->vals.as<int>() : R->vals2.as<int>();
+    CK(radix_sort_pairs<unsigned long long>(k0, k1, v0, v1, n, 0, end_bit, R->temp.p, R->temp.cap, false,
+                                            &alt2, st));
+    CK(tail(alt2 ? v1 : v0));
+  }
+  return cudaSuccess;
 }
 
 cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cudaStream_t st) {
@@ -1113,6 +1124,7 @@ void raster_destroy(RasterCtx* R) {
   if (R->host_pin.p) cudaFreeHost(R->host_pin.p);
   for (int i = 0; i < 4; ++i)
     if (R->ev[i]) cudaEventDestroy(R->ev[i]);
+  if (R->ev_runs) cudaEventDestroy(R->ev_runs);
   delete R;
 }
 
