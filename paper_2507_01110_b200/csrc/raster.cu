@@ -22,6 +22,11 @@
 #ifndef GLOD_PBWD_MINB
 #define GLOD_PBWD_MINB 4
 #endif
+// resident CTAs per SM blend_bwd is compiled for (10: 48 registers, more
+// warps, but 1.74 -> 1.79 ms; the forward likewise got slower at 8)
+#ifndef GLOD_BWD_MINB
+#define GLOD_BWD_MINB 8
+#endif
 #ifndef GLOD_DIRECT_LANES
 #define GLOD_DIRECT_LANES 2
 #endif
@@ -610,7 +615,7 @@ GLOD_DEV BwdPix bwd_init(const CamD& cam, int px, int py, const float* __restric
 // warp-reduced (transposed reduction) and nine lanes issue one fp64
 // reduction each (or, with one or two hitting lanes, those lanes issue
 // theirs directly).
-__global__ void __launch_bounds__(kBlendTB, 8)
+__global__ void __launch_bounds__(kBlendTB, GLOD_BWD_MINB)
 blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
                  const int2* __restrict__ range, CamD cam, const float* __restrict__ dimg,
                  const double* __restrict__ t_final, const int* __restrict__ last_in,
