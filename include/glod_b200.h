@@ -518,6 +518,10 @@ int glod_sort_pairs_u32(uint32_t* keys, uint32_t* keys_alt, int32_t* vals, int32
  * never queues behind bulk D2H DMA).  The caller synchronises the stream
  * before reading host_pinned. */
 int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream);
+/* Up to 8 such read-backs (4-byte aligned, multiples of 4 bytes) in one
+ * kernel launch. */
+int glod_readback_multi(int32_t n, void* const* host_pinned, const void* const* src, const int64_t* bytes,
+                        void* stream);
 /* The reverse: a stream-ordered small host→device upload read by a kernel
  * from page-locked memory (no copy-engine queueing behind the cache's bulk
  * prefetch DMA).  host_pinned must stay unchanged until the stream has run

@@ -164,6 +164,7 @@ SIGNATURES = {
     "glod_xchg_scatter_params": (C.c_int, [P, P, C.c_int64, P]),
     "glod_xchg_stats": (C.c_int, [P, P]),
     "glod_readback": (C.c_int, [P, P, C.c_int64, P]),
+    "glod_readback_multi": (C.c_int, [C.c_int32, P, P, P, P]),
     "glod_upload": (C.c_int, [P, P, C.c_int64, P]),
     "glod_debug_select_phases": (C.c_int, [P]),
     "glod_sort_scratch_bytes": (C.c_int64, [C.c_int64]),
@@ -252,6 +253,21 @@ def upload(dst, host_pinned, nbytes: int | None = None, stream=None):
     tensor (kernel-read through the mapped address; see glod_upload)."""
     n = host_pinned.numel() * host_pinned.element_size() if nbytes is None else nbytes
     check(lib().glod_upload(ptr(dst), ptr(host_pinned), int(n), stream_ptr(stream)))
+
+
+def readback_multi(pairs, stream=None):
+    """Several read-backs (host_pinned, src[, nbytes]) in one kernel launch
+    (glod_readback_multi; ≤ 8)."""
+    n = len(pairs)
+    dst = (C.c_void_p * n)()
+    src = (C.c_void_p * n)()
+    nb = (C.c_int64 * n)()
+    for i, p in enumerate(pairs):
+        h, s = p[0], p[1]
+        dst[i] = ptr(h)
+        src[i] = ptr(s)
+        nb[i] = p[2] if len(p) > 2 else s.numel() * s.element_size()
+    check(lib().glod_readback_multi(n, dst, src, nb, stream_ptr(stream)))
 
 
 def readback(host_pinned, src, nbytes: int | None = None, stream=None):

@@ -36,6 +36,8 @@ cudaError_t launch_convert(const void* in, void* out, long long n, int to_f64, c
 cudaError_t launch_store_xfer(const glod_store_view& sv, const glod_prefix_item* items, int n_items,
                               long long total, int load, cudaStream_t st);
 cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, cudaStream_t st);
+cudaError_t launch_readback_multi(int n, void* const* host_pinned, const void* const* src, const long long* bytes,
+                                  cudaStream_t st);
 cudaError_t select_phase_ns(long long* out7);
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 }  // namespace glod
@@ -267,6 +269,16 @@ int glod_debug_select_phases(int64_t* ns_out7) {
 int glod_upload(void* dst, const void* host_pinned, int64_t bytes, void* stream) {
   if ((!host_pinned || !dst) && bytes > 0) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::launch_upload(dst, host_pinned, bytes, static_cast<cudaStream_t>(stream)), "glod_upload");
+}
+
+int glod_readback_multi(int32_t n, void* const* host_pinned, const void* const* src, const int64_t* bytes,
+                        void* stream) {
+  if (n < 0 || n > 8 || (n > 0 && (!host_pinned || !src || !bytes)))
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "n must be 0..8 with non-null arrays");
+  long long b[8];
+  for (int r = 0; r < n; ++r) b[r] = bytes[r];
+  return check(glod::launch_readback_multi(n, host_pinned, src, b, static_cast<cudaStream_t>(stream)),
+               "glod_readback_multi");
 }
 
 int glod_readback(void* host_pinned, const void* src, int64_t bytes, void* stream) {

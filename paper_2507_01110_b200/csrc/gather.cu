@@ -566,6 +566,47 @@ cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes,
   return cudaGetLastError();
 }
 
+// Up to 8 read-backs in one launch (blockIdx.y = range): the select's four
+// per-view tables cost one kernel instead of four.
+namespace {
+struct ReadbackList {
+  const unsigned* src[8];
+  unsigned* dst[8];
+  long long words[8];
+};
+__global__ void readback_multi_kernel(ReadbackList L) {
+  const int r = blockIdx.y;
+  const unsigned* __restrict__ s = L.src[r];
+  unsigned* __restrict__ d = L.dst[r];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L.words[r];
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+}  // namespace
+
+cudaError_t launch_readback_multi(int n, void* const* host_pinned, const void* const* src, const long long* bytes,
+                                  cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > 8) return cudaErrorInvalidValue;
+  ReadbackList L = {};
+  long long maxw = 0;
+  for (int r = 0; r < n; ++r) {
+    void* dst = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dst, host_pinned[r], 0);
+    if (e != cudaSuccess) return e;
+    if (((reinterpret_cast<uintptr_t>(src[r]) | reinterpret_cast<uintptr_t>(dst)) & 3) || (bytes[r] & 3))
+      return cudaErrorInvalidValue;
+    L.src[r] = static_cast<const unsigned*>(src[r]);
+    L.dst[r] = static_cast<unsigned*>(dst);
+    L.words[r] = bytes[r] > 0 ? bytes[r] >> 2 : 0;
+    maxw = L.words[r] > maxw ? L.words[r] : maxw;
+  }
+  const int gx = int(maxw > 256 * 16 ? 16 : (maxw + 255) / 256 > 0 ? (maxw + 255) / 256 : 1);
+  count_launch();
+  readback_multi_kernel<<<dim3(gx, n), 256, 0, st>>>(L);
+  return cudaGetLastError();
+}
+
 // Stream-ordered small host→device upload from page-locked memory, read by
 // a kernel through the mapped address: the copy engines may be busy with
 // the cache's bulk prefetch DMA, and a main-stream cudaMemcpyAsync would

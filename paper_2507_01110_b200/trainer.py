@@ -392,13 +392,11 @@ class Trainer:
         sc = self.scene
         sel = sc.lod.select(cam, self.cfg.lod, cull=True)
         S1 = max(sc.lod.S, 1)
-        rb = _lib.readback      # kernel-written: never queues behind the write-back DMA
+        # kernel-written read-backs: never queue behind the write-back DMA
 
         def read(sel, h, hd):
-            rb(h[:4], sel.counts[:4])
-            rb(h[4:4 + S1], sel.spt_ids[:S1])
-            rb(h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1])
-            rb(hd, sel.d_root[:S1])
+            _lib.readback_multi([(h[:4], sel.counts[:4]), (h[4:4 + S1], sel.spt_ids[:S1]),
+                                 (h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1]), (hd, sel.d_root[:S1])])
 
         read(sel, self._h_sel, self._h_droot)
         if self._sel_ev is None:
