@@ -430,6 +430,8 @@ typedef struct glod_cache_stats_t {
   int64_t entries, resident_bytes, hits, misses, loaded_rows;
   int64_t prefetched_rows, prefetch_used_rows;
   int64_t pool_allocs, grow_events;   /* block-arena misses, staging re-allocations */
+  int64_t host_ns_step, host_ns_prefetch;  /* host time spent in cache_step / cache_prefetch */
+  int64_t pf_copies;                       /* prefetch prefixes issued (one copy each) */
 } glod_cache_stats_t;
 
 /* slot_start: host int64[num_spts], first store slot of each SPT
@@ -468,6 +470,9 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n,
                         const int32_t* spt_ids, const double* d_root, const int32_t* prefix_len,
                         int64_t max_rows, int64_t* rows_out, void* stream);
 int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out);
+/* Diagnostics: cumulative host ns per glod_cache_step phase (decisions,
+ * disk reads, materialize, loads, write-back staging, -, -, -). */
+int glod_cache_debug_profile(const glod_cache* c, int64_t* ns_out8);
 /* Implicit block refresh.  A cache block holds its prefix's 23*rows f64
  * values (section-major) followed by one "touched" bit per row
  * (ceil(rows/64) u64).  ADAM (glod_adam_step_records with a refresh plan)

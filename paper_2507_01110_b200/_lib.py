@@ -97,7 +97,8 @@ class PrefixItem(C.Structure):
 class CacheStats(C.Structure):
     _fields_ = [("entries", C.c_int64), ("resident_bytes", C.c_int64), ("hits", C.c_int64),
                 ("misses", C.c_int64), ("loaded_rows", C.c_int64), ("prefetched_rows", C.c_int64),
-                ("prefetch_used_rows", C.c_int64), ("pool_allocs", C.c_int64), ("grow_events", C.c_int64)]
+                ("prefetch_used_rows", C.c_int64), ("pool_allocs", C.c_int64), ("grow_events", C.c_int64),
+                ("host_ns_step", C.c_int64), ("host_ns_prefetch", C.c_int64), ("pf_copies", C.c_int64)]
 
 
 # name -> (restype, argtypes)
@@ -144,6 +145,7 @@ SIGNATURES = {
     "glod_cache_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, P, P, P, P, P]),
     "glod_cache_end_step": (C.c_int, [P, C.POINTER(StoreView), C.c_int64, C.c_int32, P]),
     "glod_cache_prefetch": (C.c_int, [P, C.POINTER(StoreView), C.c_int32, P, P, P, C.c_int64, P, P]),
+    "glod_cache_debug_profile": (C.c_int, [P, P]),
     "glod_cache_stats": (C.c_int, [P, C.POINTER(CacheStats)]),
     "glod_cache_set_master": (C.c_int, [P, P, C.c_int64, C.c_int64, P, P, C.c_int32]),
     "glod_cache_materialize": (C.c_int, [P, P]),

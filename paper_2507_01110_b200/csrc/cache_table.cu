@@ -14,6 +14,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <list>
 #include <map>
 #include <set>
@@ -239,6 +240,11 @@ struct CacheTable {
   cudaEvent_t ev_pf = nullptr, ev_pf_free = nullptr;
   int64_t pf_issued_rows = 0, pf_used_rows = 0;
   int64_t pool_allocs = 0, grow_events = 0;     // arena misses, staging re-allocations
+  int64_t host_ns_step = 0, host_ns_prefetch = 0, pf_copies = 0;
+  // host ns per cache_step phase: [0] checks + decisions, [1] disk reads,
+  // [2] materialize, [3] loads (tables + kernels), [4] write-back staging,
+  // [5] release of the step's prefetches (glod_cache_debug_profile)
+  int64_t prof_ns[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
   cudaError_t init(const glod_store_view& sv) {
     if (ready) return cudaSuccess;
@@ -563,9 +569,16 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     if (e != cudaSuccess) return e;
   }
   // before the loads: overlays read these blocks
+  auto tq = std::chrono::steady_clock::now();
+  auto lap = [&](int k) {
+    const auto now = std::chrono::steady_clock::now();
+    c->prof_ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - tq).count();
+    tq = now;
+  };
   e = materialize(c, wbs, st, reinterpret_cast<char*>(c->h_items) + (load_bytes + 15) / 16 * 16 +
                                   (wb_bytes + 15) / 16 * 16);
   if (e != cudaSuccess) return e;
+  lap(2);
   if (!loads.empty()) {
     glod_prefix_item* d = nullptr;
     const int2* bm = nullptr;
@@ -575,6 +588,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e != cudaSuccess) return e;
   }
+  lap(3);
   if (!wbs.empty()) {
     glod_prefix_item* d = nullptr;
     const int2* bm = nullptr;
@@ -634,6 +648,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     }
     c->pending.push_back(std::move(w));
   }
+  lap(4);
   return cudaEventRecord(c->items_done, st);
 }
 
@@ -666,6 +681,7 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
   }
   // write-backs of earlier steps already finished: nothing to wait for
   if (!c->wb_prev.empty() && cudaEventQuery(c->ev_wb) == cudaSuccess) c->wb_prev.clear();
+  const auto tp0 = std::chrono::steady_clock::now();
   std::vector<Xfer> loads, wbs;
   std::unordered_map<int32_t, std::pair<const double*, int64_t>> evicted;   // dirty, this step
   bool join = false, wait_pf = false;
@@ -785,6 +801,8 @@ cudaError_t cache_step(CacheTable* c, const glod_store_view& sv, int32_t n, cons
       if (e != cudaSuccess) return e;
     }
   }
+  const auto tp1 = std::chrono::steady_clock::now();
+  c->prof_ns[0] += std::chrono::duration_cast<std::chrono::nanoseconds>(tp1 - tp0).count();
   e = run_batch(c, loads, wbs, join, wait_pf, sv, st);
   if (e != cudaSuccess) return e;
   // every prefetch of the last step is done with once the load kernel ran
@@ -920,6 +938,7 @@ cudaError_t cache_prefetch(CacheTable* c, const glod_store_view& sv, int32_t n, 
     }
     for (const Want& w : v) {
       const int64_t slot = c->slot_start[w.sid];
+      ++c->pf_copies;
       if (c->interleaved) {
         cudaError_t er = cudaMemcpyAsync(w.buf, c->dsec[0] + slot * kFloats, size_t(w.rows) * kFloats * sizeof(float),
                                          cudaMemcpyDefault, c->pf_st);
@@ -1008,9 +1027,11 @@ int glod_cache_step(glod_cache* c, const glod_store_view* store, int32_t n, cons
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   if (store->row_stride != 0 && store->row_stride != 23)
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = glod::cache_step(&c->t, *store, n, spt_ids, d_root, prefix_len, dist_out, block_out,
                                    rows_out, counters_out, counters_out + 1,
                                    static_cast<cudaStream_t>(stream));
+  c->t.host_ns_step += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
   if (e == cudaErrorNotPermitted)
     return glod::set_error(GLOD_ERR_OVER_BUDGET, "cache entry exceeds the byte budget");
   if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
@@ -1035,8 +1056,10 @@ int glod_cache_prefetch(glod_cache* c, const glod_store_view* store, int32_t n, 
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   if (store->row_stride != 0 && store->row_stride != 23)
     return glod::set_error(GLOD_ERR_INVALID_ARGUMENT, "store row_stride must be 0 or 23");
+  const auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = glod::cache_prefetch(&c->t, *store, n, spt_ids, d_root, prefix_len, max_rows, rows_out,
                                        static_cast<cudaStream_t>(stream));
+  c->t.host_ns_prefetch += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
   if (e != cudaSuccess) return glod::set_error(GLOD_ERR_CUDA, cudaGetErrorString(e));
   return GLOD_OK;
 }
@@ -1089,6 +1112,12 @@ int glod_memcpy_d2h(void* dst, const void* src, int64_t bytes) {
   return GLOD_OK;
 }
 
+int glod_cache_debug_profile(const glod_cache* c, int64_t* ns_out8) {
+  if (!c || !ns_out8) return GLOD_ERR_INVALID_ARGUMENT;
+  for (int k = 0; k < 8; ++k) ns_out8[k] = c->t.prof_ns[k];
+  return GLOD_OK;
+}
+
 int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out) {
   if (!c || !out) return GLOD_ERR_INVALID_ARGUMENT;
   out->entries = int64_t(c->t.lru.size());
@@ -1100,6 +1129,9 @@ int glod_cache_stats(const glod_cache* c, glod_cache_stats_t* out) {
   out->prefetch_used_rows = c->t.pf_used_rows;
   out->pool_allocs = c->t.pool_allocs;
   out->grow_events = c->t.grow_events;
+  out->host_ns_step = c->t.host_ns_step;
+  out->host_ns_prefetch = c->t.host_ns_prefetch;
+  out->pf_copies = c->t.pf_copies;
   return GLOD_OK;
 }
 

@@ -33,7 +33,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--leaves", type=int, default=60_000_000)
     ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=40)   # the 4 GB cache fills over ~20 steps
     ap.add_argument("--budget-mb", type=int, default=4096)
     ap.add_argument("--aerial", type=int, default=24)
     ap.add_argument("--street", type=int, default=24)
@@ -61,6 +61,11 @@ def main():
         tr.train_step(it)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st0 = tr.cache.stats()
+    import ctypes as C
+    from paper_2507_01110_b200 import _lib
+    pr0 = np.zeros(8, np.int64)
+    _lib.check(_lib.lib().glod_cache_debug_profile(tr.cache._h, pr0.ctypes.data_as(C.c_void_p)))
     e0.record()
     recs = []
     for _ in range(a.steps):
@@ -69,6 +74,20 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
+    st1 = tr.cache.stats()
+    per_step = {k: (st1[k] - st0[k]) / a.steps for k in ("pf_copies", "prefetched_rows", "loaded_rows",
+                                                        "host_ns_step", "host_ns_prefetch", "pool_allocs",
+                                                        "grow_events")}
+    pr1 = np.zeros(8, np.int64)
+    _lib.check(_lib.lib().glod_cache_debug_profile(tr.cache._h, pr1.ctypes.data_as(C.c_void_p)))
+    per_step["step_phase_ms"] = dict(zip(["decide", "disk", "materialize", "loads", "wb_staging"],
+                                         ((pr1 - pr0)[:5] / a.steps / 1e6).round(3).tolist()))
+    tr.enable_timing(True)
+    for _ in range(6):
+        it += 1
+        tr.train_step(it)
+    stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
+    tr.enable_timing(False)
     # e2e: targets from pinned host memory every step
     tr.targets = [t.cpu().pin_memory() for t in tr.targets]
     tr.device_targets = False
@@ -106,6 +125,7 @@ def main():
         "mean_rendered": float(np.mean([r["gaussians_rendered"] for r in recs])),
         "mean_loaded_rows_per_step": float(np.mean([r["gaussians_loaded_from_store"] for r in recs])),
         "prefetched_rows": st["prefetched_rows"], "prefetch_used_rows": st["prefetch_used_rows"],
+        "per_step_cache": per_step, "stage_ms": stage_ms,
         "render": fps, "hbm_peak_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
         "hbm_reserved_gb_incl_arenas": round((torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9, 1),
         "scene_build_s": round(build_s, 1), "setup_s": round(setup_s, 1),

@@ -60,10 +60,14 @@ def main():
     wrap(tr.rast, "loss", "rast.loss")
     wrap(tr, "_gather_view")
     wrap(tr, "train_step")
+    s0 = tr.cache.stats()
     for _ in range(a.steps):
         it += 1
         tr.train_step(it)
     torch.cuda.synchronize()
+    s1 = tr.cache.stats()
+    print(f"C++ cache_step {(s1['host_ns_step'] - s0['host_ns_step']) / a.steps / 1e6:.3f} ms/step, "
+          f"cache_prefetch {(s1['host_ns_prefetch'] - s0['host_ns_prefetch']) / a.steps / 1e6:.3f} ms/step")
     for k, v in sorted(T.items(), key=lambda kv: -sum(kv[1])):
         print(f"{k:18s} calls/step {len(v) / a.steps:4.1f}  mean {1e3 * np.mean(v):7.3f} ms  "
               f"per step {1e3 * sum(v) / a.steps:7.3f} ms")
