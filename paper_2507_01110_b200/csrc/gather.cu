@@ -92,25 +92,29 @@ gather_rows_t_kernel(glod_gather_plan p, long long R, double* __restrict__ out, 
     if (row_node) row_node[r0 + threadIdx.x] = node;
   }
   __syncthreads();
-  const int ne = nr * 23;
-  constexpr int kPer = (kTRows * 23 + kTThreads - 1) / kTThreads;
-  double v[kPer];
+  // thread t reads column c = t mod 23 of rows t/23, t/23 + 11, ... (256 =
+  // 11·23 + 3; three threads idle): the column's section, offset and width
+  // are fixed per thread, so an element costs one address computation
+  constexpr int kRowsPerPass = kTThreads / 23;                 // 11
+  constexpr int kIter = (kTRows + kRowsPerPass - 1) / kRowsPerPass;
+  const int c = int(threadIdx.x) % 23, r_0 = int(threadIdx.x) / 23;
+  const bool active = threadIdx.x < kRowsPerPass * 23;
+  const int off = c < 3 ? 0 : c < 6 ? 3 : c < 10 ? 6 : c < 11 ? 10 : c < 14 ? 11 : 14;
+  const int cols = c < 6 ? 3 : c < 10 ? 4 : c < 11 ? 1 : c < 14 ? 3 : 9;
+  double v[kIter];
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {                 // every load in flight before the tile writes
-    const int e = threadIdx.x + k * kTThreads;
-    if (e < ne) {
-      const int lw = e / 23, col = e - lw * 23;
-      int sec = 0;
-#pragma unroll
-      for (int q = 1; q < 6; ++q) sec += col >= kSecOff[q];
-      const Src s = {s_base[lw], s_rows[lw], s_idx[lw]};
-      v[k] = src_at(s, kSecOff[sec], kSecCols[sec], col - kSecOff[sec]);
+  for (int k = 0; k < kIter; ++k) {                // every load in flight before the tile writes
+    const int lw = r_0 + k * kRowsPerPass;
+    if (active && lw < nr) {
+      const double* base = s_base[lw];
+      const long long rows = s_rows[lw], idx = s_idx[lw];
+      v[k] = rows > 0 ? base[off * rows + idx * cols + (c - off)] : base[idx * (-rows) + c];
     }
   }
 #pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int e = threadIdx.x + k * kTThreads;
-    if (e < ne) tile[e / 23][e % 23] = v[k];
+  for (int k = 0; k < kIter; ++k) {
+    const int lw = r_0 + k * kRowsPerPass;
+    if (active && lw < nr) tile[lw][c] = v[k];
   }
   __syncthreads();
   // section-major output: per section a contiguous run of nr·cols values
