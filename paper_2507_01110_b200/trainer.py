@@ -390,7 +390,7 @@ class Trainer:
         the GPU while the host makes this step's cache decisions; its
         per-SPT table is read later (`_spec_table`, before the prefetch)."""
         sc = self.scene
-        sel = sc.lod.select(cam, self.cfg.lod, cull=True)
+        sel = sc.lod.select(cam, self.cfg.lod, cull=True, frustum=self._frustum(cam))
         S1 = max(sc.lod.S, 1)
         # kernel-written read-backs: never queue behind the write-back DMA
 
@@ -404,7 +404,8 @@ class Trainer:
         self._sel_ev.record()
         self._spec = None
         if spec_cam is not None:
-            read(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True), self._h_sel2, self._h_droot2)
+            read(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True, frustum=self._frustum(spec_cam)),
+                 self._h_sel2, self._h_droot2)
             self._spec_ev.record()
             self._spec = "pending"
         self._sel_ev.synchronize()
@@ -412,6 +413,24 @@ class Trainer:
         n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
         return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
+
+    def _frustum(self, cam: Camera):
+        """Frustum.from_camera, memoised per camera (the host BLAS calls cost
+        ~0.2 ms per select; a run's views repeat)."""
+        cache = getattr(self, "_frusta", None)
+        if cache is None:
+            cache = self._frusta = {}
+        # keyed on everything the planes depend on (Camera is mutable)
+        key = (np.asarray(cam.position, dtype=np.float64).tobytes(),
+               np.asarray(cam.orientation, dtype=np.float64).tobytes(), tuple(cam.focal),
+               tuple(cam.principal_point), tuple(cam.resolution), float(cam.near), float(cam.far))
+        fr = cache.get(key)
+        if fr is None:
+            from .core import Frustum
+            fr = cache[key] = Frustum.from_camera(cam)
+            if len(cache) > 4096:
+                cache.pop(next(iter(cache)))
+        return fr
 
     def _spec_table(self):
         """The speculative select's per-SPT table (spt ids, d_root,
