@@ -61,6 +61,12 @@ def _grow(h: Hierarchy, extra: int) -> list:
     return list(range(old, old + extra))
 
 
+def _trim(h: Hierarchy, cap: int) -> None:
+    h.attrs = h.attrs.take(slice(0, cap))
+    h.parent = h.parent[:cap].copy()
+    h.children = h.children[:cap].copy()
+
+
 def _alloc2(h: Hierarchy) -> list:
     slots = []
     while h.free and len(slots) < 2:
@@ -135,6 +141,12 @@ class Moments:
     def grow_to(self, n: int):
         if n == self.step.size:
             return
+        if n < self.step.size:            # densify_tree's trim of unused pre-grown slots
+            for blk in (self.m, self.v):
+                for name, arr in blk.arrays():
+                    setattr(blk, name, arr[:n].copy())
+            self.step = self.step[:n].copy()
+            return
         extra = n - self.step.size
         for blk in (self.m, self.v):
             for name, arr in blk.arrays():
@@ -149,32 +161,87 @@ class Moments:
         self.step[ids] = 0
 
 
+def _choice1(rng: np.random.Generator, a: np.ndarray, p: np.ndarray):
+    """rng.choice(a, size=1, replace=False, p=p)[0] with numpy's exact
+    arithmetic and draws (one rng.random((1,)), cumsum, normalise by the
+    last value, searchsorted 'right' — numpy/random/_generator.pyx),
+    without the argument validation passes (tests/test_densify.py checks
+    the two agree, index and generator state)."""
+    x = rng.random((1,))
+    cdf = np.cumsum(p)
+    cdf /= cdf[-1]
+    return a[int(cdf.searchsorted(x, side="right")[0])]
+
+
 def densify_tree(h: Hierarchy, opt: Moments, rng: np.random.Generator, dead_opacity_threshold: float = 0.005,
                  spawns_per_densify: int | None = None) -> dict:
     """The host part of trainer.densify (trainer.py:411-440), in the
     reference's order: respawn every dead leaf into an opacity-sampled
     target, then spawn children under sampled leaves; moments of new /
-    respawned nodes are zeroed."""
+    respawned nodes are zeroed.
+
+    Same draws, same tree and the same slot ids as the reference, without
+    its per-edit O(capacity) passes: the sorted leaf list and its weights
+    are updated in place across respawns (each draw still normalises and
+    accumulates the whole distribution, exactly as numpy's choice does),
+    and the arrays grow once for all spawns (slot ids assigned as the
+    reference's allocator would: free slots first, then new ones in
+    order) instead of twice per spawn."""
     leaves = h.leaf_ids
     dead = leaves[h.attrs.opacities[leaves] < dead_opacity_threshold]
+    wl = np.maximum(h.attrs.opacities[leaves], 1e-12)
     respawned = 0
     for d in dead:
         d = int(d)
         if h.children[d, 0] != NONE or d == h.root:
             continue                      # structure changed under a previous respawn
         parent = int(h.parent[d])
-        targets = sample_leaves(h, 1, rng, exclude={d, parent})
-        if targets.size == 0:
+        # sample_leaves(h, 1, rng, exclude={d, parent}): parent is internal
+        i = int(np.searchsorted(leaves, d))
+        lv, w = np.delete(leaves, i), np.delete(wl, i)
+        if lv.size == 0:
             continue
-        respawn_dead(h, d, int(targets[0]), rng)
+        target = int(_choice1(rng, lv, w / w.sum()))
+        respawn_dead(h, d, target, rng)
         opt.reset_nodes([d, parent])
         respawned += 1
+        # leaves: the target is internal now, the old parent a leaf; d and
+        # the parent carry the split attributes
+        j = int(np.searchsorted(leaves, target))
+        leaves, wl = np.delete(leaves, j), np.delete(wl, j)
+        k = int(np.searchsorted(leaves, parent))
+        leaves, wl = np.insert(leaves, k, parent), np.insert(wl, k, max(float(h.attrs.opacities[parent]), 1e-12))
+        wl[int(np.searchsorted(leaves, d))] = max(float(h.attrs.opacities[d]), 1e-12)
     n_spawn = spawns_per_densify if spawns_per_densify is not None else max(h.leaf_count // 200, 0)
     spawned = 0
-    for leaf in sample_leaves(h, n_spawn, rng):
-        left, right = densify_spawn(h, int(leaf), rng)
+    picks = sample_leaves(h, n_spawn, rng)
+    # the reference's allocator (_alloc2) pops free slots first and grows by
+    # the shortfall: grow once by the total shortfall, hand out the new ids
+    # in the same order, trim what a failed spawn would leave unused
+    cap0 = h.capacity
+    need = max(0, 2 * len(picks) - len(h.free))
+    if need:
+        _grow(h, need)
         opt.grow_to(h.capacity)
+    nxt = cap0
+    for leaf in picks:
+        leaf = int(leaf)
+        if h.children[leaf, 0] != NONE:
+            raise InvalidTargetError(f"node {leaf} is internal, cannot spawn")
+        slots = []
+        while h.free and len(slots) < 2:
+            slots.append(h.free.pop())
+        while len(slots) < 2:
+            slots.append(nxt)
+            nxt += 1
+        left, right = sorted(slots)
+        h.attrs.put(np.array([left, right]), split_attributes(h.attrs, leaf, rng))
+        h.children[leaf] = (left, right)
+        h.parent[left] = leaf
+        h.parent[right] = leaf
         opt.reset_nodes([left, right])
         spawned += 1
+    if nxt < h.capacity:
+        _trim(h, nxt)
     opt.grow_to(h.capacity)
     return {"spawned": spawned, "respawned": respawned}

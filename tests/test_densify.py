@@ -117,3 +117,19 @@ def test_trainer_densify_matches_reference():
         assert tr.rng.random() == float(cd["out_next_draw"])
         # the re-laid-out scene keeps training
         tr.train_step(1)
+
+
+def test_choice1_matches_numpy_choice():
+    """densify's single weighted draw equals rng.choice(a, 1, replace=False,
+    p=p) — same element and the same generator state afterwards."""
+    from paper_2507_01110_b200.densify import _choice1
+    for trial in range(300):
+        r = np.random.default_rng(trial)
+        n = int(r.integers(1, 3000))
+        a = np.sort(r.choice(10 ** 6, n, replace=False))
+        w = np.maximum(r.random(n) ** 3, 1e-12)
+        p = w / w.sum()
+        r1, r2 = np.random.default_rng(trial + 7), np.random.default_rng(trial + 7)
+        for _ in range(3):
+            assert r1.choice(a, size=1, replace=False, p=p)[0] == _choice1(r2, a, p)
+        assert r1.bit_generator.state == r2.bit_generator.state
