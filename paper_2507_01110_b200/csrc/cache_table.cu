@@ -32,9 +32,9 @@ long long transfer_chunks(long long rows);
 cudaError_t launch_materialize(const glod_mat_item* items, int n_items, long long total, const double* master,
                                long long cap, long long mstride, const int* rec_node, cudaStream_t st);
 cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
-                               long long nblocks, cudaStream_t st);
+                               long long nblocks, const glod_master_ref& mref, cudaStream_t st);
 cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
-                               int interleaved, cudaStream_t st);
+                               int interleaved, const glod_master_ref& mref, cudaStream_t st);
 
 namespace {
 
@@ -513,14 +513,16 @@ size_t mat_bytes(const std::vector<Xfer>& v) { return (v.size() * sizeof(glod_ma
 size_t table_bytes(const std::vector<Xfer>& v) {
   long long nb = 0;
   for (const Xfer& x : v) nb += transfer_chunks(x.rows);
-  return (v.size() * sizeof(glod_prefix_item) + 15) / 16 * 16 + size_t(nb) * sizeof(int2);
+  return (v.size() * sizeof(glod_prefix_item) + 15) / 16 * 16 + (size_t(nb) * sizeof(int2) + 15) / 16 * 16 +
+         v.size() * sizeof(long long);
 }
 
 // Writes `v` and its block map into the pinned table at byte offset `off`
 // and uploads both (main-stream ordered; the caller frees the device copy
 // after its kernel).  Returns the device items, block map and block count.
 cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, cudaStream_t st,
-                        glod_prefix_item** d_items, const int2** d_bmap, long long* nblocks) {
+                        glod_prefix_item** d_items, const int2** d_bmap, long long* nblocks,
+                        const long long** d_rec_off) {
   char* base = reinterpret_cast<char*>(c->h_items) + off;
   glod_prefix_item* h = reinterpret_cast<glod_prefix_item*>(base);
   const size_t items_bytes = (v.size() * sizeof(glod_prefix_item) + 15) / 16 * 16;
@@ -538,7 +540,11 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
     const long long nc = transfer_chunks(v[i].rows);
     for (long long k = 0; k < nc; ++k) bm[nb++] = make_int2(int(i), int(k));
   }
-  const size_t bytes = items_bytes + size_t(nb) * sizeof(int2);
+  // each item's first SPT record (its rows' master rows: touched bits)
+  const size_t bmap_bytes = (size_t(nb) * sizeof(int2) + 15) / 16 * 16;
+  long long* ro = reinterpret_cast<long long*>(base + items_bytes + bmap_bytes);
+  for (size_t i = 0; i < v.size(); ++i) ro[i] = c->m_master ? c->m_rec_off[v[i].spt_id] : 0;
+  const size_t bytes = items_bytes + bmap_bytes + v.size() * sizeof(long long);
   void* d = nullptr;
   cudaError_t e = c->dalloc(&d, bytes, st);
   if (e != cudaSuccess) return e;
@@ -546,6 +552,7 @@ cudaError_t stage_items(CacheTable* c, const std::vector<Xfer>& v, size_t off, c
   if (e != cudaSuccess) return e;
   *d_items = static_cast<glod_prefix_item*>(d);
   *d_bmap = reinterpret_cast<const int2*>(static_cast<char*>(d) + items_bytes);
+  *d_rec_off = reinterpret_cast<const long long*>(static_cast<char*>(d) + items_bytes + bmap_bytes);
   *nblocks = nb;
   return cudaSuccess;
 }
@@ -568,23 +575,22 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     e = cudaStreamWaitEvent(st, c->ev_pf, 0);
     if (e != cudaSuccess) return e;
   }
-  // before the loads: overlays read these blocks
+  // touched rows of written-back / overlaid blocks are taken from the
+  // master by the pack / load kernels themselves (no materialise pass)
   auto tq = std::chrono::steady_clock::now();
   auto lap = [&](int k) {
     const auto now = std::chrono::steady_clock::now();
     c->prof_ns[k] += std::chrono::duration_cast<std::chrono::nanoseconds>(now - tq).count();
     tq = now;
   };
-  e = materialize(c, wbs, st, reinterpret_cast<char*>(c->h_items) + (load_bytes + 15) / 16 * 16 +
-                                  (wb_bytes + 15) / 16 * 16);
-  if (e != cudaSuccess) return e;
+  glod_master_ref mref = {c->m_master, c->m_cap, c->m_stride, c->m_rec_node, nullptr};
   lap(2);
   if (!loads.empty()) {
     glod_prefix_item* d = nullptr;
     const int2* bm = nullptr;
     long long nb = 0;
-    e = stage_items(c, loads, 0, st, &d, &bm, &nb);
-    if (e == cudaSuccess) e = launch_load_blocks(sv, d, bm, nb, st);
+    e = stage_items(c, loads, 0, st, &d, &bm, &nb, &mref.item_rec_off);
+    if (e == cudaSuccess) e = launch_load_blocks(sv, d, bm, nb, mref, st);
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e != cudaSuccess) return e;
   }
@@ -594,7 +600,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     const int2* bm = nullptr;
     long long nb = 0, total = 0;
     for (const Xfer& x : wbs) total += kFloats * x.rows;
-    e = stage_items(c, wbs, (load_bytes + 15) / 16 * 16, st, &d, &bm, &nb);
+    e = stage_items(c, wbs, (load_bytes + 15) / 16 * 16, st, &d, &bm, &nb, &mref.item_rec_off);
     if (e != cudaSuccess) return e;
     const int sb = c->stage_next;
     c->stage_next ^= 1;
@@ -618,7 +624,7 @@ cudaError_t run_batch(CacheTable* c, const std::vector<Xfer>& loads, const std::
     }
     float* staging = c->stage[sb];
     e = cudaStreamWaitEvent(st, c->ev_stage[sb], 0);
-    if (e == cudaSuccess) e = launch_pack_blocks(d, bm, nb, staging, c->interleaved, st);
+    if (e == cudaSuccess) e = launch_pack_blocks(d, bm, nb, staging, c->interleaved, mref, st);
     if (e == cudaSuccess) e = c->dfree(d, st);
     if (e == cudaSuccess) e = cudaEventRecord(c->ev_packed[sb], st);
     if (e != cudaSuccess) return e;

@@ -21,6 +21,18 @@ cudaError_t launch_upload(void* dst, const void* host_pinned, long long bytes, c
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 cudaError_t launch_set_bytes(void* dst, const void* src, int bytes, cudaStream_t st);
 
+// The master rows behind a cache block's touched bits (cache_table.cu →
+// gather.cu load/pack kernels): node records of `stride` doubles (or packed
+// section-major rows of `cap`), the LoD scene's record → node map, and the
+// first record of each transfer item's SPT.  master == nullptr: no block
+// row is ever touched.
+struct glod_master_ref {
+  const double* master;
+  long long cap, stride;
+  const int* rec_node;
+  const long long* item_rec_off;
+};
+
 // Host-side count of kernel launches issued by this library (reported by
 // bench.py as gpu_launches; defined in capi.cu).
 void count_launch(unsigned long long n = 1);

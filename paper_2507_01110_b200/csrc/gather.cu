@@ -44,6 +44,24 @@ GLOD_DEV bool row_touched(const double* blk, long long rows, long long pos) {
   return (block_bits(blk, rows)[pos >> 6] >> (pos & 63)) & 1ull;
 }
 
+// Column col of node `node`'s master row.
+GLOD_DEV double master_val(const glod_master_ref& m, long long node, int col) {
+  if (m.stride) return m.master[node * m.stride + col];
+  const int off = col < 3 ? 0 : col < 6 ? 3 : col < 10 ? 6 : col < 11 ? 10 : col < 14 ? 11 : 14;
+  const int cols = col < 6 ? 3 : col < 10 ? 4 : col < 11 ? 1 : col < 14 ? 3 : 9;
+  return m.master[off * m.cap + node * cols + (col - off)];
+}
+
+// Rows [r0, r0 + nr) of the tile whose bit is set in `blk` (rows `rows`)
+// take the master row (the implicit ADAM refresh, materialised on the fly).
+GLOD_DEV void touched_from_master(float* tile, const double* blk, long long rows, long long r0, int nr,
+                                  const glod_master_ref& m, long long rec_off) {
+  for (int t = threadIdx.x; t < nr * 23; t += blockDim.x) {
+    const int r = t / 23, col = t - r * 23;
+    if (row_touched(blk, rows, r0 + r)) tile[r * 23 + col] = float(master_val(m, m.rec_node[rec_off + r0 + r], col));
+  }
+}
+
 GLOD_DEV long long master_rows(const glod_gather_plan& p) {
   return p.master_stride ? -p.master_stride : p.capacity;
 }
@@ -338,7 +356,7 @@ GLOD_DEV void for_section_runs(long long rows, long long r0, int nr, F f) {
 
 __global__ void __launch_bounds__(256)
 load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ items,
-                   const int2* __restrict__ bmap) {
+                   const int2* __restrict__ bmap, glod_master_ref mref) {
   __shared__ float tile[kChunkRows * kTileLd];
   const int2 bm = bmap[blockIdx.x];
   const glod_prefix_item I = items[bm.x];
@@ -372,6 +390,10 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
   if (nov > 0) {
     __syncthreads();
     for_section_runs(I.overlay_rows, r0, nov, [&](int t, long long k) { tile[t] = float(I.overlay[k]); });
+    if (mref.master) {                           // its touched rows hold the master values
+      __syncthreads();
+      touched_from_master(tile, I.overlay, I.overlay_rows, r0, nov, mref, mref.item_rec_off[bm.x]);
+    }
   }
   __syncthreads();
   // 3. the f64 block, section-major
@@ -382,19 +404,27 @@ load_blocks_kernel(glod_store_view sv, const glod_prefix_item* __restrict__ item
 // an interleaved store, so one copy per prefix moves it).
 __global__ void __launch_bounds__(256)
 pack_blocks_kernel(const glod_prefix_item* __restrict__ items, const int2* __restrict__ bmap,
-                   float* __restrict__ out, int interleaved) {
+                   float* __restrict__ out, int interleaved, glod_master_ref mref) {
   __shared__ float tile[kChunkRows * kTileLd];
   const int2 bm = bmap[blockIdx.x];
   const glod_prefix_item I = items[bm.x];
   const long long r0 = (long long)bm.y * kChunkRows;
   const int nr = int(min((long long)kChunkRows, I.rows - r0));
   float* o = out + I.elem_start;
-  if (!interleaved) {                  // same layout as the block: a straight convert
+  if (!interleaved && !mref.master) {  // same layout as the block: a straight convert
     for_section_runs(I.rows, r0, nr, [&](int, long long k) { o[k] = float(I.block[k]); });
     return;
   }
   for_section_runs(I.rows, r0, nr, [&](int t, long long k) { tile[t] = float(I.block[k]); });
+  if (mref.master) {                   // touched rows are written back with their master values
+    __syncthreads();
+    touched_from_master(tile, I.block, I.rows, r0, nr, mref, mref.item_rec_off[bm.x]);
+  }
   __syncthreads();
+  if (!interleaved) {
+    for_section_runs(I.rows, r0, nr, [&](int t, long long k) { o[k] = tile[t]; });
+    return;
+  }
   float* dst = o + r0 * 23;
   for (int i = threadIdx.x; i < nr * 23; i += blockDim.x) dst[i] = tile[i];
 }
@@ -668,18 +698,18 @@ cudaError_t launch_refresh_resident(const double* master, long long cap, long lo
 long long transfer_chunks(long long rows) { return (rows + kChunkRows - 1) / kChunkRows; }
 
 cudaError_t launch_load_blocks(const glod_store_view& sv, const glod_prefix_item* items, const int2* bmap,
-                               long long nblocks, cudaStream_t st) {
+                               long long nblocks, const glod_master_ref& mref, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
   count_launch();
-  load_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(sv, items, bmap);
+  load_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(sv, items, bmap, mref);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_blocks(const glod_prefix_item* items, const int2* bmap, long long nblocks, float* out,
-                               int interleaved, cudaStream_t st) {
+                               int interleaved, const glod_master_ref& mref, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
   count_launch();
-  pack_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(items, bmap, out, interleaved);
+  pack_blocks_kernel<<<unsigned(nblocks), 256, 0, st>>>(items, bmap, out, interleaved, mref);
   return cudaGetLastError();
 }
 
