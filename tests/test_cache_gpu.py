@@ -244,3 +244,26 @@ def test_store_transfer_capi(interleaved):
             off += c * p
     for k, sec in enumerate(st.sections):
         np.testing.assert_array_equal(sec.numpy(), host[k])
+
+
+@pytest.mark.gpu
+def test_kernel_upload_and_readbacks():
+    """glod_upload / glod_readback / glod_readback_multi (kernel copies
+    through mapped pinned memory): exact bytes, stream-ordered, odd sizes,
+    unaligned pinned sources fall back to cudaMemcpyAsync."""
+    from paper_2507_01110_b200 import _lib
+    rng = np.random.default_rng(0)
+    for n in (1, 7, 1000, 123457):
+        h = torch.from_numpy(rng.integers(0, 2 ** 31, n, dtype=np.int64)).pin_memory()
+        d = torch.empty(n, dtype=torch.int64, device="cuda")
+        _lib.upload(d, h)
+        back = torch.empty(n, dtype=torch.int64).pin_memory()
+        _lib.readback(back, d)
+        torch.cuda.synchronize()
+        assert torch.equal(back, h)
+    srcs = [torch.arange(k, dtype=torch.int32, device="cuda") * (k + 1) for k in (4, 33, 1024, 70000)]
+    dsts = [torch.empty(s.numel(), dtype=torch.int32).pin_memory() for s in srcs]
+    _lib.readback_multi(list(zip(dsts, srcs)))
+    torch.cuda.synchronize()
+    for s, dd in zip(srcs, dsts):
+        assert torch.equal(dd, s.cpu())
