@@ -331,7 +331,7 @@ def cpu_baseline(trainer, args) -> dict:
     R = int(trainer.last_render_rows)
     view = trainer.current_view
     cam, _ = trainer.views[view]
-    rows = AttributeArrays.from_packed(trainer._rows[:23 * R].cpu().numpy(), R)
+    rows = AttributeArrays.from_packed(trainer.gathered_rows().cpu().numpy(), R)
     A = {n: getattr(rows, n) for n, _ in SECTIONS}
     g = trainer._last_grads[:23 * R].cpu().numpy()
     nz = np.zeros(R, bool)

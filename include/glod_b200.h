@@ -297,6 +297,15 @@ typedef struct glod_gather_plan {
  * n_upper+n_pass+n_sel rows); row_node (optional) receives each row's node. */
 int glod_gather_render_rows(const glod_gather_plan* plan, double* out, int32_t* row_node,
                             void* stream);
+/* glod_gather_render_rows fused into glod_render_forward: the rasteriser
+ * reads render row r from the source the gather would copy it from (so the
+ * image, the finiteness check and the following glod_render_backward are
+ * those of glod_render_forward on the gathered rows) and writes row_node[r];
+ * the packed render-set copy is never made.  R = n_upper+n_pass+n_sel.  The
+ * plan's device arrays, blocks and master must stay unchanged until the
+ * matching glod_render_backward has run. */
+int glod_render_forward_plan(glod_raster* r, const glod_gather_plan* plan, int32_t* row_node,
+                             const glod_camera* cam, float* image, void* stream);
 /* entry.block.attrs.put(pos, h.attrs.take(node_ids)) for every SPT row. */
 int glod_scatter_to_blocks(const glod_gather_plan* plan, void* stream);
 /* Serve path: wire payloads of the cut-delta protocol

@@ -128,6 +128,7 @@ SIGNATURES = {
     "glod_adam_step_records": (C.c_int, [P, C.c_int64, P, P, P, C.c_int64, C.c_int64,
                                          C.POINTER(C.c_double), P, C.c_int64, P, P]),
     "glod_gather_render_rows": (C.c_int, [C.POINTER(GatherPlan), P, P, P]),
+    "glod_render_forward_plan": (C.c_int, [P, C.POINTER(GatherPlan), P, C.POINTER(Camera), P, P]),
     "glod_scatter_to_blocks": (C.c_int, [C.POINTER(GatherPlan), P]),
     "glod_wire_pack": (C.c_int, [P, C.c_int64, P, P, C.c_int32, C.c_int64, P, P]),
     "glod_refresh_resident_blocks": (C.c_int, [P, C.c_int64, C.c_int64, P, C.c_int64, P, P, P, P, P, P]),

@@ -135,13 +135,7 @@ int glod_raster_destroy(glod_raster* r) {
   return GLOD_OK;
 }
 
-int glod_render_forward(glod_raster* r, const double* attrs, int64_t n, const glod_camera* cam,
-                        float* image, void* stream) {
-  if (!r || !cam || !image || (n > 0 && !attrs)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
-  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
-    return fail(GLOD_ERR_INVALID_ARGUMENT, "camera resolution out of range");
-  if (n < 0 || n > 0x7fffffffll) return fail(GLOD_ERR_INVALID_ARGUMENT, "n out of range");
-  cudaError_t e = glod::raster_forward(r->ctx, attrs, n, *cam, image, static_cast<cudaStream_t>(stream));
+static int render_result(glod_raster* r, cudaError_t e, const char* what) {
   int sec, idx;
   if (glod::raster_bad_input(r->ctx, &sec, &idx)) {
     static const char* names[6] = {"means", "scales", "rotations", "opacities", "base_colors", "sh_rest"};
@@ -149,7 +143,32 @@ int glod_render_forward(glod_raster* r, const double* attrs, int64_t n, const gl
     snprintf(buf, sizeof(buf), "non-finite %s on Gaussian %d", names[sec], idx);
     return fail(GLOD_ERR_INVALID_INPUT, buf);
   }
-  return check(e, "glod_render_forward");
+  return check(e, what);
+}
+
+int glod_render_forward(glod_raster* r, const double* attrs, int64_t n, const glod_camera* cam,
+                        float* image, void* stream) {
+  if (!r || !cam || !image || (n > 0 && !attrs)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "camera resolution out of range");
+  if (n < 0 || n > 0x7fffffffll) return fail(GLOD_ERR_INVALID_ARGUMENT, "n out of range");
+  cudaError_t e = glod::raster_forward(r->ctx, attrs, n, *cam, image, static_cast<cudaStream_t>(stream));
+  return render_result(r, e, "glod_render_forward");
+}
+
+int glod_render_forward_plan(glod_raster* r, const glod_gather_plan* plan, int32_t* row_node,
+                             const glod_camera* cam, float* image, void* stream) {
+  if (!r || !plan || !cam || !image) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (cam->width < 1 || cam->height < 1 || cam->width > 32767 || cam->height > 32767)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "camera resolution out of range");
+  const long long n = (long long)plan->n_upper + plan->n_pass + plan->n_sel;
+  if (plan->n_upper < 0 || plan->n_pass < 0 || plan->n_sel < 0 || n > 0x7fffffffll)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "row counts out of range");
+  if (n > 0 && (!row_node || !plan->master)) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  if (plan->master_stride != 0 && plan->master_stride != GLOD_NODE_RECORD)
+    return fail(GLOD_ERR_INVALID_ARGUMENT, "master_stride must be 0 or GLOD_NODE_RECORD");
+  cudaError_t e = glod::raster_forward_plan(r->ctx, *plan, row_node, *cam, image, static_cast<cudaStream_t>(stream));
+  return render_result(r, e, "glod_render_forward_plan");
 }
 
 int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, void* stream) {

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "../../include/glod_b200.h"
 
 namespace glod {
@@ -19,30 +20,6 @@ namespace {
 
 __constant__ int kSecOff[7] = {0, 3, 6, 10, 11, 14, 23};   // column offsets per section
 __constant__ int kSecCols[6] = {3, 3, 4, 1, 3, 9};
-
-struct Src {
-  const double* base;
-  long long rows;       // section stride (section-major blocks), or -record stride
-  long long idx;
-};
-
-// Element (section offset OFF, column col) of a source row: section-major
-// blocks/master (rows > 0) or node records (rows = -GLOD_NODE_RECORD).
-GLOD_DEV double src_at(const Src& s, int OFF, int COLS, int col) {
-  return s.rows > 0 ? s.base[OFF * s.rows + s.idx * COLS + col] : s.base[s.idx * (-s.rows) + OFF + col];
-}
-
-// Cache blocks carry one "touched" bit per row after their 23·rows values:
-// ADAM sets it instead of writing the updated master row into the block
-// (trainer.py:363's refresh made implicit) — a touched row's value IS the
-// master row; readers take it from there, and blocks are materialised
-// before they are written back.
-GLOD_DEV unsigned long long* block_bits(const double* blk, long long rows) {
-  return reinterpret_cast<unsigned long long*>(const_cast<double*>(blk) + 23 * rows);
-}
-GLOD_DEV bool row_touched(const double* blk, long long rows, long long pos) {
-  return (block_bits(blk, rows)[pos >> 6] >> (pos & 63)) & 1ull;
-}
 
 // Column col of node `node`'s master row.
 GLOD_DEV double master_val(const glod_master_ref& m, long long node, int col) {
@@ -60,31 +37,6 @@ GLOD_DEV void touched_from_master(float* tile, const double* blk, long long rows
     const int r = t / 23, col = t - r * 23;
     if (row_touched(blk, rows, r0 + r)) tile[r * 23 + col] = float(master_val(m, m.rec_node[rec_off + r0 + r], col));
   }
-}
-
-GLOD_DEV long long master_rows(const glod_gather_plan& p) {
-  return p.master_stride ? -p.master_stride : p.capacity;
-}
-
-GLOD_DEV Src row_source(const glod_gather_plan& p, long long r, int& node) {
-  const long long n_mem = (long long)p.n_upper + p.n_pass;
-  Src s;
-  if (r < p.n_upper) {
-    node = p.upper_ids[r];
-    s = {p.master, master_rows(p), node};
-  } else if (r < n_mem) {
-    node = p.pass_ids[r - p.n_upper];
-    s = {p.master, master_rows(p), node};
-  } else {
-    const long long k = r - n_mem;
-    const int j = p.sel_seg[k];
-    node = p.sel_node[k];
-    const double* blk = reinterpret_cast<const double*>(p.seg_block[j]);
-    const long long P = p.seg_rows[j], pos = p.sel_pos[k];
-    if (p.spt_from_master || row_touched(blk, P, pos)) s = {p.master, master_rows(p), node};
-    else s = {blk, P, pos};
-  }
-  return s;
 }
 
 // Transposing gather: one CTA per kTRows render rows.  Row sources are

@@ -14,6 +14,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "gather.cuh"
 #include "raster.cuh"
 
 #ifndef GLOD_PRE_MINB
@@ -67,11 +68,17 @@ CamD make_cam(const glod_camera& c) {
   return k;
 }
 
-// Section offsets in a packed attribute block of n rows.
-struct Sec {
-  const double *mean, *scale, *rot, *opac, *base, *sh;
-  GLOD_DEV Sec(const double* a, long long n)
-      : mean(a), scale(a + 3 * n), rot(a + 6 * n), opac(a + 10 * n), base(a + 11 * n), sh(a + 14 * n) {}
+// Where the rasteriser reads render row i: a packed section-major block of
+// n rows (glod_render_forward), or straight through the K4 gather plan
+// (glod_render_forward_plan): the same source row the gather kernel would
+// copy (row_source, gather.cuh), so the values are identical and the
+// gathered copy is never materialised.  In plan mode the preprocess also
+// writes each row's node id (the gather's row_node output).
+struct AttrSrc {
+  const double* attrs;
+  long long n;
+  glod_gather_plan plan;
+  int* row_node;
 };
 
 // Everything the forward and backward passes derive from one Gaussian.
@@ -89,8 +96,8 @@ struct Proj {
   double col[3];
 };
 
-GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
-  const double m0 = s.mean[3 * i], m1 = s.mean[3 * i + 1], m2 = s.mean[3 * i + 2];
+GLOD_DEV void project(const RowView& s, const CamD& c, Proj& P) {
+  const double m0 = s.mean[0], m1 = s.mean[1], m2 = s.mean[2];
   const double d0 = sub(m0, c.p[0]), d1 = sub(m1, c.p[1]), d2 = sub(m2, c.p[2]);
   // t = (μ − p) @ Wᵀ through dgemm: fma(c2,w2,fma(c1,w1,c0*w0))
 #pragma unroll
@@ -99,7 +106,7 @@ GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
   const double tz = P.t[2];
   P.m2[0] = add(div(mul(c.fx, P.t[0]), tz), c.cx);
   P.m2[1] = add(div(mul(c.fy, P.t[1]), tz), c.cy);
-  double q0 = s.rot[4 * i], q1 = s.rot[4 * i + 1], q2 = s.rot[4 * i + 2], q3 = s.rot[4 * i + 3];
+  double q0 = s.rot[0], q1 = s.rot[1], q2 = s.rot[2], q3 = s.rot[3];
   P.qnorm = sqrt_(add(add(add(mul(q0, q0), mul(q1, q1)), mul(q2, q2)), mul(q3, q3)));
   const double w = q0 / P.qnorm, x = q1 / P.qnorm, y = q2 / P.qnorm, z = q3 / P.qnorm;
   P.qn[0] = w; P.qn[1] = x; P.qn[2] = y; P.qn[3] = z;
@@ -107,7 +114,7 @@ GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
   R[0] = 1 - 2 * (y * y + z * z); R[1] = 2 * (x * y - w * z); R[2] = 2 * (x * z + w * y);
   R[3] = 2 * (x * y + w * z); R[4] = 1 - 2 * (x * x + z * z); R[5] = 2 * (y * z - w * x);
   R[6] = 2 * (x * z - w * y); R[7] = 2 * (y * z + w * x); R[8] = 1 - 2 * (x * x + y * y);
-  const double s0 = s.scale[3 * i], s1 = s.scale[3 * i + 1], s2 = s.scale[3 * i + 2];
+  const double s0 = s.scale[0], s1 = s.scale[1], s2 = s.scale[2];
   const double ss[3] = {s0 * s0, s1 * s1, s2 * s2};
   double Sg[9];
 #pragma unroll
@@ -141,10 +148,10 @@ GLOD_DEV void project(const Sec& s, long long i, const CamD& c, Proj& P) {
   P.rng = norm3_plain(d0, d1, d2);
   const double inv = P.rng > 0 ? P.rng : 1.0;
   P.v[0] = d0 / inv; P.v[1] = d1 / inv; P.v[2] = d2 / inv;
-  const double* f = s.sh + 9 * i;
+  const double* f = s.sh;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
-    P.col[k] = s.base[3 * i + k] + kShC1 * (-P.v[1] * f[k] + P.v[2] * f[3 + k] - P.v[0] * f[6 + k]);
+    P.col[k] = s.base[k] + kShC1 * (-P.v[1] * f[k] + P.v[2] * f[3 + k] - P.v[0] * f[6 + k]);
 }
 
 GLOD_DEV bool finite(double x) { return isfinite(x); }
@@ -202,24 +209,23 @@ constexpr int kFwdTB = 32 * kFwdWarps;
 
 // One Gaussian; returns its tile count (0 = contributes nothing) and sets
 // its depth key.
-GLOD_DEV int preprocess_one(const double* __restrict__ attrs, long long n, long long i, const CamD& cam,
+GLOD_DEV int preprocess_one(const RowView& s, long long i, const CamD& cam,
                             Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
                             int* __restrict__ vals, int* __restrict__ tiles, int* __restrict__ bad) {
-  Sec s(attrs, n);
   // _check_finite (renderer.py:67-72): first section, then first row
-  const int cols[6] = {3, 3, 4, 1, 3, 9};
-  const double* base[6] = {s.mean, s.scale, s.rot, s.opac, s.base, s.sh};
-#pragma unroll
-  for (int k = 0; k < 6; ++k) {
+  auto check = [&](const double* v, int cols, int k) {
     bool ok = true;
-    for (int c = 0; c < cols[k]; ++c) ok &= finite(base[k][cols[k] * i + c]);
+#pragma unroll
+    for (int c = 0; c < cols; ++c) ok &= finite(v[c]);
     if (!ok) atomicMin(bad + k, int(i));
-  }
+  };
+  check(s.mean, 3, 0); check(s.scale, 3, 1); check(s.rot, 4, 2);
+  check(s.opac, 1, 3); check(s.base, 3, 4); check(s.sh, 9, 5);
   vals[i] = int(i);
   keys[i] = ~0ull;
   tiles[i] = 0;
   Proj P;
-  project(s, i, cam, P);
+  project(s, cam, P);
   const double depth = P.t[2];
   if (!(depth > cam.near_)) return 0;            // ok = depth > near
   const double det = P.c00 * P.c11 - P.c01 * P.c01;
@@ -242,7 +248,7 @@ GLOD_DEV int preprocess_one(const double* __restrict__ attrs, long long n, long 
   sp.ca = float(P.c11 / det);
   sp.cb = float(-P.c01 / det);
   sp.cc = float(P.c00 / det);
-  sp.opac = float(s.opac[i]);
+  sp.opac = float(s.opac[0]);
   sp.x0 = int16_t(x0); sp.y0 = int16_t(y0); sp.x1 = int16_t(x1); sp.y1 = int16_t(y1);
   sp.r = float(P.col[0]); sp.g = float(P.col[1]); sp.b = float(P.col[2]);
   sp.idx = int(i);
@@ -265,14 +271,10 @@ GLOD_DEV int preprocess_one(const double* __restrict__ attrs, long long n, long 
 // K5 over all Gaussians.  Also reduces, for the one host read-back of the
 // forward pass, stats = {Σ tile instances, min key, max key} over the
 // contributing splats (the depth sort only needs the bits where they differ).
-__global__ void __launch_bounds__(256, GLOD_PRE_MINB)
-preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat* __restrict__ splats,
-                  unsigned long long* __restrict__ keys, int* __restrict__ vals, int* __restrict__ tiles,
-                  int* __restrict__ bad, unsigned long long* __restrict__ stats) {
+// Block reduction of the forward's read-back stats (Σ tile instances, min/max key).
+GLOD_DEV void reduce_stats(int nt, long long i, const unsigned long long* __restrict__ keys,
+                           unsigned long long* __restrict__ stats) {
   __shared__ unsigned long long red[3][8];
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  int nt = 0;
-  if (i < n) nt = preprocess_one(attrs, n, i, cam, splats, keys, vals, tiles, bad);
   unsigned long long cnt = (unsigned long long)nt;
   unsigned long long kmn = ~0ull, kmx = 0;
   if (nt) kmn = kmx = keys[i];
@@ -303,6 +305,85 @@ preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat
       atomicMax(stats + 2, kmx);
     }
   }
+}
+
+__global__ void __launch_bounds__(256, GLOD_PRE_MINB)
+preprocess_kernel(const double* __restrict__ attrs, long long n, CamD cam, Splat* __restrict__ splats,
+                  unsigned long long* __restrict__ keys, int* __restrict__ vals, int* __restrict__ tiles,
+                  int* __restrict__ bad, unsigned long long* __restrict__ stats) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int nt = 0;
+  if (i < n) nt = preprocess_one(row_view(Src{attrs, n, i}), i, cam, splats, keys, vals, tiles, bad);
+  reduce_stats(nt, i, keys, stats);
+}
+
+// K4 + K5 fused (glod_render_forward_plan): a CTA resolves the sources of
+// its 256 render rows (row_source, exactly the gather kernel's), reads them
+// into a shared tile the way gather_rows_t_kernel does — thread t owns
+// column t mod 23, so each row is fetched as contiguous runs and every
+// thread has several independent loads in flight — and preprocesses row t
+// from the tile.  The gathered copy never goes through HBM.
+template <int kThreads>
+GLOD_DEV void stage_rows(double* __restrict__ tile, const double* const* s_base, const long long* s_rows,
+                         const long long* s_idx, int nr) {
+  // thread t reads column c = t mod 23 of rows t/23 + k·(kThreads/23):
+  // the column's section, offset and width are fixed per thread
+  constexpr int kRowsPerPass = kThreads / 23;
+  constexpr int kBatch = 8;
+  const int c = int(threadIdx.x) % 23, rt = int(threadIdx.x) / 23;
+  const bool active = threadIdx.x < kRowsPerPass * 23;
+  const int off = c < 3 ? 0 : c < 6 ? 3 : c < 10 ? 6 : c < 11 ? 10 : c < 14 ? 11 : 14;
+  const int cols = c < 6 ? 3 : c < 10 ? 4 : c < 11 ? 1 : c < 14 ? 3 : 9;
+  for (int b = 0; b * kBatch * kRowsPerPass < nr; ++b) {
+    double v[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {          // the batch's loads in flight before its tile writes
+      const int lw = rt + (b * kBatch + k) * kRowsPerPass;
+      if (active && lw < nr) {
+        const double* base = s_base[lw];
+        const long long rows = s_rows[lw], idx = s_idx[lw];
+        v[k] = rows > 0 ? base[off * rows + idx * cols + (c - off)] : base[idx * (-rows) + c];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+      const int lw = rt + (b * kBatch + k) * kRowsPerPass;
+      if (active && lw < nr) tile[lw * 23 + c] = v[k];
+    }
+  }
+}
+
+constexpr int kPlanRows = 256;
+constexpr size_t kPlanSmem = sizeof(double) * kPlanRows * 23 + (sizeof(void*) + 16) * kPlanRows;
+
+__global__ void __launch_bounds__(kPlanRows, GLOD_PRE_MINB)
+preprocess_plan_kernel(const glod_gather_plan p, long long n, int* __restrict__ row_node, CamD cam,
+                       Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
+                       int* __restrict__ vals, int* __restrict__ tiles, int* __restrict__ bad,
+                       unsigned long long* __restrict__ stats) {
+  extern __shared__ __align__(16) double plan_smem[];
+  double* tile = plan_smem;                                           // [kPlanRows][23]
+  const double** s_base = reinterpret_cast<const double**>(tile + kPlanRows * 23);
+  long long* s_rows = reinterpret_cast<long long*>(s_base + kPlanRows);
+  long long* s_idx = s_rows + kPlanRows;
+  const long long r0 = (long long)blockIdx.x * kPlanRows;
+  const int nr = int(min((long long)kPlanRows, n - r0));
+  if (threadIdx.x < nr) {
+    int node;
+    const Src s = row_source(p, r0 + threadIdx.x, node);
+    s_base[threadIdx.x] = s.base;
+    s_rows[threadIdx.x] = s.rows;
+    s_idx[threadIdx.x] = s.idx;
+    row_node[r0 + threadIdx.x] = node;
+  }
+  __syncthreads();
+  stage_rows<kPlanRows>(tile, s_base, s_rows, s_idx, nr);
+  __syncthreads();
+  const long long i = r0 + threadIdx.x;
+  int nt = 0;
+  if (i < n) nt = preprocess_one(row_view(Src{tile + threadIdx.x * 23, -23, 0}), i, cam, splats, keys, vals,
+                                 tiles, bad);
+  reduce_stats(nt, i, keys, stats);
 }
 
 // Top-bits depth sort fix-up: within each run of keys whose bits
@@ -691,28 +772,24 @@ blend_bwd_kernel(const Splat* __restrict__ sorted, const int* __restrict__ ival,
 }
 
 // K9: 2D partials → gradients of the raw attributes (renderer.py:262-303).
-__global__ void __launch_bounds__(128, GLOD_PBWD_MINB) preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam,
-                                      const int* __restrict__ tiles_of, const double* __restrict__ g2,
-                                      double* __restrict__ grads) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Sec s(attrs, n);
+// A row that contributed no tile instance has zero gradients.
+GLOD_DEV void bwd_zero(long long i, long long n, double* __restrict__ grads) {
+  for (int k = 0; k < 3; ++k) { grads[3 * i + k] = 0; grads[3 * n + 3 * i + k] = 0; grads[11 * n + 3 * i + k] = 0; }
+  for (int k = 0; k < 4; ++k) grads[6 * n + 4 * i + k] = 0;
+  for (int k = 0; k < 9; ++k) grads[14 * n + 9 * i + k] = 0;
+  grads[10 * n + i] = 0;
+}
+
+GLOD_DEV void bwd_one(const RowView& s, long long i, long long n, const CamD& cam, const double* __restrict__ a2,
+                      double* __restrict__ grads) {
   double* gm = grads;                 // means [3n]
   double* gsc = grads + 3 * n;        // scales
   double* grot = grads + 6 * n;       // rotations
   double* gop = grads + 10 * n;       // opacities
   double* gbase = grads + 11 * n;     // base colours
   double* gsh = grads + 14 * n;       // sh_rest
-  const double* a2 = g2 + (long long)kG2 * i;
-  if (tiles_of[i] == 0) {
-    for (int k = 0; k < 3; ++k) { gm[3 * i + k] = 0; gsc[3 * i + k] = 0; gbase[3 * i + k] = 0; }
-    for (int k = 0; k < 4; ++k) grot[4 * i + k] = 0;
-    for (int k = 0; k < 9; ++k) gsh[9 * i + k] = 0;
-    gop[i] = 0;
-    return;
-  }
   Proj P;
-  project(s, i, cam, P);
+  project(s, cam, P);
   const double det = P.c00 * P.c11 - P.c01 * P.c01;
   const double ca = P.c11 / det, cb = -P.c01 / det, cc = P.c00 / det;
   const double dcol[3] = {a2[0], a2[1], a2[2]};
@@ -772,7 +849,7 @@ __global__ void __launch_bounds__(128, GLOD_PBWD_MINB) preprocess_bwd_kernel(con
 #pragma unroll
   for (int k = 0; k < 3; ++k) dmean[k] = W[k] * dt[0] + W[3 + k] * dt[1] + W[6 + k] * dt[2];
   // colour path (renderer.py:281-291)
-  const double* f = s.sh + 9 * i;
+  const double* f = s.sh;
   const double* v = P.v;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -797,7 +874,7 @@ __global__ void __launch_bounds__(128, GLOD_PBWD_MINB) preprocess_bwd_kernel(con
 #pragma unroll
     for (int b = 0; b < 3; ++b) sym[3 * a + b] = 0.5 * (dS[3 * a + b] + dS[3 * b + a]);
   const double* R = P.R;
-  const double sc[3] = {s.scale[3 * i], s.scale[3 * i + 1], s.scale[3 * i + 2]};
+  const double sc[3] = {s.scale[0], s.scale[1], s.scale[2]};
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     double acc = 0;
@@ -833,6 +910,29 @@ __global__ void __launch_bounds__(128, GLOD_PBWD_MINB) preprocess_bwd_kernel(con
   for (int k = 0; k < 4; ++k) grot[4 * i + k] = (dq[k] - P.qn[k] * qd) / P.qnorm;
 }
 
+__global__ void __launch_bounds__(128, GLOD_PBWD_MINB)
+preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam, const int* __restrict__ tiles_of,
+                      const double* __restrict__ g2, double* __restrict__ grads) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (tiles_of[i] == 0) return bwd_zero(i, n, grads);
+  bwd_one(row_view(Src{attrs, n, i}), i, n, cam, g2 + (long long)kG2 * i, grads);
+}
+
+// K9 reading each contributing render row through the gather plan (the
+// forward's preprocess_plan_kernel).  Read in place, not staged: only ~40 %
+// of the rows contributed, and a staged tile costs more in barriers and
+// idle lanes than the row-source indirection does.
+__global__ void __launch_bounds__(128, GLOD_PBWD_MINB)
+preprocess_bwd_plan_kernel(const glod_gather_plan p, long long n, CamD cam, const int* __restrict__ tiles_of,
+                           const double* __restrict__ g2, double* __restrict__ grads) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (tiles_of[i] == 0) return bwd_zero(i, n, grads);
+  int node;
+  bwd_one(row_view(row_source(p, i, node)), i, n, cam, g2 + (long long)kG2 * i, grads);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -865,7 +965,8 @@ struct RasterCtx {
   bool long_runs = false;       // last forward finished its depth order with full-width passes
   cudaEvent_t ev_runs = nullptr;  // the long-run flag's read-back landed
   CamD cam{};
-  const double* attrs = nullptr;
+  AttrSrc src{};
+  bool plan_src = false;
   long long n = 0, n_inst = 0, n_visible = 0;
   int bad_section = -1, bad_index = -1;
   cudaStream_t stream = nullptr;
@@ -927,10 +1028,12 @@ static int bits_for(long long v) {
     if (_e != cudaSuccess) return _e;           \
   } while (0)
 
-cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const glod_camera& c,
-                           float* image, cudaStream_t st) {
+static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool plan, const glod_camera& c,
+                               float* image, cudaStream_t st) {
+  const long long n = src.n;
   R->cam = make_cam(c);
-  R->attrs = attrs;
+  R->src = src;
+  R->plan_src = plan;
   R->n = n;
   R->stream = st;
   R->have_forward = true;
@@ -978,8 +1081,19 @@ cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const
   const int TB = 256;
   const int nb = int((n + TB - 1) / TB);
   count_launch();
-  preprocess_kernel<<<nb, TB, 0, st>>>(attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
-                                       R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>(), stats);
+  if (plan) {
+    static bool smem_set = false;
+    if (!smem_set) {
+      CK(cudaFuncSetAttribute(preprocess_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPlanSmem)));
+      smem_set = true;
+    }
+    preprocess_plan_kernel<<<int((n + kPlanRows - 1) / kPlanRows), kPlanRows, kPlanSmem, st>>>(
+        src.plan, n, src.row_node, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(), R->vals.as<int>(),
+        R->tiles.as<int>(), R->bad.as<int>(), stats);
+  } else {
+    preprocess_kernel<<<nb, TB, 0, st>>>(src.attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
+                                         R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>(), stats);
+  }
   CK(cudaGetLastError());
   unsigned char* hp = static_cast<unsigned char*>(R->host_pin.p);
   CK(launch_readback(hp, R->bad.p, 64, st));
@@ -1097,9 +1211,31 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   CK(cudaGetLastError());
   const int TB = 128;
   count_launch();
-  preprocess_bwd_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->attrs, n, cam, R->tiles.as<int>(),
-                                                               R->g2.as<double>(), grads);
+  if (R->plan_src) {
+    preprocess_bwd_plan_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->src.plan, n, cam, R->tiles.as<int>(),
+                                                                      R->g2.as<double>(), grads);
+  } else {
+    preprocess_bwd_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->src.attrs, n, cam, R->tiles.as<int>(),
+                                                                 R->g2.as<double>(), grads);
+  }
   return cudaGetLastError();
+}
+
+cudaError_t raster_forward(RasterCtx* R, const double* attrs, long long n, const glod_camera& cam,
+                           float* image, cudaStream_t st) {
+  AttrSrc a{};
+  a.attrs = attrs;
+  a.n = n;
+  return raster_forward_src(R, a, false, cam, image, st);
+}
+
+cudaError_t raster_forward_plan(RasterCtx* R, const glod_gather_plan& plan, int* row_node,
+                                const glod_camera& cam, float* image, cudaStream_t st) {
+  AttrSrc a{};
+  a.n = (long long)plan.n_upper + plan.n_pass + plan.n_sel;
+  a.plan = plan;
+  a.row_node = row_node;
+  return raster_forward_src(R, a, true, cam, image, st);
 }
 
 RasterCtx* raster_create() { return new RasterCtx(); }

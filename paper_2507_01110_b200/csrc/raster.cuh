@@ -33,6 +33,11 @@ RasterCtx* raster_create();
 void raster_destroy(RasterCtx* r);
 cudaError_t raster_forward(RasterCtx* r, const double* attrs, long long n, const glod_camera& cam,
                            float* image, cudaStream_t st);
+// The same forward reading render row r straight from its gather-plan
+// source (gather.cuh row_source) and writing row_node[r]; the plan's device
+// arrays must stay unchanged until the matching raster_backward.
+cudaError_t raster_forward_plan(RasterCtx* r, const glod_gather_plan& plan, int* row_node,
+                                const glod_camera& cam, float* image, cudaStream_t st);
 cudaError_t raster_backward(RasterCtx* r, const float* dimg, double* grads, cudaStream_t st);
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 void raster_stats(const RasterCtx* r, glod_render_stats* out);

@@ -109,6 +109,23 @@ class Rasterizer:
                                                   _lib.stream_ptr(stream)))
         return image
 
+    def forward_plan(self, plan, row_node: torch.Tensor, n: int, cam: Camera, image: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+        """`forward` of the render set a gather plan describes, read in place
+        (glod_render_forward_plan: the K4 gather fused into the preprocess);
+        fills row_node.  The plan's arrays must stay valid until `backward`."""
+        w, h = cam.resolution
+        if image is None:
+            image = torch.empty((h, w, 3), dtype=torch.float32, device=row_node.device)
+        self._cam_struct = camera_struct(cam)
+        self.cam = cam
+        self.last_n = int(n)
+        self._attrs = (plan, row_node)
+        _lib.check(_lib.lib().glod_render_forward_plan(self._h, C.byref(plan), _lib.ptr(row_node),
+                                                       C.byref(self._cam_struct), _lib.ptr(image),
+                                                       _lib.stream_ptr(stream)))
+        return image
+
     def backward(self, dl_dimage: torch.Tensor, grads: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         if grads is None:
             grads = torch.empty(23 * max(self.last_n, 1), dtype=torch.float64, device=dl_dimage.device)

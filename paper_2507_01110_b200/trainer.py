@@ -74,6 +74,10 @@ class TrainConfig:
     skybox_points: int = 0                  # initialize() only (host)
     size_threshold: float | None = None     # initialize() only (host)
     min_subtree: int = 32                   # hspt.DEFAULT_MIN_SUBTREE
+    # the rasteriser reads the render rows in place through the gather plan
+    # (glod_render_forward_plan) instead of a K4-gathered packed copy; the
+    # values, image and gradients are the same (not in the reference)
+    fuse_gather: bool = True
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -494,7 +498,8 @@ class Trainer:
         self._mark("compact")
         n_sel = int(self._h_total[0])
         R = n_up + n_pa + n_sel
-        rows = self._ensure("_rows", FLOATS_PER_GAUSSIAN * R, torch.float64)[:FLOATS_PER_GAUSSIAN * R]
+        rows = None if self.cfg.fuse_gather else \
+            self._ensure("_rows", FLOATS_PER_GAUSSIAN * R, torch.float64)[:FLOATS_PER_GAUSSIAN * R]
         row_node = self._ensure("_row_node", R, torch.int32)[:max(R, 1)]
         plan = _lib.GatherPlan(
             master=_lib.ptr(sc.records), capacity=sc.cap, upper_ids=_lib.ptr(sel.upper),
@@ -502,8 +507,12 @@ class Trainer:
             sel_seg=_lib.ptr(cmp.sel_seg), sel_pos=_lib.ptr(cmp.sel_pos), sel_node=_lib.ptr(cmp.sel_node),
             n_sel=n_sel, seg_block=_lib.ptr(self._d_blk), seg_rows=_lib.ptr(self._d_blk[S1:]),
             master_stride=NODE_RECORD, spt_from_master=int(self.spt_from_master))
-        _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
-                                                      _lib.stream_ptr()))
+        self._plan, self._plan_R = plan, R
+        if self.cfg.fuse_gather:
+            rows = None          # the forward reads the rows through the plan
+        else:
+            _lib.check(_lib.lib().glod_gather_render_rows(C.byref(plan), _lib.ptr(rows), _lib.ptr(row_node),
+                                                          _lib.stream_ptr()))
         self._mark("gather")
         self.last_stats = {"n_upper": n_up, "n_pass": n_pa, "n_spt": n_sp,
                            "prefix_total": int(prefix.sum()) if n_sp else 0}
@@ -511,6 +520,22 @@ class Trainer:
                     "cache_hits": int(hits),
                     "bytes_streamed": int(loaded * sc.store.bytes_per_gaussian)}
         return R, rows, row_node, plan, None, counters
+
+    def _forward(self, rows, row_node, plan, R: int, cam: Camera, image: torch.Tensor | None = None):
+        if rows is None:
+            return self.rast.forward_plan(plan, row_node, R, cam, image=image)
+        return self.rast.forward(rows, R, cam, image=image)
+
+    def gathered_rows(self) -> torch.Tensor:
+        """Packed f64 render rows of the last view (K4 gather of its plan,
+        23·R values) — what the rasteriser read.  After a train step the
+        plan's sources hold the updated parameters."""
+        R = self._plan_R
+        rows = self._ensure("_rows", FLOATS_PER_GAUSSIAN * max(R, 1), torch.float64)
+        row_node = self._ensure("_row_node", max(R, 1), torch.int32)
+        _lib.check(_lib.lib().glod_gather_render_rows(C.byref(self._plan), _lib.ptr(rows), _lib.ptr(row_node),
+                                                      _lib.stream_ptr()))
+        return rows[:FLOATS_PER_GAUSSIAN * R]
 
     def render_view(self, view: int, image: torch.Tensor | None = None,
                     next_view: int | None = None) -> torch.Tensor:
@@ -522,8 +547,8 @@ class Trainer:
         counters are unchanged."""
         cam, _ = self.views[view]
         self._next_view = next_view if self.cfg.prefetch else None
-        R, rows, _, _, _, counters = self._gather_view(cam, view)
-        img = self.rast.forward(rows, R, cam, image=image)
+        R, rows, row_node, plan, _, counters = self._gather_view(cam, view)
+        img = self._forward(rows, row_node, plan, R, cam, image=image)
         self.cache.end_step(-1, mark_dirty=False)
         self._prefetch_next()
         self._mark("forward")
@@ -563,7 +588,7 @@ class Trainer:
         R, rows, row_node, plan, _, counters = self._gather_view(cam, self.current_view)
         L = _lib.lib()
         st = _lib.stream_ptr()
-        image = self.rast.forward(rows, R, cam)
+        image = self._forward(rows, row_node, plan, R, cam)
         self._mark("forward")
         if tgt_ready is not None:
             torch.cuda.current_stream().wait_event(tgt_ready)

@@ -136,7 +136,7 @@ def _render_and_check(tr, h, hs, cfg, cam, view, rows=None, tag=""):
     rs = oracle_cut(h, hs, cfg, cam)
     want_ids = np.concatenate([rs["upper"], rs["passthrough"]] + list(rs["selected"])).astype(np.int64)
     np.testing.assert_array_equal(ids, want_ids, err_msg=f"{tag} render-row ids")
-    A = AttributeArrays.from_packed(tr._rows[:23 * R].cpu().numpy(), R)
+    A = AttributeArrays.from_packed(tr.gathered_rows().cpu().numpy(), R)
     n_mem = rs["upper"].size + rs["passthrough"].size
     for k in NAMES:   # upper/passthrough rows from the f64 master, SPT rows f32 from the store
         src = np.asarray(getattr(h.attrs, k))[want_ids]

@@ -286,3 +286,50 @@ def test_disk_store_matches_host_store(tmp_path):
     assert same_state(a.scene.mv, b.scene.mv)
     for sa_, sb_ in zip(a.scene.store.sections, b.scene.store.sections):
         assert same_state(sa_, sb_)
+
+
+def test_fused_gather_matches_gathered_rows():
+    """glod_render_forward_plan (the K4 gather fused into the preprocess:
+    render rows read in place from the master records and cache blocks,
+    touched rows from the master) against the rasteriser on the K4-gathered
+    packed copy: identical images, losses, gradients, row node ids and
+    parameters over 12 train steps (misses, hits, flushes), and identical
+    render_view frames (gradients and parameters up to the fp64-atomic
+    ordering of the backward blend, see same_state)."""
+    a, _, _ = make_case()
+    b, _, _ = make_case()
+    a.cfg.fuse_gather = True
+    b.cfg.fuse_gather = False
+    for it in range(1, 13):
+        ra, rb = a.train_step(it), b.train_step(it)
+        la, lb = ra.pop("loss"), rb.pop("loss")
+        assert ra == rb and abs(la - lb) <= 1e-6 * abs(lb), it
+        R = ra["gaussians_rendered"]
+        assert torch.allclose(a._last_image, b._last_image, rtol=0, atol=1e-6), it
+        assert same_state(a._last_grads[:23 * R], b._last_grads[:23 * R]), it
+        assert torch.equal(a._last_rows, b._last_rows), it
+    torch.cuda.synchronize()
+    assert same_state(a.scene.records, b.scene.records)
+    for v in range(len(a.views)):
+        assert torch.allclose(a.render_view(v), b.render_view(v), rtol=0, atol=1e-6), v
+        assert torch.equal(a._row_node[:a._plan_R], b._row_node[:b._plan_R]), v
+        assert same_state(a.gathered_rows(), b.gathered_rows()), v
+
+
+def test_fused_gather_render_bit_identical():
+    """On one state and one plan, the frame rendered through the gather plan
+    equals the frame rendered from the K4-gathered rows of that plan bit for
+    bit (the forward is deterministic; only the backward's fp64 atomics are
+    order-dependent)."""
+    a, _, _ = make_case()
+    for it in range(1, 6):
+        a.train_step(it)
+    a.cfg.fuse_gather = True
+    for v in range(len(a.views)):
+        i1 = a.render_view(v).clone()
+        n1 = a._row_node[:a._plan_R].clone()
+        rows = a.gathered_rows()
+        assert torch.equal(n1, a._row_node[:a._plan_R]), v
+        i2 = a.rast.forward(rows, a._plan_R, a.views[v][0])
+        d = (i1 - i2).abs()
+        assert torch.equal(i1, i2), (v, float(d.max()), int((d > 0).sum()))
