@@ -171,7 +171,10 @@ def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
       adam:      1340 B per row (576-B node record — params, (m, v), step —
                  read and written, grads 184, id 4) + 8 B per SPT row (the
                  touched-bit atomic of the implicit cache-block refresh)
-      gather:    372 B per row (184 read, 184 write, 4 node id)
+      preprocess_plan (K4 gather fused into K5): 216 B per render row
+                 (184-B source row, 12-B plan entry, 4-B node id written,
+                 depth key 8 + index 4 + tile count 4 written; the 48-B
+                 splat records of contributing rows not counted)
 
     `traffic` is the ncu-measured DRAM bytes per launch of the same kernel
     (profiles/ncu_traffic.json, from the committed --set full capture)."""
@@ -215,8 +218,9 @@ def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
         issue_line("blend_fwd_kernel", kt["fwd_alg"], kt["fwd_ms"], "front-to-back compositing, fp64 T"),
         line("adam_records_kernel", kt["adam_alg"], stage_ms.get("adam"),
              "HBM (random 576-B node records); ms = adam stage"),
-        line("gather_rows_t_kernel", kt["gather_alg"], stage_ms.get("gather"),
-             "HBM (sparse rows); ms = gather stage"),
+        line("preprocess_plan_kernel", kt["pre_alg"], kt["pre_ms"],
+             "render rows read in place through the gather plan (staged in shared memory) + fp64 "
+             "projection; ms = mean launch duration timed live here"),
     ]
     return main
 
@@ -446,7 +450,7 @@ def run_ours(args):
     if os.environ.get("GLOD_BENCH_STEP_TIMES") == "1":
         tr.host_timing = {}
     npix = args.width * args.height
-    alg = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0, "gather": 0.0}
+    alg = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0, "pre": 0.0}
     n_t = max(3, args.steps // 4)
     for _ in range(n_t):
         it += 1
@@ -456,7 +460,7 @@ def run_ours(args):
         alg["fwd"] += inst * 52 + npix * 24
         alg["bwd"] += inst * 52 + npix * 24 + R * 144
         alg["adam"] += R * 1340 + n_spt_rows * 8      # + the touched-bit atomic per SPT row
-        alg["gather"] += R * 372
+        alg["pre"] += R * 216
     bt = tr.rast.blend_timing(False)
     stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
     if tr.host_timing is not None:
@@ -466,7 +470,7 @@ def run_ours(args):
     tr.enable_timing(False)
     kt = {"fwd_ms": bt["fwd_ms"] / max(bt["fwd_launches"], 1), "bwd_ms": bt["bwd_ms"] / max(bt["bwd_launches"], 1),
           "fwd_alg": alg["fwd"] / n_t, "bwd_alg": alg["bwd"] / n_t, "adam_alg": alg["adam"] / n_t,
-          "gather_alg": alg["gather"] / n_t}
+          "pre_ms": bt["pre_ms"] / max(bt["pre_launches"], 1), "pre_alg": alg["pre"] / n_t}
     stats = dict(tr.last_stats)
     stats["rendered"] = recs[-1]["gaussians_rendered"]
     # ---- render FPS (cut + cache gather + forward) ------------------------

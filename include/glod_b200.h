@@ -212,6 +212,9 @@ int glod_render_stats_get(const glod_raster* r, glod_render_stats* out);
  * launches_out[2]; then enable >= 0 resets the sums and turns timing on
  * (1) or off (0); enable < 0 leaves both as they are. */
 int glod_render_blend_timing(glod_raster* r, int32_t enable, double* ms_out, int64_t* launches_out);
+/* The same with the preprocess kernel (K5, or K4+K5 fused) as a third
+ * entry: ms_out[3], launches_out[3]. */
+int glod_render_kernel_timing(glod_raster* r, int32_t enable, double* ms_out, int64_t* launches_out);
 
 /* Replaces loss (renderer.py:322-360): (1-lam)*L1 + lam*(1-SSIM), 11-tap
  * sigma=1.5 window, zero padding.  rendered/target/grad: [dev] f32

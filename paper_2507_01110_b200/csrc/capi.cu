@@ -180,11 +180,20 @@ int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, 
 int glod_render_blend_timing(glod_raster* r, int32_t enable, double* ms_out, int64_t* launches_out) {
   if (!r) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   long long n[2] = {0, 0};
-  glod::raster_timing_collect(r->ctx, enable, ms_out, ms_out ? ms_out + 1 : nullptr, n);
+  glod::raster_timing_collect(r->ctx, enable, ms_out, n, 2);
   if (launches_out) {
     launches_out[0] = n[0];
     launches_out[1] = n[1];
   }
+  return GLOD_OK;
+}
+
+int glod_render_kernel_timing(glod_raster* r, int32_t enable, double* ms_out, int64_t* launches_out) {
+  if (!r) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  long long n[3] = {0, 0, 0};
+  glod::raster_timing_collect(r->ctx, enable, ms_out, n, 3);
+  if (launches_out)
+    for (int k = 0; k < 3; ++k) launches_out[k] = n[k];
   return GLOD_OK;
 }
 

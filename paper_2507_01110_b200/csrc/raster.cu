@@ -959,6 +959,8 @@ struct Buf {
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+constexpr int kTimed = 3;   // timed kernels: blend_fwd, blend_bwd, preprocess
+
 struct RasterCtx {
   Buf splats, sorted, keys, keys2, vals, vals2, tiles, tiles_sorted, offs;
   Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin;
@@ -973,18 +975,19 @@ struct RasterCtx {
   bool have_forward = false;
   const unsigned* ikey_sorted = nullptr;
   const int* ival_sorted = nullptr;
-  // optional CUDA-event timing of the two blend kernels (bench.py roofline)
+  // optional CUDA-event timing of the two blend kernels and the preprocess
+  // (bench.py roofline)
   bool timing = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-  double blend_ms[2] = {0.0, 0.0};
-  long long blend_n[2] = {0, 0};
-  bool pending[2] = {false, false};
+  cudaEvent_t ev[2 * kTimed] = {};
+  double blend_ms[kTimed] = {};
+  long long blend_n[kTimed] = {};
+  bool pending[kTimed] = {};
 };
 
 static void timing_begin(RasterCtx* R, int k, cudaStream_t st) {
   if (!R->timing) return;
   if (!R->ev[0])
-    for (int i = 0; i < 4; ++i) cudaEventCreate(&R->ev[i]);
+    for (int i = 0; i < 2 * kTimed; ++i) cudaEventCreate(&R->ev[i]);
   cudaEventRecord(R->ev[2 * k], st);
 }
 
@@ -995,8 +998,8 @@ static void timing_end(RasterCtx* R, int k, cudaStream_t st) {
 }
 
 // Accumulate the finished launches' durations (synchronises on the events).
-void raster_timing_collect(RasterCtx* R, int enable, double* fwd_ms, double* bwd_ms, long long* n) {
-  for (int k = 0; k < 2; ++k)
+void raster_timing_collect(RasterCtx* R, int enable, double* ms_out, long long* n, int nk) {
+  for (int k = 0; k < kTimed; ++k)
     if (R->pending[k]) {
       float ms = 0.f;
       cudaEventSynchronize(R->ev[2 * k + 1]);
@@ -1006,13 +1009,16 @@ void raster_timing_collect(RasterCtx* R, int enable, double* fwd_ms, double* bwd
       }
       R->pending[k] = false;
     }
-  if (fwd_ms) *fwd_ms = R->blend_ms[0];
-  if (bwd_ms) *bwd_ms = R->blend_ms[1];
-  if (n) { n[0] = R->blend_n[0]; n[1] = R->blend_n[1]; }
+  for (int k = 0; k < nk && k < kTimed; ++k) {
+    if (ms_out) ms_out[k] = R->blend_ms[k];
+    if (n) n[k] = R->blend_n[k];
+  }
   if (enable >= 0) {
     R->timing = enable != 0;
-    R->blend_ms[0] = R->blend_ms[1] = 0.0;
-    R->blend_n[0] = R->blend_n[1] = 0;
+    for (int k = 0; k < kTimed; ++k) {
+      R->blend_ms[k] = 0.0;
+      R->blend_n[k] = 0;
+    }
   }
 }
 
@@ -1081,6 +1087,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
   const int TB = 256;
   const int nb = int((n + TB - 1) / TB);
   count_launch();
+  timing_begin(R, 2, st);
   if (plan) {
     static bool smem_set = false;
     if (!smem_set) {
@@ -1094,6 +1101,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
     preprocess_kernel<<<nb, TB, 0, st>>>(src.attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
                                          R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>(), stats);
   }
+  timing_end(R, 2, st);
   CK(cudaGetLastError());
   unsigned char* hp = static_cast<unsigned char*>(R->host_pin.p);
   CK(launch_readback(hp, R->bad.p, 64, st));
@@ -1263,7 +1271,7 @@ void raster_destroy(RasterCtx* R) {
                 &R->tfinal, &R->last, &R->g2, &R->temp, &R->bad};
   for (Buf* b : all) b->release(st);
   if (R->host_pin.p) cudaFreeHost(R->host_pin.p);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 2 * kTimed; ++i)
     if (R->ev[i]) cudaEventDestroy(R->ev[i]);
   if (R->ev_runs) cudaEventDestroy(R->ev_runs);
   delete R;

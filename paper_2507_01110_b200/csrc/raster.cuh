@@ -42,6 +42,6 @@ cudaError_t raster_backward(RasterCtx* r, const float* dimg, double* grads, cuda
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 void raster_stats(const RasterCtx* r, glod_render_stats* out);
 bool raster_bad_input(const RasterCtx* r, int* section, int* index);
-void raster_timing_collect(RasterCtx* r, int enable, double* fwd_ms, double* bwd_ms, long long* n);
+void raster_timing_collect(RasterCtx* r, int enable, double* ms_out, long long* n, int nk);
 
 }  // namespace glod

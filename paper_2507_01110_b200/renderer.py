@@ -136,11 +136,12 @@ class Rasterizer:
     def blend_timing(self, enable: bool | None = None) -> dict:
         """CUDA-event durations of the blend kernels since the last call
         (measurement only); `enable` then resets and switches timing."""
-        ms = (C.c_double * 2)()
-        n = (C.c_int64 * 2)()
-        _lib.check(_lib.lib().glod_render_blend_timing(self._h, -1 if enable is None else int(bool(enable)),
-                                                       ms, n))
-        return {"fwd_ms": ms[0], "bwd_ms": ms[1], "fwd_launches": n[0], "bwd_launches": n[1]}
+        ms = (C.c_double * 3)()
+        n = (C.c_int64 * 3)()
+        _lib.check(_lib.lib().glod_render_kernel_timing(self._h, -1 if enable is None else int(bool(enable)),
+                                                        ms, n))
+        return {"fwd_ms": ms[0], "bwd_ms": ms[1], "fwd_launches": n[0], "bwd_launches": n[1],
+                "pre_ms": ms[2], "pre_launches": n[2]}
 
     def stats(self) -> dict:
         s = _lib.RenderStats()
