@@ -5,8 +5,11 @@
 //                SPT, cache-block rows at the cut positions (AttributeArrays
 //                .take + concat, core.py:120-159) — one transposing kernel;
 //                a block row whose touched bit is set is read from the master
-//                (the implicit refresh of trainer.py:363, see block_bits)
-//  materialize   touched rows → block before a write-back / overlay
+//                (the implicit refresh of trainer.py:363, see block_bits);
+//                the train/render step fuses it into the rasteriser's
+//                preprocess instead (raster.cu preprocess_plan_kernel)
+//  materialize   touched rows → block (glod_cache_materialize: host reads of
+//                a block; write-back and overlay take them on the fly)
 //  scatter_back  explicit block[pos] = master[node] (public C-ABI)
 //  convert       f32 store prefix ↔ f64 cache block (store.py:334,330)
 #include <string.h>
