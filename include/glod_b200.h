@@ -200,6 +200,16 @@ int glod_raster_destroy(glod_raster* r);
 int glod_render_forward(glod_raster* r, const double* attrs, int64_t n,
                         const glod_camera* cam, float* image, void* stream);
 
+/* Frame pipelining (no reference counterpart; same images): with deferral
+ * enabled, glod_render_forward(_plan) enqueues everything up to the
+ * compositing kernel and returns; glod_render_blend enqueues the blend of
+ * that forward (GLOD_ERR_INVALID_ARGUMENT if none is pending).  A caller
+ * puts independent work — the next frame's LoD select — between the two so
+ * its host read-back is not queued behind the blend.  glod_render_backward
+ * fails while a blend is pending. */
+int glod_render_defer_blend(glod_raster* r, int32_t enable);
+int glod_render_blend(glod_raster* r, void* stream);
+
 /* Replaces backward (renderer.py:197-304) for the last forward call.
  * dl_dimage: [dev] f32 (height, width, 3).  grads: [dev] packed f64 block
  * of n rows (same layout as attrs; raw scale/opacity, not log/logit). */

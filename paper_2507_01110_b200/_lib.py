@@ -122,6 +122,8 @@ SIGNATURES = {
     "glod_render_stats_get": (C.c_int, [P, C.POINTER(RenderStats)]),
     "glod_render_blend_timing": (C.c_int, [P, C.c_int32, P, P]),
     "glod_render_kernel_timing": (C.c_int, [P, C.c_int32, P, P]),
+    "glod_render_defer_blend": (C.c_int, [P, C.c_int32]),
+    "glod_render_blend": (C.c_int, [P, P]),
     "glod_loss_scratch_bytes": (C.c_int64, [C.c_int32, C.c_int32]),
     "glod_loss_l1_ssim": (C.c_int, [P, P, C.c_int32, C.c_int32, C.c_double, P, P, P, C.c_int64, P]),
     "glod_adam_step": (C.c_int, [P, P, P, C.c_int64, P, P, P, C.c_int64, C.c_int64,

@@ -171,6 +171,19 @@ int glod_render_forward_plan(glod_raster* r, const glod_gather_plan* plan, int32
   return render_result(r, e, "glod_render_forward_plan");
 }
 
+int glod_render_defer_blend(glod_raster* r, int32_t enable) {
+  if (!r) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  glod::raster_set_defer_blend(r->ctx, enable != 0);
+  return GLOD_OK;
+}
+
+int glod_render_blend(glod_raster* r, void* stream) {
+  if (!r) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
+  cudaError_t e = glod::raster_blend(r->ctx, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorInvalidValue) return fail(GLOD_ERR_INVALID_ARGUMENT, "no deferred blend pending");
+  return check(e, "glod_render_blend");
+}
+
 int glod_render_backward(glod_raster* r, const float* dl_dimage, double* grads, void* stream) {
   if (!r || !dl_dimage || !grads) return fail(GLOD_ERR_INVALID_ARGUMENT, "null argument");
   return check(glod::raster_backward(r->ctx, dl_dimage, grads, static_cast<cudaStream_t>(stream)),

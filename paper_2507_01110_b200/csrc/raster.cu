@@ -973,6 +973,8 @@ struct RasterCtx {
   int bad_section = -1, bad_index = -1;
   cudaStream_t stream = nullptr;
   bool have_forward = false;
+  bool defer_blend = false, blend_pending = false;   // raster_set_defer_blend / raster_blend
+  float* blend_image = nullptr;
   const unsigned* ikey_sorted = nullptr;
   const int* ival_sorted = nullptr;
   // optional CUDA-event timing of the two blend kernels and the preprocess
@@ -1034,6 +1036,40 @@ static int bits_for(long long v) {
     if (_e != cudaSuccess) return _e;           \
   } while (0)
 
+// K7 of the last forward (its ranges, sorted splats and instance list).
+static cudaError_t blend_forward(RasterCtx* R, float* image, cudaStream_t st) {
+  const CamD& cam = R->cam;
+  count_launch();
+  timing_begin(R, 0, st);
+  blend_fwd_kernel<<<cam.tw * cam.th, kFwdTB, 0, st>>>(R->n_inst > 0 ? R->sorted.as<Splat>() : nullptr,
+                                                      R->n_inst > 0 ? R->ival_sorted : nullptr,
+                                                      R->range.as<int2>(), cam, image, R->tfinal.as<double>(),
+                                                      R->last.as<int>());
+  timing_end(R, 0, st);
+  return cudaGetLastError();
+}
+
+// With blend deferral on (raster_set_defer_blend), the forward stops before
+// K7 and raster_blend enqueues it: a caller can put other work (the next
+// frame's LoD select) between the tile sort and the blend.
+static cudaError_t blend_or_defer(RasterCtx* R, float* image, cudaStream_t st) {
+  if (R->defer_blend) {
+    R->blend_image = image;
+    R->blend_pending = true;
+    return cudaSuccess;
+  }
+  R->blend_pending = false;
+  return blend_forward(R, image, st);
+}
+
+void raster_set_defer_blend(RasterCtx* R, bool on) { R->defer_blend = on; }
+
+cudaError_t raster_blend(RasterCtx* R, cudaStream_t st) {
+  if (!R->blend_pending) return cudaErrorInvalidValue;
+  R->blend_pending = false;
+  return blend_forward(R, R->blend_image, st);
+}
+
 static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool plan, const glod_camera& c,
                                float* image, cudaStream_t st) {
   const long long n = src.n;
@@ -1057,10 +1093,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
     R->n_inst = 0;
     R->n_visible = 0;
     // T=1 everywhere, no contributors: the blend kernel writes exactly that
-    count_launch();
-    blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(nullptr, nullptr, R->range.as<int2>(), cam,
-                                                         image, R->tfinal.as<double>(), R->last.as<int>());
-    return cudaGetLastError();
+    return blend_or_defer(R, image, st);
   }
   CK(R->splats.ensure(sizeof(Splat) * n, st));
   CK(R->sorted.ensure(sizeof(Splat) * n, st));
@@ -1163,13 +1196,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
       ranges_kernel<<<int((n_inst + TB - 1) / TB), TB, 0, st>>>(R->ikey_sorted, n_inst, R->range.as<int2>());
       CK(cudaGetLastError());
     }
-    count_launch();
-    timing_begin(R, 0, st);
-    blend_fwd_kernel<<<ntiles, kFwdTB, 0, st>>>(R->sorted.as<Splat>(), R->ival_sorted,
-                                                         R->range.as<int2>(), cam, image,
-                                                         R->tfinal.as<double>(), R->last.as<int>());
-    timing_end(R, 0, st);
-    return cudaGetLastError();
+    return blend_or_defer(R, image, st);
   };
   if (begin_bit == 0) return tail(order);
   count_launch();
@@ -1201,6 +1228,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
 }
 
 cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cudaStream_t st) {
+  if (R->blend_pending) return cudaErrorInvalidValue;     // the deferred blend never ran
   const CamD& cam = R->cam;
   const long long n = R->n;
   if (n == 0) return cudaSuccess;

@@ -38,6 +38,10 @@ cudaError_t raster_forward(RasterCtx* r, const double* attrs, long long n, const
 // arrays must stay unchanged until the matching raster_backward.
 cudaError_t raster_forward_plan(RasterCtx* r, const glod_gather_plan& plan, int* row_node,
                                 const glod_camera& cam, float* image, cudaStream_t st);
+// Blend deferral: while on, raster_forward(_plan) enqueues everything up to
+// the blend; raster_blend enqueues the blend of the last forward.
+void raster_set_defer_blend(RasterCtx* r, bool on);
+cudaError_t raster_blend(RasterCtx* r, cudaStream_t st);
 cudaError_t raster_backward(RasterCtx* r, const float* dimg, double* grads, cudaStream_t st);
 cudaError_t launch_readback(void* host_pinned, const void* src, long long bytes, cudaStream_t st);
 void raster_stats(const RasterCtx* r, glod_render_stats* out);

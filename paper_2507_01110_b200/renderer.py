@@ -126,6 +126,14 @@ class Rasterizer:
                                                        _lib.stream_ptr(stream)))
         return image
 
+    def defer_blend(self, enable: bool):
+        """While on, `forward`/`forward_plan` stop before the compositing
+        kernel; `blend` enqueues it (glod_render_defer_blend)."""
+        _lib.check(_lib.lib().glod_render_defer_blend(self._h, int(bool(enable))))
+
+    def blend(self, stream=None):
+        _lib.check(_lib.lib().glod_render_blend(self._h, _lib.stream_ptr(stream)))
+
     def backward(self, dl_dimage: torch.Tensor, grads: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         if grads is None:
             grads = torch.empty(23 * max(self.last_n, 1), dtype=torch.float64, device=dl_dimage.device)

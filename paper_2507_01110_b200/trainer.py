@@ -78,6 +78,11 @@ class TrainConfig:
     # (glod_render_forward_plan) instead of a K4-gathered packed copy; the
     # values, image and gradients are the same (not in the reference)
     fuse_gather: bool = True
+    # render_view(view, next_view): the next frame's LoD select is enqueued
+    # between this frame's tile sort and its blend, so the next call's cache
+    # decisions run on the host while this blend runs (not in the reference;
+    # images and counters unchanged)
+    pipeline_render: bool = True
 
     def __post_init__(self):
         for name, lr in self.learning_rates.items():
@@ -251,6 +256,8 @@ class Trainer:
         self._sel_ev = self._spec_ev = None
         self._h_sel2 = torch.empty(4 + 4 * S1, dtype=torch.int32).pin_memory()
         self._h_droot2 = torch.empty(S1, dtype=torch.float64).pin_memory()
+        self._presel = None                  # (view, SelectResult) enqueued by render_view
+        self._pipelined = False
         self._spt_of_node = None
 
     def train(self, metrics_out=None) -> list:
@@ -387,36 +394,58 @@ class Trainer:
         return t
 
     # ------------------------------------------------------------------
-    def select(self, cam: Camera, spec_cam: Camera | None = None):
+    def select(self, cam: Camera, spec_cam: Camera | None = None, pre=None):
         """LoD select + one D2H of the per-SPT table (the step's host sync).
         With `spec_cam`, a speculative select of that (predicted next) view
         is enqueued after the read-back the host waits for, so it runs on
         the GPU while the host makes this step's cache decisions; its
         per-SPT table is read later (`_spec_table`, before the prefetch)."""
         sc = self.scene
-        sel = sc.lod.select(cam, self.cfg.lod, cull=True, frustum=self._frustum(cam))
         S1 = max(sc.lod.S, 1)
-        # kernel-written read-backs: never queue behind the write-back DMA
-
-        def read(sel, h, hd):
-            _lib.readback_multi([(h[:4], sel.counts[:4]), (h[4:4 + S1], sel.spt_ids[:S1]),
-                                 (h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1]), (hd, sel.d_root[:S1])])
-
-        read(sel, self._h_sel, self._h_droot)
-        if self._sel_ev is None:
-            self._sel_ev, self._spec_ev = torch.cuda.Event(), torch.cuda.Event()
-        self._sel_ev.record()
-        self._spec = None
-        if spec_cam is not None:
-            read(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True, frustum=self._frustum(spec_cam)),
-                 self._h_sel2, self._h_droot2)
-            self._spec_ev.record()
-            self._spec = "pending"
-        self._sel_ev.synchronize()
-        h = self._h_sel
+        if pre is not None:
+            # enqueued by the previous frame (_preselect): alternate buffers
+            sel = pre
+            self._spec_ev.synchronize()
+            self._spec = None
+            h, hd = self._h_sel2, self._h_droot2
+        else:
+            sel = sc.lod.select(cam, self.cfg.lod, cull=True, frustum=self._frustum(cam))
+            self._read_select(sel, self._h_sel, self._h_droot)
+            if self._sel_ev is None:
+                self._sel_ev, self._spec_ev = torch.cuda.Event(), torch.cuda.Event()
+            self._sel_ev.record()
+            self._spec = None
+            if spec_cam is not None:
+                self._read_select(sc.lod.select(spec_cam, self.cfg.lod, cull=True, alt=True,
+                                                frustum=self._frustum(spec_cam)), self._h_sel2, self._h_droot2)
+                self._spec_ev.record()
+                self._spec = "pending"
+            self._sel_ev.synchronize()
+            h, hd = self._h_sel, self._h_droot
         n_up, n_pa, n_sp = (int(x) for x in h[:3].tolist())
         dev_ids = h[4:4 + n_sp].numpy().astype(np.int64)
-        return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), self._h_droot[:n_sp].numpy()
+        return sel, n_up, n_pa, n_sp, dev_ids, h[4 + S1:4 + S1 + n_sp].numpy(), hd[:n_sp].numpy()
+
+    def _read_select(self, sel, h, hd):
+        """Kernel-written read-back of a select's per-SPT table (never queues
+        behind the write-back DMA)."""
+        S1 = max(self.scene.lod.S, 1)
+        _lib.readback_multi([(h[:4], sel.counts[:4]), (h[4:4 + S1], sel.spt_ids[:S1]),
+                             (h[4 + S1:4 + 2 * S1], sel.prefix_len[:S1]), (hd, sel.d_root[:S1])])
+
+    def _preselect(self, view: int):
+        """Enqueue the LoD select of the next frame's view into the alternate
+        device/host buffers (read by that frame's `select` and, before it,
+        by the prefetch through `_spec_table`)."""
+        sc = self.scene
+        cam = self.views[view][0]
+        sel = sc.lod.select(cam, self.cfg.lod, cull=True, alt=True, frustum=self._frustum(cam))
+        self._read_select(sel, self._h_sel2, self._h_droot2)
+        if self._sel_ev is None:
+            self._sel_ev, self._spec_ev = torch.cuda.Event(), torch.cuda.Event()
+        self._spec_ev.record()
+        self._spec = "pending"
+        self._presel = (view, sel)
 
     def _frustum(self, cam: Camera):
         """Frustum.from_camera, memoised per camera (the host BLAS calls cost
@@ -471,8 +500,11 @@ class Trainer:
         sc = self.scene
         self._mark("start")
         nv = self._next_view
-        spec_cam = self.views[nv][0] if nv is not None and nv != view and nv not in self._hist else None
-        sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam, spec_cam)
+        pre, self._presel = self._presel, None
+        pre = pre[1] if pre is not None and pre[0] == view else None
+        spec_cam = self.views[nv][0] if (nv is not None and nv != view and nv not in self._hist
+                                         and not self._pipelined) else None
+        sel, n_up, n_pa, n_sp, dev_ids, prefix, d_root = self.select(cam, spec_cam, pre=pre)
         self._mark("select")
         spt_ids = sc.lod.spt_perm[dev_ids]
         S1 = max(sc.lod.S, 1)
@@ -484,6 +516,11 @@ class Trainer:
         # the copy engines once this step's backward is queued (train_step)
         # or its frame is rendered (render_view)
         self._pred = self._hist.get(nv, self._spec) if nv is not None else None   # "pending": spec
+        if self._pipelined and self._pred is not None and not isinstance(self._pred, str):
+            # render with a known next view: its misses start copying now,
+            # under this whole frame rather than only its blend
+            self._prefetch_next()
+            self._pred = None
         if n_sp:
             # the prefix at the cached distance is the entry's prefix_len
             self._h_pref.numpy()[:n_sp] = hb[S1:S1 + n_sp]
@@ -547,8 +584,26 @@ class Trainer:
         counters are unchanged."""
         cam, _ = self.views[view]
         self._next_view = next_view if self.cfg.prefetch else None
-        R, rows, row_node, plan, _, counters = self._gather_view(cam, view)
-        img = self._forward(rows, row_node, plan, R, cam, image=image)
+        pipe = self.cfg.pipeline_render and next_view is not None and next_view != view
+        self._pipelined = pipe
+        try:
+            R, rows, row_node, plan, _, counters = self._gather_view(cam, view)
+        finally:
+            self._pipelined = False
+        if pipe:
+            # this frame up to its tile sort, the next frame's select, then
+            # this frame's blend: the next call's cache decisions overlap it
+            self.rast.defer_blend(True)
+            try:
+                img = self._forward(rows, row_node, plan, R, cam, image=image)
+            finally:
+                self.rast.defer_blend(False)
+            self._preselect(next_view)
+            self.rast.blend()
+            if self.cfg.prefetch and next_view not in self._hist:
+                self._pred = "pending"          # the preselect's table (_spec_table)
+        else:
+            img = self._forward(rows, row_node, plan, R, cam, image=image)
         self.cache.end_step(-1, mark_dirty=False)
         self._prefetch_next()
         self._mark("forward")

@@ -333,3 +333,48 @@ def test_fused_gather_render_bit_identical():
         i2 = a.rast.forward(rows, a._plan_R, a.views[v][0])
         d = (i1 - i2).abs()
         assert torch.equal(i1, i2), (v, float(d.max()), int((d > 0).sum()))
+
+
+def test_pipelined_render_matches():
+    """render_view(view, next_view) with the next frame's select enqueued
+    between this frame's tile sort and its blend (TrainConfig.pipeline_render)
+    against the unpipelined path: identical frames and counters, also when
+    the announced next view is not the one rendered next (the preselect is
+    dropped) or no next view is given."""
+    a, _, _ = make_case(budget_frac=0.3)
+    b, _, _ = make_case(budget_frac=0.3)
+    b.cfg.pipeline_render = False
+    n = len(a.views)
+    seq = [(3 * f) % n for f in range(14)]
+    for f, v in enumerate(seq):
+        nv = seq[f + 1] if f + 1 < len(seq) else None
+        if f == 6:
+            nv = (v + 1) % n if (v + 1) % n != seq[f + 1] else (v + 2) % n   # wrong guess
+        if f == 9:
+            nv = None
+        ia = a.render_view(v, next_view=nv)
+        ib = b.render_view(v, next_view=nv)
+        assert a.last_render == b.last_render, f
+        assert torch.equal(ia, ib), f
+    torch.cuda.synchronize()
+
+
+def test_deferred_blend_capi():
+    """glod_render_defer_blend / glod_render_blend: the deferred frame equals
+    the direct one; a blend with none pending and a backward before the
+    deferred blend are refused."""
+    from paper_2507_01110_b200 import _lib
+    a, _, _ = make_case()
+    a.train_step(1)
+    rows = a.gathered_rows()
+    R, cam = a._plan_R, a.views[a.current_view][0]
+    want = a.rast.forward(rows, R, cam).clone()
+    a.rast.defer_blend(True)
+    img = a.rast.forward(rows, R, cam)
+    a.rast.defer_blend(False)
+    with pytest.raises((_lib.GlodError, ValueError)):
+        a.rast.backward(torch.zeros_like(img))
+    a.rast.blend()
+    assert torch.equal(img, want)
+    with pytest.raises((_lib.GlodError, ValueError)):
+        a.rast.blend()

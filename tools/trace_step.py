@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--out", default="gpurun_out/trace.json")
+    ap.add_argument("--render", action="store_true", help="trace render_view frames (next view known)")
     a = ap.parse_args()
     args = bench.parse_args_for_tools(leaves=a.leaves)
     h, hs, cfg, cams, E, _ = bench.make_workload(args, device="cuda")
@@ -37,11 +38,18 @@ def main():
         tr.train_step(it)
     torch.cuda.synchronize()
     acts = [torch.profiler.ProfilerActivity.CPU, torch.profiler.ProfilerActivity.CUDA]
+    nv = len(cams)
+    if a.render:
+        for f in range(3):
+            tr.render_view(f % nv, next_view=(f + 1) % nv)
     with torch.profiler.profile(activities=acts) as prof:
-        for _ in range(a.steps):
+        for f in range(a.steps):
             it += 1
             with torch.profiler.record_function(f"step{it}"):
-                tr.train_step(it)
+                if a.render:
+                    tr.render_view((3 + f) % nv, next_view=(4 + f) % nv)
+                else:
+                    tr.train_step(it)
         torch.cuda.synchronize()
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     prof.export_chrome_trace(a.out)
