@@ -482,14 +482,29 @@ __global__ void __launch_bounds__(1024)
 segscan_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws, int with_prefix) {
   __shared__ long long sm[1024 / 32 + 1];
   const int n_spt = *in.n_spt;
-  if (with_prefix) {
+  // known prefix lengths (the select's): one thread per SPT, the length
+  // computed in the scan loop itself; else a warp per SPT searches first
+  const bool known = with_prefix && in.known_prefix;
+  if (with_prefix && !known) {
     for (long long j = threadIdx.x >> 5; j < n_spt; j += blockDim.x >> 5) spt_prefix<K>(sc, in, out, j, threadIdx.x & 31);
     __syncthreads();
   }
   long long carry = 0;
   for (int base = 0; base < n_spt; base += blockDim.x) {
     const int j = base + threadIdx.x;
-    const long long len = j < n_spt ? out.seg_start[j] : 0;
+    long long len = 0;
+    if (j < n_spt) {
+      if (known) {
+        const int s = in.spt_ids[j];
+        const int pl = in.known_prefix[j];
+        const int rr = in.dist[j] >= double(static_cast<const K*>(sc.key_self)[sc.spt_offset[s] + sc.spt_root_rec[s]]);
+        out.prefix_len[j] = pl;
+        out.root_rule[j] = rr;
+        len = ((rr ? 1 : pl) + kAlign - 1) / kAlign * kAlign;
+      } else {
+        len = out.seg_start[j];
+      }
+    }
     const long long ex = block_excl_scan(len, sm);
     const long long tot = sm[(blockDim.x + 31) >> 5];
     __syncthreads();
@@ -571,6 +586,48 @@ struct Groups {
     }
   }
 
+  // Fast path, warp-uniform: the warp's whole span lies inside the valid
+  // records of one cached segment without the root rule (the common case
+  // for prefixes longer than a span).  Returns that segment, else -1.
+  static GLOD_DEV int span_segment(const SegCache& c, int nseg, long long w_lo, long long t_hi) {
+    constexpr long long kSpan = 32 * kAlign * G;
+    if (w_lo + kSpan > t_hi) return -1;
+    int a = 0, b = nseg;                         // last cached segment starting <= w_lo
+    while (a < b) { const int m = (a + b) >> 1; if (c.vstart[m] <= w_lo) a = m + 1; else b = m; }
+    const int cur = a - 1;
+    if (cur < 0 || c.rr[cur] || w_lo + kSpan > c.vstart[cur] + c.len[cur]) return -1;
+    return cur;
+  }
+  GLOD_DEV void locate_span(const SegCache& c, int cur, long long w_lo, int lane) {
+    rrmask = 0;
+    const int loc0 = int(w_lo - c.vstart[cur]) + lane * kAlign;
+    const long long off = c.off[cur];
+    const int ln = c.len[cur];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      seg[g] = cur;
+      loc[g] = loc0 + g * (32 * kAlign);
+      len[g] = ln;
+      addr[g] = off + loc[g];
+    }
+  }
+  // every record of every group valid and in segment `cur`
+  GLOD_DEV void evaluate_span(const LodScene& sc, const SegCache& c, int cur) {
+    const K* key_self = static_cast<const K*>(sc.key_self);
+    K kv[G][kAlign];
+#pragma unroll
+    for (int g = 0; g < G; ++g) load4(key_self, addr[g], kv[g]);
+    const double d = c.d[cur];
+    const float df = c.df[cur];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      unsigned m = 0;
+#pragma unroll
+      for (int e = 0; e < kAlign; ++e) m |= key_le(kv[g][e], d, df) ? (1u << e) : 0u;
+      mask[g] = m;
+    }
+  }
+
   // the keys of every group (all loads issued first), then the masks
   GLOD_DEV void evaluate(const LodScene& sc, const CompactIn& in, const SegCache& c) {
     const K* key_self = static_cast<const K*>(sc.key_self);
@@ -605,6 +662,7 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   __shared__ SegCache c;
   __shared__ long long sub_cnt[kSubTiles][kCWarps];
   __shared__ unsigned masks[kSubTiles][kCThreads];
+  __shared__ int2 stage[kCWarps][kWarpRecs];        // pass B staging (span path)
   __shared__ unsigned int tile_sh;
   __shared__ int j0_sh;
   __shared__ long long excl_sh;
@@ -662,9 +720,15 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
 #pragma unroll 1
     for (int st = 0; st < nsub; ++st) {
       Groups<K, G> gr;
-      gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt,
-                t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs, t_hi, lane);
-      gr.evaluate(sc, in, c);
+      const long long w_lo = t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs;
+      const int span = Groups<K, G>::span_segment(c, nseg, w_lo, t_hi);
+      if (span >= 0) {
+        gr.locate_span(c, span, w_lo, lane);
+        gr.evaluate_span(sc, c, span);
+      } else {
+        gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt, w_lo, t_hi, lane);
+        gr.evaluate(sc, in, c);
+      }
       int cnt = 0;
       unsigned packed_mask = 0;
 #pragma unroll
@@ -722,8 +786,10 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
         st_tot += sub_cnt[st][w];
       }
       Groups<K, G> gr;
-      gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt,
-                t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs, t_hi, lane);
+      const long long w_lo = t_lo + (long long)st * kSubTile + (long long)warp * kWarpRecs;
+      const int span = Groups<K, G>::span_segment(c, nseg, w_lo, t_hi);
+      if (span >= 0) gr.locate_span(c, span, w_lo, lane);
+      else gr.locate(sc, in, out, c, j0, nseg, cache_end, n_spt, w_lo, t_hi, lane);
       const unsigned packed_mask = masks[st][threadIdx.x];
 #pragma unroll
       for (int g = 0; g < G; ++g) gr.mask[g] = (packed_mask >> (kAlign * g)) & ((1u << kAlign) - 1u);
@@ -753,8 +819,38 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
           else nd[g] = *reinterpret_cast<const int4*>(sc.rec_node + gr.addr[g]);
         }
       }
-      long long gsum = 0;
       const long long base = run + w_off;
+      if (span >= 0) {
+        // one segment: (pos, node) staged at their warp-local ranks, then
+        // the warp's run written with consecutive lanes on consecutive
+        // outputs (coalesced, one store per array per 32 selections)
+        int2* sb = stage[warp];
+        int gs = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const unsigned x = (incl[g >> 2] >> (8 * (g & 3))) & 0xffu;
+          const unsigned cg = (packed[g >> 2] >> (8 * (g & 3))) & 0xffu;
+          const int gt = int(__shfl_sync(0xffffffffu, x, 31));
+          int o = gs + int(x - cg);
+          const int n4[4] = {nd[g].x, nd[g].y, nd[g].z, nd[g].w};
+#pragma unroll
+          for (int e = 0; e < kAlign; ++e)
+            if (gr.mask[g] & (1u << e)) sb[o++] = make_int2(gr.loc[g] + e, n4[e]);
+          gs += gt;
+        }
+        __syncwarp();
+        const int j = j0 + span;
+        for (int k = lane; k < gs; k += 32) {
+          const int2 v = sb[k];
+          out.sel_seg[base + k] = j;
+          out.sel_pos[base + k] = v.x;
+          out.sel_node[base + k] = v.y;
+        }
+        __syncwarp();
+        run += st_tot;
+        continue;
+      }
+      long long gsum = 0;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const unsigned x = (incl[g >> 2] >> (8 * (g & 3))) & 0xffu;
