@@ -401,6 +401,9 @@ template <typename K> struct CTile {
   static constexpr int kWarpRecs = 32 * kAlign * G;           // 512 / 256
   static constexpr int kTile = kCWarps * kWarpRecs;           // 2048 / 1024
 };
+#ifndef GLOD_K1_ROUNDS
+#define GLOD_K1_ROUNDS 1   // tiles per CTA the sub-tile count aims at (1 vs 2: 10M records 61 -> 51 us, C4 step 79 -> 70 us; 4 no better)
+#endif
 constexpr int kSubTiles = 8;                                // sub-tiles per look-back tile
 constexpr int kMinTile = 1024;
 constexpr int kSegCache = 128;                               // segments cached per tile
@@ -672,7 +675,7 @@ compact_kernel(LodScene sc, CompactIn in, CompactOut out, CompactScratch ws) {
   // sub-tiles per look-back tile: as many as keep every CTA busy (large
   // inputs amortise the look-back over more records, small ones keep
   // their parallelism)
-  const long long nsub_ll = total / (2ll * gridDim.x * kSubTile);
+  const long long nsub_ll = total / ((long long)GLOD_K1_ROUNDS * gridDim.x * kSubTile);
   const int nsub = int(nsub_ll < 1 ? 1 : (nsub_ll > kSubTiles ? kSubTiles : nsub_ll));
   const long long kTile = (long long)nsub * kSubTile;
   const long long ntiles = (total + kTile - 1) / kTile;
