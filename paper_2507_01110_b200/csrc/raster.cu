@@ -353,6 +353,18 @@ GLOD_DEV void stage_rows(double* __restrict__ tile, const double* const* s_base,
   }
 }
 
+// A render row's resolved source (row_source), kept by the plan forward
+// for the backward: 16 B per row, so the backward reaches the row's values
+// in one dependent load instead of the plan's three (segment → block →
+// touched bit).  The sources cannot change in between: cache decisions
+// precede the forward, and ADAM (which sets touched bits) follows the
+// backward.
+struct __align__(16) RowSrc {
+  const double* base;
+  int rows;       // Src::rows (block rows, or -GLOD_NODE_RECORD)
+  int idx;        // Src::idx (block position, or node id)
+};
+
 constexpr int kPlanRows = 256;
 constexpr size_t kPlanSmem = sizeof(double) * kPlanRows * 23 + (sizeof(void*) + 16) * kPlanRows;
 
@@ -360,7 +372,7 @@ __global__ void __launch_bounds__(kPlanRows, GLOD_PRE_MINB)
 preprocess_plan_kernel(const glod_gather_plan p, long long n, int* __restrict__ row_node, CamD cam,
                        Splat* __restrict__ splats, unsigned long long* __restrict__ keys,
                        int* __restrict__ vals, int* __restrict__ tiles, int* __restrict__ bad,
-                       unsigned long long* __restrict__ stats) {
+                       unsigned long long* __restrict__ stats, RowSrc* __restrict__ rsrc) {
   extern __shared__ __align__(16) double plan_smem[];
   double* tile = plan_smem;                                           // [kPlanRows][23]
   const double** s_base = reinterpret_cast<const double**>(tile + kPlanRows * 23);
@@ -375,6 +387,7 @@ preprocess_plan_kernel(const glod_gather_plan p, long long n, int* __restrict__ 
     s_rows[threadIdx.x] = s.rows;
     s_idx[threadIdx.x] = s.idx;
     row_node[r0 + threadIdx.x] = node;
+    rsrc[r0 + threadIdx.x] = RowSrc{s.base, int(s.rows), int(s.idx)};
   }
   __syncthreads();
   stage_rows<kPlanRows>(tile, s_base, s_rows, s_idx, nr);
@@ -919,18 +932,18 @@ preprocess_bwd_kernel(const double* __restrict__ attrs, long long n, CamD cam, c
   bwd_one(row_view(Src{attrs, n, i}), i, n, cam, g2 + (long long)kG2 * i, grads);
 }
 
-// K9 reading each contributing render row through the gather plan (the
-// forward's preprocess_plan_kernel).  Read in place, not staged: only ~40 %
-// of the rows contributed, and a staged tile costs more in barriers and
-// idle lanes than the row-source indirection does.
+// K9 after a plan forward: each contributing render row is read in place
+// through the source the forward resolved for it (RowSrc), not staged: only
+// part of the rows contributed, and a staged tile costs more in barriers
+// and idle lanes than the indirection does.
 __global__ void __launch_bounds__(128, GLOD_PBWD_MINB)
-preprocess_bwd_plan_kernel(const glod_gather_plan p, long long n, CamD cam, const int* __restrict__ tiles_of,
-                           const double* __restrict__ g2, double* __restrict__ grads) {
+preprocess_bwd_src_kernel(const RowSrc* __restrict__ rsrc, long long n, CamD cam, const int* __restrict__ tiles_of,
+                          const double* __restrict__ g2, double* __restrict__ grads) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (tiles_of[i] == 0) return bwd_zero(i, n, grads);
-  int node;
-  bwd_one(row_view(row_source(p, i, node)), i, n, cam, g2 + (long long)kG2 * i, grads);
+  const RowSrc r = rsrc[i];
+  bwd_one(row_view(Src{r.base, r.rows, r.idx}), i, n, cam, g2 + (long long)kG2 * i, grads);
 }
 
 }  // namespace
@@ -963,7 +976,7 @@ constexpr int kTimed = 3;   // timed kernels: blend_fwd, blend_bwd, preprocess
 
 struct RasterCtx {
   Buf splats, sorted, keys, keys2, vals, vals2, tiles, tiles_sorted, offs;
-  Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin;
+  Buf ikey, ikey2, ival, ival2, range, tfinal, last, g2, temp, bad, host_pin, rsrc;
   bool long_runs = false;       // last forward finished its depth order with full-width passes
   cudaEvent_t ev_runs = nullptr;  // the long-run flag's read-back landed
   CamD cam{};
@@ -1121,6 +1134,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
   const int nb = int((n + TB - 1) / TB);
   count_launch();
   timing_begin(R, 2, st);
+  if (plan) CK(R->rsrc.ensure(sizeof(RowSrc) * n, st));
   if (plan) {
     static bool smem_set = false;
     if (!smem_set) {
@@ -1129,7 +1143,7 @@ static cudaError_t raster_forward_src(RasterCtx* R, const AttrSrc& src, bool pla
     }
     preprocess_plan_kernel<<<int((n + kPlanRows - 1) / kPlanRows), kPlanRows, kPlanSmem, st>>>(
         src.plan, n, src.row_node, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(), R->vals.as<int>(),
-        R->tiles.as<int>(), R->bad.as<int>(), stats);
+        R->tiles.as<int>(), R->bad.as<int>(), stats, R->rsrc.as<RowSrc>());
   } else {
     preprocess_kernel<<<nb, TB, 0, st>>>(src.attrs, n, cam, R->splats.as<Splat>(), R->keys.as<unsigned long long>(),
                                          R->vals.as<int>(), R->tiles.as<int>(), R->bad.as<int>(), stats);
@@ -1248,8 +1262,8 @@ cudaError_t raster_backward(RasterCtx* R, const float* dimg, double* grads, cuda
   const int TB = 128;
   count_launch();
   if (R->plan_src) {
-    preprocess_bwd_plan_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->src.plan, n, cam, R->tiles.as<int>(),
-                                                                      R->g2.as<double>(), grads);
+    preprocess_bwd_src_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->rsrc.as<RowSrc>(), n, cam,
+                                                                     R->tiles.as<int>(), R->g2.as<double>(), grads);
   } else {
     preprocess_bwd_kernel<<<int((n + TB - 1) / TB), TB, 0, st>>>(R->src.attrs, n, cam, R->tiles.as<int>(),
                                                                  R->g2.as<double>(), grads);
