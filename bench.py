@@ -171,9 +171,10 @@ def roofline_for(kt: dict, stage_ms: dict, args, peaks: dict) -> dict:
       adam:      1340 B per row (576-B node record — params, (m, v), step —
                  read and written, grads 184, id 4) + 8 B per SPT row (the
                  touched-bit atomic of the implicit cache-block refresh)
-      preprocess_plan (K4 gather fused into K5): 216 B per render row
+      preprocess_plan (K4 gather fused into K5): 232 B per render row
                  (184-B source row, 12-B plan entry, 4-B node id written,
-                 depth key 8 + index 4 + tile count 4 written; the 48-B
+                 depth key 8 + index 4 + tile count 4 written, 16-B
+                 resolved source kept for the backward; the 48-B
                  splat records of contributing rows not counted)
 
     `traffic` is the ncu-measured DRAM bytes per launch of the same kernel
@@ -460,7 +461,7 @@ def run_ours(args):
         alg["fwd"] += inst * 52 + npix * 24
         alg["bwd"] += inst * 52 + npix * 24 + R * 144
         alg["adam"] += R * 1340 + n_spt_rows * 8      # + the touched-bit atomic per SPT row
-        alg["pre"] += R * 216
+        alg["pre"] += R * 232
     bt = tr.rast.blend_timing(False)
     stage_ms = {k: float(np.mean(v)) for k, v in tr.timing.items()}
     if tr.host_timing is not None:
