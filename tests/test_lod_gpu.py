@@ -88,3 +88,63 @@ def test_cut_spt_large_f32_keys():
         pl2, sel2 = O.cut_spt(ks, kp, nodes, spt.root, dd)
         assert pl == pl2
         np.testing.assert_array_equal(sel, sel2)
+
+
+@pytest.mark.parametrize("f64", [False, True], ids=["f32_keys", "f64_keys"])
+def test_compact_span_boundaries(f64):
+    """K1 over many SPTs at once, with prefix lengths on and around the
+    span (512 / 256 records), sub-tile (2048 / 1024) and tile boundaries, a
+    share of SPTs taking the root rule, and per-SPT distances: the selected
+    node ids, their (segment, position) and the prefix lengths are
+    bit-exact against the C oracle (spt.py:67-75) — the span fast path and
+    the general path must agree wherever a warp's span starts."""
+    import torch
+    from paper_2507_01110_b200.device import DeviceLodScene
+    from paper_2507_01110_b200.hierarchy import Hierarchy
+    from paper_2507_01110_b200.hspt import Hspt
+    rng = np.random.default_rng(5)
+    lens = [1, 2, 3, 4, 5, 255, 256, 257, 511, 512, 513, 1023, 1024, 1025, 2047, 2048, 2049,
+            4095, 4096, 4097, 16383, 16384, 16385, 70001] + [int(x) for x in rng.integers(1, 40_000, 40)]
+    spts, base = [], 0
+    for n in lens:
+        ks = 25.0 / rng.uniform(0.03, 0.3, n) + rng.uniform(0, 5, n)
+        if not f64:
+            ks = ks.astype(np.float32).astype(np.float64)
+        kp = np.sort(ks)[::-1].copy()
+        kp[0] = np.inf
+        nodes = (base + rng.permutation(n)).astype(np.int64)
+        base += n
+        ks[0] = ks.max()
+        spts.append(Spt(root=int(nodes[0]), root_center=np.zeros(3), nodes=nodes, key_self=ks, key_parent=kp))
+    stub = Hierarchy(attrs=None, parent=np.full(base, -1, np.int32), children=np.full((base, 2), -1, np.int32),
+                     root=0)
+    hs = Hspt(upper_nodes=np.zeros(0, np.int64), spts=spts, passthrough_roots=np.zeros(0, np.int64),
+              size_threshold=1.0, min_subtree=1, lod=LodConfig(1.0))
+    dev = DeviceLodScene(stub, hs)
+    assert dev.key_f64 == f64
+    S = len(spts)
+    order = [spts[int(dev.spt_perm[j])] for j in range(S)]
+    for trial in range(3):
+        d = np.array([s.key_self.max() + 1.0 if rng.uniform() < 0.1 else
+                      float(np.quantile(s.key_self, rng.uniform(0.02, 0.98))) for s in order])
+        res = dev.compact(torch.tensor([S], dtype=torch.int32, device="cuda"),
+                          torch.arange(S, dtype=torch.int32, device="cuda"),
+                          torch.tensor(d, dtype=torch.float64, device="cuda"))
+        total = int(res.total[0].item())
+        want_pl, want_nodes, counts = [], [], []
+        for s, dd in zip(order, d):
+            pl, sel = O.cut_spt(s.key_self, s.key_parent, s.nodes, s.root, dd)
+            want_pl.append(pl)
+            want_nodes.append(np.asarray(sel, np.int64))
+            counts.append(len(sel))
+        want = np.concatenate(want_nodes)
+        assert total == want.size, trial
+        np.testing.assert_array_equal(res.prefix_len[:S].cpu().numpy(), np.asarray(want_pl))
+        got_nodes = res.sel_node[:total].cpu().numpy().astype(np.int64)
+        np.testing.assert_array_equal(got_nodes, want)
+        seg = res.sel_seg[:total].cpu().numpy()
+        np.testing.assert_array_equal(seg, np.repeat(np.arange(S), counts))
+        pos = res.sel_pos[:total].cpu().numpy()
+        flat_nodes = np.concatenate([s.nodes for s in order])
+        offs = np.concatenate([[0], np.cumsum([len(s.nodes) for s in order])[:-1]])
+        np.testing.assert_array_equal(flat_nodes[offs[seg] + pos], want)
