@@ -18,6 +18,15 @@ constexpr int TW = 32, TH = 16;  // output tile
 constexpr int IW = TW + 2 * R, IH = TH + 2 * R;
 constexpr int NT = 256;
 constexpr double C1 = 1e-4, C2 = 9e-4;
+// Pass 2 blurs the f32-stored derivative maps: its window sums in fp32
+// (the inputs are already rounded to f32; a 121-tap f32 sum adds ≲ 1e-6
+// relative, far inside the image-gradient tolerance) unless built with
+// GLOD_SSIM2_F64.
+#ifdef GLOD_SSIM2_F64
+typedef double Acc2;
+#else
+typedef float Acc2;
+#endif
 
 __constant__ double kWin[2 * R + 1];
 
@@ -105,7 +114,7 @@ ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
            const float* __restrict__ dmu, const float* __restrict__ dx2, const float* __restrict__ dxy,
            float* __restrict__ grad, double lam, double inv_n) {
   __shared__ float s0[IH][IW], s1[IH][IW], s2[IH][IW];
-  __shared__ double v[3][TH][IW];
+  __shared__ Acc2 v[3][TH][IW];
   const int ox = blockIdx.x * TW, oy = blockIdx.y * TH;
   for (int c = 0; c < 3; ++c) {
   __syncthreads();
@@ -118,10 +127,10 @@ ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
   __syncthreads();
   for (int k = threadIdx.x; k < TH * IW; k += NT) {
     const int r = k / IW, q = k % IW;
-    double a = 0, b = 0, d = 0;
+    Acc2 a = 0, b = 0, d = 0;
 #pragma unroll
     for (int t = 0; t <= 2 * R; ++t) {
-      const double w = kWin[t];
+      const Acc2 w = Acc2(kWin[t]);
       a += w * s0[r + t][q]; b += w * s1[r + t][q]; d += w * s2[r + t][q];
     }
     v[0][r][q] = a; v[1][r][q] = b; v[2][r][q] = d;
@@ -131,10 +140,10 @@ ssim_pass2(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
     const int r = k / TW, q = k % TW;
     const int x = ox + q, y = oy + r;
     if (x >= W || y >= H) continue;
-    double a = 0, b = 0, d = 0;
+    Acc2 a = 0, b = 0, d = 0;
 #pragma unroll
     for (int t = 0; t <= 2 * R; ++t) {
-      const double w = kWin[t];
+      const Acc2 w = Acc2(kWin[t]);
       a += w * v[0][r][q + t]; b += w * v[1][r][q + t]; d += w * v[2][r][q + t];
     }
     const long long o = 3 * ((long long)y * W + x) + c;
