@@ -80,10 +80,13 @@ ssim_pass1(const float* __restrict__ X, const float* __restrict__ Y, int W, int 
     const double vx = ux2 - mx * mx, vy = uy2 - my * my, cv = uxy - mx * my;
     const double a1 = 2 * mx * my + C1, a2 = 2 * cv + C2;
     const double b1 = mx * mx + my * my + C1, b2 = vx + vy + C2;
-    const double s = (a1 * a2) / (b1 * b2);
-    const double ds_dmu = (2 * my * a2) / (b1 * b2) - s * 2 * mx / b1;
-    const double ds_dvx = -s / b2;
-    const double ds_dcv = 2 * a1 / (b1 * b2);
+    // one division: 1/b1 = b2/(b1·b2), 1/b2 = b1/(b1·b2) (the five fp64
+    // divisions were the larger half of this pass's fp64 work)
+    const double inv = 1.0 / (b1 * b2);
+    const double s = (a1 * a2) * inv;
+    const double ds_dmu = (2 * my * a2) * inv - s * 2 * mx * (b2 * inv);
+    const double ds_dvx = -s * (b1 * inv);
+    const double ds_dcv = 2 * a1 * inv;
     const long long o = 3 * ((long long)y * W + x) + c;
     dmu[o] = float((ds_dmu - 2 * mx * ds_dvx - my * ds_dcv) * inv_n);
     dx2[o] = float(ds_dvx * inv_n);
